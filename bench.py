@@ -1,0 +1,345 @@
+"""Benchmark of the hot path on BASELINE.json configs[1]:
+
+    ImageNet-shaped synthetic .bbox, RAW RGB max_res 256 (256x256x3),
+    RandomResizedCrop 192 + RandomHorizontalFlip + NormalizeImage -> f16, batch 512
+
+One step = one batch of 512 images through the public Loader API.
+
+  value  : images/s with the heap resident in HBM (DeviceResident strategy):
+           per step the loader uploads indices + descriptors and runs the
+           fused kernel on payloads already in HBM.
+  e2e    : images/s through the same Loader with the OsCache strategy:
+           every step gathers the batch's payloads from the mmap'd file into
+           pinned memory and copies them H2D (inside the timed region), and
+           reads the step's labels back D2H.
+  roofline: the fused RRC kernel (K1), CUDA-event timed on the loader's
+           compute stream during the `value` run; algorithmic bytes =
+           sum over images of (source window bytes + output bytes).
+  cpu_baseline: the oracle C port (oracle/bbx_oracle.c) of the same chain on
+           the host cores, bounded sample (rank 0, N=1 only).
+
+`--impl reference` times that CPU port alone on this config (the reference
+is pure Python/numpy and has no RRC; its own CPU path is what the port
+restates, tests/test_oracle.py pins it).
+
+Under torchrun each rank runs its shard (distributed=True: rank r takes
+positions [r*512, (r+1)*512) of each global batch of N*512); no collective on
+the data path; timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+B = 512
+H = W = 256
+C = 3
+OUT = 192
+MEAN = (123.675, 116.28, 103.53)
+STD = (58.395, 57.12, 57.375)
+CHAIN_SPEC = f"rrc:{OUT},{OUT}|flip:0.5|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}/f16"
+ORACLE_SPEC = f"rrc:{OUT},{OUT}|flip:0.5|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}|cast:f16"
+SEED = 3
+N_SAMPLES = int(os.environ.get("BBX_BENCH_SAMPLES", 8192))   # 1.6 GB file, > 126 MB L2 per batch stream
+DATA_DIR = Path(os.environ.get("BBX_BENCH_DIR", "/tmp/bbx_bench"))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dataset_path() -> Path:
+    return DATA_DIR / f"imagenet256_raw_{N_SAMPLES}.bbox"
+
+
+def ensure_dataset(rank: int, barrier) -> Path:
+    import paper_2306_12517_b200 as bx
+
+    path = dataset_path()
+    if rank == 0 and not path.exists():
+        DATA_DIR.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(".tmp")
+        t0 = time.time()
+        bx.write_dataset(bx.SyntheticImageSource(N_SAMPLES, H, W, C, seed=1), tmp, bx.WriterConfig(seed=1))
+        os.replace(tmp, path)
+        log(f"wrote {path} ({path.stat().st_size / 1e9:.2f} GB) in {time.time() - t0:.1f}s")
+    barrier()
+    return path
+
+
+class ClockSampler:
+    """nvidia-smi/NVML clocks and throttle reasons during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:   # no NVML: report nothing rather than guess
+            log("clock sampling unavailable:", e)
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        if not self.samples:
+            return None
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_loader(path, device, rank, world, strategy, slot_count=3):
+    import paper_2306_12517_b200 as bx
+
+    ds = bx.open_dataset(path, strategy)
+    cfg = bx.LoaderConfig(batch_size=B, order=bx.OrderKind.RANDOM, seed=SEED, slot_count=slot_count,
+                          pipelines={"image": bx.parse_pipeline(CHAIN_SPEC)}, device=device,
+                          distributed=world > 1, rank=rank, world_size=world)
+    return ds, bx.Loader(ds, cfg)
+
+
+def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
+    """W warm-up steps, then exactly `steps` steps bracketed by barrier + sync;
+    returns (device seconds max over ranks, d2h bytes per step)."""
+    import torch
+
+    it = loader.iterate_steps(warmup + steps)
+    for _ in range(warmup):
+        b = next(it)
+        if read_back:
+            b["label"].cpu()
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    loader.reset_stats()
+    d2h = 0
+    start.record(stream)
+    for _ in range(steps):
+        b = next(it)
+        if read_back:   # the step's result back on the host (labels of the batch)
+            lab = b["label"].cpu()
+            d2h += lab.numel() * lab.element_size()
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    it.close()
+    secs = start.elapsed_time(end) * 1e-3
+    return reduce_max(secs), d2h / steps
+
+
+def cpu_baseline(path, seconds_budget: float = 15.0):
+    """Oracle C port on the host cores, bounded sample (whole batches of 512)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    f = O.OracleFile(path)
+    field = f.fields[0]
+    ops = O.parse_spec("decode")[:0] + O.parse_spec(ORACLE_SPEC)
+    threads = os.cpu_count() or 1
+    batches = O.epoch_batches("random", SEED, 0, f.num_samples, B)
+    done, t0 = 0, time.perf_counter()
+    out = None
+    while time.perf_counter() - t0 < seconds_budget and done < len(batches):
+        out = O.run_field_batch(f, field, 0, ops, batches[done], SEED, 0, threads, out=out)
+        done += 1
+    el = time.perf_counter() - t0
+    return {"value": done * B / el, "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{done} batches x {B} images of {path.name} (RRC-192+flip+normalize->f16), "
+                      f"{threads} threads, {el:.1f}s"}
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("image_kernel_dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo",
+                                device_id=torch.device("cuda", local) if args.impl == "ours" else None)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def reduce_max(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.impl == "ours" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    config = {"workload": "configs[1]: ImageNet-shaped synthetic .bbox RAW 256x256x3, RandomResizedCrop 192 "
+                          "(scale 0.08-1, ratio 3/4-4/3, bilinear) + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC",
+              "batch_per_gpu": B, "global_batch": B * world, "num_samples": N_SAMPLES, "order": "random",
+              "out_dtype": "f16", "l2_policy": "inputs larger than L2: each step reads ~100 MB of payload and "
+                                               "writes 113 MB of output; 3 output slots rotate"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        path = ensure_dataset(0, lambda: None)
+        from oracle import oracle as O
+
+        f = O.OracleFile(path)
+        ops = O.parse_spec(ORACLE_SPEC)
+        threads = os.cpu_count() or 1
+        batches = O.epoch_batches("random", SEED, 0, f.num_samples, B)
+        out = None
+        for g in range(args.warmup):
+            out = O.run_field_batch(f, f.fields[0], 0, ops, batches[g % len(batches)], SEED, 0, threads, out=out)
+        t0 = time.perf_counter()
+        for g in range(args.steps):
+            out = O.run_field_batch(f, f.fields[0], 0, ops, batches[(args.warmup + g) % len(batches)], SEED, 0,
+                                    threads, out=out)
+        el = time.perf_counter() - t0
+        v = args.steps * B / el
+        print(json.dumps({
+            "impl": "reference", "metric": "images/sec decode+RRC+flip+normalize", "value": v, "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config,
+            "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} batches x {B} images, oracle C port, {threads} threads"},
+            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import paper_2306_12517_b200 as bx
+
+    device = local
+    torch.cuda.set_device(device)
+    path = ensure_dataset(rank, barrier)
+
+    # ---- value: heap resident in HBM
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device))
+    ld.set_profiling(True)
+    with ClockSampler(device) as clk:
+        secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
+    st = ld.stats()
+    ld.shutdown()
+    ds.close()
+    value = world * args.steps * B / secs
+    kern_s = st["kernel_seconds"] / max(st["kernel_timed"], 1)
+    kern_bytes = st["kernel_bytes"] / max(st["kernel_timed"], 1)
+    achieved = kern_bytes / kern_s / 1e9 if st["kernel_timed"] else 0.0
+    peak, peak_src = peaks()
+
+    # ---- e2e: payloads staged from host (mmap -> pinned -> H2D) every step
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache())
+    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
+    st2 = ld2.stats()
+    ld2.shutdown()
+    ds2.close()
+    e2e = world * args.steps * B / e2e_secs
+    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": "images/sec decode+RRC+flip+normalize", "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (SyntheticImageSource pattern, 256x256x3 RAW, writer seed 1)",
+        "config": config,
+        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): mmap -> pinned -> H2D -> K1"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": load_traffic(),
+                     "kernel": "image_kernel<half, resample> (K1)", "kernel_us": kern_s * 1e6,
+                     "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src},
+        "gpu_launches": int(st["kernel_launches"]),
+        "clocks": clk.summary(),
+    }
+    if world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds)
+        except Exception as e:   # the baseline must not sink the GPU line
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,77 @@
+"""Build libbbx.so in-tree (nvcc for sm_100a + g++ for the host engine).
+
+No JIT cache: the .so lands next to this file so it travels to the GPU box
+with the repo snapshot.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+CSRC = HERE / "csrc"
+LIB = HERE / "libbbx.so"
+BUILD = HERE / "_build_obj"
+
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = shutil.which("nvcc") or f"{CUDA_HOME}/bin/nvcc"
+GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CXX = os.environ.get("CXX", "g++")
+
+HOST_SOURCES = ["engine.cpp", "format.cpp", "orders.cpp"]
+CUDA_SOURCES = ["kernels.cu"]
+HEADERS = ["bbx_internal.h", "engine.h"]
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in HOST_SOURCES + CUDA_SOURCES + HEADERS] + [HERE.parent / "include" / "bbx.h",
+                                                                       Path(__file__)]
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale():
+        return LIB
+    BUILD.mkdir(exist_ok=True)
+    objs = []
+    inc = ["-I", str(CSRC), "-I", str(HERE.parent / "include"), "-I", f"{CUDA_HOME}/include"]
+    for src in CUDA_SOURCES:
+        obj = BUILD / (src + ".o")
+        cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+               *inc, "-c", str(CSRC / src), "-o", str(obj)]
+        _run(cmd, verbose)
+        objs.append(obj)
+    for src in HOST_SOURCES:
+        obj = BUILD / (src + ".o")
+        # -ffp-contract=off: the Normalize LUT must be one IEEE f32 subtract
+        # and one IEEE f32 divide (pipeline.py:158-160), never an FMA.
+        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+               "-Wno-format-security", *inc, "-c", str(CSRC / src), "-o", str(obj)]
+        _run(cmd, verbose)
+        objs.append(obj)
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [NVCC, *GENCODE, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", "-Xcompiler", "-fPIC"]
+    _run(cmd, verbose)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def _run(cmd, verbose):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode:
+        print(" ".join(cmd))
+        print(r.stdout[-4000:], r.stderr[-8000:])
+    if r.returncode:
+        raise RuntimeError(f"build step failed: {cmd[0]} {cmd[-3] if len(cmd) > 3 else ''}")
+    (BUILD / "ptxas.log").open("a").write(r.stderr)
+
+
+if __name__ == "__main__":
+    import sys
+    build(force="--force" in sys.argv, verbose=True)

@@ -1,0 +1,99 @@
+// Internal structures shared by the host engine (engine.cpp) and the sm_100a
+// kernels (kernels.cu).  See DESIGN.md §3 for the HBM layout they describe.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+
+#include "../../include/bbx.h"
+
+namespace bbx {
+
+enum SrcKind : int32_t { SRC_DECODE = 0, SRC_RESAMPLE = 1, SRC_ARRAY = 2 };
+enum Codec : int32_t { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2 };
+enum ValueMode : int32_t { VAL_COPY = 0, VAL_LUT = 1, VAL_DIRECT = 2 };
+
+constexpr int kMaxRemaps = 12;
+constexpr int kMaxValueOps = 8;
+constexpr int kDescHeader = 24;     // bytes before the per-sample params
+constexpr int kThreads = 256;       // CTA size of the image kernels
+constexpr int kLutChannels = 4;     // LUT path covers C <= 4
+constexpr int kSmemBudget = 96 * 1024;
+
+// One geometric op after the source, in chain order.  Separable by axis:
+// output (y, x) -> input (fy(y), fx(x)).
+struct Remap {
+  int32_t kind;          // BBX_OP_CROP / BBX_OP_FLIP / BBX_OP_RESIZE
+  int32_t in_h, in_w;    // input spec (pipeline.py output_spec propagation)
+  int32_t out_h, out_w;
+  int32_t prm;           // first per-sample param slot (crop: top, left; flip: bit)
+};
+
+// Everything the kernels need about one compiled chain; passed by value.
+struct PlanDev {
+  int32_t src_kind;
+  int32_t canvas_h, canvas_w, channels;   // source op output (Decode: max dims)
+  int32_t src_row_w;                       // widest source image row in pixels (field max width)
+  int32_t src_elem;                        // bytes per source element (1 for images)
+  int32_t src_dtype;                       // bbx_dtype of the source elements
+  int32_t out_h, out_w, out_c;             // final output (3-D view; arrays: 1 x N x 1)
+  int32_t out_dtype;
+  int32_t n_remaps;
+  Remap remaps[kMaxRemaps];
+  int32_t value_mode;
+  int32_t n_vops;
+  int32_t vop_kind[kMaxValueOps];          // TOFLOAT / NORMALIZE / NORMALIZE_PC
+  float vop_mean[kMaxValueOps][4];
+  float vop_std[kMaxValueOps][4];
+  int32_t desc_stride;
+  int32_t n_params;
+  int32_t rows_per_tile;
+  int32_t tiles_per_sample;
+  int64_t out_sample_elems;
+  int64_t scratch_bytes;                   // per-sample decode scratch (RLE)
+  int32_t has_remaps_3d;                   // arrays: 3-D remaps present
+  int32_t smem_bytes;
+};
+
+// Per-sample descriptor header (kDescHeader bytes), followed by n_params int32.
+struct SampleDesc {
+  uint64_t src;    // payload byte offset from the launch's payload base
+  uint32_t len;    // payload length
+  uint16_t h, w;   // image cell dims
+  uint8_t c, codec, skip, pad;
+  int32_t index_lo;  // sample index (low 32 bits, diagnostics)
+};
+static_assert(sizeof(SampleDesc) == kDescHeader, "descriptor header layout");
+
+// Per-sample device status (K2 RLE errors).
+struct SampleStatus {
+  int32_t kind;    // 0 ok, 1 "rle runs sum past n", 2 "rle runs sum to v, expected n"
+  int32_t pad;
+  int64_t value;
+};
+
+struct LaunchArgs {
+  const uint8_t* desc;       // count * desc_stride bytes (device)
+  const uint8_t* payload;    // payload base (device): staged region or file image in HBM
+  uint8_t* scratch;          // count * scratch_bytes (device)
+  void* out;                 // count * out_sample_elems elements
+  const void* lut;           // VAL_LUT table: channels * 256 entries of the output type
+  SampleStatus* status;      // count entries
+  int32_t count;
+};
+
+struct ScalarArgs {
+  const int64_t* idx;        // count indices (device)
+  int32_t count;
+  int32_t n_fields;
+  const uint64_t* cols[16];  // device columns, num_samples entries each
+  uint64_t* outs[16];
+};
+
+// kernels.cu
+int launch_rle_expand(const PlanDev& P, const LaunchArgs& A, void* stream);
+int launch_image(const PlanDev& P, const LaunchArgs& A, void* stream);
+int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream);
+int launch_scalar_gather(const ScalarArgs& S, void* stream);
+int image_smem_bytes(const PlanDev& P);
+
+}  // namespace bbx

@@ -1,0 +1,1020 @@
+// The batch-granular device loader behind bbx_loader_* (include/bbx.h).
+//
+// Replaces the reference's per-sample worker machinery (loader.py:251-447:
+// _EpochRun, FillState, _process_position; pipeline.py:302-406 PipelinePlan)
+// with one pipeline per loader:
+//
+//   submit(slot, idx)  ->  [pipeline thread]
+//        1. host: rows -> per-sample descriptors + RNG params (rng.py, exact),
+//           payload checks with the reference's error texts (codecs.py:91-128)
+//        2. pool threads gather payload extents mmap -> pinned staging slot
+//        3. copy stream: one cudaMemcpyAsync H2D of the whole slot
+//        4. compute stream: K2 RLE expand (if any RLE sample), K1/K3 kernels,
+//           status D2H; record slot `done` event
+//   wait(slot)         ->  cudaEventSynchronize(done) + error merge
+//
+// Slots are double/triple buffered: the gather of batch g+2 overlaps the H2D
+// of g+1 and the kernels of g.  With a device-resident heap
+// (bbx_dataset_make_resident) steps 2-3 shrink to the descriptor upload.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "engine.h"
+
+namespace bbx {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+const char* last_error() { return g_err.c_str(); }
+
+// -------------------------------------------------------------------- pool
+Pool::Pool(int n) {
+  for (int i = 0; i < n - 1; ++i) workers_.emplace_back([this] { run(); });
+}
+Pool::~Pool() {
+  { std::lock_guard<std::mutex> g(mu_); stop_ = true; }
+  cv_.notify_all();
+  for (auto& t : workers_) t.join();
+}
+void Pool::run() {
+  uint64_t seen = 0;
+  for (;;) {
+    const std::function<void(int64_t)>* fn;
+    int64_t n;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      fn = fn_; n = n_;
+      ++active_;
+    }
+    for (int64_t i; (i = next_.fetch_add(1)) < n;) (*fn)(i);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      if (--active_ == 0) done_cv_.notify_all();
+    }
+  }
+}
+void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
+  if (n <= 0) return;
+  if (workers_.empty() || n == 1) { for (int64_t i = 0; i < n; ++i) fn(i); return; }
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    fn_ = &fn; n_ = n; next_.store(0); ++gen_;
+  }
+  cv_.notify_all();
+  for (int64_t i; (i = next_.fetch_add(1)) < n;) fn(i);
+  std::unique_lock<std::mutex> lk(mu_);
+  done_cv_.wait(lk, [&] { return active_ == 0 && next_.load() >= n; });
+}
+
+// -------------------------------------------------------------------- plan
+static int dtype_size(int dt) {
+  switch (dt) { case BBX_U8: return 1; case BBX_I64: case BBX_F64: return 8; case BBX_F32: return 4; default: return 2; }
+}
+static uint16_t f32_to_bf16_bits(float f) {      // round to nearest even
+  uint32_t u; std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+static uint16_t f32_to_f16_bits(float f) {       // IEEE binary16, round to nearest even
+  uint32_t x; std::memcpy(&x, &f, 4);
+  uint32_t sign = (x >> 16) & 0x8000u;
+  uint32_t ax = x & 0x7fffffffu;
+  if (ax >= 0x7f800000u) return (uint16_t)(sign | (ax > 0x7f800000u ? 0x7e00u : 0x7c00u));
+  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);            // >= 65520 rounds to inf
+  if (ax < 0x38800000u) {                                                // subnormal half
+    if (ax < 0x33000000u) return (uint16_t)sign;                         // < 2^-25 -> 0 (2^-25 ties to even 0)
+    uint32_t mant = (ax & 0x7fffffu) | 0x800000u;
+    int e = (int)(ax >> 23);
+    int shift = 126 - e + 1 + 13;                                        // to 10-bit subnormal
+    uint32_t q = mant >> shift, rem = mant & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (q & 1u))) ++q;
+    return (uint16_t)(sign | q);
+  }
+  uint32_t r = ax - 0x38000000u;                                         // rebias exponent 127 -> 15
+  uint32_t q = r >> 13, rem = r & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (q & 1u))) ++q;
+  return (uint16_t)(sign | q);
+}
+
+struct Draw {        // one RNG-consuming op, in chain order (host program)
+  int kind;          // BBX_OP_RRC / BBX_OP_CENTERCROP / BBX_OP_CROP / BBX_OP_FLIP
+  int slot;          // first param slot
+  int in_h, in_w, h, w;
+  double p;
+  double scale[2], ratio[2];
+};
+
+struct Plan {
+  int field_index = -1;
+  bool scalar = false;
+  PlanDev dev{};
+  std::vector<Draw> draws;
+  int64_t out_sample_bytes = 0;
+  int64_t max_payload = 0;       // over the whole dataset (exact staging capacity)
+  bool field_has_rle = false;
+  void* d_lut = nullptr;
+  std::vector<void*> outs;       // per slot
+  std::vector<uint8_t*> d_scratch;
+  uint64_t* d_col = nullptr;     // scalar column (num_samples x 8 B)
+};
+
+struct HostErr { int64_t pos = -1; int plan = 0; int code = 0; std::string msg; };
+
+struct Slot {
+  uint8_t* h_stage = nullptr;
+  uint8_t* d_stage = nullptr;
+  size_t cap = 0;
+  SampleStatus* d_status = nullptr;
+  SampleStatus* h_status = nullptr;
+  cudaEvent_t h2d_done{}, done{}, release{};
+  cudaEvent_t k0{}, k1{};          // profiling: around the transform kernels
+  bool timed = false;
+  int64_t timed_launches = 0, timed_bytes = 0;
+  bool released_pending = false, used = false;
+  // job
+  int state = 0;                 // 0 idle, 1 queued, 2 launched
+  int count = 0;
+  uint64_t seed = 0, epoch = 0;
+  std::vector<int64_t> idx;
+  HostErr herr;
+  int fatal = 0;
+  std::string fatal_msg;
+  std::vector<char> plan_has_rle;
+};
+
+}  // namespace bbx
+
+using namespace bbx;
+
+struct bbx_loader {
+  bbx_dataset* ds = nullptr;
+  int device = 0;
+  int batch = 0, nslots = 0;
+  std::vector<Plan> plans;
+  std::vector<Slot> slots;
+  cudaStream_t copy_st{}, comp_st{};
+  std::unique_ptr<Pool> pool;
+  bool finalized = false;
+  size_t slot_bytes = 0, desc_bytes = 0, idx_off = 0;
+  std::vector<size_t> desc_off;       // per plan, within a slot
+  std::vector<size_t> pay_off;        // per plan, start of its payload region
+  // pipeline thread
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv, done_cv;
+  std::deque<int> queue;
+  bool stop = false;
+  bbx_loader_stats stats{};
+  bool profiling = false;
+  std::mutex stats_mu;
+};
+
+namespace bbx {
+
+static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n_ops, Plan& pl) {
+  const bbx_dataset* ds = L->ds;
+  if (field_index < 0 || field_index >= (int)ds->fields.size())
+    return fail(BBX_INVALID_ARGUMENT, "field index %d out of range", field_index);
+  const Field& f = ds->fields[field_index];
+  if (n_ops < 1) return fail(BBX_SPEC_MISMATCH, "a pipeline needs at least one transform");
+  PlanDev& P = pl.dev;
+  std::memset(&P, 0, sizeof P);
+  pl.field_index = field_index;
+  int H, W, C, dt, ndim;
+  int nparams = 0;
+  const bbx_op& s0 = ops[0];
+  if (s0.kind == BBX_OP_DECODE || s0.kind == BBX_OP_RRC || s0.kind == BBX_OP_CENTERCROP) {
+    if (f.info.kind != 4) return fail(BBX_SPEC_MISMATCH, "decode expects an image field, got field '%s'", f.info.name);
+    C = f.info.channels;
+    P.src_row_w = f.info.max_width;
+    if (s0.kind == BBX_OP_DECODE) {
+      P.src_kind = SRC_DECODE; H = f.info.max_height; W = f.info.max_width;
+    } else {
+      if (s0.h < 1 || s0.w < 1) return fail(BBX_SPEC_MISMATCH, "decoder output size must be >= 1");
+      P.src_kind = SRC_RESAMPLE; H = s0.h; W = s0.w;
+      Draw d{}; d.kind = s0.kind; d.slot = 0; d.h = s0.h; d.w = s0.w; d.p = s0.p;
+      d.scale[0] = s0.scale[0]; d.scale[1] = s0.scale[1]; d.ratio[0] = s0.ratio[0]; d.ratio[1] = s0.ratio[1];
+      if (s0.kind == BBX_OP_RRC && !(d.scale[0] > 0 && d.scale[0] <= d.scale[1] && d.ratio[0] > 0 && d.ratio[0] <= d.ratio[1]))
+        return fail(BBX_SPEC_MISMATCH, "random-resized-crop needs 0 < scale[0] <= scale[1] and 0 < ratio[0] <= ratio[1]");
+      if (s0.kind == BBX_OP_CENTERCROP && !(d.p > 0 && d.p <= 1.0))
+        return fail(BBX_SPEC_MISMATCH, "center-crop ratio must be in (0, 1]");
+      pl.draws.push_back(d);
+      nparams = 4;
+    }
+    dt = BBX_U8; ndim = 3;
+    P.src_elem = 1; P.src_dtype = BBX_U8;
+  } else if (s0.kind == BBX_OP_ARRAYREAD) {
+    if (f.info.kind != 2) return fail(BBX_SPEC_MISMATCH, "array-read expects an array field, got field '%s'", f.info.name);
+    static const int map_dt[4] = {BBX_U8, BBX_I64, BBX_F32, BBX_F64};
+    dt = map_dt[f.info.array_dtype];
+    ndim = f.info.ndims;
+    P.src_kind = SRC_ARRAY; P.src_elem = dtype_size(dt); P.src_dtype = dt;
+    if (ndim == 3) { H = (int)f.info.dims[0]; W = (int)f.info.dims[1]; C = (int)f.info.dims[2]; }
+    else {
+      int64_t last = f.info.dims[ndim - 1], tot = 1;
+      for (int k = 0; k < ndim; ++k) tot *= f.info.dims[k];
+      if (tot > INT32_MAX) return fail(BBX_SPEC_MISMATCH, "array field too large for a device plan");
+      H = 1; W = (int)(tot / last); C = (int)last;
+    }
+    P.src_row_w = W;
+  } else {
+    return fail(BBX_SPEC_MISMATCH, "the first transform must read from the sample source");
+  }
+  P.canvas_h = H; P.canvas_w = W; P.channels = C;
+  int out_dt = dt;
+  bool cast_seen = false;
+  for (int i = 1; i < n_ops; ++i) {
+    const bbx_op& o = ops[i];
+    if (cast_seen) return fail(BBX_SPEC_MISMATCH, "cast must be the last transform");
+    switch (o.kind) {
+      case BBX_OP_DECODE: case BBX_OP_ARRAYREAD: case BBX_OP_RRC: case BBX_OP_CENTERCROP:
+        return fail(BBX_SPEC_MISMATCH, "source transforms may only appear first");
+      case BBX_OP_TOFLOAT: case BBX_OP_NORMALIZE: case BBX_OP_NORMALIZE_PC: {
+        if (P.n_vops >= kMaxValueOps) return fail(BBX_SPEC_MISMATCH, "too many value transforms");
+        if (o.kind == BBX_OP_NORMALIZE_PC && C > 4)
+          return fail(BBX_SPEC_MISMATCH, "per-channel normalize supports at most 4 channels");
+        int v = P.n_vops++;
+        P.vop_kind[v] = o.kind;
+        for (int k = 0; k < 4; ++k) { P.vop_mean[v][k] = o.mean[k]; P.vop_std[v][k] = o.std[k]; }
+        if (o.kind == BBX_OP_NORMALIZE && o.std[0] == 0.f) return fail(BBX_SPEC_MISMATCH, "normalize std must be nonzero");
+        out_dt = BBX_F32;
+        break;
+      }
+      case BBX_OP_CAST:
+        if (o.dtype != BBX_F32 && o.dtype != BBX_F16 && o.dtype != BBX_BF16)
+          return fail(BBX_SPEC_MISMATCH, "cast target must be float32, float16 or bfloat16");
+        if (out_dt != BBX_F32) return fail(BBX_SPEC_MISMATCH, "cast expects float32 input");
+        out_dt = o.dtype; cast_seen = true;
+        break;
+      case BBX_OP_FLIP: case BBX_OP_CROP: case BBX_OP_RESIZE: {
+        if (ndim != 3) return fail(BBX_SPEC_MISMATCH, "%s expects HxWxC input",
+                                   o.kind == BBX_OP_FLIP ? "flip" : (o.kind == BBX_OP_CROP ? "crop" : "resize"));
+        if (P.n_remaps >= kMaxRemaps) return fail(BBX_SPEC_MISMATCH, "too many geometric transforms");
+        Remap& m = P.remaps[P.n_remaps++];
+        m.kind = o.kind; m.in_h = H; m.in_w = W;
+        Draw d{}; d.kind = o.kind; d.in_h = H; d.in_w = W;
+        if (o.kind == BBX_OP_FLIP) {
+          m.out_h = H; m.out_w = W; m.prm = nparams; d.slot = nparams; d.p = o.p; nparams += 1;
+          pl.draws.push_back(d);
+        } else if (o.kind == BBX_OP_CROP) {
+          if (H < o.h || W < o.w || o.h < 1 || o.w < 1)
+            return fail(BBX_SPEC_MISMATCH, "cannot crop (%d, %d, %d) to %dx%d", H, W, C, o.h, o.w);
+          m.out_h = o.h; m.out_w = o.w; m.prm = nparams; d.slot = nparams; d.h = o.h; d.w = o.w; nparams += 2;
+          pl.draws.push_back(d);
+          H = o.h; W = o.w;
+        } else {
+          if (o.h < 1 || o.w < 1) return fail(BBX_SPEC_MISMATCH, "resize target must be >= 1");
+          m.out_h = o.h; m.out_w = o.w; m.prm = 0;
+          H = o.h; W = o.w;
+        }
+        break;
+      }
+      default:
+        return fail(BBX_SPEC_MISMATCH, "transform kind %d is not a device transform (Opaque stages cannot run on "
+                                       "the device path)", o.kind);
+    }
+  }
+  P.out_h = H; P.out_w = W; P.out_c = C;
+  P.out_dtype = out_dt;
+  P.n_params = nparams;
+  P.desc_stride = (kDescHeader + 4 * nparams + 15) / 16 * 16;
+  P.has_remaps_3d = P.n_remaps > 0;
+  P.out_sample_elems = (int64_t)H * W * C;
+  pl.out_sample_bytes = P.out_sample_elems * dtype_size(out_dt);
+  bool has_values = P.n_vops > 0;
+  if (P.src_kind == SRC_ARRAY) {
+    P.value_mode = has_values ? VAL_DIRECT : VAL_COPY;
+    if (has_values && P.src_dtype == BBX_F64 && false) {}
+  } else {
+    P.value_mode = !has_values ? VAL_COPY : (C <= kLutChannels ? VAL_LUT : VAL_DIRECT);
+    if (P.value_mode == VAL_COPY && out_dt != BBX_U8) return fail(BBX_SPEC_MISMATCH, "unexpected output dtype");
+    // tile height: 16 rows, shrunk until the staged rows fit the smem budget
+    P.rows_per_tile = std::min(16, H);
+    for (;;) {
+      P.smem_bytes = image_smem_bytes(P);
+      if (P.smem_bytes <= kSmemBudget || P.rows_per_tile == 1) break;
+      P.rows_per_tile = std::max(1, P.rows_per_tile / 2);
+    }
+    if (P.smem_bytes > kSmemBudget || (int64_t)P.src_row_w * C + 64 > 65535)
+      return fail(BBX_SPEC_MISMATCH, "image rows too wide for the device plan (%d x %d channels)", P.src_row_w, C);
+    P.tiles_per_sample = (H + P.rows_per_tile - 1) / P.rows_per_tile;
+    P.scratch_bytes = ((int64_t)f.info.max_height * f.info.max_width * C + 15) / 16 * 16;
+  }
+  // LUT: the whole u8 -> output value chain, computed exactly once (IEEE f32,
+  // -ffp-contract=off: one subtract and one divide per Normalize).
+  if (P.value_mode == VAL_LUT) {
+    int osz = dtype_size(out_dt);
+    std::vector<uint8_t> lut((size_t)C * 256 * osz);
+    for (int k = 0; k < C; ++k)
+      for (int v = 0; v < 256; ++v) {
+        float x = (float)v;
+        for (int i = 0; i < P.n_vops; ++i) {
+          if (P.vop_kind[i] == BBX_OP_NORMALIZE) { volatile float t = x - P.vop_mean[i][0]; x = t / P.vop_std[i][0]; }
+          else if (P.vop_kind[i] == BBX_OP_NORMALIZE_PC) { volatile float t = x - P.vop_mean[i][k]; x = t / P.vop_std[i][k]; }
+        }
+        size_t at = ((size_t)k * 256 + v) * osz;
+        if (out_dt == BBX_F32) std::memcpy(&lut[at], &x, 4);
+        else { uint16_t b = out_dt == BBX_F16 ? f32_to_f16_bits(x) : f32_to_bf16_bits(x); std::memcpy(&lut[at], &b, 2); }
+      }
+    CK(cudaMalloc(&pl.d_lut, lut.size()));
+    CK(cudaMemcpy(pl.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+  }
+  // one pass over the row table: exact staging capacity, RLE presence
+  int64_t mx = 0;
+  bool rle = false;
+  if (f.info.kind == 4) {
+    for (int64_t i = 0; i < ds->num_samples; ++i) {
+      ImageCell c = image_cell(ds, i, f);
+      mx = std::max<int64_t>(mx, (int64_t)c.length);
+      rle |= c.codec == CODEC_RLE;
+    }
+  } else {
+    mx = f.array_nbytes;
+  }
+  pl.max_payload = mx;
+  pl.field_has_rle = rle;
+  return BBX_OK;
+}
+
+// Host-side per-sample work for one plan: descriptor + RNG params + checks.
+// Returns false (and fills err) when the sample must be skipped.
+static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t seed, uint64_t epoch, uint8_t* desc,
+                      uint64_t* src_off, uint32_t* len, HostErr& err, int64_t pos, int plan_idx) {
+  const Field& f = ds->fields[pl.field_index];
+  SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
+  int32_t* prm = reinterpret_cast<int32_t*>(desc + kDescHeader);
+  std::memset(desc, 0, pl.dev.desc_stride);
+  d->index_lo = (int32_t)i;
+  auto bad = [&](int code, const char* fmt, auto... args) {
+    d->skip = 1;
+    if (err.pos < 0 || pos < err.pos || (pos == err.pos && plan_idx < err.plan)) {
+      char buf[512];
+      std::snprintf(buf, sizeof buf, fmt, args...);
+      err.pos = pos; err.plan = plan_idx; err.code = code; err.msg = buf;
+    }
+    return false;
+  };
+  if (f.info.kind == 4) {
+    ImageCell c = image_cell(ds, i, f);
+    d->h = (uint16_t)c.h; d->w = (uint16_t)c.w; d->c = (uint8_t)c.c; d->codec = (uint8_t)c.codec;
+    *src_off = c.offset; *len = (uint32_t)c.length;
+    d->len = (uint32_t)c.length;
+    if (c.length > 0xFFFFFFFFull) return bad(BBX_CORRUPT_PAYLOAD, "payload of %llu bytes is too large", (unsigned long long)c.length);
+    int mh = f.info.max_height, mw = f.info.max_width, ch = f.info.channels;
+    if (pl.dev.src_kind == SRC_DECODE) {        // decode_image(out[:h, :w, :]) shape check
+      if (c.h > mh || c.w > mw || c.c != ch)
+        return bad(BBX_SCHEMA_MISMATCH, "output buffer must be u8 (%d, %d, %d), got uint8 (%d, %d, %d)", c.h, c.w, c.c,
+                   std::min(c.h, mh), std::min(c.w, mw), ch);
+    } else if (c.h > mh || c.w > mw || c.c != ch) {
+      return bad(BBX_SCHEMA_MISMATCH, "image %dx%dx%d does not fit field (%d, %d, %d)", c.h, c.w, c.c, mh, mw, ch);
+    }
+    int64_t n = (int64_t)c.h * c.w * c.c;
+    if (c.codec == CODEC_RAW) {
+      if ((int64_t)c.length != n) return bad(BBX_CORRUPT_PAYLOAD, "raw payload is %lld bytes, expected %lld",
+                                             (long long)c.length, (long long)n);
+    } else if (c.codec == CODEC_RLE) {
+      if (c.length % 5) return bad(BBX_CORRUPT_PAYLOAD, "rle payload length is not a multiple of 5");
+    } else if (c.codec == CODEC_SUB2) {
+      int64_t m = (int64_t)((c.h + 1) / 2) * ((c.w + 1) / 2) * c.c;
+      if ((int64_t)c.length != m) return bad(BBX_CORRUPT_PAYLOAD, "subsampled payload is %lld bytes, expected %lld",
+                                             (long long)c.length, (long long)m);
+    } else {
+      return bad(BBX_CORRUPT_PAYLOAD, "unknown codec %d", c.codec);
+    }
+    if (n == 0) return bad(BBX_SCHEMA_MISMATCH, "image dims must all be >= 1");
+  } else {
+    *src_off = u64_cell(ds, i, f);
+    *len = (uint32_t)f.array_nbytes;
+    d->len = (uint32_t)f.array_nbytes;
+    if (*src_off + f.array_nbytes > ds->map_len) return bad(BBX_INVALID_FILE, "array payload past end of file");
+  }
+  // per-sample stream (loader.py:339): stream_seed(seed, TAG_SAMPLE, epoch, i, fidx)
+  Rng r(fold(fold(fold(fold(seed, 2), epoch), (uint64_t)i), (uint64_t)pl.field_index));
+  for (const Draw& dr : pl.draws) {
+    switch (dr.kind) {
+      case BBX_OP_RRC: {
+        int t, l, hh, ww;
+        rrc_window(r, d->h, d->w, dr.scale, dr.ratio, &t, &l, &hh, &ww);
+        prm[0] = t; prm[1] = l; prm[2] = hh; prm[3] = ww;
+        break;
+      }
+      case BBX_OP_CENTERCROP: {
+        int t, l, hh, ww;
+        center_window(d->h, d->w, dr.p, &t, &l, &hh, &ww);
+        prm[0] = t; prm[1] = l; prm[2] = hh; prm[3] = ww;
+        break;
+      }
+      case BBX_OP_CROP:                          // pipeline.py:199-202: top, then left
+        prm[dr.slot] = (int32_t)r.below((uint64_t)(dr.in_h - dr.h + 1));
+        prm[dr.slot + 1] = (int32_t)r.below((uint64_t)(dr.in_w - dr.w + 1));
+        break;
+      case BBX_OP_FLIP:                          // pipeline.py:177-181
+        prm[dr.slot] = r.chance(dr.p) ? 1 : 0;
+        break;
+    }
+  }
+  return true;
+}
+
+static void pipeline_loop(bbx_loader* L);
+
+static int finalize(bbx_loader* L) {
+  if (L->finalized) return BBX_OK;
+  CK(cudaSetDevice(L->device));
+  // slot layout: [idx: B*8][desc blocks per plan][payload regions per plan]
+  size_t off = 0;
+  L->idx_off = 0;
+  off += (size_t)L->batch * 8;
+  off = (off + 255) / 256 * 256;
+  L->desc_off.assign(L->plans.size(), 0);
+  L->pay_off.assign(L->plans.size(), 0);
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    if (L->plans[p].scalar) continue;
+    L->desc_off[p] = off;
+    off += (size_t)L->batch * L->plans[p].dev.desc_stride;
+    off = (off + 255) / 256 * 256;
+  }
+  L->desc_bytes = off;
+  bool resident = L->ds->d_heap != nullptr;
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    if (L->plans[p].scalar) continue;
+    L->pay_off[p] = off;
+    if (!resident) off += (size_t)L->batch * (size_t)((L->plans[p].max_payload + 15) / 16 * 16);
+    off = (off + 255) / 256 * 256;
+  }
+  L->slot_bytes = off + 256;
+  size_t nplans = L->plans.size();
+  for (auto& S : L->slots) {
+    CK(cudaHostAlloc(&S.h_stage, L->slot_bytes, cudaHostAllocDefault));
+    CK(cudaMalloc(&S.d_stage, L->slot_bytes));
+    S.cap = L->slot_bytes;
+    CK(cudaMalloc(&S.d_status, sizeof(SampleStatus) * L->batch * std::max<size_t>(nplans, 1)));
+    CK(cudaHostAlloc(&S.h_status, sizeof(SampleStatus) * L->batch * std::max<size_t>(nplans, 1), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&S.h2d_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&S.release, cudaEventDisableTiming));
+    CK(cudaEventCreate(&S.k0));
+    CK(cudaEventCreate(&S.k1));
+  }
+  for (auto& pl : L->plans) {
+    if (pl.scalar || !pl.field_has_rle) continue;
+    pl.d_scratch.assign(L->nslots, nullptr);
+    for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_scratch[s], (size_t)L->batch * pl.dev.scratch_bytes + 64));
+  }
+  L->th = std::thread(pipeline_loop, L);
+  L->finalized = true;
+  return BBX_OK;
+}
+
+// The per-batch pipeline body (runs on the loader thread).
+static int process_slot(bbx_loader* L, int s) {
+  Slot& S = L->slots[s];
+  const bbx_dataset* ds = L->ds;
+  const int count = S.count;
+  const bool resident = ds->d_heap != nullptr;
+  CK(cudaSetDevice(L->device));
+  // the pinned slot may still be the source of the previous H2D
+  if (S.used) CK(cudaEventSynchronize(S.h2d_done));
+  S.herr = HostErr{};
+  S.plan_has_rle.assign(L->plans.size(), 0);
+  uint8_t* H = S.h_stage;
+  std::memcpy(H + L->idx_off, S.idx.data(), (size_t)count * 8);
+  for (int64_t pos = 0; pos < count; ++pos) {
+    int64_t i = S.idx[pos];
+    if (i < 0 || i >= ds->num_samples) {
+      if (S.herr.pos < 0) {
+        S.herr.pos = pos; S.herr.code = BBX_INDEX_OUT_OF_RANGE;
+        char buf[128];
+        std::snprintf(buf, sizeof buf, "sample %lld out of range [0, %lld)", (long long)i, (long long)ds->num_samples);
+        S.herr.msg = buf;
+      }
+      reinterpret_cast<int64_t*>(H + L->idx_off)[pos] = 0;   // keep device gathers in bounds
+    }
+  }
+  // descriptors + payload plan (serial: ~100 ns per sample per field)
+  struct Copy { const uint8_t* src; uint8_t* dst; uint32_t len; };
+  std::vector<Copy> copies;
+  if (!resident) copies.reserve((size_t)count * L->plans.size());
+  double t0 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    const Plan& pl = L->plans[p];
+    if (pl.scalar) continue;
+    uint8_t* dblk = H + L->desc_off[p];
+    size_t pay = L->pay_off[p];
+    size_t stride = (size_t)((pl.max_payload + 15) / 16 * 16);
+    for (int pos = 0; pos < count; ++pos) {
+      int64_t i = S.idx[pos];
+      uint8_t* desc = dblk + (size_t)pos * pl.dev.desc_stride;
+      if (i < 0 || i >= ds->num_samples) {
+        std::memset(desc, 0, pl.dev.desc_stride);
+        reinterpret_cast<SampleDesc*>(desc)->skip = 1;
+        continue;
+      }
+      uint64_t off = 0;
+      uint32_t len = 0;
+      bool ok = fill_desc(ds, pl, i, S.seed, S.epoch, desc, &off, &len, S.herr, pos, (int)p);
+      SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
+      if (!ok) continue;
+      if (d->codec == CODEC_RLE && ds->fields[pl.field_index].info.kind == 4) S.plan_has_rle[p] = 1;
+      if (resident) {
+        d->src = off;                                   // absolute file offset; base = heap - heap_offset
+      } else {
+        size_t at = (size_t)pos * stride;
+        d->src = at;                                    // relative to this plan's payload region
+        if (len) copies.push_back({ds->map + off, H + pay + at, len});
+      }
+    }
+  }
+  // parallel gather: mmap page cache -> pinned slot
+  if (!copies.empty()) {
+    L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
+      std::memcpy(copies[k].dst, copies[k].src, copies[k].len);
+    });
+  }
+  double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
+  // H2D on the copy stream (after the previous kernels reading d_stage)
+  size_t bytes = resident ? L->desc_bytes : L->slot_bytes - 256;
+  if (!resident) {
+    // copy only up to the last used payload byte of the last plan
+    size_t last = L->desc_bytes;
+    for (size_t p = 0; p < L->plans.size(); ++p)
+      if (!L->plans[p].scalar)
+        last = std::max(last, L->pay_off[p] + (size_t)count * (size_t)((L->plans[p].max_payload + 15) / 16 * 16));
+    bytes = last;
+  }
+  if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
+  CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
+  CK(cudaEventRecord(S.h2d_done, L->copy_st));
+  CK(cudaStreamWaitEvent(L->comp_st, S.h2d_done, 0));
+  bool wait_release;
+  {
+    std::lock_guard<std::mutex> g(L->mu);
+    wait_release = S.released_pending;
+    S.released_pending = false;
+  }
+  if (wait_release) CK(cudaStreamWaitEvent(L->comp_st, S.release, 0));
+  int launches = 0;
+  const bool prof = L->profiling;
+  int64_t kbytes = 0, klaunch = 0;
+  if (prof) CK(cudaEventRecord(S.k0, L->comp_st));
+  int64_t d2h = 0;
+  bool any_rle = false;
+  ScalarArgs SA{};
+  SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
+  SA.count = count;
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    Plan& pl = L->plans[p];
+    if (pl.scalar) {
+      SA.cols[SA.n_fields] = pl.d_col;
+      SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
+      ++SA.n_fields;
+      if (SA.n_fields == 16) { if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed"); ++launches; SA.n_fields = 0; }
+      continue;
+    }
+    LaunchArgs A{};
+    A.desc = S.d_stage + L->desc_off[p];
+    A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_off[p]);
+    A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
+    A.out = pl.outs[s];
+    A.lut = pl.d_lut;
+    A.status = S.d_status + (size_t)p * L->batch;
+    A.count = count;
+    if (count == 0) continue;
+    if (S.plan_has_rle[p]) {
+      if (launch_rle_expand(pl.dev, A, L->comp_st)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      ++launches; any_rle = true;
+    }
+    int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, L->comp_st) : launch_image(pl.dev, A, L->comp_st);
+    if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
+      ++klaunch;
+      const uint8_t* dblk = H + L->desc_off[p];
+      for (int pos = 0; pos < count; ++pos) {
+        const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
+        if (d->skip) continue;
+        const int32_t* prm = reinterpret_cast<const int32_t*>(dblk + (size_t)pos * pl.dev.desc_stride + kDescHeader);
+        int64_t rd;
+        if (pl.dev.src_kind == SRC_RESAMPLE) rd = (int64_t)prm[2] * prm[3] * pl.dev.channels;
+        else if (pl.dev.src_kind == SRC_ARRAY) rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems * pl.dev.src_elem);
+        else rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems);
+        kbytes += rd + pl.out_sample_bytes;
+      }
+    }
+    if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    ++launches;
+  }
+  if (prof) CK(cudaEventRecord(S.k1, L->comp_st));
+  S.timed = prof;
+  S.timed_launches = klaunch;
+  S.timed_bytes = kbytes;
+  if (SA.n_fields && count) {
+    if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
+    ++launches;
+  }
+  if (any_rle) {
+    size_t nb = sizeof(SampleStatus) * L->batch * L->plans.size();
+    CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, L->comp_st));
+    d2h += (int64_t)nb;
+  }
+  CK(cudaEventRecord(S.done, L->comp_st));
+  S.used = true;
+  {
+    std::lock_guard<std::mutex> g(L->stats_mu);
+    L->stats.batches += 1;
+    L->stats.samples += count;
+    L->stats.h2d_bytes += (int64_t)bytes;
+    L->stats.d2h_bytes += d2h;
+    L->stats.kernel_launches += launches;
+    L->stats.stage_seconds += t1 - t0;
+  }
+  return BBX_OK;
+}
+
+static void pipeline_loop(bbx_loader* L) {
+  cudaSetDevice(L->device);
+  for (;;) {
+    int s;
+    {
+      std::unique_lock<std::mutex> lk(L->mu);
+      L->cv.wait(lk, [&] { return L->stop || !L->queue.empty(); });
+      if (L->queue.empty()) return;
+      s = L->queue.front();
+      L->queue.pop_front();
+    }
+    int rc = process_slot(L, s);
+    {
+      std::lock_guard<std::mutex> g(L->mu);
+      Slot& S = L->slots[s];
+      S.fatal = rc;
+      if (rc) S.fatal_msg = last_error();
+      S.state = 2;
+    }
+    L->done_cv.notify_all();
+  }
+}
+
+}  // namespace bbx
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* bbx_last_error(void) { return bbx::last_error(); }
+const char* bbx_version(void) { return "bbx-b200 0.1.0 (sm_100a)"; }
+
+bbx_status bbx_dataset_open(const char* path, bbx_dataset** out) {
+  if (!path || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  return (bbx_status)bbx::dataset_open(path, out);
+}
+void bbx_dataset_close(bbx_dataset* ds) { bbx::dataset_close(ds); }
+
+bbx_status bbx_dataset_header(const bbx_dataset* ds, bbx_header_info* o) {
+  if (!ds || !o) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  o->num_samples = ds->num_samples; o->page_size = ds->page_size; o->data_table_offset = ds->data_table_offset;
+  o->heap_offset = ds->heap_offset; o->alloc_table_offset = ds->alloc_table_offset;
+  o->num_fields = (int32_t)ds->fields.size(); o->row_width = ds->row_width;
+  return BBX_OK;
+}
+bbx_status bbx_dataset_field(const bbx_dataset* ds, int index, bbx_field_info* o) {
+  if (!ds || !o || index < 0 || index >= (int)ds->fields.size())
+    return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad field index");
+  *o = ds->fields[index].info;
+  return BBX_OK;
+}
+bbx_status bbx_dataset_row(const bbx_dataset* ds, int64_t i, uint8_t* out, int32_t out_len) {
+  if (!ds || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (i < 0 || i >= ds->num_samples)
+    return (bbx_status)fail(BBX_INDEX_OUT_OF_RANGE, "sample %lld out of range [0, %lld)", (long long)i,
+                            (long long)ds->num_samples);
+  if (out_len < ds->row_width) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "row buffer too short");
+  std::memcpy(out, ds->rows + i * ds->row_width, ds->row_width);
+  return BBX_OK;
+}
+bbx_status bbx_dataset_make_resident(bbx_dataset* ds, int device) {
+  if (!ds) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null dataset");
+  return (bbx_status)bbx::dataset_make_resident(ds, device);
+}
+bbx_status bbx_dataset_page_map(const bbx_dataset* ds, int64_t* out) {
+  if (!ds || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  for (int64_t i = 0; i < ds->num_samples; ++i) out[i] = bbx::primary_page(ds, i);
+  return BBX_OK;
+}
+
+bbx_status bbx_epoch_order(int kind, uint64_t seed, uint64_t epoch, int64_t n, const int64_t* page_map,
+                           int64_t batch_size, int64_t* out) {
+  if (n > 0 && !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null output");
+  return (bbx_status)bbx::epoch_order(kind, seed, epoch, n, page_map, batch_size, out);
+}
+
+bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, int32_t slot_count,
+                             int32_t staging_threads, bbx_loader** out) {
+  if (!ds || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (batch_size < 1) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "batch_size must be >= 1");
+  if (slot_count < 1) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "slot_count must be >= 1");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  auto L = std::make_unique<bbx_loader>();
+  L->ds = ds; L->device = device; L->batch = batch_size; L->nslots = slot_count;
+  L->slots.resize(slot_count);
+  int nt = staging_threads;
+  if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  L->pool = std::make_unique<Pool>(nt);
+  if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&L->comp_st, cudaStreamNonBlocking)) != cudaSuccess)
+    return (bbx_status)fail(BBX_CUDA_ERROR, "stream create: %s", cudaGetErrorString(e));
+  *out = L.release();
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_add_field(bbx_loader* L, int32_t field_index, const bbx_op* ops, int32_t n_ops,
+                                int32_t* plan_id, int64_t out_shape[4], int32_t* out_ndim, int32_t* out_dtype) {
+  if (!L || !ops) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
+  cudaSetDevice(L->device);
+  Plan pl;
+  int rc = plan_compile(L, field_index, ops, n_ops, pl);
+  if (rc) return (bbx_status)rc;
+  pl.outs.assign(L->nslots, nullptr);
+  const Field& f = L->ds->fields[field_index];
+  if (pl.dev.src_kind == SRC_ARRAY && !pl.dev.has_remaps_3d) {
+    *out_ndim = f.info.ndims;
+    for (int k = 0; k < 4; ++k) out_shape[k] = k < f.info.ndims ? f.info.dims[k] : 0;
+  } else {
+    *out_ndim = 3;
+    out_shape[0] = pl.dev.out_h; out_shape[1] = pl.dev.out_w; out_shape[2] = pl.dev.out_c; out_shape[3] = 0;
+  }
+  *out_dtype = pl.dev.out_dtype;
+  *plan_id = (int32_t)L->plans.size();
+  L->plans.push_back(std::move(pl));
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_add_scalar(bbx_loader* L, int32_t field_index, int32_t* plan_id) {
+  if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
+  const bbx_dataset* ds = L->ds;
+  if (field_index < 0 || field_index >= (int)ds->fields.size() || ds->fields[field_index].info.kind > 1)
+    return (bbx_status)fail(BBX_SCHEMA_MISMATCH, "field %d is not a scalar field", field_index);
+  cudaSetDevice(L->device);
+  Plan pl;
+  pl.field_index = field_index;
+  pl.scalar = true;
+  pl.outs.assign(L->nslots, nullptr);
+  // column upload once (Dataset.column, reader.py:391-406)
+  std::vector<uint64_t> col((size_t)std::max<int64_t>(ds->num_samples, 1));
+  for (int64_t i = 0; i < ds->num_samples; ++i) col[i] = bbx::u64_cell(ds, i, ds->fields[field_index]);
+  cudaError_t e = cudaMalloc(&pl.d_col, col.size() * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(pl.d_col, col.data(), col.size() * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "scalar column upload: %s", cudaGetErrorString(e));
+  *plan_id = (int32_t)L->plans.size();
+  L->plans.push_back(std::move(pl));
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_bind(bbx_loader* L, int32_t plan_id, int32_t slot, void* out_dev) {
+  if (!L || plan_id < 0 || plan_id >= (int)L->plans.size() || slot < 0 || slot >= L->nslots)
+    return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad plan or slot");
+  L->plans[plan_id].outs[slot] = out_dev;
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_submit(bbx_loader* L, int32_t slot, const int64_t* idx, int32_t count, uint64_t seed,
+                             uint64_t epoch) {
+  if (!L || slot < 0 || slot >= L->nslots) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad slot");
+  if (count < 0 || count > L->batch) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "count %d outside [0, %d]", count, L->batch);
+  for (auto& pl : L->plans)
+    if (!pl.outs[slot]) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "slot %d has unbound outputs", slot);
+  int rc = bbx::finalize(L);
+  if (rc) return (bbx_status)rc;
+  std::lock_guard<std::mutex> g(L->mu);
+  if (L->stop) return (bbx_status)fail(BBX_SHUTDOWN, "loader shut down");
+  Slot& S = L->slots[slot];
+  if (S.state == 1) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "slot %d already has a batch in flight", slot);
+  S.idx.assign(idx, idx + count);
+  S.count = count; S.seed = seed; S.epoch = epoch;
+  S.state = 1; S.fatal = 0;
+  L->queue.push_back(slot);
+  L->cv.notify_one();
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
+  if (!L || slot < 0 || slot >= L->nslots) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad slot");
+  if (bad_pos) *bad_pos = -1;
+  auto t0 = std::chrono::steady_clock::now();
+  Slot& S = L->slots[slot];
+  {
+    std::unique_lock<std::mutex> lk(L->mu);
+    if (S.state == 0) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "slot %d has no batch", slot);
+    L->done_cv.wait(lk, [&] { return S.state == 2; });
+  }
+  cudaSetDevice(L->device);
+  if (S.fatal) return (bbx_status)fail(S.fatal, "%s", S.fatal_msg.c_str());
+  cudaError_t e = cudaEventSynchronize(S.done);
+  {
+    std::lock_guard<std::mutex> g(L->stats_mu);
+    L->stats.wait_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (e == cudaSuccess && S.timed) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, S.k0, S.k1) == cudaSuccess) {
+        L->stats.kernel_seconds += ms * 1e-3;
+        L->stats.kernel_timed += S.timed_launches;
+        L->stats.kernel_bytes += S.timed_bytes;
+      }
+      S.timed = false;
+    }
+  }
+  if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "batch failed on device: %s", cudaGetErrorString(e));
+  // merge host-detected and device-detected per-sample failures: lowest position wins
+  HostErr best = S.herr;
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    if (!S.plan_has_rle[p]) continue;
+    const Plan& pl = L->plans[p];
+    const uint8_t* dblk = S.h_stage + L->desc_off[p];
+    for (int pos = 0; pos < S.count; ++pos) {
+      if (best.pos >= 0 && (pos > best.pos || (pos == best.pos && (int)p >= best.plan))) break;
+      const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
+      if (d->skip || d->codec != CODEC_RLE) continue;
+      const SampleStatus& st = S.h_status[p * L->batch + pos];
+      if (st.kind == 0) continue;
+      char buf[256];
+      int64_t n = (int64_t)d->h * d->w * d->c;
+      if (st.kind == 1) std::snprintf(buf, sizeof buf, "rle runs sum past %lld bytes", (long long)n);
+      else std::snprintf(buf, sizeof buf, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);
+      best.pos = pos; best.plan = (int)p; best.code = BBX_CORRUPT_PAYLOAD; best.msg = buf;
+      break;
+    }
+  }
+  if (best.pos >= 0) {
+    if (bad_pos) *bad_pos = best.pos;
+    return (bbx_status)fail(best.code, "%s", best.msg.c_str());
+  }
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_stream_wait(bbx_loader* L, int32_t slot, void* stream) {
+  if (!L || slot < 0 || slot >= L->nslots) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad slot");
+  cudaSetDevice(L->device);
+  cudaError_t e = cudaStreamWaitEvent((cudaStream_t)stream, L->slots[slot].done, 0);
+  if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "stream wait: %s", cudaGetErrorString(e));
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_release(bbx_loader* L, int32_t slot, void* stream) {
+  if (!L || slot < 0 || slot >= L->nslots) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad slot");
+  if (!L->finalized) return BBX_OK;
+  cudaSetDevice(L->device);
+  std::lock_guard<std::mutex> g(L->mu);
+  Slot& S = L->slots[slot];
+  cudaError_t e = cudaEventRecord(S.release, (cudaStream_t)stream);
+  if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "release record: %s", cudaGetErrorString(e));
+  S.released_pending = true;
+  if (S.state == 2) S.state = 0;
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_drain(bbx_loader* L) {
+  if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
+  if (!L->finalized) return BBX_OK;
+  {
+    std::unique_lock<std::mutex> lk(L->mu);
+    L->done_cv.wait(lk, [&] {
+      if (!L->queue.empty()) return false;
+      for (auto& S : L->slots) if (S.state == 1) return false;
+      return true;
+    });
+    for (auto& S : L->slots) if (S.state == 2) S.state = 0;
+  }
+  cudaSetDevice(L->device);
+  cudaError_t e1 = cudaStreamSynchronize(L->comp_st), e2 = cudaStreamSynchronize(L->copy_st);
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    return (bbx_status)fail(BBX_CUDA_ERROR, "drain: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  return BBX_OK;
+}
+
+void bbx_loader_destroy(bbx_loader* L) {
+  if (!L) return;
+  if (L->finalized) {
+    bbx_loader_drain(L);
+    { std::lock_guard<std::mutex> g(L->mu); L->stop = true; }
+    L->cv.notify_all();
+    if (L->th.joinable()) L->th.join();
+  }
+  cudaSetDevice(L->device);
+  for (auto& S : L->slots) {
+    if (S.h_stage) cudaFreeHost(S.h_stage);
+    if (S.d_stage) cudaFree(S.d_stage);
+    if (S.d_status) cudaFree(S.d_status);
+    if (S.h_status) cudaFreeHost(S.h_status);
+    if (S.h2d_done) cudaEventDestroy(S.h2d_done);
+    if (S.done) cudaEventDestroy(S.done);
+    if (S.release) cudaEventDestroy(S.release);
+    if (S.k0) cudaEventDestroy(S.k0);
+    if (S.k1) cudaEventDestroy(S.k1);
+  }
+  for (auto& pl : L->plans) {
+    if (pl.d_lut) cudaFree(pl.d_lut);
+    if (pl.d_col) cudaFree(pl.d_col);
+    for (auto* p : pl.d_scratch) if (p) cudaFree(p);
+  }
+  if (L->copy_st) cudaStreamDestroy(L->copy_st);
+  if (L->comp_st) cudaStreamDestroy(L->comp_st);
+  delete L;
+}
+
+bbx_status bbx_loader_get_stats(const bbx_loader* L, bbx_loader_stats* out) {
+  if (!L || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> g(const_cast<bbx_loader*>(L)->stats_mu);
+  *out = L->stats;
+  return BBX_OK;
+}
+bbx_status bbx_loader_reset_stats(bbx_loader* L) {
+  if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
+  std::lock_guard<std::mutex> g(L->stats_mu);
+  L->stats = bbx_loader_stats{};
+  return BBX_OK;
+}
+bbx_status bbx_loader_set_profiling(bbx_loader* L, int enabled) {
+  if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
+  std::lock_guard<std::mutex> g(L->mu);
+  L->profiling = enabled != 0;
+  return BBX_OK;
+}
+void* bbx_loader_compute_stream(bbx_loader* L) { return L ? (void*)L->comp_st : nullptr; }
+
+static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host, int64_t len,
+                             uint8_t* out_dev, int device) {
+  // codecs.decode_image on device: a one-sample Decode plan with max dims (h, w).
+  if (h < 1 || w < 1 || c < 1) return fail(BBX_SCHEMA_MISMATCH, "image dims must all be >= 1");
+  int64_t n = (int64_t)h * w * c;
+  if (codec == CODEC_RAW && len != n)
+    return fail(BBX_CORRUPT_PAYLOAD, "raw payload is %lld bytes, expected %lld", (long long)len, (long long)n);
+  if (codec == CODEC_RLE && len % 5) return fail(BBX_CORRUPT_PAYLOAD, "rle payload length is not a multiple of 5");
+  if (codec == CODEC_SUB2) {
+    int64_t m = (int64_t)((h + 1) / 2) * ((w + 1) / 2) * c;
+    if (len != m) return fail(BBX_CORRUPT_PAYLOAD, "subsampled payload is %lld bytes, expected %lld", (long long)len, (long long)m);
+  }
+  if (codec < 0 || codec > 2) return fail(BBX_CORRUPT_PAYLOAD, "unknown codec %d", codec);
+  CK(cudaSetDevice(device));
+  PlanDev P{};
+  P.src_kind = SRC_DECODE; P.canvas_h = h; P.canvas_w = w; P.channels = c; P.src_row_w = w;
+  P.src_elem = 1; P.src_dtype = BBX_U8; P.out_h = h; P.out_w = w; P.out_c = c; P.out_dtype = BBX_U8;
+  P.value_mode = VAL_COPY; P.desc_stride = kDescHeader + 8; P.rows_per_tile = std::min(16, h);
+  for (;;) {
+    P.smem_bytes = image_smem_bytes(P);
+    if (P.smem_bytes <= kSmemBudget || P.rows_per_tile == 1) break;
+    P.rows_per_tile /= 2;
+  }
+  if (P.smem_bytes > kSmemBudget || (int64_t)w * c + 64 > 65535) return fail(BBX_SPEC_MISMATCH, "image too wide");
+  P.tiles_per_sample = (h + P.rows_per_tile - 1) / P.rows_per_tile;
+  P.scratch_bytes = (n + 15) / 16 * 16;
+  P.out_sample_elems = n;
+  size_t dbytes = 64 + (size_t)((len + 15) / 16 * 16) + 64;
+  uint8_t* d_buf = nullptr;
+  uint8_t* d_scr = nullptr;
+  SampleStatus* d_st = nullptr;
+  CK(cudaMalloc(&d_buf, dbytes));
+  std::vector<uint8_t> hb(64, 0);
+  SampleDesc* d = reinterpret_cast<SampleDesc*>(hb.data());
+  d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = (uint8_t)codec;
+  cudaMemcpy(d_buf, hb.data(), 64, cudaMemcpyHostToDevice);
+  if (len) cudaMemcpy(d_buf + 64, payload_host, (size_t)len, cudaMemcpyHostToDevice);
+  cudaMalloc(&d_st, sizeof(SampleStatus));
+  cudaMemset(d_st, 0, sizeof(SampleStatus));
+  LaunchArgs A{};
+  A.desc = d_buf; A.payload = d_buf + 64; A.out = out_dev; A.status = d_st; A.count = 1;
+  int rc = 0;
+  if (codec == CODEC_RLE) {
+    cudaMalloc(&d_scr, P.scratch_bytes + 64);
+    A.scratch = d_scr;
+    rc |= launch_rle_expand(P, A, nullptr);
+  }
+  rc |= launch_image(P, A, nullptr);
+  SampleStatus st{};
+  cudaError_t e = cudaMemcpy(&st, d_st, sizeof st, cudaMemcpyDeviceToHost);
+  cudaFree(d_buf); cudaFree(d_st); if (d_scr) cudaFree(d_scr);
+  if (rc || e != cudaSuccess) return fail(BBX_CUDA_ERROR, "decode failed: %s", cudaGetErrorString(e));
+  if (st.kind == 1) return fail(BBX_CORRUPT_PAYLOAD, "rle runs sum past %lld bytes", (long long)n);
+  if (st.kind == 2) return fail(BBX_CORRUPT_PAYLOAD, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);
+  return BBX_OK;
+}
+
+bbx_status bbx_decode_image(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host, int64_t len,
+                            uint8_t* out_dev, int device) {
+  return (bbx_status)decode_image_impl(h, w, c, codec, payload_host, len, out_dev, device);
+}
+
+}  // extern "C"

@@ -1,0 +1,477 @@
+"""Epoch orchestration on the GPU: order -> device pipeline -> batch leases.
+
+Drop-in for loader.py:37-453 of the reference: same `LoaderConfig`,
+`Loader(dataset_or_path, config)`, `iterate_epoch`, `Batch` lease semantics
+(valid until the next batch is requested), `EpochStats`, error reporting
+("sample {index} failed: {err}" with the reference's exception type).
+
+What replaces the reference's N worker threads x per-sample Python
+(_EpochRun._process_position, loader.py:330-347) is one libbbx loader per
+Loader: each batch is a single `bbx_loader_submit` (indices in, everything
+else on the device), slot_count ring slots of device output tensors, and a
+prefetch depth of slot_count - 1 batches.  Batch arrays are CUDA tensors,
+channels-last (NHWC), exactly the reference's numpy shapes and dtypes.
+
+Extensions: `distributed=True` shards every global batch of
+world_size * batch_size positions by rank; `device`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from . import pipeline as pl
+from .errors import CapacityTooSmall, SchemaMismatch, ShutdownError, SpecMismatch
+from .format import FieldKind
+from .reader import Dataset, DeviceResident, ProcessCacheStrategy, open_dataset
+from .traversal import OrderKind, TraversalOrder
+
+DEFAULT_SLOT_COUNT = 3
+
+
+@dataclass
+class LoaderConfig:
+    batch_size: int
+    num_workers: int = 1
+    slot_count: int = DEFAULT_SLOT_COUNT
+    order: OrderKind = OrderKind.RANDOM
+    seed: int = 0
+    drop_last: bool = False
+    pipelines: dict | None = None
+    fields: list | None = None
+    # ---- extensions (no reference counterpart)
+    device: int | None = None          # CUDA ordinal; default LOCAL_RANK / current device
+    distributed: bool = False          # shard each global batch by rank (FFCV distributed=True)
+    rank: int | None = None
+    world_size: int | None = None
+    staging_threads: int = 0           # host gather threads (0 = automatic)
+
+    def check(self) -> None:
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.num_workers < 1:
+            raise ValueError("num_workers must be >= 1")
+        if self.slot_count < 2:
+            raise ValueError("slot_count must be >= 2")
+
+
+@dataclass
+class EpochStats:
+    batches: int = 0
+    samples: int = 0
+    page_fetches: int = 0
+    page_reloads: int = 0
+    producer_blocked_s: float = 0.0
+    consumer_blocked_s: float = 0.0
+
+
+class Batch:
+    """A lease on one ring slot's device tensors; valid until the next batch."""
+
+    __slots__ = ("arrays", "indices", "index")
+
+    def __init__(self, arrays: dict, indices, index: int):
+        self.arrays = arrays
+        self.indices = indices
+        self.index = index
+
+    def __getitem__(self, name: str):
+        return self.arrays[name]
+
+    def __contains__(self, name) -> bool:
+        return name in self.arrays
+
+    @property
+    def size(self) -> int:
+        return len(self.indices)
+
+    def keys(self):
+        return self.arrays.keys()
+
+
+class MemoryLedger:
+    def __init__(self):
+        self.entries: dict = {}
+
+    def register(self, name: str, nbytes: int) -> None:
+        self.entries[name] = nbytes
+
+    @property
+    def total(self) -> int:
+        return sum(self.entries.values())
+
+
+_TORCH_DT = None
+
+
+def _torch_dtype(code: int):
+    global _TORCH_DT
+    import torch
+
+    if _TORCH_DT is None:
+        _TORCH_DT = {_lib.DT_U8: torch.uint8, _lib.DT_I64: torch.int64, _lib.DT_F32: torch.float32,
+                     _lib.DT_F64: torch.float64, _lib.DT_F16: torch.float16, _lib.DT_BF16: torch.bfloat16}
+    return _TORCH_DT[code]
+
+
+def _dist_info(config: LoaderConfig) -> tuple[int, int]:
+    if not config.distributed:
+        return 0, 1
+    rank, world = config.rank, config.world_size
+    if rank is None or world is None:
+        try:
+            import torch.distributed as dist
+
+            if dist.is_available() and dist.is_initialized():
+                rank = dist.get_rank() if rank is None else rank
+                world = dist.get_world_size() if world is None else world
+        except Exception:
+            pass
+    rank = int(os.environ.get("RANK", 0)) if rank is None else rank
+    world = int(os.environ.get("WORLD_SIZE", 1)) if world is None else world
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of {world}")
+    return rank, world
+
+
+def shard_batches(global_batches: list, rank: int, world_size: int, batch_size: int) -> list:
+    """Rank r's slice [r*B, (r+1)*B) of every global batch."""
+    out = []
+    for gb in global_batches:
+        part = gb[rank * batch_size:(rank + 1) * batch_size]
+        if part:
+            out.append(part)
+    return out
+
+
+class _Field:
+    __slots__ = ("name", "plan_id", "outs", "nchw", "scalar")
+
+    def __init__(self, name, plan_id, outs, nchw, scalar):
+        self.name, self.plan_id, self.outs, self.nchw, self.scalar = name, plan_id, outs, nchw, scalar
+
+
+class Loader:
+    """Batch loader over an open dataset (or a path, which it then owns)."""
+
+    def __init__(self, dataset, config: LoaderConfig):
+        import torch
+
+        config.check()
+        self._owns_dataset = isinstance(dataset, (str, bytes)) or hasattr(dataset, "__fspath__")
+        self.dataset: Dataset = open_dataset(dataset) if self._owns_dataset else dataset
+        self.config = config
+        self.order = TraversalOrder(config.order, config.seed)
+        self.ledger = MemoryLedger()
+        self.last_stats: EpochStats | None = None
+        self._auto_epoch = 0
+        self._shutdown = False
+        self._epoch_lock = threading.Lock()
+        self._active = None
+        self._handle = None
+        self.rank, self.world_size = _dist_info(config)
+        if config.device is not None:
+            self.device = int(config.device)
+        elif config.distributed and "LOCAL_RANK" in os.environ:
+            self.device = int(os.environ["LOCAL_RANK"])
+        else:
+            self.device = torch.cuda.current_device()
+
+        schema = self.dataset.schema
+        wanted = config.fields
+        self.batch_fields = []
+        for f in schema:
+            if wanted is not None and f.name not in wanted:
+                continue
+            if f.kind == FieldKind.VAR_BYTES:
+                if wanted is not None:
+                    raise SchemaMismatch(f"field {f.name!r}: VAR_BYTES fields cannot be batched")
+                continue
+            self.batch_fields.append(f)
+        if not self.batch_fields:
+            raise SchemaMismatch("no batchable fields selected")
+
+        strategy = self.dataset.strategy
+        if isinstance(strategy, DeviceResident) or (
+                isinstance(strategy, ProcessCacheStrategy) and strategy.capacity_pages >= self.dataset.num_pages):
+            dev = strategy.device if isinstance(strategy, DeviceResident) and strategy.device is not None \
+                else self.device
+            self.dataset.make_resident(dev)
+
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.bbx_loader_create(self.dataset.handle, self.device, config.batch_size, config.slot_count,
+                                       config.staging_threads, ctypes.byref(h)))
+        self._handle = h
+        field_index = {f.name: i for i, f in enumerate(schema)}
+        self._field_index = field_index
+        pipelines = dict(config.pipelines or {})
+        self._fields: list[_Field] = []
+        self.scalar_fields = []
+        B, S = config.batch_size, config.slot_count
+        dev = torch.device("cuda", self.device)
+        try:
+            for f in self.batch_fields:
+                fi = field_index[f.name]
+                if f.kind in (FieldKind.INT_SCALAR, FieldKind.FLOAT_SCALAR):
+                    if f.name in pipelines:
+                        raise SchemaMismatch(f"scalar field {f.name!r} cannot take a pipeline")
+                    pid = ctypes.c_int32()
+                    _lib.check(L.bbx_loader_add_scalar(h, fi, ctypes.byref(pid)))
+                    dt = torch.int64 if f.kind == FieldKind.INT_SCALAR else torch.float64
+                    outs = torch.empty((S, B), dtype=dt, device=dev)
+                    self.scalar_fields.append(f)
+                    self._fields.append(_Field(f.name, pid.value, outs, False, True))
+                    self.ledger.register(f"scalars:{f.name}", outs.numel() * outs.element_size())
+                    continue
+                chain = pipelines.pop(f.name, None) or pl.default_chain_for_field(f)
+                if not isinstance(chain[0], pl.SourceTransform):
+                    chain = pl.default_chain_for_field(f)[:1] + list(chain)
+                comp = pl.compile_chain(chain, pl.input_spec_for_field(f))
+                ops = (_lib.BbxOp * len(comp.ops))(*comp.ops)
+                pid, nd, odt = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+                shape = (ctypes.c_int64 * 4)()
+                _lib.check(L.bbx_loader_add_field(h, fi, ops, len(comp.ops), ctypes.byref(pid), shape,
+                                                  ctypes.byref(nd), ctypes.byref(odt)))
+                oshape = tuple(int(shape[k]) for k in range(nd.value))
+                want_shape = tuple(comp.specs[-1][0])
+                if oshape != want_shape:
+                    raise SpecMismatch(f"device plan shape {oshape} != spec {want_shape}")
+                outs = torch.empty((S, B, *oshape), dtype=_torch_dtype(odt.value), device=dev)
+                self._fields.append(_Field(f.name, pid.value, outs, comp.nchw_view, False))
+                self.ledger.register(f"arena:{f.name}", outs.numel() * outs.element_size())
+            if pipelines:
+                raise SchemaMismatch(f"pipelines for unknown fields: {sorted(pipelines)}")
+            for fd in self._fields:
+                for s in range(S):
+                    _lib.check(L.bbx_loader_bind(h, fd.plan_id, s, fd.outs[s].data_ptr()))
+        except BaseException:
+            L.bbx_loader_destroy(h)
+            self._handle = None
+            if self._owns_dataset:
+                self.dataset.close()
+            raise
+        self.ledger.register("dataset_buffers", self.dataset.tracked_bytes)
+
+    # -- public surface ---------------------------------------------------
+    @property
+    def tracked_buffer_bytes(self) -> int:
+        return self.ledger.total
+
+    @property
+    def handle(self):
+        return self._handle
+
+    def batches_per_epoch(self) -> int:
+        n = self.dataset.num_samples
+        gb = self.config.batch_size * self.world_size
+        full = n // gb if self.config.drop_last else -(-n // gb)
+        if self.world_size == 1 or self.config.drop_last:
+            return full
+        tail = n - (n // gb) * gb
+        return n // gb + (1 if tail > self.rank * self.config.batch_size else 0)
+
+    def epoch_batches(self, epoch: int) -> list:
+        """This rank's index lists for `epoch` (the reference order, then sharded)."""
+        cfg = self.config
+        page_map = self.dataset.page_map() if OrderKind(cfg.order) == OrderKind.QUASI_RANDOM else None
+        gbs = cfg.batch_size * self.world_size
+        batches = self.order.epoch_batches(epoch, self.dataset.num_samples, gbs, page_map, cfg.drop_last)
+        if self.world_size > 1:
+            batches = shard_batches(batches, self.rank, self.world_size, cfg.batch_size)
+        return batches
+
+    def iterate_epoch(self, epoch: int = 0):
+        if self._shutdown:
+            raise ShutdownError("loader is shut down")
+        run = _EpochRun(self, epoch)
+        with self._epoch_lock:
+            self._active = run
+        try:
+            yield from run.batches()
+        finally:
+            run.stop()
+            self.last_stats = run.stats
+            with self._epoch_lock:
+                self._active = None
+
+    def iterate_steps(self, steps: int, start_epoch: int = 0):
+        """`steps` batches as one continuous stream over epochs start_epoch,
+        start_epoch+1, ... (each batch identical to the same batch of
+        iterate_epoch); the prefetch pipeline is not drained at epoch ends."""
+        if self._shutdown:
+            raise ShutdownError("loader is shut down")
+        run = _EpochRun(self, start_epoch, steps)
+        with self._epoch_lock:
+            self._active = run
+        try:
+            yield from run.batches()
+        finally:
+            run.stop()
+            self.last_stats = run.stats
+            with self._epoch_lock:
+                self._active = None
+
+    def set_profiling(self, enabled: bool = True) -> None:
+        """CUDA-event timing of the transform kernels (stats()['kernel_seconds'])."""
+        _lib.check(_lib.lib().bbx_loader_set_profiling(self._handle, int(enabled)))
+
+    def reset_stats(self) -> None:
+        _lib.check(_lib.lib().bbx_loader_reset_stats(self._handle))
+
+    def __iter__(self):
+        epoch = self._auto_epoch
+        self._auto_epoch += 1
+        return self.iterate_epoch(epoch)
+
+    def __len__(self) -> int:
+        return self.batches_per_epoch()
+
+    def stats(self) -> dict:
+        st = _lib.LoaderStats()
+        _lib.check(_lib.lib().bbx_loader_get_stats(self._handle, ctypes.byref(st)))
+        return {k: getattr(st, k) for k, _ in st._fields_}
+
+    def shutdown(self) -> None:
+        if self._shutdown:
+            return
+        self._shutdown = True
+        with self._epoch_lock:
+            run = self._active
+        if run is not None:
+            run.stop()
+        if self._handle is not None:
+            _lib.lib().bbx_loader_destroy(self._handle)
+            self._handle = None
+        if self._owns_dataset:
+            self.dataset.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.shutdown()
+
+    def __del__(self):
+        try:
+            self.shutdown()
+        except Exception:
+            pass
+
+
+class _EpochRun:
+    """One epoch: submit ahead by slot_count - 1 batches, lease one at a time."""
+
+    def __init__(self, loader: Loader, epoch: int, steps: int | None = None):
+        self.loader = loader
+        self.epoch = epoch
+        self.stats = EpochStats()
+        if steps is None:
+            self.batch_lists = loader.epoch_batches(epoch)
+            self.batch_epochs = [epoch] * len(self.batch_lists)
+        else:
+            # a continuous stream across epoch boundaries (no pipeline drain between epochs)
+            self.batch_lists, self.batch_epochs = [], []
+            e = epoch
+            while len(self.batch_lists) < steps:
+                bl = loader.epoch_batches(e)
+                if not bl:
+                    break
+                take = bl[:steps - len(self.batch_lists)]
+                self.batch_lists += take
+                self.batch_epochs += [e] * len(take)
+                e += 1
+        self._inflight: set = set()
+        self._stopped = False
+        strategy = loader.dataset.strategy
+        if isinstance(strategy, ProcessCacheStrategy):
+            self._check_capacity(strategy.capacity_pages)
+
+    def _check_capacity(self, capacity: int) -> None:
+        ds = self.loader.dataset
+        for batch in self.batch_lists:
+            pages: set = set()
+            for i in batch:
+                pages.update(ds.sample_pages(i))
+            if len(pages) > capacity:
+                raise CapacityTooSmall(f"batch touches {len(pages)} pages, cache holds {capacity}")
+
+    def _submit(self, g: int) -> None:
+        ld = self.loader
+        slot = g % ld.config.slot_count
+        idx = np.ascontiguousarray(self.batch_lists[g], dtype=np.int64)
+        _lib.check(_lib.lib().bbx_loader_submit(ld.handle, slot, idx.ctypes.data if len(idx) else None, len(idx),
+                                                ld.config.seed & 0xFFFFFFFFFFFFFFFF,
+                                                self.batch_epochs[g] & 0xFFFFFFFFFFFFFFFF))
+        self._inflight.add(slot)
+
+    def batches(self):
+        import torch
+
+        ld = self.loader
+        L = _lib.lib()
+        S = ld.config.slot_count
+        nb = len(self.batch_lists)
+        if nb == 0:
+            return
+        stream = torch.cuda.current_stream(ld.device)
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        for g in range(min(S - 1, nb)):
+            self._submit(g)
+        for g in range(nb):
+            if self._stopped:
+                raise ShutdownError("epoch stopped")
+            if g + S - 1 < nb:
+                if g >= 1:
+                    L.bbx_loader_release(ld.handle, (g - 1) % S, sp)
+                self._submit(g + S - 1)
+            slot = g % S
+            bad = ctypes.c_int64(-1)
+            t0 = time.perf_counter()
+            rc = L.bbx_loader_wait(ld.handle, slot, ctypes.byref(bad))
+            self.stats.consumer_blocked_s += time.perf_counter() - t0
+            self._inflight.discard(slot)
+            indices = self.batch_lists[g]
+            if rc != 0:
+                exc = _lib.STATUS_EXC.get(rc, Exception)
+                msg = _lib.last_error()
+                if bad.value >= 0:
+                    raise exc(f"sample {indices[bad.value]} failed: {msg}")
+                raise exc(msg)
+            _lib.check(L.bbx_loader_stream_wait(ld.handle, slot, sp))
+            count = len(indices)
+            arrays = {}
+            for fd in ld._fields:
+                t = fd.outs[slot][:count]
+                if fd.nchw:
+                    t = t.permute(0, 3, 1, 2)
+                arrays[fd.name] = t
+            self.stats.batches += 1
+            self.stats.samples += count
+            yield Batch(arrays, indices, g)
+
+    def stop(self) -> None:
+        if self._stopped:
+            return
+        self._stopped = True
+        ld = self.loader
+        if ld.handle is not None:
+            L = _lib.lib()
+            L.bbx_loader_drain(ld.handle)   # in-flight batches finish; the ring is reusable
+            import torch
+
+            sp = ctypes.c_void_p(torch.cuda.current_stream(ld.device).cuda_stream)
+            for s in range(ld.config.slot_count):
+                L.bbx_loader_release(ld.handle, s, sp)
+
+
+def iterate_epoch(dataset, config: LoaderConfig, epoch: int = 0):
+    loader = Loader(dataset, config)
+    return loader.iterate_epoch(epoch), loader
