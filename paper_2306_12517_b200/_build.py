@@ -22,8 +22,8 @@ GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXX = os.environ.get("CXX", "g++")
 
 HOST_SOURCES = ["engine.cpp", "format.cpp", "orders.cpp"]
-CUDA_SOURCES = ["kernels.cu"]
-HEADERS = ["bbx_internal.h", "engine.h"]
+CUDA_SOURCES = ["kernels.cu", "kernels_img_u8.cu", "kernels_img_f32.cu", "kernels_img_f16.cu", "kernels_img_bf16.cu"]
+HEADERS = ["bbx_internal.h", "engine.h", "image_kernel.cuh"]
 
 
 def _stale() -> bool:
@@ -39,22 +39,25 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     BUILD.mkdir(exist_ok=True)
-    objs = []
+    (BUILD / "ptxas.log").write_text("")
     inc = ["-I", str(CSRC), "-I", str(HERE.parent / "include"), "-I", f"{CUDA_HOME}/include"]
+    jobs = []
     for src in CUDA_SOURCES:
         obj = BUILD / (src + ".o")
-        cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-               *inc, "-c", str(CSRC / src), "-o", str(obj)]
-        _run(cmd, verbose)
-        objs.append(obj)
+        jobs.append((obj, [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+                           *inc, "-c", str(CSRC / src), "-o", str(obj)]))
     for src in HOST_SOURCES:
         obj = BUILD / (src + ".o")
-        # -ffp-contract=off: the Normalize LUT must be one IEEE f32 subtract
-        # and one IEEE f32 divide (pipeline.py:158-160), never an FMA.
-        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
-               "-Wno-format-security", *inc, "-c", str(CSRC / src), "-o", str(obj)]
-        _run(cmd, verbose)
-        objs.append(obj)
+        # -ffp-contract=off: the host-side proof of the divide-free normalize
+        # (verify_fma_normalize) needs one IEEE subtract + one IEEE divide,
+        # never a contracted FMA (pipeline.py:158-160).
+        jobs.append((obj, [CXX, "-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall",
+                           "-Wno-format-security", *inc, "-c", str(CSRC / src), "-o", str(obj)]))
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        list(ex.map(lambda j: _run(j[1], verbose), jobs))
+    objs = [o for o, _ in jobs]
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *GENCODE, "-shared", "-o", str(tmp), *map(str, objs), "-lpthread", "-Xcompiler", "-fPIC"]
     _run(cmd, verbose)

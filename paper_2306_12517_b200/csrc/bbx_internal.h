@@ -10,14 +10,14 @@ namespace bbx {
 
 enum SrcKind : int32_t { SRC_DECODE = 0, SRC_RESAMPLE = 1, SRC_ARRAY = 2 };
 enum Codec : int32_t { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2 };
-enum ValueMode : int32_t { VAL_COPY = 0, VAL_LUT = 1, VAL_DIRECT = 2 };
+enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_FMA1 = 3 };
 
 constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
 constexpr int kDescHeader = 24;     // bytes before the per-sample params
 constexpr int kThreads = 256;       // CTA size of the image kernels
-constexpr int kLutChannels = 4;     // LUT path covers C <= 4
-constexpr int kSmemBudget = 96 * 1024;
+constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
+constexpr int kSmemBudget = 200 * 1024;
 
 // One geometric op after the source, in chain order.  Separable by axis:
 // output (y, x) -> input (fy(y), fx(x)).
@@ -41,9 +41,10 @@ struct PlanDev {
   Remap remaps[kMaxRemaps];
   int32_t value_mode;
   int32_t n_vops;
-  int32_t vop_kind[kMaxValueOps];          // TOFLOAT / NORMALIZE / NORMALIZE_PC
+  // normalize ops only (ToFloat is implicit); scalar Normalize is replicated over [4]
   float vop_mean[kMaxValueOps][4];
   float vop_std[kMaxValueOps][4];
+  float vop_inv[kMaxValueOps][4];          // RN(1/std), for VAL_FMA
   int32_t desc_stride;
   int32_t n_params;
   int32_t rows_per_tile;
@@ -52,6 +53,8 @@ struct PlanDev {
   int64_t scratch_bytes;                   // per-sample decode scratch (RLE)
   int32_t has_remaps_3d;                   // arrays: 3-D remaps present
   int32_t smem_bytes;
+  int32_t lin32;                           // bilinear axis math fits 32-bit
+  uint32_t ow_magic, gpr_magic;            // ceil(2^32/d) fast-division constants, 0 = use /
 };
 
 // Per-sample descriptor header (kDescHeader bytes), followed by n_params int32.
@@ -76,7 +79,7 @@ struct LaunchArgs {
   const uint8_t* payload;    // payload base (device): staged region or file image in HBM
   uint8_t* scratch;          // count * scratch_bytes (device)
   void* out;                 // count * out_sample_elems elements
-  const void* lut;           // VAL_LUT table: channels * 256 entries of the output type
+  const void* unused;
   SampleStatus* status;      // count entries
   int32_t count;
 };

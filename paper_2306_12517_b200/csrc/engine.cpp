@@ -84,33 +84,6 @@ void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
 static int dtype_size(int dt) {
   switch (dt) { case BBX_U8: return 1; case BBX_I64: case BBX_F64: return 8; case BBX_F32: return 4; default: return 2; }
 }
-static uint16_t f32_to_bf16_bits(float f) {      // round to nearest even
-  uint32_t u; std::memcpy(&u, &f, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return (uint16_t)(u >> 16);
-}
-static uint16_t f32_to_f16_bits(float f) {       // IEEE binary16, round to nearest even
-  uint32_t x; std::memcpy(&x, &f, 4);
-  uint32_t sign = (x >> 16) & 0x8000u;
-  uint32_t ax = x & 0x7fffffffu;
-  if (ax >= 0x7f800000u) return (uint16_t)(sign | (ax > 0x7f800000u ? 0x7e00u : 0x7c00u));
-  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);            // >= 65520 rounds to inf
-  if (ax < 0x38800000u) {                                                // subnormal half
-    if (ax < 0x33000000u) return (uint16_t)sign;                         // < 2^-25 -> 0 (2^-25 ties to even 0)
-    uint32_t mant = (ax & 0x7fffffu) | 0x800000u;
-    int e = (int)(ax >> 23);
-    int shift = 126 - e + 1 + 13;                                        // to 10-bit subnormal
-    uint32_t q = mant >> shift, rem = mant & ((1u << shift) - 1), half = 1u << (shift - 1);
-    if (rem > half || (rem == half && (q & 1u))) ++q;
-    return (uint16_t)(sign | q);
-  }
-  uint32_t r = ax - 0x38000000u;                                         // rebias exponent 127 -> 15
-  uint32_t q = r >> 13, rem = r & 0x1fffu;
-  if (rem > 0x1000u || (rem == 0x1000u && (q & 1u))) ++q;
-  return (uint16_t)(sign | q);
-}
-
 struct Draw {        // one RNG-consuming op, in chain order (host program)
   int kind;          // BBX_OP_RRC / BBX_OP_CENTERCROP / BBX_OP_CROP / BBX_OP_FLIP
   int slot;          // first param slot
@@ -186,6 +159,28 @@ struct bbx_loader {
 
 namespace bbx {
 
+// The kernel's divide-free normalize (kernels.cu: apply_vops_fma) must equal
+// the IEEE quotient bit for bit; a u8 plan has only 256 inputs per channel,
+// so prove it by enumeration (host fma == device fma: both correctly rounded).
+static bool verify_fma_normalize(const PlanDev& P, int C) {
+  for (int k = 0; k < std::min(C, 4); ++k)
+    for (int v = 0; v < 256; ++v) {
+      float x = (float)v, y = (float)v;
+      for (int i = 0; i < P.n_vops; ++i) {
+        volatile float t = x - P.vop_mean[i][k];
+        x = t / P.vop_std[i][k];
+        volatile float dd = y - P.vop_mean[i][k];
+        float d = dd;
+        volatile float q0v = d * P.vop_inv[i][k];
+        float q0 = q0v;
+        float r = std::fma(-q0, P.vop_std[i][k], d);
+        y = std::fma(r, P.vop_inv[i][k], q0);
+        if (std::memcmp(&x, &y, 4) != 0) return false;
+      }
+    }
+  return true;
+}
+
 static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n_ops, Plan& pl) {
   const bbx_dataset* ds = L->ds;
   if (field_index < 0 || field_index >= (int)ds->fields.size())
@@ -248,11 +243,18 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
         if (P.n_vops >= kMaxValueOps) return fail(BBX_SPEC_MISMATCH, "too many value transforms");
         if (o.kind == BBX_OP_NORMALIZE_PC && C > 4)
           return fail(BBX_SPEC_MISMATCH, "per-channel normalize supports at most 4 channels");
-        int v = P.n_vops++;
-        P.vop_kind[v] = o.kind;
-        for (int k = 0; k < 4; ++k) { P.vop_mean[v][k] = o.mean[k]; P.vop_std[v][k] = o.std[k]; }
-        if (o.kind == BBX_OP_NORMALIZE && o.std[0] == 0.f) return fail(BBX_SPEC_MISMATCH, "normalize std must be nonzero");
         out_dt = BBX_F32;
+        if (o.kind == BBX_OP_TOFLOAT) break;     // u8/int -> f32 is implicit in every value op
+        int v = P.n_vops++;
+        for (int k = 0; k < 4; ++k) {             // scalar Normalize is replicated per channel
+          int kk = o.kind == BBX_OP_NORMALIZE ? 0 : k;
+          P.vop_mean[v][k] = o.mean[kk];
+          P.vop_std[v][k] = o.std[kk];
+          if (o.kind == BBX_OP_NORMALIZE_PC && k >= C) { P.vop_mean[v][k] = 0.f; P.vop_std[v][k] = 1.f; }
+          if (P.vop_std[v][k] == 0.f) return fail(BBX_SPEC_MISMATCH, "normalize std must be nonzero");
+          volatile float one = 1.0f;
+          P.vop_inv[v][k] = one / P.vop_std[v][k];
+        }
         break;
       }
       case BBX_OP_CAST:
@@ -296,43 +298,39 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
   P.has_remaps_3d = P.n_remaps > 0;
   P.out_sample_elems = (int64_t)H * W * C;
   pl.out_sample_bytes = P.out_sample_elems * dtype_size(out_dt);
-  bool has_values = P.n_vops > 0;
+  const bool has_values = out_dt != dt || P.n_vops > 0;   // any ToFloat / Normalize / cast
   if (P.src_kind == SRC_ARRAY) {
     P.value_mode = has_values ? VAL_DIRECT : VAL_COPY;
-    if (has_values && P.src_dtype == BBX_F64 && false) {}
   } else {
-    P.value_mode = !has_values ? VAL_COPY : (C <= kLutChannels ? VAL_LUT : VAL_DIRECT);
+    // u8 source: values 0..255 only, so the divide-free normalize can be
+    // proven exact for this plan by exhausting its inputs.
+    if (has_values && P.n_vops == 0) {          // ToFloat only == Normalize(0, 1), exactly
+      for (int k = 0; k < 4; ++k) { P.vop_mean[0][k] = 0.f; P.vop_std[0][k] = 1.f; P.vop_inv[0][k] = 1.f; }
+      P.n_vops = 1;
+    }
+    P.value_mode = !has_values ? VAL_COPY
+                 : !verify_fma_normalize(P, C) ? VAL_DIRECT
+                 : (P.n_vops == 1 ? VAL_FMA1 : VAL_FMA);
     if (P.value_mode == VAL_COPY && out_dt != BBX_U8) return fail(BBX_SPEC_MISMATCH, "unexpected output dtype");
-    // tile height: 16 rows, shrunk until the staged rows fit the smem budget
+    // tile height: 16 rows, shrunk until the smem layout allows 4 CTAs per SM
     P.rows_per_tile = std::min(16, H);
     for (;;) {
       P.smem_bytes = image_smem_bytes(P);
-      if (P.smem_bytes <= kSmemBudget || P.rows_per_tile == 1) break;
+      if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1) break;
       P.rows_per_tile = std::max(1, P.rows_per_tile / 2);
     }
     if (P.smem_bytes > kSmemBudget || (int64_t)P.src_row_w * C + 64 > 65535)
       return fail(BBX_SPEC_MISMATCH, "image rows too wide for the device plan (%d x %d channels)", P.src_row_w, C);
     P.tiles_per_sample = (H + P.rows_per_tile - 1) / P.rows_per_tile;
     P.scratch_bytes = ((int64_t)f.info.max_height * f.info.max_width * C + 15) / 16 * 16;
-  }
-  // LUT: the whole u8 -> output value chain, computed exactly once (IEEE f32,
-  // -ffp-contract=off: one subtract and one divide per Normalize).
-  if (P.value_mode == VAL_LUT) {
-    int osz = dtype_size(out_dt);
-    std::vector<uint8_t> lut((size_t)C * 256 * osz);
-    for (int k = 0; k < C; ++k)
-      for (int v = 0; v < 256; ++v) {
-        float x = (float)v;
-        for (int i = 0; i < P.n_vops; ++i) {
-          if (P.vop_kind[i] == BBX_OP_NORMALIZE) { volatile float t = x - P.vop_mean[i][0]; x = t / P.vop_std[i][0]; }
-          else if (P.vop_kind[i] == BBX_OP_NORMALIZE_PC) { volatile float t = x - P.vop_mean[i][k]; x = t / P.vop_std[i][k]; }
-        }
-        size_t at = ((size_t)k * 256 + v) * osz;
-        if (out_dt == BBX_F32) std::memcpy(&lut[at], &x, 4);
-        else { uint16_t b = out_dt == BBX_F16 ? f32_to_f16_bits(x) : f32_to_bf16_bits(x); std::memcpy(&lut[at], &b, 2); }
-      }
-    CK(cudaMalloc(&pl.d_lut, lut.size()));
-    CK(cudaMemcpy(pl.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+    // fast-division constants (exact when n * d < 2^32)
+    const uint64_t two32 = 1ull << 32;
+    const int nslot = P.rows_per_tile * (P.src_kind == SRC_RESAMPLE ? 2 : 1);
+    if (W > 1 && (uint64_t)nslot * W * W < two32) P.ow_magic = (uint32_t)((two32 + W - 1) / W);
+    const int V = 16 / dtype_size(out_dt), gpr = W / V;
+    if (gpr > 1 && (uint64_t)P.rows_per_tile * gpr * gpr < two32) P.gpr_magic = (uint32_t)((two32 + gpr - 1) / gpr);
+    const uint64_t ax = std::max((uint64_t)H * f.info.max_height, (uint64_t)W * f.info.max_width);
+    P.lin32 = 2 * ax < two32 ? 1 : 0;
   }
   // one pass over the row table: exact staging capacity, RLE presence
   int64_t mx = 0;
@@ -591,7 +589,6 @@ static int process_slot(bbx_loader* L, int s) {
     A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_off[p]);
     A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
     A.out = pl.outs[s];
-    A.lut = pl.d_lut;
     A.status = S.d_status + (size_t)p * L->batch;
     A.count = count;
     if (count == 0) continue;

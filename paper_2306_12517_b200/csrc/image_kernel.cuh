@@ -1,0 +1,484 @@
+#pragma once
+// image_kernel.cuh — K1 and the helpers shared by every kernel TU.
+// sm_100a kernels of the bbox hot path.  See DESIGN.md §4 for the roofline of
+// each kernel.  Nothing here is a dense contraction, so no tensor cores: the
+// image kernel is an HBM-bound gather/expand.  Every global load is a 16-byte
+// vector into shared memory and every store a 16-byte vector of the
+// channels-last (NHWC) output.
+//
+//   K1 image_kernel       Decode (RAW/SUBSAMPLE2/expanded-RLE canvas, zero pad)
+//                         + RandomCrop/RandomFlip/Resize remaps + value ops
+//                         (ToFloat/Normalize/per-channel/cast), or the bilinear
+//                         RandomResizedCrop / CenterCrop decoders.
+//                         Reference: pipeline.py:95-231, codecs.py:91-128.
+//   K2 rle_expand_kernel  codecs.py:101-114 (RLE runs -> dense canvas), with
+//                         the reference's error semantics as a status word.
+//   K3 scalar_gather      loader.py:333-335 (label[b] = column[idx[b]]).
+//   K3' array_kernel      ArrayRead (pipeline.py:128-129) + chain.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "bbx_internal.h"
+
+namespace bbx {
+
+constexpr int VAL_GENERIC = 100;   // template tag: runtime choice between VAL_FMA and VAL_DIRECT
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Output-to-input coordinate through the remaps, applied last-to-first.
+// Every remap is monotone per axis (crop: shift, flip: reversal, nearest
+// resize: floor scaling), so the composition is monotone too.
+__device__ __forceinline__ int back_y(const PlanDev& P, const int32_t* prm, int y) {
+  for (int i = P.n_remaps - 1; i >= 0; --i) {
+    const Remap& m = P.remaps[i];
+    if (m.kind == BBX_OP_CROP) y += prm[m.prm];
+    else if (m.kind == BBX_OP_RESIZE) y = (int)(((int64_t)y * m.in_h) / m.out_h);
+  }
+  return y;
+}
+__device__ __forceinline__ int back_x(const PlanDev& P, const int32_t* prm, int x) {
+  for (int i = P.n_remaps - 1; i >= 0; --i) {
+    const Remap& m = P.remaps[i];
+    if (m.kind == BBX_OP_CROP) x += prm[m.prm + 1];
+    else if (m.kind == BBX_OP_FLIP) { if (prm[m.prm]) x = m.in_w - 1 - x; }
+    else if (m.kind == BBX_OP_RESIZE) x = (int)(((int64_t)x * m.in_w) / m.out_w);
+  }
+  return x;
+}
+
+// Bilinear axis (extension; identical integer rule in oracle/bbx_oracle.c
+// lin_axis): half-pixel centres, replicated border, 11-bit weight of i1.
+__device__ __forceinline__ void lin_axis(int o, int out_n, int in_n, bool fits32, int& i0, int& i1, int& w1) {
+  int64_t num = (int64_t)(2 * o + 1) * in_n - out_n, den = 2 * (int64_t)out_n;
+  if (num <= 0) { i0 = 0; i1 = 0; w1 = 0; return; }
+  int64_t q, r;
+  if (fits32) {
+    uint32_t n32 = (uint32_t)num, d32 = (uint32_t)den;
+    uint32_t q32 = n32 / d32;
+    q = q32; r = n32 - q32 * d32;
+  } else {
+    q = num / den; r = num - q * den;
+  }
+  if (q >= in_n - 1) { i0 = in_n - 1; i1 = in_n - 1; w1 = 0; return; }
+  i0 = (int)q; i1 = (int)q + 1;
+  w1 = fits32 ? (int)(((uint32_t)r * 2048u + (uint32_t)(den >> 1)) / (uint32_t)den)
+              : (int)((r * 2048 + den / 2) / den);
+}
+
+__device__ __forceinline__ float to_f32(const uint8_t* p, int dt) {
+  switch (dt) {
+    case BBX_U8: return (float)*p;
+    case BBX_I64: { long long v; memcpy(&v, p, 8); return __ll2float_rn(v); }
+    case BBX_F32: { float v; memcpy(&v, p, 4); return v; }
+    case BBX_F64: { double v; memcpy(&v, p, 8); return __double2float_rn(v); }
+  }
+  return 0.f;
+}
+
+// Value ops in strict IEEE f32 (pipeline.py:158-160: one subtract, one divide).
+__device__ __forceinline__ float apply_vops(const PlanDev& P, float v, int k) {
+  for (int i = 0; i < P.n_vops; ++i) v = __fdiv_rn(__fsub_rn(v, P.vop_mean[i][k & 3]), P.vop_std[i][k & 3]);
+  return v;
+}
+// Same results, without the divide: q0 = d * RN(1/s), one exact-residual
+// correction.  Used only when the host proved it equal to the IEEE quotient
+// for every reachable input of the plan (engine.cpp: verify_fma_normalize).
+__device__ __forceinline__ float apply_vops_fma(const PlanDev& P, float v, int k) {
+  for (int i = 0; i < P.n_vops; ++i) {
+    float d = __fsub_rn(v, P.vop_mean[i][k & 3]);
+    float inv = P.vop_inv[i][k & 3];
+    float q0 = __fmul_rn(d, inv);
+    float r = __fmaf_rn(-q0, P.vop_std[i][k & 3], d);
+    v = __fmaf_rn(r, inv, q0);
+  }
+  return v;
+}
+
+template <typename T> __device__ __forceinline__ T cvt_out(float v);
+template <> __device__ __forceinline__ float cvt_out<float>(float v) { return v; }
+template <> __device__ __forceinline__ __half cvt_out<__half>(float v) { return __float2half_rn(v); }
+template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ uint8_t cvt_out<uint8_t>(float v) { return (uint8_t)v; }
+
+// Per-thread copy of a single normalize op's constants (VAL_FMA1), so the
+// element loop reads registers, not the constant bank.
+template <int kC>
+struct NormRegs {
+  float m[kC > 0 ? kC : 1], inv[kC > 0 ? kC : 1], s[kC > 0 ? kC : 1];
+  __device__ __forceinline__ void load(const PlanDev& P) {
+#pragma unroll
+    for (int k = 0; k < (kC > 0 ? kC : 1); ++k) {
+      m[k] = P.vop_mean[0][k & 3]; inv[k] = P.vop_inv[0][k & 3]; s[k] = P.vop_std[0][k & 3];
+    }
+  }
+};
+
+template <typename OutT, int kVal, int kC>
+__device__ __forceinline__ OutT value_of(const PlanDev& P, const NormRegs<kC>& N, uint32_t b, int k) {
+  if constexpr (kVal == VAL_COPY) {
+    return (OutT)b;
+  } else if constexpr (kVal == VAL_FMA1 && kC > 0) {
+    float d = __fsub_rn((float)b, N.m[k]);
+    float q0 = __fmul_rn(d, N.inv[k]);
+    float r = __fmaf_rn(-q0, N.s[k], d);
+    return cvt_out<OutT>(__fmaf_rn(r, N.inv[k], q0));
+  } else {   // VAL_GENERIC: several normalize ops (or C not specialised)
+    return cvt_out<OutT>(P.value_mode == VAL_DIRECT ? apply_vops(P, (float)b, k) : apply_vops_fma(P, (float)b, k));
+  }
+}
+
+// Shared-memory layout of the image kernel (host + device).
+__host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+struct ImgSmem {
+  int nslot;        // staged source rows (R nearest, 2R bilinear)
+  int span_pad;     // bytes per staged source row
+  int hrow_pad;     // bytes per horizontally-resampled row
+  int xt_off, meta_off, src_off, h_off, total;
+};
+
+__host__ __device__ inline ImgSmem img_layout(const PlanDev& P) {
+  ImgSmem L;
+  const bool res = P.src_kind == SRC_RESAMPLE;
+  const int R = P.rows_per_tile;
+  L.nslot = res ? 2 * R : R;
+  L.span_pad = align_up(P.src_row_w * P.channels, 16) + 32;
+  L.hrow_pad = align_up(P.out_w * P.channels * (res ? 4 : 1), 16) + 16;
+  L.xt_off = 0;
+  L.meta_off = align_up(P.out_w * 4, 16);
+  // meta: slot_row[nslot], row_a[R], row_b[R], row_wy[R] (int32)
+  L.src_off = L.meta_off + align_up((L.nslot + 3 * R) * 4 + 16, 16);
+  L.h_off = L.src_off + L.nslot * L.span_pad;
+  L.total = L.h_off + L.nslot * L.hrow_pad;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t magic) { return __umulhi(n, magic); }
+
+// --------------------------------------------------------------------- K1
+// grid = (tiles_per_sample, count); CTA = 256 threads; a tile = R output rows.
+//
+//  A. per output column: source byte offset (nearest) or (offset, 11-bit
+//     weight) (bilinear) through the composed remaps -> xt[ow];
+//     per output row: source row slot(s) -> meta.  Rows are deduplicated by
+//     mapping the contiguous source-row range of the tile onto slots.
+//  B. every needed source row segment -> smem, 16-byte vector loads.
+//  H. horizontal pass, once per staged row: u8 (nearest) or the 2-tap
+//     fixed-point sum (bilinear, u32) for every output column and channel.
+//  V. vertical pass / value ops / store: each thread owns one group of
+//     kC x 16 B of output (V pixels), so the channel of every element is a
+//     compile-time constant; 16-byte coalesced NHWC stores.
+template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
+__global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, const LaunchArgs A) {
+  constexpr int V = kVec ? (16 / (int)sizeof(OutT)) : 1;
+  const int s = blockIdx.y;
+  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+  const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
+  if (d->skip) return;
+  const int C = kC > 0 ? kC : P.channels;
+  const int r0 = blockIdx.x * P.rows_per_tile;
+  const int R = min(P.rows_per_tile, P.out_h - r0);
+  if (R <= 0) return;
+  const int OW = P.out_w;
+  const int rowlen = OW * C;
+  const int h = d->h, w = d->w;
+  const int tid = threadIdx.x;
+
+  const uint8_t* base;
+  int sh;
+  int64_t rstride;
+  if (d->codec == CODEC_RLE) {
+    base = A.scratch + (size_t)s * P.scratch_bytes; sh = 0; rstride = (int64_t)w * C;
+  } else {
+    base = A.payload + d->src; sh = d->codec == CODEC_SUB2 ? 1 : 0;
+    rstride = (int64_t)(sh ? (w + 1) >> 1 : w) * C;
+  }
+  const int src_rows = sh ? (h + 1) >> 1 : h;
+
+  extern __shared__ __align__(16) uint8_t smem[];
+  const ImgSmem L = img_layout(P);
+  uint32_t* xt = reinterpret_cast<uint32_t*>(smem + L.xt_off);
+  int* slot_row = reinterpret_cast<int*>(smem + L.meta_off);   // source row of slot j, -1 = none
+  int* row_a = slot_row + L.nslot;                              // per output row: slot (-1: zero row)
+  int* row_b = row_a + R;                                       // bilinear second slot
+  int* row_wy = row_b + R;
+  uint8_t* srcbuf = smem + L.src_off;
+  uint8_t* hbuf = smem + L.h_off;
+  __shared__ int s_shift[2 * 16];
+  NormRegs<kC> N;
+  if constexpr (kVal == VAL_FMA1) N.load(P);
+  __shared__ int s_mode;   // 1: contiguous row range -> slots
+
+  // ---- A: column range (monotone maps: extremes at the ends) and tables
+  int col_lo, col_hi;                     // source columns (after >> sh), inclusive
+  int top = 0, left = 0, ch = 0, cw = 0;
+  if constexpr (kRes) {
+    top = prm[0]; left = prm[1]; ch = prm[2]; cw = prm[3];
+    int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
+    int a0, a1, aw, b0, b1, bw;
+    lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, a0, a1, aw);
+    lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, b0, b1, bw);
+    col_lo = (left + a0) >> sh; col_hi = (left + b1) >> sh;
+  } else {
+    int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
+    int lo = min(xa, xb), hi = min(max(xa, xb), w - 1);
+    col_lo = lo >> sh; col_hi = hi >> sh;   // col_lo > col_hi: every column is padding
+  }
+  const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+
+  for (int ox = tid; ox < OW; ox += kThreads) {
+    if constexpr (kRes) {
+      int cx = back_x(P, prm, ox), x0, x1, wx;
+      lin_axis(cx, P.canvas_w, cw, P.lin32, x0, x1, wx);
+      int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
+      xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+    } else {
+      int cx = back_x(P, prm, ox);
+      xt[ox] = cx < w ? (uint32_t)(((cx >> sh) - col_lo) * C) : 0xFFFFFFFFu;
+    }
+  }
+  // rows: source row (after >> sh) of every output row; contiguous-range slots when they fit
+  if (tid < R) {
+    int r = tid;
+    if constexpr (kRes) {
+      int cy = back_y(P, prm, r0 + r), y0, y1, wy;
+      lin_axis(cy, P.canvas_h, ch, P.lin32, y0, y1, wy);
+      row_a[r] = (top + y0) >> sh; row_b[r] = (top + y1) >> sh; row_wy[r] = wy;
+    } else {
+      int cy = back_y(P, prm, r0 + r);
+      row_a[r] = (cy < h && span_bytes > 0) ? (cy >> sh) : -1;
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * 16) s_shift[tid] = 0;
+  if (tid == 0) {
+    int lo = row_a[0], hi = kRes ? row_b[R - 1] : row_a[R - 1];
+    if (!kRes && lo < 0) { lo = hi = -1; }
+    if (!kRes && hi < 0) {   // trailing padding rows: range over the valid prefix
+      hi = -1;
+      for (int r = R - 1; r >= 0; --r) if (row_a[r] >= 0) { hi = row_a[r]; break; }
+    }
+    s_mode = (lo >= 0 && hi >= lo && hi - lo + 1 <= L.nslot) ? 1 : 0;
+    if (s_mode) {
+      for (int j = 0; j < L.nslot; ++j) slot_row[j] = (lo + j <= hi && lo + j < src_rows) ? lo + j : -1;
+    }
+  }
+  __syncthreads();
+  const bool contiguous = s_mode != 0;
+  if (tid < R) {   // rewrite row_a/row_b as slot indices
+    int r = tid;
+    if (contiguous) {
+      int lo = slot_row[0];
+      if (row_a[r] >= 0) row_a[r] -= lo;
+      if constexpr (kRes) row_b[r] -= lo;
+    } else {
+      if constexpr (kRes) {
+        slot_row[2 * r] = row_a[r]; slot_row[2 * r + 1] = row_b[r];
+        row_a[r] = 2 * r; row_b[r] = 2 * r + 1;
+      } else {
+        slot_row[r] = row_a[r];
+        if (row_a[r] >= 0) row_a[r] = r;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- B: stage source row segments (warp per slot, 16 B vectors)
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < L.nslot; j += kThreads / 32) {
+    int srow = slot_row[j];
+    if (srow < 0 || span_bytes == 0) continue;
+    const uint8_t* src = base + (int64_t)srow * rstride + (int64_t)col_lo * C;
+    uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    uintptr_t a0 = a & ~(uintptr_t)15;
+    int shift = (int)(a - a0);
+    int n16 = (shift + span_bytes + 15) >> 4;
+    uint8_t* dst = srcbuf + (size_t)j * L.span_pad;
+    const uint8_t* s0 = reinterpret_cast<const uint8_t*>(a0);
+    for (int c = lane; c < n16; c += 32) *reinterpret_cast<uint4*>(dst + 16 * c) = ld_nc_v4(s0 + 16 * c);
+    if (lane == 0) s_shift[j] = shift;
+  }
+  __syncthreads();
+
+  // ---- H: horizontal pass, one thread per (slot, output column)
+  {
+    const int total = L.nslot * OW;
+    for (int idx = tid; idx < total; idx += kThreads) {
+      int j = P.ow_magic ? (int)fast_div((uint32_t)idx, P.ow_magic) : idx / OW;
+      int ox = idx - j * OW;
+      if (slot_row[j] < 0) continue;
+      const uint8_t* row = srcbuf + (size_t)j * L.span_pad + s_shift[j];
+      uint32_t e = xt[ox];
+      if constexpr (kRes) {
+        uint32_t* hr = reinterpret_cast<uint32_t*>(hbuf + (size_t)j * L.hrow_pad) + ox * C;
+        int off0 = (int)(e & 0xFFFFu), wx = (int)((e >> 16) & 0xFFFu);
+        int off1 = (e >> 28) ? off0 : off0 + C;
+        uint32_t w0 = 2048u - (uint32_t)wx, w1 = (uint32_t)wx;
+#pragma unroll
+        for (int k = 0; k < (kC > 0 ? kC : 1); ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+        if constexpr (kC == 0)
+          for (int k = 1; k < C; ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+      } else {
+        uint8_t* hr = hbuf + (size_t)j * L.hrow_pad + ox * C;
+        const bool pad = e == 0xFFFFFFFFu;
+        const uint32_t eo = pad ? 0u : e;    // never form an out-of-window smem address
+#pragma unroll
+        for (int k = 0; k < (kC > 0 ? kC : 1); ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
+        if constexpr (kC == 0)
+          for (int k = 1; k < C; ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- V: vertical pass + value ops + 16-byte stores
+  OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * rowlen;
+  if constexpr (kC > 0) {
+    // group = V pixels = kC vectors of V elements; element i of vector j has channel (j*V+i) % kC
+    const int gpr = OW / V;                     // full groups per row
+    const int ngroups = R * gpr;
+    for (int idx = tid; idx < ngroups; idx += kThreads) {
+      int r = (kVec && P.gpr_magic) ? (int)fast_div((uint32_t)idx, P.gpr_magic) : idx / gpr;
+      int g = idx - r * gpr;
+      int e0 = g * V * kC;
+      int a = row_a[r];
+      OutT* orow = out + (size_t)r * rowlen + e0;
+#pragma unroll
+      for (int j = 0; j < kC; ++j) {
+        union { OutT v[V]; uint4 u; } pk;
+        if constexpr (kRes) {
+          const uint32_t* h0 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)a * L.hrow_pad) + e0 + j * V;
+          const uint32_t* h1 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)row_b[r] * L.hrow_pad) + e0 + j * V;
+          const uint32_t wy1 = (uint32_t)row_wy[r], wy0 = 2048u - wy1;
+          uint32_t t0[V], t1[V];
+          if constexpr (V % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < V; i += 4) {
+              uint4 x = *reinterpret_cast<const uint4*>(h0 + i), y = *reinterpret_cast<const uint4*>(h1 + i);
+              t0[i] = x.x; t0[i + 1] = x.y; t0[i + 2] = x.z; t0[i + 3] = x.w;
+              t1[i] = y.x; t1[i + 1] = y.y; t1[i + 2] = y.z; t1[i + 3] = y.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) { t0[i] = h0[i]; t1[i] = h1[i]; }
+          }
+#pragma unroll
+          for (int i = 0; i < V; ++i) {
+            uint32_t b = (wy0 * t0[i] + wy1 * t1[i] + (1u << 21)) >> 22;
+            pk.v[i] = value_of<OutT, kVal, kC>(P, N, b, (j * V + i) % kC);
+          }
+        } else {
+          uint8_t bytes[V];
+          if (a < 0) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) bytes[i] = 0;
+          } else {
+            const uint8_t* h0 = hbuf + (size_t)a * L.hrow_pad + e0 + j * V;
+            if constexpr (V == 16) *reinterpret_cast<uint4*>(bytes) = *reinterpret_cast<const uint4*>(h0);
+            else if constexpr (V == 8) *reinterpret_cast<uint2*>(bytes) = *reinterpret_cast<const uint2*>(h0);
+            else if constexpr (V == 4) *reinterpret_cast<uint32_t*>(bytes) = *reinterpret_cast<const uint32_t*>(h0);
+            else {
+#pragma unroll
+              for (int i = 0; i < V; ++i) bytes[i] = h0[i];
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < V; ++i) pk.v[i] = value_of<OutT, kVal, kC>(P, N, bytes[i], (j * V + i) % kC);
+        }
+        if constexpr (kVec) *reinterpret_cast<uint4*>(orow + j * V) = pk.u;
+        else orow[j * V] = pk.v[0];
+      }
+    }
+    // tail columns (OW % V) element-wise
+    const int tail0 = gpr * V;
+    if (tail0 < OW) {
+      const int tl = (OW - tail0) * C;
+      for (int idx = tid; idx < R * tl; idx += kThreads) {
+        int r = idx / tl, q = tail0 * C + (idx - r * tl);
+        int k = q % C, a = row_a[r];
+        uint32_t b;
+        if constexpr (kRes) {
+          const uint32_t* h0 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)a * L.hrow_pad);
+          const uint32_t* h1 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)row_b[r] * L.hrow_pad);
+          b = ((2048u - (uint32_t)row_wy[r]) * h0[q] + (uint32_t)row_wy[r] * h1[q] + (1u << 21)) >> 22;
+        } else {
+          b = hbuf[(size_t)max(a, 0) * L.hrow_pad + q];
+          if (a < 0) b = 0u;
+        }
+        out[(size_t)r * rowlen + q] = value_of<OutT, kVal, kC>(P, N, b, k);
+      }
+    }
+  } else {
+    // dynamic channel count: element-wise
+    for (int idx = tid; idx < R * rowlen; idx += kThreads) {
+      int r = idx / rowlen, q = idx - r * rowlen;
+      int k = q % C, a = row_a[r];
+      uint32_t b;
+      if constexpr (kRes) {
+        const uint32_t* h0 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)a * L.hrow_pad);
+        const uint32_t* h1 = reinterpret_cast<const uint32_t*>(hbuf + (size_t)row_b[r] * L.hrow_pad);
+        b = ((2048u - (uint32_t)row_wy[r]) * h0[q] + (uint32_t)row_wy[r] * h1[q] + (1u << 21)) >> 22;
+      } else {
+        b = hbuf[(size_t)max(a, 0) * L.hrow_pad + q];
+        if (a < 0) b = 0u;
+      }
+      out[(size_t)r * rowlen + q] = value_of<OutT, kVal, kC>(P, N, b, k);
+    }
+  }
+}
+
+
+// ------------------------------------------------------------ K1 dispatch
+template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
+static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
+  dim3 grid(P.tiles_per_sample, A.count);
+  int smem = img_layout(P).total;
+  auto k = image_kernel<OutT, kRes, kVal, kC, kVec>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k<<<grid, kThreads, smem, st>>>(P, A);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <typename OutT, bool kRes, int kVal>
+static int launch_img_c(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec) {
+  switch (P.channels) {
+    case 1: return vec ? launch_img_t<OutT, kRes, kVal, 1, true>(P, A, st) : launch_img_t<OutT, kRes, kVal, 1, false>(P, A, st);
+    case 3: return vec ? launch_img_t<OutT, kRes, kVal, 3, true>(P, A, st) : launch_img_t<OutT, kRes, kVal, 3, false>(P, A, st);
+    default: return launch_img_t<OutT, kRes, kVal, 0, false>(P, A, st);
+  }
+}
+
+template <typename OutT, int kVal>
+static int launch_img_r(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec) {
+  return P.src_kind == SRC_RESAMPLE ? launch_img_c<OutT, true, kVal>(P, A, st, vec)
+                                    : launch_img_c<OutT, false, kVal>(P, A, st, vec);
+}
+
+template <typename OutT>
+static int launch_img_typed(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec) {
+  if constexpr (sizeof(OutT) == 1) {
+    return launch_img_r<OutT, VAL_COPY>(P, A, st, vec);
+  } else {
+    if (P.value_mode == VAL_FMA1) return launch_img_r<OutT, VAL_FMA1>(P, A, st, vec);
+    return launch_img_r<OutT, VAL_GENERIC>(P, A, st, vec);
+  }
+}
+
+// one translation unit per output type (parallel build): kernels_img_*.cu
+int launch_img_u8(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec);
+int launch_img_f32(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec);
+int launch_img_f16(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec);
+int launch_img_bf16(const PlanDev& P, const LaunchArgs& A, cudaStream_t st, bool vec);
+
+}  // namespace bbx
