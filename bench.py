@@ -323,12 +323,15 @@ def main():
         "data": "synthetic (SyntheticImageSource pattern, 256x256x3 RAW, writer seed 1)",
         "config": config,
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): mmap -> pinned -> H2D -> K1"},
+                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): mmap -> pinned -> H2D -> K1",
+                "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
+                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": load_traffic(),
                      "kernel": "image_kernel<half, resample> (K1)", "kernel_us": kern_s * 1e6,
                      "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src},
         "gpu_launches": int(st["kernel_launches"]),
+        "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
         "clocks": clk.summary(),
     }
     if world == 1:

@@ -14,7 +14,7 @@ enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_FMA1 =
 
 constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
-constexpr int kDescHeader = 24;     // bytes before the per-sample params
+constexpr int kDescHeader = 32;     // bytes before the per-sample params
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
@@ -26,6 +26,14 @@ struct Remap {
   int32_t in_h, in_w;    // input spec (pipeline.py output_spec propagation)
   int32_t out_h, out_w;
   int32_t prm;           // first per-sample param slot (crop: top, left; flip: bit)
+};
+
+// Shared-memory layout of K1 for one plan (computed once on the host).
+struct SmemLayout {
+  int32_t nslot;        // staged source rows (R nearest, 2R bilinear)
+  int32_t span_pad;     // bytes per staged source row
+  int32_t hrow_pad;     // bytes per horizontally-resampled row
+  int32_t xt_off, meta_off, src_off, h_off, total;
 };
 
 // Everything the kernels need about one compiled chain; passed by value.
@@ -55,6 +63,8 @@ struct PlanDev {
   int32_t smem_bytes;
   int32_t lin32;                           // bilinear axis math fits 32-bit
   uint32_t ow_magic, gpr_magic;            // ceil(2^32/d) fast-division constants, 0 = use /
+  uint32_t linx_magic, liny_magic;         // for 2*canvas_w / 2*canvas_h (bilinear axes), 0 = use /
+  SmemLayout lay;
 };
 
 // Per-sample descriptor header (kDescHeader bytes), followed by n_params int32.
@@ -62,9 +72,12 @@ struct SampleDesc {
   uint64_t src;    // payload byte offset from the launch's payload base
   uint32_t len;    // payload length
   uint16_t h, w;   // image cell dims
-  uint8_t c, codec, skip, pad;
+  uint8_t c, codec, skip, flags;  // flags bit0: staged payload is a window (RAW only)
   int32_t index_lo;  // sample index (low 32 bits, diagnostics)
+  uint32_t wstride;  // windowed: bytes per staged row
+  uint16_t wy0, wx0; // windowed: image coordinates of the window's first row / column
 };
+constexpr uint8_t kDescWindowed = 1;
 static_assert(sizeof(SampleDesc) == kDescHeader, "descriptor header layout");
 
 // Per-sample device status (K2 RLE errors).
@@ -98,5 +111,6 @@ int launch_image(const PlanDev& P, const LaunchArgs& A, void* stream);
 int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream);
 int launch_scalar_gather(const ScalarArgs& S, void* stream);
 int image_smem_bytes(const PlanDev& P);
+SmemLayout img_layout_host(const PlanDev& P);
 
 }  // namespace bbx

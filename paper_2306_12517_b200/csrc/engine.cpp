@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.h"
@@ -145,7 +146,8 @@ struct bbx_loader {
   bool finalized = false;
   size_t slot_bytes = 0, desc_bytes = 0, idx_off = 0;
   std::vector<size_t> desc_off;       // per plan, within a slot
-  std::vector<size_t> pay_off;        // per plan, start of its payload region
+  size_t pay_base = 0;                // start of the compact payload region
+  bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
   // pipeline thread
   std::thread th;
   std::mutex mu;
@@ -315,7 +317,8 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     // tile height: 16 rows, shrunk until the smem layout allows 4 CTAs per SM
     P.rows_per_tile = std::min(16, H);
     for (;;) {
-      P.smem_bytes = image_smem_bytes(P);
+      P.lay = img_layout_host(P);
+      P.smem_bytes = P.lay.total;
       if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1) break;
       P.rows_per_tile = std::max(1, P.rows_per_tile / 2);
     }
@@ -331,6 +334,15 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     if (gpr > 1 && (uint64_t)P.rows_per_tile * gpr * gpr < two32) P.gpr_magic = (uint32_t)((two32 + gpr - 1) / gpr);
     const uint64_t ax = std::max((uint64_t)H * f.info.max_height, (uint64_t)W * f.info.max_width);
     P.lin32 = 2 * ax < two32 ? 1 : 0;
+    if (P.src_kind == SRC_RESAMPLE) {   // lin_axis divides by 2*canvas extent: exact when n*d < 2^32
+      auto magic_ok = [&](uint64_t den, uint64_t in_max) {
+        return 2048 * den * den < two32 && den * den * in_max < two32;
+      };
+      uint64_t dx = 2ull * P.canvas_w, dy = 2ull * P.canvas_h;
+      if (magic_ok(dx, f.info.max_width)) P.linx_magic = (uint32_t)((two32 + dx - 1) / dx);
+      if (magic_ok(dy, f.info.max_height)) P.liny_magic = (uint32_t)((two32 + dy - 1) / dy);
+    }
+    P.lay = img_layout_host(P);
   }
   // one pass over the row table: exact staging capacity, RLE presence
   int64_t mx = 0;
@@ -351,6 +363,40 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
 
 // Host-side per-sample work for one plan: descriptor + RNG params + checks.
 // Returns false (and fills err) when the sample must be skipped.
+// Host twins of the kernel's back_x/back_y (image_kernel.cuh): the composed
+// remaps are monotone, so the referenced canvas range is spanned by the ends.
+static int host_back_y(const PlanDev& P, const int32_t* prm, int y) {
+  for (int i = P.n_remaps - 1; i >= 0; --i) {
+    const Remap& m = P.remaps[i];
+    if (m.kind == BBX_OP_CROP) y += prm[m.prm];
+    else if (m.kind == BBX_OP_RESIZE) y = (int)(((int64_t)y * m.in_h) / m.out_h);
+  }
+  return y;
+}
+static int host_back_x(const PlanDev& P, const int32_t* prm, int x) {
+  for (int i = P.n_remaps - 1; i >= 0; --i) {
+    const Remap& m = P.remaps[i];
+    if (m.kind == BBX_OP_CROP) x += prm[m.prm + 1];
+    else if (m.kind == BBX_OP_FLIP) { if (prm[m.prm]) x = m.in_w - 1 - x; }
+    else if (m.kind == BBX_OP_RESIZE) x = (int)(((int64_t)x * m.in_w) / m.out_w);
+  }
+  return x;
+}
+// Image rows [y0, y1) x columns [x0, x1) a RAW sample's chain reads (empty when
+// the output only sees zero padding).  Resample decoders read exactly their
+// window (lin_axis indices stay inside it).
+static void read_window(const PlanDev& P, const SampleDesc* d, const int32_t* prm, int* y0, int* y1, int* x0, int* x1) {
+  if (P.src_kind == SRC_RESAMPLE) {
+    *y0 = prm[0]; *y1 = prm[0] + prm[2]; *x0 = prm[1]; *x1 = prm[1] + prm[3];
+    return;
+  }
+  int ya = host_back_y(P, prm, 0), yb = host_back_y(P, prm, P.out_h - 1);
+  int xa = host_back_x(P, prm, 0), xb = host_back_x(P, prm, P.out_w - 1);
+  *y0 = std::min(ya, yb); *y1 = std::min(std::max(ya, yb) + 1, (int)d->h);
+  *x0 = std::min(xa, xb); *x1 = std::min(std::max(xa, xb) + 1, (int)d->w);
+  if (*y0 >= *y1 || *x0 >= *x1) { *y0 = *y1 = *x0 = *x1 = 0; }
+}
+
 static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t seed, uint64_t epoch, uint8_t* desc,
                       uint64_t* src_off, uint32_t* len, HostErr& err, int64_t pos, int plan_idx) {
   const Field& f = ds->fields[pl.field_index];
@@ -434,13 +480,12 @@ static void pipeline_loop(bbx_loader* L);
 static int finalize(bbx_loader* L) {
   if (L->finalized) return BBX_OK;
   CK(cudaSetDevice(L->device));
-  // slot layout: [idx: B*8][desc blocks per plan][payload regions per plan]
+  // slot layout: [idx: B*8][desc blocks per plan][one compact payload region]
   size_t off = 0;
   L->idx_off = 0;
   off += (size_t)L->batch * 8;
   off = (off + 255) / 256 * 256;
   L->desc_off.assign(L->plans.size(), 0);
-  L->pay_off.assign(L->plans.size(), 0);
   for (size_t p = 0; p < L->plans.size(); ++p) {
     if (L->plans[p].scalar) continue;
     L->desc_off[p] = off;
@@ -449,11 +494,10 @@ static int finalize(bbx_loader* L) {
   }
   L->desc_bytes = off;
   bool resident = L->ds->d_heap != nullptr;
-  for (size_t p = 0; p < L->plans.size(); ++p) {
-    if (L->plans[p].scalar) continue;
-    L->pay_off[p] = off;
-    if (!resident) off += (size_t)L->batch * (size_t)((L->plans[p].max_payload + 15) / 16 * 16);
-    off = (off + 255) / 256 * 256;
+  L->pay_base = off;
+  for (size_t p = 0; p < L->plans.size(); ++p) {   // capacity: every sample's whole payload
+    if (L->plans[p].scalar || resident) continue;
+    off += (size_t)L->batch * (size_t)((L->plans[p].max_payload + 15) / 16 * 16);
   }
   L->slot_bytes = off + 256;
   size_t nplans = L->plans.size();
@@ -505,16 +549,18 @@ static int process_slot(bbx_loader* L, int s) {
     }
   }
   // descriptors + payload plan (serial: ~100 ns per sample per field)
-  struct Copy { const uint8_t* src; uint8_t* dst; uint32_t len; };
+  struct Copy { const uint8_t* src; uint8_t* dst; uint32_t row_bytes, rows, src_stride; };
   std::vector<Copy> copies;
   if (!resident) copies.reserve((size_t)count * L->plans.size());
   double t0 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
+  // one compact payload region for every plan: [pay_base, cursor)
+  const size_t pay_base = L->pay_base;
+  size_t cursor = pay_base;
   for (size_t p = 0; p < L->plans.size(); ++p) {
     const Plan& pl = L->plans[p];
     if (pl.scalar) continue;
     uint8_t* dblk = H + L->desc_off[p];
-    size_t pay = L->pay_off[p];
-    size_t stride = (size_t)((pl.max_payload + 15) / 16 * 16);
+    const bool image = ds->fields[pl.field_index].info.kind == 4;
     for (int pos = 0; pos < count; ++pos) {
       int64_t i = S.idx[pos];
       uint8_t* desc = dblk + (size_t)pos * pl.dev.desc_stride;
@@ -531,30 +577,39 @@ static int process_slot(bbx_loader* L, int s) {
       if (d->codec == CODEC_RLE && ds->fields[pl.field_index].info.kind == 4) S.plan_has_rle[p] = 1;
       if (resident) {
         d->src = off;                                   // absolute file offset; base = heap - heap_offset
-      } else {
-        size_t at = (size_t)pos * stride;
-        d->src = at;                                    // relative to this plan's payload region
-        if (len) copies.push_back({ds->map + off, H + pay + at, len});
+        continue;
       }
+      d->src = cursor - pay_base;                       // relative to the payload region
+      if (image && d->codec == CODEC_RAW && L->window_staging) {
+        int y0, y1, x0, x1;
+        read_window(pl.dev, d, reinterpret_cast<const int32_t*>(desc + kDescHeader), &y0, &y1, &x0, &x1);
+        const uint32_t wb = (uint32_t)(x1 - x0) * d->c, wr = (uint32_t)(y1 - y0);
+        if ((uint64_t)wb * wr * 10 < (uint64_t)len * 9) {   // worth it: < 90% of the payload
+          d->flags |= kDescWindowed;
+          d->wstride = wb; d->wy0 = (uint16_t)y0; d->wx0 = (uint16_t)x0;
+          if (wb && wr)
+            copies.push_back({ds->map + off + ((uint64_t)y0 * d->w + x0) * d->c, H + cursor, wb, wr,
+                              (uint32_t)d->w * d->c});
+          cursor += ((size_t)wb * wr + 15) / 16 * 16;
+          continue;
+        }
+      }
+      if (len) copies.push_back({ds->map + off, H + cursor, len, 1, len});
+      cursor += ((size_t)len + 15) / 16 * 16;
     }
   }
-  // parallel gather: mmap page cache -> pinned slot
+  // parallel gather: mmap page cache -> pinned slot (row segments for windows)
   if (!copies.empty()) {
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
-      std::memcpy(copies[k].dst, copies[k].src, copies[k].len);
+      const Copy& c = copies[k];
+      if (c.rows == 1) { std::memcpy(c.dst, c.src, c.row_bytes); return; }
+      for (uint32_t r = 0; r < c.rows; ++r)
+        std::memcpy(c.dst + (size_t)r * c.row_bytes, c.src + (size_t)r * c.src_stride, c.row_bytes);
     });
   }
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // H2D on the copy stream (after the previous kernels reading d_stage)
-  size_t bytes = resident ? L->desc_bytes : L->slot_bytes - 256;
-  if (!resident) {
-    // copy only up to the last used payload byte of the last plan
-    size_t last = L->desc_bytes;
-    for (size_t p = 0; p < L->plans.size(); ++p)
-      if (!L->plans[p].scalar)
-        last = std::max(last, L->pay_off[p] + (size_t)count * (size_t)((L->plans[p].max_payload + 15) / 16 * 16));
-    bytes = last;
-  }
+  const size_t bytes = resident ? L->desc_bytes : cursor;
   if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
   CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
   CK(cudaEventRecord(S.h2d_done, L->copy_st));
@@ -586,7 +641,7 @@ static int process_slot(bbx_loader* L, int s) {
     }
     LaunchArgs A{};
     A.desc = S.d_stage + L->desc_off[p];
-    A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_off[p]);
+    A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
     A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
     A.out = pl.outs[s];
     A.status = S.d_status + (size_t)p * L->batch;
@@ -726,6 +781,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   auto L = std::make_unique<bbx_loader>();
   L->ds = ds; L->device = device; L->batch = batch_size; L->nslots = slot_count;
   L->slots.resize(slot_count);
+  if (const char* e = std::getenv("BBX_WINDOW_STAGING")) L->window_staging = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   L->pool = std::make_unique<Pool>(nt);
@@ -971,7 +1027,8 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
   P.src_elem = 1; P.src_dtype = BBX_U8; P.out_h = h; P.out_w = w; P.out_c = c; P.out_dtype = BBX_U8;
   P.value_mode = VAL_COPY; P.desc_stride = kDescHeader + 8; P.rows_per_tile = std::min(16, h);
   for (;;) {
-    P.smem_bytes = image_smem_bytes(P);
+    P.lay = img_layout_host(P);
+    P.smem_bytes = P.lay.total;
     if (P.smem_bytes <= kSmemBudget || P.rows_per_tile == 1) break;
     P.rows_per_tile /= 2;
   }

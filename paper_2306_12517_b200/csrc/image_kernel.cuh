@@ -59,10 +59,21 @@ __device__ __forceinline__ int back_x(const PlanDev& P, const int32_t* prm, int 
 
 // Bilinear axis (extension; identical integer rule in oracle/bbx_oracle.c
 // lin_axis): half-pixel centres, replicated border, 11-bit weight of i1.
-__device__ __forceinline__ void lin_axis(int o, int out_n, int in_n, bool fits32, int& i0, int& i1, int& w1) {
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t magic) { return __umulhi(n, magic); }
+
+__device__ __forceinline__ void lin_axis(int o, int out_n, int in_n, bool fits32, uint32_t magic, int& i0, int& i1,
+                                         int& w1) {
   int64_t num = (int64_t)(2 * o + 1) * in_n - out_n, den = 2 * (int64_t)out_n;
   if (num <= 0) { i0 = 0; i1 = 0; w1 = 0; return; }
   int64_t q, r;
+  if (magic) {   // den is the plan's 2*canvas extent: exact reciprocal multiply
+    uint32_t q32 = fast_div((uint32_t)num, magic);
+    uint32_t r32 = (uint32_t)num - q32 * (uint32_t)den;
+    if (q32 >= (uint32_t)(in_n - 1)) { i0 = in_n - 1; i1 = in_n - 1; w1 = 0; return; }
+    i0 = (int)q32; i1 = (int)q32 + 1;
+    w1 = (int)fast_div(r32 * 2048u + (uint32_t)(den >> 1), magic);
+    return;
+  }
   if (fits32) {
     uint32_t n32 = (uint32_t)num, d32 = (uint32_t)den;
     uint32_t q32 = n32 / d32;
@@ -141,15 +152,8 @@ __device__ __forceinline__ OutT value_of(const PlanDev& P, const NormRegs<kC>& N
 // Shared-memory layout of the image kernel (host + device).
 __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
 
-struct ImgSmem {
-  int nslot;        // staged source rows (R nearest, 2R bilinear)
-  int span_pad;     // bytes per staged source row
-  int hrow_pad;     // bytes per horizontally-resampled row
-  int xt_off, meta_off, src_off, h_off, total;
-};
-
-__host__ __device__ inline ImgSmem img_layout(const PlanDev& P) {
-  ImgSmem L;
+__host__ __device__ inline SmemLayout img_layout(const PlanDev& P) {
+  SmemLayout L;
   const bool res = P.src_kind == SRC_RESAMPLE;
   const int R = P.rows_per_tile;
   L.nslot = res ? 2 * R : R;
@@ -164,7 +168,6 @@ __host__ __device__ inline ImgSmem img_layout(const PlanDev& P) {
   return L;
 }
 
-__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t magic) { return __umulhi(n, magic); }
 
 // --------------------------------------------------------------------- K1
 // grid = (tiles_per_sample, count); CTA = 256 threads; a tile = R output rows.
@@ -200,6 +203,11 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   int64_t rstride;
   if (d->codec == CODEC_RLE) {
     base = A.scratch + (size_t)s * P.scratch_bytes; sh = 0; rstride = (int64_t)w * C;
+  } else if (d->flags & kDescWindowed) {
+    // only the rows/columns the chain reads were staged: a virtual origin makes
+    // every in-window image coordinate address its staged byte
+    rstride = d->wstride; sh = 0;
+    base = A.payload + d->src - (int64_t)d->wy0 * rstride - (int64_t)d->wx0 * C;
   } else {
     base = A.payload + d->src; sh = d->codec == CODEC_SUB2 ? 1 : 0;
     rstride = (int64_t)(sh ? (w + 1) >> 1 : w) * C;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   const int src_rows = sh ? (h + 1) >> 1 : h;
 
   extern __shared__ __align__(16) uint8_t smem[];
-  const ImgSmem L = img_layout(P);
+  const SmemLayout& L = P.lay;
   uint32_t* xt = reinterpret_cast<uint32_t*>(smem + L.xt_off);
   int* slot_row = reinterpret_cast<int*>(smem + L.meta_off);   // source row of slot j, -1 = none
   int* row_a = slot_row + L.nslot;                              // per output row: slot (-1: zero row)
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   __shared__ int s_shift[2 * 16];
   NormRegs<kC> N;
   if constexpr (kVal == VAL_FMA1) N.load(P);
-  __shared__ int s_mode;   // 1: contiguous row range -> slots
+  __shared__ int s_mode, s_lo, s_hi;   // s_mode 1: contiguous row range -> slots
 
   // ---- A: column range (monotone maps: extremes at the ends) and tables
   int col_lo, col_hi;                     // source columns (after >> sh), inclusive
@@ -227,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
     top = prm[0]; left = prm[1]; ch = prm[2]; cw = prm[3];
     int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
     int a0, a1, aw, b0, b1, bw;
-    lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, a0, a1, aw);
-    lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, b0, b1, bw);
+    lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, a0, a1, aw);
+    lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, b0, b1, bw);
     col_lo = (left + a0) >> sh; col_hi = (left + b1) >> sh;
   } else {
     int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   for (int ox = tid; ox < OW; ox += kThreads) {
     if constexpr (kRes) {
       int cx = back_x(P, prm, ox), x0, x1, wx;
-      lin_axis(cx, P.canvas_w, cw, P.lin32, x0, x1, wx);
+      lin_axis(cx, P.canvas_w, cw, P.lin32, P.linx_magic, x0, x1, wx);
       int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
       xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
     } else {
@@ -249,11 +257,12 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
     }
   }
   // rows: source row (after >> sh) of every output row; contiguous-range slots when they fit
+  if (tid < L.nslot) { slot_row[tid] = -1; s_shift[tid] = 0; }   // a tail tile uses fewer slots
   if (tid < R) {
     int r = tid;
     if constexpr (kRes) {
       int cy = back_y(P, prm, r0 + r), y0, y1, wy;
-      lin_axis(cy, P.canvas_h, ch, P.lin32, y0, y1, wy);
+      lin_axis(cy, P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
       row_a[r] = (top + y0) >> sh; row_b[r] = (top + y1) >> sh; row_wy[r] = wy;
     } else {
       int cy = back_y(P, prm, r0 + r);
@@ -261,7 +270,6 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
     }
   }
   __syncthreads();
-  if (tid < 2 * 16) s_shift[tid] = 0;
   if (tid == 0) {
     int lo = row_a[0], hi = kRes ? row_b[R - 1] : row_a[R - 1];
     if (!kRes && lo < 0) { lo = hi = -1; }
@@ -270,16 +278,18 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
       for (int r = R - 1; r >= 0; --r) if (row_a[r] >= 0) { hi = row_a[r]; break; }
     }
     s_mode = (lo >= 0 && hi >= lo && hi - lo + 1 <= L.nslot) ? 1 : 0;
-    if (s_mode) {
-      for (int j = 0; j < L.nslot; ++j) slot_row[j] = (lo + j <= hi && lo + j < src_rows) ? lo + j : -1;
-    }
+    s_lo = lo; s_hi = hi;
   }
   __syncthreads();
   const bool contiguous = s_mode != 0;
+  if (contiguous && tid < L.nslot) {
+    int y = s_lo + tid;
+    slot_row[tid] = (y <= s_hi && y < src_rows) ? y : -1;
+  }
   if (tid < R) {   // rewrite row_a/row_b as slot indices
     int r = tid;
     if (contiguous) {
-      int lo = slot_row[0];
+      int lo = s_lo;
       if (row_a[r] >= 0) row_a[r] -= lo;
       if constexpr (kRes) row_b[r] -= lo;
     } else {
@@ -311,32 +321,39 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   }
   __syncthreads();
 
-  // ---- H: horizontal pass, one thread per (slot, output column)
+  // ---- H: horizontal pass; a thread owns one output column (its table entry
+  // decoded once) and walks the slots; short rows put several threads per column
   {
-    const int total = L.nslot * OW;
-    for (int idx = tid; idx < total; idx += kThreads) {
-      int j = P.ow_magic ? (int)fast_div((uint32_t)idx, P.ow_magic) : idx / OW;
-      int ox = idx - j * OW;
-      if (slot_row[j] < 0) continue;
-      const uint8_t* row = srcbuf + (size_t)j * L.span_pad + s_shift[j];
-      uint32_t e = xt[ox];
+    const int ncg = max(1, kThreads / OW);          // threads per column
+    for (int c0 = tid; c0 < OW * ncg; c0 += kThreads) {
+      const int j0 = P.ow_magic ? (int)fast_div((uint32_t)c0, P.ow_magic) : c0 / OW;
+      const int ox = c0 - j0 * OW;
+      const uint32_t e = xt[ox];
       if constexpr (kRes) {
-        uint32_t* hr = reinterpret_cast<uint32_t*>(hbuf + (size_t)j * L.hrow_pad) + ox * C;
-        int off0 = (int)(e & 0xFFFFu), wx = (int)((e >> 16) & 0xFFFu);
-        int off1 = (e >> 28) ? off0 : off0 + C;
-        uint32_t w0 = 2048u - (uint32_t)wx, w1 = (uint32_t)wx;
+        const int off0 = (int)(e & 0xFFFFu), wx = (int)((e >> 16) & 0xFFFu);
+        const int off1 = (e >> 28) ? off0 : off0 + C;
+        const uint32_t w0 = 2048u - (uint32_t)wx, w1 = (uint32_t)wx;
+        for (int j = j0; j < L.nslot; j += ncg) {
+          if (slot_row[j] < 0) continue;
+          const uint8_t* row = srcbuf + j * L.span_pad + s_shift[j];
+          uint32_t* hr = reinterpret_cast<uint32_t*>(hbuf + j * L.hrow_pad) + ox * C;
 #pragma unroll
-        for (int k = 0; k < (kC > 0 ? kC : 1); ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
-        if constexpr (kC == 0)
-          for (int k = 1; k < C; ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+          for (int k = 0; k < (kC > 0 ? kC : 1); ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+          if constexpr (kC == 0)
+            for (int k = 1; k < C; ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+        }
       } else {
-        uint8_t* hr = hbuf + (size_t)j * L.hrow_pad + ox * C;
         const bool pad = e == 0xFFFFFFFFu;
         const uint32_t eo = pad ? 0u : e;    // never form an out-of-window smem address
+        for (int j = j0; j < L.nslot; j += ncg) {
+          if (slot_row[j] < 0) continue;
+          const uint8_t* row = srcbuf + j * L.span_pad + s_shift[j];
+          uint8_t* hr = hbuf + j * L.hrow_pad + ox * C;
 #pragma unroll
-        for (int k = 0; k < (kC > 0 ? kC : 1); ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
-        if constexpr (kC == 0)
-          for (int k = 1; k < C; ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
+          for (int k = 0; k < (kC > 0 ? kC : 1); ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
+          if constexpr (kC == 0)
+            for (int k = 1; k < C; ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
+        }
       }
     }
   }
@@ -443,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
   dim3 grid(P.tiles_per_sample, A.count);
-  int smem = img_layout(P).total;
+  int smem = P.lay.total;
   auto k = image_kernel<OutT, kRes, kVal, kC, kVec>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k<<<grid, kThreads, smem, st>>>(P, A);
