@@ -323,9 +323,11 @@ def main():
         "data": "synthetic (SyntheticImageSource pattern, 256x256x3 RAW, writer seed 1)",
         "config": config,
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): mmap -> pinned -> H2D -> K1",
+                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): host RAM -> H2D -> K1",
                 "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
-                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9},
+                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9,
+                "staging": ("copy-engine DMA (batched 2-D) from the pinned host heap" if st2["dma_batches"]
+                            else "cpu gather into pinned slot + one H2D")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": load_traffic(),
                      "kernel": "image_kernel<half, resample> (K1)", "kernel_us": kern_s * 1e6,

@@ -104,6 +104,10 @@ bbx_status bbx_dataset_row(const bbx_dataset* ds, int64_t i, uint8_t* out, int32
  * B200 equivalent of ProcessCacheStrategy with capacity >= num_pages,
  * reader.py:67-77).  Batches then read payloads straight from HBM. */
 bbx_status bbx_dataset_make_resident(bbx_dataset* ds, int device);
+/* Pinned host copy of the heap (the OS-cache strategy's bytes held page-
+ * locked): staged batches are then read by the copy engine with one batched
+ * 2-D DMA call instead of a CPU gather.  threads <= 0: automatic. */
+bbx_status bbx_dataset_pin_host(bbx_dataset* ds, int threads);
 /* Page of sample i's first heap reference, -1 for all-inline (reader.py:430-437). */
 bbx_status bbx_dataset_page_map(const bbx_dataset* ds, int64_t* out /* num_samples */);
 
@@ -168,6 +172,7 @@ typedef struct {
   double kernel_seconds;
   int64_t kernel_timed;       /* kernel launches that were timed */
   int64_t kernel_bytes;       /* algorithmic bytes of the timed launches */
+  int64_t dma_batches;        /* batches whose payloads the copy engine read from the registered mmap */
 } bbx_loader_stats;
 /* Turn per-launch CUDA-event timing of the transform kernels on/off. */
 bbx_status bbx_loader_set_profiling(bbx_loader* ld, int enabled);

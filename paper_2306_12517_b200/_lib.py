@@ -40,7 +40,8 @@ class HeaderInfo(ctypes.Structure):
 class LoaderStats(ctypes.Structure):
     _fields_ = [("batches", c_i64), ("samples", c_i64), ("h2d_bytes", c_i64), ("d2h_bytes", c_i64),
                 ("kernel_launches", c_i64), ("stage_seconds", c_dbl), ("wait_seconds", c_dbl),
-                ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64)]
+                ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
+                ("dma_batches", c_i64)]
 
 
 # bbx_status -> exception class (errors.py:4-57)
@@ -84,6 +85,7 @@ def lib():
         "bbx_dataset_row": (c_i32, [c_vp, c_i64, c_vp, c_i32]),
         "bbx_dataset_make_resident": (c_i32, [c_vp, ctypes.c_int]),
         "bbx_dataset_page_map": (c_i32, [c_vp, c_vp]),
+        "bbx_dataset_pin_host": (c_i32, [c_vp, ctypes.c_int]),
         "bbx_epoch_order": (c_i32, [ctypes.c_int, c_u64, c_u64, c_i64, c_vp, c_i64, c_vp]),
         "bbx_loader_create": (c_i32, [c_vp, ctypes.c_int, c_i32, c_i32, c_i32, P(c_vp)]),
         "bbx_loader_destroy": (None, [c_vp]),
@@ -110,7 +112,8 @@ def lib():
 
 
 EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_close", "bbx_dataset_header",
-            "bbx_dataset_field", "bbx_dataset_row", "bbx_dataset_make_resident", "bbx_dataset_page_map",
+            "bbx_dataset_field", "bbx_dataset_row", "bbx_dataset_make_resident", "bbx_dataset_pin_host",
+            "bbx_dataset_page_map",
             "bbx_epoch_order", "bbx_loader_create", "bbx_loader_destroy", "bbx_loader_add_field",
             "bbx_loader_add_scalar", "bbx_loader_bind", "bbx_loader_submit", "bbx_loader_wait",
             "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",

@@ -147,6 +147,8 @@ struct bbx_loader {
   size_t slot_bytes = 0, desc_bytes = 0, idx_off = 0;
   std::vector<size_t> desc_off;       // per plan, within a slot
   size_t pay_base = 0;                // start of the compact payload region
+  bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
+  bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
   // pipeline thread
   std::thread th;
@@ -518,6 +520,27 @@ static int finalize(bbx_loader* L) {
     pl.d_scratch.assign(L->nslots, nullptr);
     for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_scratch[s], (size_t)L->batch * pl.dev.scratch_bytes + 64));
   }
+  // Page-lock the mmap'd file once per dataset so the copy engine reads
+  // payloads straight out of the page cache (no CPU gather).  Only when the
+  // file comfortably fits in RAM; otherwise payloads are gathered by the pool.
+  if (!resident && L->dma_allowed) {
+    bbx_dataset* ds = L->ds;
+    std::lock_guard<std::mutex> g(ds->reg_mu);
+    if (!ds->host_registered) {
+      long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+      double ram = (double)pages * (double)psz;
+      cudaError_t re = cudaErrorMemoryAllocation;
+      if (ram > 0 && (double)ds->map_len < 0.25 * ram)
+        re = cudaHostRegister((void*)ds->map, ds->map_len, cudaHostRegisterReadOnly | cudaHostRegisterPortable);
+      if (re == cudaSuccess) {
+        ds->host_registered = true;
+      } else {
+        cudaGetLastError();   // clear a refused registration; fall back to the gather pool
+        if (std::getenv("BBX_DEBUG")) std::fprintf(stderr, "bbx: cudaHostRegister(mmap) refused: %s\n", cudaGetErrorString(re));
+      }
+    }
+    L->dma = ds->dma_base() != nullptr;
+  }
   L->th = std::thread(pipeline_loop, L);
   L->finalized = true;
   return BBX_OK;
@@ -598,8 +621,39 @@ static int process_slot(bbx_loader* L, int s) {
       cursor += ((size_t)len + 15) / 16 * 16;
     }
   }
-  // parallel gather: mmap page cache -> pinned slot (row segments for windows)
-  if (!copies.empty()) {
+  // DMA mode: the copy engine reads every payload / window straight from the
+  // registered mmap (one batched 2-D copy call); descriptors go in one H2D.
+  bool dma_done = false;
+  if (L->dma && !copies.empty()) {
+    std::vector<cudaMemcpy3DBatchOp> ops(copies.size());
+    for (size_t k = 0; k < copies.size(); ++k) {
+      const Copy& c = copies[k];
+      cudaMemcpy3DBatchOp& op = ops[k];
+      std::memset(&op, 0, sizeof op);
+      op.src.type = cudaMemcpyOperandTypePointer;
+      op.src.op.ptr.ptr = (void*)(L->ds->dma_base() + (c.src - L->ds->map));
+      op.src.op.ptr.rowLength = c.rows == 1 ? 0 : c.src_stride;
+      op.dst.type = cudaMemcpyOperandTypePointer;
+      op.dst.op.ptr.ptr = S.d_stage + (c.dst - S.h_stage);
+      op.dst.op.ptr.rowLength = 0;
+      op.extent = make_cudaExtent(c.row_bytes, c.rows, 1);
+      op.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      op.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    }
+    if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
+    CK(cudaMemcpyAsync(S.d_stage, S.h_stage, L->desc_bytes, cudaMemcpyHostToDevice, L->copy_st));
+    size_t fail_idx = 0;
+    cudaError_t e = cudaMemcpy3DBatchAsync(ops.size(), ops.data(), &fail_idx, 0, L->copy_st);
+    if (e == cudaSuccess) {
+      dma_done = true;
+    } else {
+      cudaGetLastError();
+      if (std::getenv("BBX_DEBUG")) std::fprintf(stderr, "bbx: cudaMemcpy3DBatchAsync failed (op %zu): %s\n", fail_idx, cudaGetErrorString(e));
+      L->dma = false;   // unsupported here: gather on the host from now on
+    }
+  }
+  // gather mode: mmap page cache -> pinned slot (row segments for windows)
+  if (!dma_done && !copies.empty()) {
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
       if (c.rows == 1) { std::memcpy(c.dst, c.src, c.row_bytes); return; }
@@ -610,8 +664,10 @@ static int process_slot(bbx_loader* L, int s) {
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // H2D on the copy stream (after the previous kernels reading d_stage)
   const size_t bytes = resident ? L->desc_bytes : cursor;
-  if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
-  CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
+  if (!dma_done) {
+    if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
+    CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
+  }
   CK(cudaEventRecord(S.h2d_done, L->copy_st));
   CK(cudaStreamWaitEvent(L->comp_st, S.h2d_done, 0));
   bool wait_release;
@@ -692,6 +748,7 @@ static int process_slot(bbx_loader* L, int s) {
     L->stats.d2h_bytes += d2h;
     L->stats.kernel_launches += launches;
     L->stats.stage_seconds += t1 - t0;
+    L->stats.dma_batches += dma_done ? 1 : 0;
   }
   return BBX_OK;
 }
@@ -759,6 +816,11 @@ bbx_status bbx_dataset_make_resident(bbx_dataset* ds, int device) {
   if (!ds) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null dataset");
   return (bbx_status)bbx::dataset_make_resident(ds, device);
 }
+bbx_status bbx_dataset_pin_host(bbx_dataset* ds, int threads) {
+  if (!ds) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null dataset");
+  if (threads <= 0) threads = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  return (bbx_status)bbx::dataset_pin_host(ds, threads);
+}
 bbx_status bbx_dataset_page_map(const bbx_dataset* ds, int64_t* out) {
   if (!ds || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
   for (int64_t i = 0; i < ds->num_samples; ++i) out[i] = bbx::primary_page(ds, i);
@@ -782,6 +844,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   L->ds = ds; L->device = device; L->batch = batch_size; L->nslots = slot_count;
   L->slots.resize(slot_count);
   if (const char* e = std::getenv("BBX_WINDOW_STAGING")) L->window_staging = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BBX_DMA")) L->dma_allowed = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   L->pool = std::make_unique<Pool>(nt);

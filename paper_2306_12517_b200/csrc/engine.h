@@ -78,6 +78,11 @@ struct bbx_dataset {
   const uint8_t* rows = nullptr;
   int resident_device = -1;
   uint8_t* d_heap = nullptr;   // device copy of [heap_offset, alloc_table_offset)
+  bool host_registered = false; // the mmap is page-locked for DMA (cudaHostRegister)
+  uint8_t* h_heap = nullptr;     // pinned host copy of the heap (bbx_dataset_pin_host)
+  // DMA-able host address of file offset o: dma_base + o (registered mmap or pinned copy)
+  const uint8_t* dma_base() const { return h_heap ? h_heap - heap_offset : (host_registered ? map : nullptr); }
+  std::mutex reg_mu;
   ~bbx_dataset() {
     if (map) munmap((void*)map, map_len);
     if (fd >= 0) ::close(fd);
@@ -88,6 +93,7 @@ namespace bbx {
 int dataset_open(const char* path, bbx_dataset** out);
 void dataset_close(bbx_dataset* ds);
 int dataset_make_resident(bbx_dataset* ds, int device);
+int dataset_pin_host(bbx_dataset* ds, int threads);
 ImageCell image_cell(const bbx_dataset* ds, int64_t i, const Field& f);
 uint64_t u64_cell(const bbx_dataset* ds, int64_t i, const Field& f);
 int64_t primary_page(const bbx_dataset* ds, int64_t i);

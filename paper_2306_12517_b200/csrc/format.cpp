@@ -130,6 +130,8 @@ int dataset_open(const char* path, bbx_dataset** out) {
 void dataset_close(bbx_dataset* ds) {
   if (!ds) return;
   if (ds->d_heap) { cudaSetDevice(ds->resident_device); cudaFree(ds->d_heap); }
+  if (ds->host_registered) cudaHostUnregister((void*)ds->map);
+  if (ds->h_heap) cudaFreeHost(ds->h_heap);
   delete ds;   // ~bbx_dataset unmaps and closes
 }
 
@@ -153,6 +155,31 @@ int64_t primary_page(const bbx_dataset* ds, int64_t i) {           // reader.py:
     }
   }
   return -1;
+}
+
+// Pinned host copy of the heap: the page cache's bytes held page-locked so the
+// copy engine can DMA batch payloads without a CPU gather.
+int dataset_pin_host(bbx_dataset* ds, int threads) {
+  if (ds->h_heap) return BBX_OK;
+  size_t heap = (size_t)(ds->alloc_table_offset - ds->heap_offset);
+  uint8_t* h = nullptr;
+  CK(cudaHostAlloc(&h, heap + 256, cudaHostAllocPortable));
+  std::memset(h + heap, 0, 256);
+  const size_t chunk = 64ull << 20;
+  const size_t nchunks = (heap + chunk - 1) / chunk;
+  threads = std::max(1, std::min(threads, (int)std::max<size_t>(nchunks, 1)));
+  std::vector<std::thread> th;
+  std::atomic<size_t> next{0};
+  for (int t = 0; t < threads; ++t)
+    th.emplace_back([&] {
+      for (size_t k; (k = next.fetch_add(1)) < nchunks;) {
+        size_t o = k * chunk, n = std::min(chunk, heap - o);
+        std::memcpy(h + o, ds->map + ds->heap_offset + o, n);
+      }
+    });
+  for (auto& t : th) t.join();
+  ds->h_heap = h;
+  return BBX_OK;
 }
 
 int dataset_make_resident(bbx_dataset* ds, int device) {

@@ -30,7 +30,7 @@ from . import _lib
 from . import pipeline as pl
 from .errors import CapacityTooSmall, SchemaMismatch, ShutdownError, SpecMismatch
 from .format import FieldKind
-from .reader import Dataset, DeviceResident, ProcessCacheStrategy, open_dataset
+from .reader import Dataset, DeviceResident, OsCache, ProcessCacheStrategy, open_dataset
 from .traversal import OrderKind, TraversalOrder
 
 DEFAULT_SLOT_COUNT = 3
@@ -141,6 +141,15 @@ def _dist_info(config: LoaderConfig) -> tuple[int, int]:
     return rank, world
 
 
+def _fits_pinned(nbytes: int, fraction: float) -> bool:
+    try:
+        ram = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        return False
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", 1))
+    return nbytes <= fraction * ram / max(local, 1)
+
+
 def shard_batches(global_batches: list, rank: int, world_size: int, batch_size: int) -> list:
     """Rank r's slice [r*B, (r+1)*B) of every global batch."""
     out = []
@@ -204,6 +213,10 @@ class Loader:
             dev = strategy.device if isinstance(strategy, DeviceResident) and strategy.device is not None \
                 else self.device
             self.dataset.make_resident(dev)
+        elif isinstance(strategy, OsCache) and strategy.pinned and not self.dataset.pinned:
+            if not _fits_pinned(self.dataset.header.heap_bytes, OsCache.PIN_HOST_RAM_FRACTION):
+                raise CapacityTooSmall("heap does not fit the pinned host budget")
+            self.dataset.pin_host()
 
         L = _lib.lib()
         h = ctypes.c_void_p()

@@ -4,7 +4,8 @@
 the device loader stages payloads from, plus a Python mmap for metadata
 (rows, scalar columns, random-access reads).  Strategies:
 
-* OsCache()                    page-cache mmap (default; reference OsCache)
+* OsCache(pinned=None)         page-cache mmap (default; reference OsCache);
+                               small heaps are also held pinned for DMA
 * Direct(read_latency_s)       accepted for API compatibility; staging reads
                                the same mmap (latency injection is a CPU-
                                benchmark device of the reference)
@@ -33,7 +34,19 @@ from .writer import read_header
 
 
 class OsCache:
-    """mmap the file; the OS page cache serves repeated reads."""
+    """mmap the file; the OS page cache serves repeated reads.
+
+    pinned: hold the heap page-locked in host RAM so the copy engine DMAs each
+    batch's payloads directly (one batched 2-D copy call, no CPU gather).
+    Measured on B200 (profiles/): the pooled CPU gather + one contiguous H2D
+    is faster for windowed RAW batches (460k vs 163k img/s), so the default
+    (None/False) gathers; True opts in (e.g. when host cores are scarce).
+    """
+
+    PIN_HOST_RAM_FRACTION = 0.2
+
+    def __init__(self, pinned: bool | None = None):
+        self.pinned = pinned
 
 
 @dataclass
@@ -104,6 +117,18 @@ class Dataset:
         _lib.check(_lib.lib().bbx_dataset_make_resident(self.handle, device))
         self._resident_device = device
         self.tracked_bytes = len(self._rows) + self.header.heap_bytes
+
+    def pin_host(self) -> None:
+        """Hold the heap page-locked in host RAM (DMA source for staged batches)."""
+        if getattr(self, "_pinned", False):
+            return
+        _lib.check(_lib.lib().bbx_dataset_pin_host(self.handle, 0))
+        self._pinned = True
+        self.tracked_bytes += self.header.heap_bytes
+
+    @property
+    def pinned(self) -> bool:
+        return getattr(self, "_pinned", False)
 
     @property
     def resident_device(self):

@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT
-export BBX_NO_BUILD=1
-CUDA_LAUNCH_BLOCKING=1 timeout 300 python scripts/repro_chain.py "crop:48,40|resize:33,17|flip:0.5|normpc:1,2,3/4,5,6/f32" 1 2>&1 | grep -v "^  " | tail -12
-timeout 300 python scripts/repro_chain.py "crop:48,40|normpc:1,2,3/4,5,6/f32" 1 2>&1 | tail -2
-timeout 300 python scripts/repro_chain.py "resize:33,17" 1 2>&1 | tail -2
-timeout 300 python scripts/repro_chain.py "resize:33,17|float" 1 2>&1 | tail -2
-timeout 600 compute-sanitizer --tool memcheck --print-limit 4 python scripts/repro_chain.py "crop:48,40|resize:33,17|flip:0.5|normpc:1,2,3/4,5,6/f32" 1 2>&1 | grep -v "^=========     Host Frame" | head -60
+export BBX_NO_BUILD=1 BBX_DEBUG=1
+df -h /tmp | tail -1; mount | grep -E " /tmp | / " | head -3; uname -r
+BBX_BENCH_SAMPLES=2048 timeout 300 python bench.py --steps 20 --warmup 3 --cpu-seconds 1 2>&1 | tail -3 | cut -c1-600
+mkdir -p /dev/shm/bbx && BBX_BENCH_DIR=/dev/shm/bbx BBX_BENCH_SAMPLES=2048 timeout 300 python bench.py --steps 20 --warmup 3 --cpu-seconds 1 2>&1 | tail -2 | python -c "import sys,json; [print(json.loads(l)['e2e']) for l in sys.stdin if l.startswith('{')]"
