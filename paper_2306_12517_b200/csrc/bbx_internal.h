@@ -10,7 +10,7 @@ namespace bbx {
 
 enum SrcKind : int32_t { SRC_DECODE = 0, SRC_RESAMPLE = 1, SRC_ARRAY = 2 };
 enum Codec : int32_t { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2 };
-enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_FMA1 = 3 };
+enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_LUT = 3 };
 
 constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
@@ -64,6 +64,8 @@ struct PlanDev {
   int32_t lin32;                           // bilinear axis math fits 32-bit
   uint32_t ow_magic, gpr_magic;            // ceil(2^32/d) fast-division constants, 0 = use /
   uint32_t linx_magic, liny_magic;         // for 2*canvas_w / 2*canvas_h (bilinear axes), 0 = use /
+  int32_t h_tpc;                           // horizontal pass: threads per output column
+  int32_t tab_stride;                      // K1 prologue table words per sample
   SmemLayout lay;
 };
 
@@ -92,7 +94,8 @@ struct LaunchArgs {
   const uint8_t* payload;    // payload base (device): staged region or file image in HBM
   uint8_t* scratch;          // count * scratch_bytes (device)
   void* out;                 // count * out_sample_elems elements
-  const void* unused;
+  const void* lut;           // VAL_LUT: channels x 256 output values (exact, host-built)
+  uint32_t* tables;          // K1 prologue tables: count x tab_stride u32
   SampleStatus* status;      // count entries
   int32_t count;
 };
@@ -112,5 +115,6 @@ int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream);
 int launch_scalar_gather(const ScalarArgs& S, void* stream);
 int image_smem_bytes(const PlanDev& P);
 SmemLayout img_layout_host(const PlanDev& P);
+int image_tab_stride(const PlanDev& P);
 
 }  // namespace bbx

@@ -85,6 +85,30 @@ void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
 static int dtype_size(int dt) {
   switch (dt) { case BBX_U8: return 1; case BBX_I64: case BBX_F64: return 8; case BBX_F32: return 4; default: return 2; }
 }
+static uint16_t f32_to_bf16_bits(float f) {      // round to nearest even
+  uint32_t u; std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+static uint16_t f32_to_f16_bits(float f) {       // IEEE binary16, round to nearest even
+  uint32_t x; std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u, ax = x & 0x7fffffffu;
+  if (ax >= 0x7f800000u) return (uint16_t)(sign | (ax > 0x7f800000u ? 0x7e00u : 0x7c00u));
+  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);            // rounds to inf
+  if (ax < 0x38800000u) {                                                // half subnormal
+    if (ax < 0x33000000u) return (uint16_t)sign;                         // <= 2^-25 ties to 0
+    uint32_t mant = (ax & 0x7fffffu) | 0x800000u;
+    int shift = 126 - (int)(ax >> 23) + 14;
+    uint32_t q = mant >> shift, rem = mant & ((1u << shift) - 1), half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (q & 1u))) ++q;
+    return (uint16_t)(sign | q);
+  }
+  uint32_t r = ax - 0x38000000u, q = r >> 13, rem = r & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (q & 1u))) ++q;
+  return (uint16_t)(sign | q);
+}
+
 struct Draw {        // one RNG-consuming op, in chain order (host program)
   int kind;          // BBX_OP_RRC / BBX_OP_CENTERCROP / BBX_OP_CROP / BBX_OP_FLIP
   int slot;          // first param slot
@@ -104,6 +128,7 @@ struct Plan {
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
+  std::vector<uint32_t*> d_tables;   // per slot: K1 prologue tables
   uint64_t* d_col = nullptr;     // scalar column (num_samples x 8 B)
 };
 
@@ -312,16 +337,19 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       for (int k = 0; k < 4; ++k) { P.vop_mean[0][k] = 0.f; P.vop_std[0][k] = 1.f; P.vop_inv[0][k] = 1.f; }
       P.n_vops = 1;
     }
+    // C <= 4: the whole value chain u8 -> output is a 256-entry table per
+    // channel, built on the host with the reference's exact arithmetic.
     P.value_mode = !has_values ? VAL_COPY
-                 : !verify_fma_normalize(P, C) ? VAL_DIRECT
-                 : (P.n_vops == 1 ? VAL_FMA1 : VAL_FMA);
+                 : C <= 4 ? VAL_LUT
+                 : verify_fma_normalize(P, C) ? VAL_FMA : VAL_DIRECT;
     if (P.value_mode == VAL_COPY && out_dt != BBX_U8) return fail(BBX_SPEC_MISMATCH, "unexpected output dtype");
     // tile height: 16 rows, shrunk until the smem layout allows 4 CTAs per SM
     P.rows_per_tile = std::min(16, H);
+    if (const char* e = std::getenv("BBX_ROWS_PER_TILE")) P.rows_per_tile = std::max(1, std::min({std::atoi(e), H, 16}));
     for (;;) {
       P.lay = img_layout_host(P);
       P.smem_bytes = P.lay.total;
-      if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1) break;
+      if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1 || std::getenv("BBX_ROWS_PER_TILE")) break;
       P.rows_per_tile = std::max(1, P.rows_per_tile / 2);
     }
     if (P.smem_bytes > kSmemBudget || (int64_t)P.src_row_w * C + 64 > 65535)
@@ -345,6 +373,26 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       if (magic_ok(dy, f.info.max_height)) P.liny_magic = (uint32_t)((two32 + dy - 1) / dy);
     }
     P.lay = img_layout_host(P);
+    P.h_tpc = std::max(1, kThreads / W);
+    P.tab_stride = image_tab_stride(P);
+    if ((W + 3 * H) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "output too large for the device plan");
+  }
+  if (P.value_mode == VAL_LUT) {   // exact u8 -> output table (pipeline.py:158-160 arithmetic)
+    const int osz = dtype_size(out_dt);
+    std::vector<uint8_t> lut((size_t)C * 256 * osz);
+    for (int k = 0; k < C; ++k)
+      for (int v = 0; v < 256; ++v) {
+        float x = (float)v;
+        for (int i = 0; i < P.n_vops; ++i) {
+          volatile float t = x - P.vop_mean[i][k];
+          x = t / P.vop_std[i][k];
+        }
+        uint8_t* at = &lut[((size_t)k * 256 + v) * osz];
+        if (out_dt == BBX_F32) std::memcpy(at, &x, 4);
+        else { uint16_t b = out_dt == BBX_F16 ? f32_to_f16_bits(x) : f32_to_bf16_bits(x); std::memcpy(at, &b, 2); }
+      }
+    CK(cudaMalloc(&pl.d_lut, lut.size()));
+    CK(cudaMemcpy(pl.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
   }
   // one pass over the row table: exact staging capacity, RLE presence
   int64_t mx = 0;
@@ -514,6 +562,11 @@ static int finalize(bbx_loader* L) {
     CK(cudaEventCreateWithFlags(&S.release, cudaEventDisableTiming));
     CK(cudaEventCreate(&S.k0));
     CK(cudaEventCreate(&S.k1));
+  }
+  for (auto& pl : L->plans) {
+    if (pl.scalar || pl.dev.src_kind == SRC_ARRAY) continue;
+    pl.d_tables.assign(L->nslots, nullptr);
+    for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_tables[s], (size_t)L->batch * pl.dev.tab_stride * 4 + 64));
   }
   for (auto& pl : L->plans) {
     if (pl.scalar || !pl.field_has_rle) continue;
@@ -699,6 +752,8 @@ static int process_slot(bbx_loader* L, int s) {
     A.desc = S.d_stage + L->desc_off[p];
     A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
     A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
+    A.tables = pl.d_tables.empty() ? nullptr : pl.d_tables[s];
+    A.lut = pl.d_lut;
     A.out = pl.outs[s];
     A.status = S.d_status + (size_t)p * L->batch;
     A.count = count;
@@ -723,7 +778,7 @@ static int process_slot(bbx_loader* L, int s) {
       }
     }
     if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    ++launches;
+    launches += pl.dev.src_kind == SRC_ARRAY ? 1 : 2;   // K1 = prologue + tile kernel
   }
   if (prof) CK(cudaEventRecord(S.k1, L->comp_st));
   S.timed = prof;
@@ -1045,6 +1100,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (pl.d_lut) cudaFree(pl.d_lut);
     if (pl.d_col) cudaFree(pl.d_col);
     for (auto* p : pl.d_scratch) if (p) cudaFree(p);
+    for (auto* p : pl.d_tables) if (p) cudaFree(p);
   }
   if (L->copy_st) cudaStreamDestroy(L->copy_st);
   if (L->comp_st) cudaStreamDestroy(L->comp_st);
@@ -1097,13 +1153,18 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
   }
   if (P.smem_bytes > kSmemBudget || (int64_t)w * c + 64 > 65535) return fail(BBX_SPEC_MISMATCH, "image too wide");
   P.tiles_per_sample = (h + P.rows_per_tile - 1) / P.rows_per_tile;
+  P.h_tpc = std::max(1, kThreads / w);
+  P.tab_stride = image_tab_stride(P);
   P.scratch_bytes = (n + 15) / 16 * 16;
   P.out_sample_elems = n;
+  if ((w + 3 * h) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "image too large");
   size_t dbytes = 64 + (size_t)((len + 15) / 16 * 16) + 64;
   uint8_t* d_buf = nullptr;
   uint8_t* d_scr = nullptr;
+  uint32_t* d_tab = nullptr;
   SampleStatus* d_st = nullptr;
   CK(cudaMalloc(&d_buf, dbytes));
+  CK(cudaMalloc(&d_tab, (size_t)P.tab_stride * 4 + 64));
   std::vector<uint8_t> hb(64, 0);
   SampleDesc* d = reinterpret_cast<SampleDesc*>(hb.data());
   d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = (uint8_t)codec;
@@ -1112,7 +1173,7 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
   cudaMalloc(&d_st, sizeof(SampleStatus));
   cudaMemset(d_st, 0, sizeof(SampleStatus));
   LaunchArgs A{};
-  A.desc = d_buf; A.payload = d_buf + 64; A.out = out_dev; A.status = d_st; A.count = 1;
+  A.desc = d_buf; A.payload = d_buf + 64; A.out = out_dev; A.status = d_st; A.count = 1; A.tables = d_tab;
   int rc = 0;
   if (codec == CODEC_RLE) {
     cudaMalloc(&d_scr, P.scratch_bytes + 64);
@@ -1122,7 +1183,7 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
   rc |= launch_image(P, A, nullptr);
   SampleStatus st{};
   cudaError_t e = cudaMemcpy(&st, d_st, sizeof st, cudaMemcpyDeviceToHost);
-  cudaFree(d_buf); cudaFree(d_st); if (d_scr) cudaFree(d_scr);
+  cudaFree(d_buf); cudaFree(d_st); cudaFree(d_tab); if (d_scr) cudaFree(d_scr);
   if (rc || e != cudaSuccess) return fail(BBX_CUDA_ERROR, "decode failed: %s", cudaGetErrorString(e));
   if (st.kind == 1) return fail(BBX_CORRUPT_PAYLOAD, "rle runs sum past %lld bytes", (long long)n);
   if (st.kind == 2) return fail(BBX_CORRUPT_PAYLOAD, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);

@@ -122,35 +122,18 @@ template <> __device__ __forceinline__ __half cvt_out<__half>(float v) { return 
 template <> __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 template <> __device__ __forceinline__ uint8_t cvt_out<uint8_t>(float v) { return (uint8_t)v; }
 
-// Per-thread copy of a single normalize op's constants (VAL_FMA1), so the
-// element loop reads registers, not the constant bank.
-template <int kC>
-struct NormRegs {
-  float m[kC > 0 ? kC : 1], inv[kC > 0 ? kC : 1], s[kC > 0 ? kC : 1];
-  __device__ __forceinline__ void load(const PlanDev& P) {
-#pragma unroll
-    for (int k = 0; k < (kC > 0 ? kC : 1); ++k) {
-      m[k] = P.vop_mean[0][k & 3]; inv[k] = P.vop_inv[0][k & 3]; s[k] = P.vop_std[0][k & 3];
-    }
-  }
-};
-
-template <typename OutT, int kVal, int kC>
-__device__ __forceinline__ OutT value_of(const PlanDev& P, const NormRegs<kC>& N, uint32_t b, int k) {
-  if constexpr (kVal == VAL_COPY) {
-    return (OutT)b;
-  } else if constexpr (kVal == VAL_FMA1 && kC > 0) {
-    float d = __fsub_rn((float)b, N.m[k]);
-    float q0 = __fmul_rn(d, N.inv[k]);
-    float r = __fmaf_rn(-q0, N.s[k], d);
-    return cvt_out<OutT>(__fmaf_rn(r, N.inv[k], q0));
-  } else {   // VAL_GENERIC: several normalize ops (or C not specialised)
-    return cvt_out<OutT>(P.value_mode == VAL_DIRECT ? apply_vops(P, (float)b, k) : apply_vops_fma(P, (float)b, k));
-  }
+template <typename OutT, int kVal>
+__device__ __forceinline__ OutT value_generic(const PlanDev& P, uint32_t b, int k) {
+  if constexpr (kVal == VAL_COPY) return (OutT)b;
+  else return cvt_out<OutT>(P.value_mode == VAL_DIRECT ? apply_vops(P, (float)b, k) : apply_vops_fma(P, (float)b, k));
 }
 
 // Shared-memory layout of the image kernel (host + device).
 __host__ __device__ inline int align_up(int v, int a) { return (v + a - 1) / a * a; }
+
+__host__ __device__ inline int out_size(const PlanDev& P) {
+  return P.out_dtype == BBX_U8 ? 1 : (P.out_dtype == BBX_F32 ? 4 : 2);
+}
 
 __host__ __device__ inline SmemLayout img_layout(const PlanDev& P) {
   SmemLayout L;
@@ -161,25 +144,163 @@ __host__ __device__ inline SmemLayout img_layout(const PlanDev& P) {
   L.hrow_pad = align_up(P.out_w * P.channels * (res ? 4 : 1), 16) + 16;
   L.xt_off = 0;
   L.meta_off = align_up(P.out_w * 4, 16);
-  // meta: slot_row[nslot], row_a[R], row_b[R], row_wy[R] (int32)
-  L.src_off = L.meta_off + align_up((L.nslot + 3 * R) * 4 + 16, 16);
+  // meta: slot_row[nslot], shift[nslot], row_a[R], row_b[R], row_wy[R] (int32)
+  const int lut = P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
+  L.src_off = L.meta_off + align_up((2 * L.nslot + 3 * R) * 4, 16) + lut;
   L.h_off = L.src_off + L.nslot * L.span_pad;
   L.total = L.h_off + L.nslot * L.hrow_pad;
   return L;
 }
+__host__ __device__ inline int lut_off(const PlanDev& P) {
+  return P.lay.meta_off + align_up((2 * P.lay.nslot + 3 * P.rows_per_tile) * 4, 16);
+}
 
+// Per-sample tables written by the prologue (u32 words, tab_stride per sample):
+//   [0] col_lo  [1] col_hi  [2..3] pad
+//   [4 .. 4+OWp)          column table xt (encoded, see below)
+//   per tile t (TM words): nvalid, slot_row[nslot], row_a[R], row_b[R], row_wy[R]
+__host__ __device__ inline int tab_owp(const PlanDev& P) { return align_up(P.out_w, 4); }
+__host__ __device__ inline int tab_tm(const PlanDev& P) {
+  const int nslot = P.rows_per_tile * (P.src_kind == SRC_RESAMPLE ? 2 : 1);
+  return align_up(1 + nslot + 3 * P.rows_per_tile, 4);
+}
+__host__ __device__ inline int tab_stride(const PlanDev& P) { return 4 + tab_owp(P) + P.tiles_per_sample * tab_tm(P); }
+
+// Source-row addressing of one sample (codec / staging dependent).
+struct SrcRows {
+  const uint8_t* base;
+  int64_t rstride;
+  int sh, rows;
+};
+__device__ __forceinline__ SrcRows src_rows_of(const PlanDev& P, const LaunchArgs& A, const SampleDesc* d, int s) {
+  SrcRows S;
+  const int C = P.channels, w = d->w, h = d->h;
+  if (d->codec == CODEC_RLE) {
+    S.base = A.scratch + (size_t)s * P.scratch_bytes; S.sh = 0; S.rstride = (int64_t)w * C;
+  } else if (d->flags & kDescWindowed) {
+    // only the rows/columns the chain reads were staged: a virtual origin makes
+    // every in-window image coordinate address its staged byte
+    S.rstride = d->wstride; S.sh = 0;
+    S.base = A.payload + d->src - (int64_t)d->wy0 * S.rstride - (int64_t)d->wx0 * C;
+  } else {
+    S.base = A.payload + d->src; S.sh = d->codec == CODEC_SUB2 ? 1 : 0;
+    S.rstride = (int64_t)(S.sh ? (w + 1) >> 1 : w) * C;
+  }
+  S.rows = S.sh ? (h + 1) >> 1 : h;
+  return S;
+}
+
+// --------------------------------------------------------------- K1 prologue
+// One CTA per sample: the remap/resample geometry that every tile of the
+// sample shares -- the encoded column table and, per tile, the source-row
+// slots -- computed once instead of once per tile.
+//   xt (bilinear): byte offset of tap 0 (16 b) | 11-bit weight of tap 1 << 16 | same-column bit << 28
+//   xt (nearest):  byte offset, or 0xFFFFFFFF for a zero-padding column
+template <bool kRes>
+__global__ void __launch_bounds__(kThreads) sample_tables_kernel(const PlanDev P, const LaunchArgs A) {
+  const int s = blockIdx.x;
+  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+  if (d->skip) return;
+  const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
+  const int OW = P.out_w, OH = P.out_h, C = P.channels, h = d->h, w = d->w, tid = threadIdx.x;
+  const SrcRows S = src_rows_of(P, A, d, s);
+  const int sh = S.sh;
+  extern __shared__ __align__(16) int tsm[];
+  int* xraw = tsm;                      // OW
+  int* ya = xraw + OW;                  // OH each
+  int* yb = ya + OH;
+  int* wyv = yb + OH;
+  __shared__ int s_clo, s_chi;
+  uint32_t* T = A.tables + (size_t)s * P.tab_stride;
+  const int top = kRes ? prm[0] : 0, left = kRes ? prm[1] : 0, ch = kRes ? prm[2] : 0, cw = kRes ? prm[3] : 0;
+  for (int ox = tid; ox < OW; ox += kThreads) xraw[ox] = back_x(P, prm, ox);
+  for (int r = tid; r < OH; r += kThreads) {
+    if constexpr (kRes) {
+      int cy = back_y(P, prm, r), y0, y1, wy;
+      lin_axis(cy, P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
+      ya[r] = (top + y0) >> sh; yb[r] = (top + y1) >> sh; wyv[r] = wy;
+    } else {
+      int cy = back_y(P, prm, r);
+      ya[r] = cy < h ? (cy >> sh) : -1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {   // the composed maps are monotone: the end columns span the range
+    int xa = xraw[0], xb = xraw[OW - 1], clo, chi;
+    if constexpr (kRes) {
+      int a0, a1, aw, b0, b1, bw;
+      lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, a0, a1, aw);
+      lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, b0, b1, bw);
+      clo = (left + a0) >> sh; chi = (left + b1) >> sh;
+    } else {
+      clo = min(xa, xb) >> sh; chi = min(max(xa, xb), w - 1) >> sh;   // clo > chi: all padding
+    }
+    s_clo = clo; s_chi = chi;
+    T[0] = (uint32_t)clo; T[1] = (uint32_t)chi;
+  }
+  __syncthreads();
+  const int col_lo = s_clo;
+  uint32_t* xt = T + 4;
+  for (int ox = tid; ox < OW; ox += kThreads) {
+    const int cx = xraw[ox];
+    if constexpr (kRes) {
+      int x0, x1, wx;
+      lin_axis(cx, P.canvas_w, cw, P.lin32, P.linx_magic, x0, x1, wx);
+      int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
+      xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+    } else {
+      xt[ox] = cx < w ? (uint32_t)(((cx >> sh) - col_lo) * C) : 0xFFFFFFFFu;
+    }
+  }
+  // per tile: contiguous source-row range -> slots when it fits, else one
+  // slot per (output row, tap)
+  const int Rt = P.rows_per_tile, nslot = kRes ? 2 * Rt : Rt, TM = tab_tm(P);
+  for (int t = tid; t < P.tiles_per_sample; t += kThreads) {
+    uint32_t* M = T + 4 + tab_owp(P) + (size_t)t * TM;
+    int* slot = reinterpret_cast<int*>(M + 1);
+    int* ra = slot + nslot;
+    int* rb = ra + Rt;
+    int* rw = rb + Rt;
+    const int r0 = t * Rt, R = min(Rt, OH - r0);
+    int lo = ya[r0], hi = kRes ? yb[r0 + R - 1] : ya[r0 + R - 1];
+    if (!kRes && lo < 0) { lo = hi = -1; }
+    if (!kRes && hi < 0) {
+      hi = -1;
+      for (int r = R - 1; r >= 0; --r) if (ya[r0 + r] >= 0) { hi = ya[r0 + r]; break; }
+    }
+    const bool contiguous = lo >= 0 && hi >= lo && hi - lo + 1 <= nslot;
+    if (contiguous) {
+      M[0] = (uint32_t)(hi - lo + 1);
+      for (int j = 0; j < nslot; ++j) slot[j] = (lo + j <= hi && lo + j < S.rows) ? lo + j : -1;
+      for (int r = 0; r < R; ++r) {
+        ra[r] = ya[r0 + r] >= 0 ? ya[r0 + r] - lo : -1;
+        if constexpr (kRes) { rb[r] = yb[r0 + r] - lo; rw[r] = wyv[r0 + r]; }
+      }
+    } else {
+      M[0] = (uint32_t)nslot;
+      for (int j = 0; j < nslot; ++j) slot[j] = -1;
+      for (int r = 0; r < R; ++r) {
+        if constexpr (kRes) {
+          slot[2 * r] = ya[r0 + r]; slot[2 * r + 1] = yb[r0 + r];
+          ra[r] = 2 * r; rb[r] = 2 * r + 1; rw[r] = wyv[r0 + r];
+        } else {
+          slot[r] = ya[r0 + r];
+          ra[r] = ya[r0 + r] >= 0 ? r : -1;
+        }
+      }
+    }
+  }
+}
 
 // --------------------------------------------------------------------- K1
 // grid = (tiles_per_sample, count); CTA = 256 threads; a tile = R output rows.
 //
-//  A. per output column: source byte offset (nearest) or (offset, 11-bit
-//     weight) (bilinear) through the composed remaps -> xt[ow];
-//     per output row: source row slot(s) -> meta.  Rows are deduplicated by
-//     mapping the contiguous source-row range of the tile onto slots.
+//  A. the tile's slice of the prologue tables -> smem (column table, row
+//     slots) and, for normalize chains, the exact u8 -> output LUT.
 //  B. every needed source row segment -> smem, 16-byte vector loads.
 //  H. horizontal pass, once per staged row: u8 (nearest) or the 2-tap
 //     fixed-point sum (bilinear, u32) for every output column and channel.
-//  V. vertical pass / value ops / store: each thread owns one group of
+//  V. vertical pass + value LUT + store: each thread owns one group of
 //     kC x 16 B of output (V pixels), so the channel of every element is a
 //     compile-time constant; 16-byte coalesced NHWC stores.
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
@@ -187,129 +308,52 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   constexpr int V = kVec ? (16 / (int)sizeof(OutT)) : 1;
   const int s = blockIdx.y;
   const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-  const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
   if (d->skip) return;
   const int C = kC > 0 ? kC : P.channels;
-  const int r0 = blockIdx.x * P.rows_per_tile;
+  const int tile = blockIdx.x;
+  const int r0 = tile * P.rows_per_tile;
   const int R = min(P.rows_per_tile, P.out_h - r0);
   if (R <= 0) return;
   const int OW = P.out_w;
   const int rowlen = OW * C;
-  const int h = d->h, w = d->w;
   const int tid = threadIdx.x;
-
-  const uint8_t* base;
-  int sh;
-  int64_t rstride;
-  if (d->codec == CODEC_RLE) {
-    base = A.scratch + (size_t)s * P.scratch_bytes; sh = 0; rstride = (int64_t)w * C;
-  } else if (d->flags & kDescWindowed) {
-    // only the rows/columns the chain reads were staged: a virtual origin makes
-    // every in-window image coordinate address its staged byte
-    rstride = d->wstride; sh = 0;
-    base = A.payload + d->src - (int64_t)d->wy0 * rstride - (int64_t)d->wx0 * C;
-  } else {
-    base = A.payload + d->src; sh = d->codec == CODEC_SUB2 ? 1 : 0;
-    rstride = (int64_t)(sh ? (w + 1) >> 1 : w) * C;
-  }
-  const int src_rows = sh ? (h + 1) >> 1 : h;
+  const SrcRows S = src_rows_of(P, A, d, s);
 
   extern __shared__ __align__(16) uint8_t smem[];
   const SmemLayout& L = P.lay;
   uint32_t* xt = reinterpret_cast<uint32_t*>(smem + L.xt_off);
   int* slot_row = reinterpret_cast<int*>(smem + L.meta_off);   // source row of slot j, -1 = none
-  int* row_a = slot_row + L.nslot;                              // per output row: slot (-1: zero row)
-  int* row_b = row_a + R;                                       // bilinear second slot
-  int* row_wy = row_b + R;
+  int* s_shift = slot_row + L.nslot;                            // 16-byte misalignment of slot j
+  int* row_a = s_shift + L.nslot;                               // per output row: slot (-1: zero row)
+  int* row_b = row_a + P.rows_per_tile;                         // bilinear second slot
+  int* row_wy = row_b + P.rows_per_tile;
+  OutT* lut = reinterpret_cast<OutT*>(smem + lut_off(P));
   uint8_t* srcbuf = smem + L.src_off;
   uint8_t* hbuf = smem + L.h_off;
-  __shared__ int s_shift[2 * 16];
-  NormRegs<kC> N;
-  if constexpr (kVal == VAL_FMA1) N.load(P);
-  __shared__ int s_mode, s_lo, s_hi;   // s_mode 1: contiguous row range -> slots
 
-  // ---- A: column range (monotone maps: extremes at the ends) and tables
-  int col_lo, col_hi;                     // source columns (after >> sh), inclusive
-  int top = 0, left = 0, ch = 0, cw = 0;
-  if constexpr (kRes) {
-    top = prm[0]; left = prm[1]; ch = prm[2]; cw = prm[3];
-    int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
-    int a0, a1, aw, b0, b1, bw;
-    lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, a0, a1, aw);
-    lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, b0, b1, bw);
-    col_lo = (left + a0) >> sh; col_hi = (left + b1) >> sh;
-  } else {
-    int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
-    int lo = min(xa, xb), hi = min(max(xa, xb), w - 1);
-    col_lo = lo >> sh; col_hi = hi >> sh;   // col_lo > col_hi: every column is padding
-  }
+  // ---- A: tables
+  const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
+  const int col_lo = (int)T[0], col_hi = (int)T[1];
   const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
-
-  for (int ox = tid; ox < OW; ox += kThreads) {
-    if constexpr (kRes) {
-      int cx = back_x(P, prm, ox), x0, x1, wx;
-      lin_axis(cx, P.canvas_w, cw, P.lin32, P.linx_magic, x0, x1, wx);
-      int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
-      xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
-    } else {
-      int cx = back_x(P, prm, ox);
-      xt[ox] = cx < w ? (uint32_t)(((cx >> sh) - col_lo) * C) : 0xFFFFFFFFu;
-    }
-  }
-  // rows: source row (after >> sh) of every output row; contiguous-range slots when they fit
-  if (tid < L.nslot) { slot_row[tid] = -1; s_shift[tid] = 0; }   // a tail tile uses fewer slots
-  if (tid < R) {
-    int r = tid;
-    if constexpr (kRes) {
-      int cy = back_y(P, prm, r0 + r), y0, y1, wy;
-      lin_axis(cy, P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
-      row_a[r] = (top + y0) >> sh; row_b[r] = (top + y1) >> sh; row_wy[r] = wy;
-    } else {
-      int cy = back_y(P, prm, r0 + r);
-      row_a[r] = (cy < h && span_bytes > 0) ? (cy >> sh) : -1;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int lo = row_a[0], hi = kRes ? row_b[R - 1] : row_a[R - 1];
-    if (!kRes && lo < 0) { lo = hi = -1; }
-    if (!kRes && hi < 0) {   // trailing padding rows: range over the valid prefix
-      hi = -1;
-      for (int r = R - 1; r >= 0; --r) if (row_a[r] >= 0) { hi = row_a[r]; break; }
-    }
-    s_mode = (lo >= 0 && hi >= lo && hi - lo + 1 <= L.nslot) ? 1 : 0;
-    s_lo = lo; s_hi = hi;
-  }
-  __syncthreads();
-  const bool contiguous = s_mode != 0;
-  if (contiguous && tid < L.nslot) {
-    int y = s_lo + tid;
-    slot_row[tid] = (y <= s_hi && y < src_rows) ? y : -1;
-  }
-  if (tid < R) {   // rewrite row_a/row_b as slot indices
-    int r = tid;
-    if (contiguous) {
-      int lo = s_lo;
-      if (row_a[r] >= 0) row_a[r] -= lo;
-      if constexpr (kRes) row_b[r] -= lo;
-    } else {
-      if constexpr (kRes) {
-        slot_row[2 * r] = row_a[r]; slot_row[2 * r + 1] = row_b[r];
-        row_a[r] = 2 * r; row_b[r] = 2 * r + 1;
-      } else {
-        slot_row[r] = row_a[r];
-        if (row_a[r] >= 0) row_a[r] = r;
-      }
-    }
+  for (int i = tid; i < OW; i += kThreads) xt[i] = T[4 + i];
+  const uint32_t* M = T + 4 + tab_owp(P) + (size_t)tile * tab_tm(P);
+  const int nvalid = (int)M[0];
+  if (tid < L.nslot) { slot_row[tid] = (int)M[1 + tid]; s_shift[tid] = 0; }
+  if (tid < 3 * P.rows_per_tile) row_a[tid] = (int)M[1 + L.nslot + tid];   // row_a, row_b, row_wy
+  if constexpr (kVal == VAL_LUT) {
+    const uint4* g = reinterpret_cast<const uint4*>(A.lut);
+    uint4* l4 = reinterpret_cast<uint4*>(lut);
+    const int n16 = C * 256 * (int)sizeof(OutT) / 16;
+    for (int i = tid; i < n16; i += kThreads) l4[i] = g[i];
   }
   __syncthreads();
 
   // ---- B: stage source row segments (warp per slot, 16 B vectors)
   const int lane = tid & 31, warp = tid >> 5;
-  for (int j = warp; j < L.nslot; j += kThreads / 32) {
+  for (int j = warp; j < nvalid; j += kThreads / 32) {
     int srow = slot_row[j];
     if (srow < 0 || span_bytes == 0) continue;
-    const uint8_t* src = base + (int64_t)srow * rstride + (int64_t)col_lo * C;
+    const uint8_t* src = S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C;
     uintptr_t a = reinterpret_cast<uintptr_t>(src);
     uintptr_t a0 = a & ~(uintptr_t)15;
     int shift = (int)(a - a0);
@@ -324,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   // ---- H: horizontal pass; a thread owns one output column (its table entry
   // decoded once) and walks the slots; short rows put several threads per column
   {
-    const int ncg = max(1, kThreads / OW);          // threads per column
+    const int ncg = P.h_tpc;                        // threads per column
     for (int c0 = tid; c0 < OW * ncg; c0 += kThreads) {
       const int j0 = P.ow_magic ? (int)fast_div((uint32_t)c0, P.ow_magic) : c0 / OW;
       const int ox = c0 - j0 * OW;
@@ -333,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
         const int off0 = (int)(e & 0xFFFFu), wx = (int)((e >> 16) & 0xFFFu);
         const int off1 = (e >> 28) ? off0 : off0 + C;
         const uint32_t w0 = 2048u - (uint32_t)wx, w1 = (uint32_t)wx;
-        for (int j = j0; j < L.nslot; j += ncg) {
+        for (int j = j0; j < nvalid; j += ncg) {
           if (slot_row[j] < 0) continue;
           const uint8_t* row = srcbuf + j * L.span_pad + s_shift[j];
           uint32_t* hr = reinterpret_cast<uint32_t*>(hbuf + j * L.hrow_pad) + ox * C;
@@ -345,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
       } else {
         const bool pad = e == 0xFFFFFFFFu;
         const uint32_t eo = pad ? 0u : e;    // never form an out-of-window smem address
-        for (int j = j0; j < L.nslot; j += ncg) {
+        for (int j = j0; j < nvalid; j += ncg) {
           if (slot_row[j] < 0) continue;
           const uint8_t* row = srcbuf + j * L.span_pad + s_shift[j];
           uint8_t* hr = hbuf + j * L.hrow_pad + ox * C;
@@ -360,6 +404,10 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
   __syncthreads();
 
   // ---- V: vertical pass + value ops + 16-byte stores
+  auto val = [&](uint32_t b, int k) -> OutT {
+    if constexpr (kVal == VAL_LUT) return lut[k * 256 + b];
+    else return value_generic<OutT, kVal>(P, b, k);
+  };
   OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * rowlen;
   if constexpr (kC > 0) {
     // group = V pixels = kC vectors of V elements; element i of vector j has channel (j*V+i) % kC
@@ -391,10 +439,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
             for (int i = 0; i < V; ++i) { t0[i] = h0[i]; t1[i] = h1[i]; }
           }
 #pragma unroll
-          for (int i = 0; i < V; ++i) {
-            uint32_t b = (wy0 * t0[i] + wy1 * t1[i] + (1u << 21)) >> 22;
-            pk.v[i] = value_of<OutT, kVal, kC>(P, N, b, (j * V + i) % kC);
-          }
+          for (int i = 0; i < V; ++i) pk.v[i] = val((wy0 * t0[i] + wy1 * t1[i] + (1u << 21)) >> 22, (j * V + i) % kC);
         } else {
           uint8_t bytes[V];
           if (a < 0) {
@@ -411,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
             }
           }
 #pragma unroll
-          for (int i = 0; i < V; ++i) pk.v[i] = value_of<OutT, kVal, kC>(P, N, bytes[i], (j * V + i) % kC);
+          for (int i = 0; i < V; ++i) pk.v[i] = val(bytes[i], (j * V + i) % kC);
         }
         if constexpr (kVec) *reinterpret_cast<uint4*>(orow + j * V) = pk.u;
         else orow[j * V] = pk.v[0];
@@ -433,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
           b = hbuf[(size_t)max(a, 0) * L.hrow_pad + q];
           if (a < 0) b = 0u;
         }
-        out[(size_t)r * rowlen + q] = value_of<OutT, kVal, kC>(P, N, b, k);
+        out[(size_t)r * rowlen + q] = val(b, k);
       }
     }
   } else {
@@ -450,15 +495,20 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
         b = hbuf[(size_t)max(a, 0) * L.hrow_pad + q];
         if (a < 0) b = 0u;
       }
-      out[(size_t)r * rowlen + q] = value_of<OutT, kVal, kC>(P, N, b, k);
+      out[(size_t)r * rowlen + q] = val(b, k);
     }
   }
 }
 
-
 // ------------------------------------------------------------ K1 dispatch
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
+  {   // prologue: per-sample geometry tables
+    auto pk = sample_tables_kernel<kRes>;
+    int tsm = (P.out_w + 3 * P.out_h) * 4;
+    if (tsm > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+    pk<<<A.count, kThreads, tsm, st>>>(P, A);
+  }
   dim3 grid(P.tiles_per_sample, A.count);
   int smem = P.lay.total;
   auto k = image_kernel<OutT, kRes, kVal, kC, kVec>;
@@ -487,7 +537,7 @@ static int launch_img_typed(const PlanDev& P, const LaunchArgs& A, cudaStream_t 
   if constexpr (sizeof(OutT) == 1) {
     return launch_img_r<OutT, VAL_COPY>(P, A, st, vec);
   } else {
-    if (P.value_mode == VAL_FMA1) return launch_img_r<OutT, VAL_FMA1>(P, A, st, vec);
+    if (P.value_mode == VAL_LUT) return launch_img_r<OutT, VAL_LUT>(P, A, st, vec);
     return launch_img_r<OutT, VAL_GENERIC>(P, A, st, vec);
   }
 }
