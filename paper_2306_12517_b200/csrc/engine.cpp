@@ -226,7 +226,10 @@ static void host_lin_axis(int o, int out_n, int in_n, int* i0, int* i1) {
 // of the step of the last source row from one group to the next.
 static void plan_stream(PlanDev& P, const Field& f) {
   P.stream = 0;
-  if (const char* e = std::getenv("BBX_STREAM")) if (std::atoi(e) == 0) return;
+  // Opt-in until the streaming variant is parity-green on the GPU (round-1
+  // run: 27 mismatching parity cases + an illegal access); the tile K1 is the default.
+  const char* en = std::getenv("BBX_STREAM");
+  if (!en || std::atoi(en) == 0) return;
   const int H = P.out_h;
   int band = 32;
   if (const char* e = std::getenv("BBX_BAND_ROWS")) band = std::max(1, std::atoi(e));
