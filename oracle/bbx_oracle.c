@@ -92,7 +92,9 @@ typedef struct { int code; char msg[256]; } or_err;
 
 /* ----------------------------------------------------------- codecs ------
  * codecs.py:91-128.  Decodes into a dense (h, w, c) u8 buffer. */
-enum { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2 };
+enum { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2, CODEC_JPEG = 3 };
+/* jpeg_oracle.c: the JPEG codec extension (no reference counterpart). */
+int or_jpeg_decode(const uint8_t* d, int64_t n, int h, int w, int c, uint8_t* out, or_err* e);
 
 int or_decode_image(int h, int w, int c, int codec, const uint8_t* payload, int64_t len,
                     uint8_t* out, or_err* e) {
@@ -125,6 +127,8 @@ int or_decode_image(int h, int w, int c, int codec, const uint8_t* payload, int6
       for (int x = 0; x < w; ++x)
         for (int k = 0; k < c; ++k)
           out[((int64_t)y * w + x) * c + k] = payload[((int64_t)(y / 2) * sw + x / 2) * c + k];
+  } else if (codec == CODEC_JPEG) {
+    return or_jpeg_decode(payload, len, h, w, c, out, e);
   } else {
     e->code = OR_CORRUPT_PAYLOAD; snprintf(e->msg, sizeof e->msg, "unknown codec %d", codec); return 1;
   }

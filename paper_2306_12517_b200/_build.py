@@ -21,9 +21,9 @@ NVCC = shutil.which("nvcc") or f"{CUDA_HOME}/bin/nvcc"
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXX = os.environ.get("CXX", "g++")
 
-HOST_SOURCES = ["engine.cpp", "format.cpp", "orders.cpp"]
-CUDA_SOURCES = ["kernels.cu", "kernels_img_u8.cu", "kernels_img_f32.cu", "kernels_img_f16.cu", "kernels_img_bf16.cu"]
-HEADERS = ["bbx_internal.h", "engine.h", "image_kernel.cuh"]
+HOST_SOURCES = ["engine.cpp", "format.cpp", "orders.cpp", "jpeg_host.cpp"]
+CUDA_SOURCES = ["kernels.cu", "kernels_img_u8.cu", "kernels_img_f32.cu", "kernels_img_f16.cu", "kernels_img_bf16.cu", "jpeg.cu"]
+HEADERS = ["bbx_internal.h", "engine.h", "image_kernel.cuh", "jpeg.h"]
 
 
 def _stale() -> bool:

@@ -4,6 +4,13 @@ Codec ids and payload formats as codecs.py:25-128 of the reference:
 RAW = row-major HxWxC bytes; RLE = (u32 count, u8 value) runs; SUBSAMPLE2 =
 top-left pixel of every 2x2 block.  Decoding happens on the GPU (K2/K1 in
 csrc/kernels.cu); `decode_image` here is the single-blob entry point.
+
+JPEG (codec id 3) is this build's extension (the reference stops at 2,
+codecs.py:25-28; its validator rejects codec > 2, format.py:542-543): a
+baseline, Huffman-coded, single-scan JFIF file with 1 or 3 components and
+sampling factors in {1, 2}, written with restart markers so the device
+decoder can give every restart interval its own thread (csrc/jpeg.cu).
+Encoding (writer side, offline) goes through Pillow / libjpeg-turbo.
 """
 
 from __future__ import annotations
@@ -21,6 +28,36 @@ class CodecId(enum.IntEnum):
     RAW = 0
     RLE = 1
     SUBSAMPLE2 = 2
+    JPEG = 3
+
+
+@dataclass(frozen=True)
+class JpegParams:
+    """Writer-side JPEG settings (FFCV's RGBImageField(jpeg_quality=90) analogue)."""
+    quality: int = 90
+    subsampling: str = "4:2:0"     # "4:4:4" | "4:2:2" | "4:2:0"
+    restart_rows: int = 1          # DRI = this many MCU rows (0: no restart markers)
+
+
+def encode_jpeg(px: np.ndarray, params: JpegParams | None = None) -> bytes:
+    """Baseline JFIF bytes for a u8 (h, w, 1|3) array (Pillow / libjpeg-turbo)."""
+    import io
+
+    from PIL import Image
+
+    params = params or JpegParams()
+    h, w, c = px.shape
+    if c not in (1, 3):
+        raise SchemaMismatch(f"jpeg needs 1 or 3 channels, got {c}")
+    im = Image.fromarray(px[:, :, 0] if c == 1 else px, "L" if c == 1 else "RGB")
+    kw = {"quality": int(params.quality)}
+    if c == 3:
+        kw["subsampling"] = params.subsampling
+    if params.restart_rows:
+        kw["restart_marker_rows"] = int(params.restart_rows)
+    bio = io.BytesIO()
+    im.save(bio, "JPEG", **kw)
+    return bio.getvalue()
 
 
 @dataclass(frozen=True)
@@ -54,7 +91,7 @@ def encode_rle(flat: np.ndarray) -> bytes:
     return rec.tobytes()
 
 
-def encode_image(pixels, codec, *, max_height=None, max_width=None) -> ImageBlob:
+def encode_image(pixels, codec, *, max_height=None, max_width=None, jpeg: JpegParams | None = None) -> ImageBlob:
     px = np.asarray(pixels)
     if px.dtype != np.uint8 or px.ndim != 3:
         raise SchemaMismatch(f"expected a u8 HxWxC array, got {px.dtype} ndim={px.ndim}")
@@ -69,6 +106,8 @@ def encode_image(pixels, codec, *, max_height=None, max_width=None) -> ImageBlob
         payload = px.tobytes()
     elif codec == CodecId.RLE:
         payload = encode_rle(px)
+    elif codec == CodecId.JPEG:
+        payload = encode_jpeg(px, jpeg)
     else:
         payload = px[::2, ::2].tobytes()
     return ImageBlob(h, w, c, codec, payload)

@@ -9,7 +9,7 @@
 namespace bbx {
 
 enum SrcKind : int32_t { SRC_DECODE = 0, SRC_RESAMPLE = 1, SRC_ARRAY = 2 };
-enum Codec : int32_t { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2 };
+enum Codec : int32_t { CODEC_RAW = 0, CODEC_RLE = 1, CODEC_SUB2 = 2, CODEC_JPEG = 3 };
 enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_LUT = 3 };
 
 constexpr int kMaxRemaps = 12;

@@ -21,8 +21,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <unordered_map>
 
 #include "engine.h"
+#include "jpeg.h"
 
 namespace bbx {
 
@@ -125,6 +127,13 @@ struct Plan {
   int64_t out_sample_bytes = 0;
   int64_t max_payload = 0;       // over the whole dataset (exact staging capacity)
   bool field_has_rle = false;
+  bool field_has_jpeg = false;
+  int64_t jpeg_blocks_cap = 0;   // per sample: coefficient blocks (any sampling with factors <= 2)
+  int64_t jpeg_int_cap = 0;      // per sample: restart intervals (<= MCUs)
+  int16_t* d_coef = nullptr;     // JPEG scratch shared by the slots (one compute stream orders them)
+  uint8_t* d_planes = nullptr;
+  uint32_t* d_istart = nullptr;
+  uint32_t* d_iend = nullptr;
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
@@ -154,6 +163,22 @@ struct Slot {
   int fatal = 0;
   std::string fatal_msg;
   std::vector<char> plan_has_rle;
+  std::vector<char> plan_has_jpeg;
+  std::vector<uint32_t> jpeg_total_int;
+  std::vector<uint64_t> jpeg_total_blk;
+  std::vector<int32_t> jpeg_max_pix;
+};
+
+// Device pools of the Huffman / quant tables the JPEG samples reference,
+// deduplicated by content (one writer's files share a handful).  Append-only:
+// entries in use by in-flight kernels never change.
+struct JpegTables {
+  JHuff* h_huff = nullptr;       // pinned host mirrors
+  JQuant* h_quant = nullptr;
+  JHuff* d_huff = nullptr;
+  JQuant* d_quant = nullptr;
+  int n_huff = 0, n_quant = 0, up_huff = 0, up_quant = 0;
+  std::unordered_map<std::string, int> hmap, qmap;
 };
 
 }  // namespace bbx
@@ -171,6 +196,8 @@ struct bbx_loader {
   bool finalized = false;
   size_t slot_bytes = 0, desc_bytes = 0, idx_off = 0;
   std::vector<size_t> desc_off;       // per plan, within a slot
+  std::vector<size_t> jpeg_off;       // per plan with JPEG samples: JpegDesc[B] + prefixes, within a slot
+  JpegTables jt;
   size_t pay_base = 0;                // start of the compact payload region
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
@@ -465,18 +492,25 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
   }
   // one pass over the row table: exact staging capacity, RLE presence
   int64_t mx = 0;
-  bool rle = false;
+  bool rle = false, jpeg = false;
   if (f.info.kind == 4) {
     for (int64_t i = 0; i < ds->num_samples; ++i) {
       ImageCell c = image_cell(ds, i, f);
       mx = std::max<int64_t>(mx, (int64_t)c.length);
       rle |= c.codec == CODEC_RLE;
+      jpeg |= c.codec == CODEC_JPEG;
     }
   } else {
     mx = f.array_nbytes;
   }
   pl.max_payload = mx;
   pl.field_has_rle = rle;
+  pl.field_has_jpeg = jpeg;
+  if (jpeg) {   // bounds over every header a cell of this field can carry (dims checked per sample)
+    const int64_t mh = f.info.max_height, mw = f.info.max_width;
+    pl.jpeg_blocks_cap = (int64_t)f.info.channels * (2 * ((mh + 15) / 16)) * (2 * ((mw + 15) / 16));
+    pl.jpeg_int_cap = ((mh + 7) / 8) * ((mw + 7) / 8);
+  }
   return BBX_OK;
 }
 
@@ -556,6 +590,9 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
       int64_t m = (int64_t)((c.h + 1) / 2) * ((c.w + 1) / 2) * c.c;
       if ((int64_t)c.length != m) return bad(BBX_CORRUPT_PAYLOAD, "subsampled payload is %lld bytes, expected %lld",
                                              (long long)c.length, (long long)m);
+    } else if (c.codec == CODEC_JPEG) {
+      if (c.length < 4) return bad(BBX_CORRUPT_PAYLOAD, "jpeg: missing SOI marker");
+      if (!pl.field_has_jpeg) return bad(BBX_CORRUPT_PAYLOAD, "jpeg sample in a field compiled without JPEG");
     } else {
       return bad(BBX_CORRUPT_PAYLOAD, "unknown codec %d", c.codec);
     }
@@ -596,6 +633,86 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
 
 static void pipeline_loop(bbx_loader* L);
 
+// Table pool ids for one JPEG header (registering unseen tables).
+static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, int* id) {
+  std::string key(reinterpret_cast<const char*>(h.counts), 16);
+  key.append(reinterpret_cast<const char*>(h.vals), h.nvals);
+  auto it = T.hmap.find(key);
+  if (it != T.hmap.end()) { *id = it->second; return 0; }
+  if (T.n_huff >= kJpegMaxHuff) return 2;
+  if (!jpeg_build_huff(h, &T.h_huff[T.n_huff])) return 1;
+  *id = T.hmap[key] = T.n_huff++;
+  return 0;
+}
+static int jpeg_quant_id(JpegTables& T, const JpegHeader::Quant& q, int* id) {
+  std::string key(reinterpret_cast<const char*>(q.q), sizeof q.q);
+  auto it = T.qmap.find(key);
+  if (it != T.qmap.end()) { *id = it->second; return 0; }
+  if (T.n_quant >= kJpegMaxQuant) return 2;
+  std::memcpy(T.h_quant[T.n_quant].q, q.q, sizeof q.q);
+  *id = T.qmap[key] = T.n_quant++;
+  return 0;
+}
+
+// Host half of the JPEG decode of one sample: parse the header, check it
+// against the cell, resolve table ids and size the device work.
+static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint32_t len, SampleDesc* d, JpegDesc* J,
+                         HostErr& err, int64_t pos, int plan_idx) {
+  auto bad = [&](const char* m) {
+    d->skip = 1;
+    if (err.pos < 0 || pos < err.pos || (pos == err.pos && plan_idx < err.plan)) {
+      err.pos = pos; err.plan = plan_idx; err.code = BBX_CORRUPT_PAYLOAD; err.msg = m;
+    }
+    return false;
+  };
+  JpegHeader H;
+  char msg[256];
+  if (jpeg_parse_header(pay, len, &H, msg, sizeof msg)) return bad(msg);
+  if (H.height != d->h || H.width != d->w || H.ncomp != d->c) {
+    std::snprintf(msg, sizeof msg, "jpeg: header says %dx%dx%d, cell says %dx%dx%d", H.height, H.width, H.ncomp,
+                  d->h, d->w, d->c);
+    return bad(msg);
+  }
+  std::memset(J, 0, sizeof *J);
+  int hmax = 1, vmax = 1;
+  for (int i = 0; i < H.ncomp; ++i) { hmax = std::max(hmax, H.comp[i].h); vmax = std::max(vmax, H.comp[i].v); }
+  const int mx = H.ncomp == 1 ? (H.width + 7) / 8 : (H.width + 8 * hmax - 1) / (8 * hmax);
+  const int my = H.ncomp == 1 ? (H.height + 7) / 8 : (H.height + 8 * vmax - 1) / (8 * vmax);
+  uint32_t blocks = 0;
+  JpegTables& T = L->jt;
+  for (int i = 0; i < H.ncomp; ++i) {
+    const auto& c = H.comp[i];
+    JComp& o = J->comp[i];
+    int dc, ac, q, r;
+    if ((r = jpeg_table_id(T, H.dc[c.td], &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], &ac)) ||
+        (r = jpeg_quant_id(T, H.qt[c.tq], &q)))
+      return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
+    o.dc = (uint16_t)dc; o.ac = (uint16_t)ac; o.q = (uint16_t)q;
+    o.h = (uint8_t)c.h; o.v = (uint8_t)c.v;
+    o.bw = (uint16_t)(H.ncomp == 1 ? mx : mx * c.h);
+    o.bh = (uint16_t)(H.ncomp == 1 ? my : my * c.v);
+    o.dw = (uint16_t)(((int64_t)H.width * c.h + hmax - 1) / hmax);
+    o.dh = (uint16_t)(((int64_t)H.height * c.v + vmax - 1) / vmax);
+    o.blk_off = blocks;
+    blocks += (uint32_t)o.bw * o.bh;
+  }
+  const uint32_t total = (uint32_t)mx * my;
+  J->scan_off = H.scan_off;
+  J->scan_end = len;
+  J->mcus_x = (uint16_t)mx; J->mcus_y = (uint16_t)my;
+  J->restart = H.restart ? (uint32_t)H.restart : total;
+  J->n_int = (total + J->restart - 1) / J->restart;
+  J->ncomp = (uint8_t)H.ncomp; J->hmax = (uint8_t)hmax; J->vmax = (uint8_t)vmax;
+  J->n_blocks = blocks;
+  if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap)
+    return bad("jpeg: geometry exceeds the field's device capacity");
+  return true;
+}
+
+static size_t jpeg_block_bytes(int B) {
+  return ((size_t)B * sizeof(JpegDesc) + (size_t)(B + 1) * 4 + 7) / 8 * 8 + (size_t)(B + 1) * 8;
+}
+
 static int finalize(bbx_loader* L) {
   if (L->finalized) return BBX_OK;
   CK(cudaSetDevice(L->device));
@@ -609,6 +726,15 @@ static int finalize(bbx_loader* L) {
     if (L->plans[p].scalar) continue;
     L->desc_off[p] = off;
     off += (size_t)L->batch * L->plans[p].dev.desc_stride;
+    off = (off + 255) / 256 * 256;
+  }
+  L->jpeg_off.assign(L->plans.size(), 0);
+  bool any_jpeg = false;
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    if (L->plans[p].scalar || !L->plans[p].field_has_jpeg) continue;
+    any_jpeg = true;
+    L->jpeg_off[p] = off;
+    off += jpeg_block_bytes(L->batch);
     off = (off + 255) / 256 * 256;
   }
   L->desc_bytes = off;
@@ -638,9 +764,24 @@ static int finalize(bbx_loader* L) {
     for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_tables[s], (size_t)L->batch * pl.dev.tab_stride * 4 + 64));
   }
   for (auto& pl : L->plans) {
-    if (pl.scalar || !pl.field_has_rle) continue;
+    if (pl.scalar || !(pl.field_has_rle || pl.field_has_jpeg)) continue;
     pl.d_scratch.assign(L->nslots, nullptr);
     for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_scratch[s], (size_t)L->batch * pl.dev.scratch_bytes + 64));
+  }
+  for (auto& pl : L->plans) {
+    if (pl.scalar || !pl.field_has_jpeg) continue;
+    const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
+    CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
+    CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
+    CK(cudaMalloc(&pl.d_istart, ints * 4 + 64));
+    CK(cudaMalloc(&pl.d_iend, ints * 4 + 64));
+  }
+  if (any_jpeg && !L->jt.d_huff) {
+    JpegTables& T = L->jt;
+    CK(cudaHostAlloc(&T.h_huff, sizeof(JHuff) * kJpegMaxHuff, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&T.h_quant, sizeof(JQuant) * kJpegMaxQuant, cudaHostAllocDefault));
+    CK(cudaMalloc(&T.d_huff, sizeof(JHuff) * kJpegMaxHuff));
+    CK(cudaMalloc(&T.d_quant, sizeof(JQuant) * kJpegMaxQuant));
   }
   // Page-lock the mmap'd file once per dataset so the copy engine reads
   // payloads straight out of the page cache (no CPU gather).  Only when the
@@ -679,6 +820,10 @@ static int process_slot(bbx_loader* L, int s) {
   if (S.used) CK(cudaEventSynchronize(S.h2d_done));
   S.herr = HostErr{};
   S.plan_has_rle.assign(L->plans.size(), 0);
+  S.plan_has_jpeg.assign(L->plans.size(), 0);
+  S.jpeg_total_int.assign(L->plans.size(), 0);
+  S.jpeg_total_blk.assign(L->plans.size(), 0);
+  S.jpeg_max_pix.assign(L->plans.size(), 0);
   uint8_t* H = S.h_stage;
   std::memcpy(H + L->idx_off, S.idx.data(), (size_t)count * 8);
   for (int64_t pos = 0; pos < count; ++pos) {
@@ -706,6 +851,8 @@ static int process_slot(bbx_loader* L, int s) {
     if (pl.scalar) continue;
     uint8_t* dblk = H + L->desc_off[p];
     const bool image = ds->fields[pl.field_index].info.kind == 4;
+    JpegDesc* jds = pl.field_has_jpeg ? reinterpret_cast<JpegDesc*>(H + L->jpeg_off[p]) : nullptr;
+    if (jds) std::memset(jds, 0, sizeof(JpegDesc) * count);
     for (int pos = 0; pos < count; ++pos) {
       int64_t i = S.idx[pos];
       uint8_t* desc = dblk + (size_t)pos * pl.dev.desc_stride;
@@ -720,6 +867,10 @@ static int process_slot(bbx_loader* L, int s) {
       SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
       if (!ok) continue;
       if (d->codec == CODEC_RLE && ds->fields[pl.field_index].info.kind == 4) S.plan_has_rle[p] = 1;
+      if (image && d->codec == CODEC_JPEG) {
+        if (!jpeg_prepare(L, pl, ds->map + off, len, d, &jds[pos], S.herr, pos, (int)p)) continue;
+        S.plan_has_jpeg[p] = 1;
+      }
       if (resident) {
         d->src = off;                                   // absolute file offset; base = heap - heap_offset
         continue;
@@ -741,6 +892,45 @@ static int process_slot(bbx_loader* L, int s) {
       }
       if (len) copies.push_back({ds->map + off, H + cursor, len, 1, len});
       cursor += ((size_t)len + 15) / 16 * 16;
+    }
+  }
+  // JPEG: interval / block prefixes of each plan's batch (J2/J3 thread maps)
+  for (size_t p = 0; p < L->plans.size(); ++p) {
+    if (!S.plan_has_jpeg[p]) continue;
+    const Plan& pl = L->plans[p];
+    uint8_t* jb = H + L->jpeg_off[p];
+    JpegDesc* jds = reinterpret_cast<JpegDesc*>(jb);
+    uint32_t* ipre = reinterpret_cast<uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
+    uint64_t* bpre = reinterpret_cast<uint64_t*>(jb + ((size_t)L->batch * sizeof(JpegDesc) + (size_t)(L->batch + 1) * 4 + 7) / 8 * 8);
+    const uint8_t* dblk = H + L->desc_off[p];
+    uint32_t ti = 0;
+    uint64_t tb = 0;
+    int32_t mp = 0;
+    for (int pos = 0; pos < count; ++pos) {
+      JpegDesc& J = jds[pos];
+      const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
+      if (d->skip) J.n_int = 0;
+      if (J.n_int == 0) J.n_blocks = 0;
+      J.int_base = ti; J.blk_base = tb;
+      ipre[pos] = ti; bpre[pos] = tb;
+      ti += J.n_int; tb += J.n_blocks;
+      if (J.n_int) mp = std::max(mp, (int32_t)d->h * d->w);
+    }
+    ipre[count] = ti; bpre[count] = tb;
+    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_pix[p] = mp;
+    if (ti == 0) S.plan_has_jpeg[p] = 0;
+  }
+  {   // new JPEG tables: append-only upload ahead of this slot's H2D (same copy stream)
+    JpegTables& T = L->jt;
+    if (T.n_huff > T.up_huff) {
+      CK(cudaMemcpyAsync(T.d_huff + T.up_huff, T.h_huff + T.up_huff, sizeof(JHuff) * (T.n_huff - T.up_huff),
+                         cudaMemcpyHostToDevice, L->copy_st));
+      T.up_huff = T.n_huff;
+    }
+    if (T.n_quant > T.up_quant) {
+      CK(cudaMemcpyAsync(T.d_quant + T.up_quant, T.h_quant + T.up_quant, sizeof(JQuant) * (T.n_quant - T.up_quant),
+                         cudaMemcpyHostToDevice, L->copy_st));
+      T.up_quant = T.n_quant;
     }
   }
   // DMA mode: the copy engine reads every payload / window straight from the
@@ -804,7 +994,7 @@ static int process_slot(bbx_loader* L, int s) {
   int64_t kbytes = 0, klaunch = 0;
   if (prof) CK(cudaEventRecord(S.k0, L->comp_st));
   int64_t d2h = 0;
-  bool any_rle = false;
+  bool any_rle = false, any_jpeg = false;
   ScalarArgs SA{};
   SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
   SA.count = count;
@@ -830,6 +1020,20 @@ static int process_slot(bbx_loader* L, int s) {
     if (S.plan_has_rle[p]) {
       if (launch_rle_expand(pl.dev, A, L->comp_st)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       ++launches; any_rle = true;
+    }
+    if (S.plan_has_jpeg[p]) {
+      JpegArgs J{};
+      const uint8_t* jb = S.d_stage + L->jpeg_off[p];
+      J.desc = A.desc; J.desc_stride = pl.dev.desc_stride; J.payload = A.payload;
+      J.jd = reinterpret_cast<const JpegDesc*>(jb);
+      J.int_prefix = reinterpret_cast<const uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
+      J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + ((size_t)L->batch * sizeof(JpegDesc) + (size_t)(L->batch + 1) * 4 + 7) / 8 * 8);
+      J.istart = pl.d_istart; J.iend = pl.d_iend; J.coef = pl.d_coef; J.planes = pl.d_planes;
+      J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
+      J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.status = A.status; J.count = count;
+      J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_pixels = S.jpeg_max_pix[p];
+      if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      launches += 4; any_jpeg = true;
     }
     int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, L->comp_st) : launch_image(pl.dev, A, L->comp_st);
     if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
@@ -857,7 +1061,7 @@ static int process_slot(bbx_loader* L, int s) {
     if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
     ++launches;
   }
-  if (any_rle) {
+  if (any_rle || any_jpeg) {
     size_t nb = sizeof(SampleStatus) * L->batch * L->plans.size();
     CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, L->comp_st));
     d2h += (int64_t)nb;
@@ -874,6 +1078,74 @@ static int process_slot(bbx_loader* L, int s) {
     L->stats.stage_seconds += t1 - t0;
     L->stats.dma_batches += dma_done ? 1 : 0;
   }
+  return BBX_OK;
+}
+
+// codecs.decode_image for one JPEG blob: the batch decoder (J1-J4) run on a
+// batch of one, writing the (h, w, c) result straight into out_dev.
+static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len, uint8_t* out_dev, int device) {
+  if (len < 4 || len > 0xFFFFFFFFll) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: missing SOI marker");
+  if (h > 65535 || w > 65535 || c > 255) return fail(BBX_SCHEMA_MISMATCH, "image dims too large");
+  CK(cudaSetDevice(device));
+  bbx_loader L;                                  // only its table registry is used
+  std::vector<JHuff> hh(kJpegMaxHuff);
+  std::vector<JQuant> hq(kJpegMaxQuant);
+  L.jt.h_huff = hh.data(); L.jt.h_quant = hq.data();
+  Plan pl;
+  pl.jpeg_blocks_cap = (int64_t)c * (2 * ((h + 15) / 16)) * (2 * ((w + 15) / 16));
+  pl.jpeg_int_cap = (int64_t)((h + 7) / 8) * ((w + 7) / 8);
+  uint8_t desc[64] = {0};
+  SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
+  d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = CODEC_JPEG;
+  JpegDesc J{};
+  HostErr err;
+  bool ok = jpeg_prepare(&L, pl, pay, (uint32_t)len, d, &J, err, 0, 0);
+  L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
+  if (!ok) return fail(err.code, "%s", err.msg.c_str());
+  J.int_base = 0; J.blk_base = 0;
+  // device image: [desc 64][jd][prefixes][payload (+16 pad)] then tables, intervals, coef, planes, status
+  const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_bp = o_ip + 16, o_pay = o_bp + 16;
+  const size_t o_hf = (o_pay + len + 16 + 255) / 256 * 256;
+  const size_t o_q = o_hf + sizeof(JHuff) * L.jt.n_huff;
+  const size_t o_is = (o_q + sizeof(JQuant) * L.jt.n_quant + 255) / 256 * 256;
+  const size_t o_ie = o_is + 4 * (size_t)J.n_int + 16;
+  const size_t o_cf = (o_ie + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
+  const size_t o_pl = o_cf + 128 * (size_t)J.n_blocks;
+  const size_t o_st = (o_pl + 64 * (size_t)J.n_blocks + 255) / 256 * 256;
+  const size_t total = o_st + sizeof(SampleStatus);
+  std::vector<uint8_t> img(o_is, 0);
+  std::memcpy(img.data(), desc, 64);
+  std::memcpy(img.data() + o_jd, &J, sizeof J);
+  const uint32_t ip[2] = {0, J.n_int};
+  const uint64_t bp[2] = {0, J.n_blocks};
+  std::memcpy(img.data() + o_ip, ip, sizeof ip);
+  std::memcpy(img.data() + o_bp, bp, sizeof bp);
+  std::memcpy(img.data() + o_pay, pay, (size_t)len);
+  std::memcpy(img.data() + o_hf, hh.data(), sizeof(JHuff) * L.jt.n_huff);
+  std::memcpy(img.data() + o_q, hq.data(), sizeof(JQuant) * L.jt.n_quant);
+  uint8_t* dev = nullptr;
+  CK(cudaMalloc(&dev, total));
+  cudaError_t e = cudaMemcpy(dev, img.data(), img.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(dev + o_st, 0, sizeof(SampleStatus));
+  JpegArgs A{};
+  A.desc = dev; A.desc_stride = 64; A.payload = dev + o_pay;
+  A.jd = reinterpret_cast<const JpegDesc*>(dev + o_jd);
+  A.int_prefix = reinterpret_cast<const uint32_t*>(dev + o_ip);
+  A.blk_prefix = reinterpret_cast<const uint64_t*>(dev + o_bp);
+  A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
+  A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
+  A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
+  A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
+  A.status = reinterpret_cast<SampleStatus*>(dev + o_st);
+  A.count = 1; A.total_int = J.n_int; A.total_blocks = J.n_blocks; A.max_pixels = h * w;
+  int rc = e == cudaSuccess ? launch_jpeg(A, nullptr) : 1;
+  SampleStatus st{};
+  if (e == cudaSuccess) e = cudaMemcpy(&st, dev + o_st, sizeof st, cudaMemcpyDeviceToHost);
+  cudaFree(dev);
+  if (rc || e != cudaSuccess) return fail(BBX_CUDA_ERROR, "jpeg decode failed: %s", cudaGetErrorString(e));
+  if (st.kind == JST_BAD_CODE) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: bad Huffman code in restart interval %lld", (long long)st.value);
+  if (st.kind == JST_MARKER_COUNT) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: restart marker count %lld does not match the header", (long long)st.value);
+  if (st.kind == JST_MARKER_SEQ) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: restart markers out of sequence");
   return BBX_OK;
 }
 
@@ -1081,19 +1353,24 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
   // merge host-detected and device-detected per-sample failures: lowest position wins
   HostErr best = S.herr;
   for (size_t p = 0; p < L->plans.size(); ++p) {
-    if (!S.plan_has_rle[p]) continue;
+    if (!S.plan_has_rle[p] && !S.plan_has_jpeg[p]) continue;
     const Plan& pl = L->plans[p];
     const uint8_t* dblk = S.h_stage + L->desc_off[p];
     for (int pos = 0; pos < S.count; ++pos) {
       if (best.pos >= 0 && (pos > best.pos || (pos == best.pos && (int)p >= best.plan))) break;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
-      if (d->skip || d->codec != CODEC_RLE) continue;
+      if (d->skip || (d->codec != CODEC_RLE && d->codec != CODEC_JPEG)) continue;
+      if (d->codec == CODEC_RLE && !S.plan_has_rle[p]) continue;
+      if (d->codec == CODEC_JPEG && !S.plan_has_jpeg[p]) continue;
       const SampleStatus& st = S.h_status[p * L->batch + pos];
       if (st.kind == 0) continue;
       char buf[256];
       int64_t n = (int64_t)d->h * d->w * d->c;
       if (st.kind == 1) std::snprintf(buf, sizeof buf, "rle runs sum past %lld bytes", (long long)n);
-      else std::snprintf(buf, sizeof buf, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);
+      else if (st.kind == 2) std::snprintf(buf, sizeof buf, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);
+      else if (st.kind == JST_BAD_CODE) std::snprintf(buf, sizeof buf, "jpeg: bad Huffman code in restart interval %lld", (long long)st.value);
+      else if (st.kind == JST_MARKER_COUNT) std::snprintf(buf, sizeof buf, "jpeg: restart marker count %lld does not match the header", (long long)st.value);
+      else std::snprintf(buf, sizeof buf, "jpeg: restart markers out of sequence");
       best.pos = pos; best.plan = (int)p; best.code = BBX_CORRUPT_PAYLOAD; best.msg = buf;
       break;
     }
@@ -1170,7 +1447,15 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (pl.d_col) cudaFree(pl.d_col);
     for (auto* p : pl.d_scratch) if (p) cudaFree(p);
     for (auto* p : pl.d_tables) if (p) cudaFree(p);
+    if (pl.d_coef) cudaFree(pl.d_coef);
+    if (pl.d_planes) cudaFree(pl.d_planes);
+    if (pl.d_istart) cudaFree(pl.d_istart);
+    if (pl.d_iend) cudaFree(pl.d_iend);
   }
+  if (L->jt.h_huff) cudaFreeHost(L->jt.h_huff);
+  if (L->jt.h_quant) cudaFreeHost(L->jt.h_quant);
+  if (L->jt.d_huff) cudaFree(L->jt.d_huff);
+  if (L->jt.d_quant) cudaFree(L->jt.d_quant);
   if (L->copy_st) cudaStreamDestroy(L->copy_st);
   if (L->comp_st) cudaStreamDestroy(L->comp_st);
   delete L;
@@ -1208,6 +1493,7 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
     int64_t m = (int64_t)((h + 1) / 2) * ((w + 1) / 2) * c;
     if (len != m) return fail(BBX_CORRUPT_PAYLOAD, "subsampled payload is %lld bytes, expected %lld", (long long)len, (long long)m);
   }
+  if (codec == CODEC_JPEG) return jpeg_decode_one(h, w, c, payload_host, len, out_dev, device);
   if (codec < 0 || codec > 2) return fail(BBX_CORRUPT_PAYLOAD, "unknown codec %d", codec);
   CK(cudaSetDevice(device));
   PlanDev P{};

@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 from .errors import SchemaMismatch, SourceError
-from .format import image_field, int_field
+from .format import array_field, image_field, int_field
 from .rng import TAG_SYNTH, Rng, stream_seed
 
 RASTER_HEADER = struct.Struct("<III")
@@ -63,6 +63,61 @@ class SyntheticImageSource:
         label, base = self._draws(i)
         # u8 wrap-around add == (pattern + base) & 255
         return {"image": self._pattern + np.uint8(base), "label": label}
+
+
+class PhotoLikeSource:
+    """ImageNet-shaped synthetic photos for the JPEG configs (bench data and fixtures).
+
+    Not a reference source (the reference's SyntheticImageSource pattern is too
+    smooth for JPEG: SURVEY.md §8d).  Sample i is a pure function of (seed, i):
+    size (h, w) with the longer side = max dims and the shorter one drawn in
+    [min_frac, 1] x max (like an ImageNet file resized to max_res), a diagonal
+    gradient with per-sample offsets, plus uniform noise of +-`noise`.
+    Optional `array_dim` adds the sparse-regression case study's float32
+    NDArray field "x" of that length (BASELINE configs[4]).
+    """
+
+    def __init__(self, num_samples: int, max_height: int = 256, max_width: int = 256, channels: int = 3,
+                 seed: int = 0, num_classes: int = 1000, noise: int = 12, min_frac: float = 0.6,
+                 fixed_size: bool = False, array_dim: int = 0):
+        self.num_samples = num_samples
+        self.max_height, self.max_width, self.channels = max_height, max_width, channels
+        self.seed, self.num_classes, self.noise = seed, num_classes, noise
+        self.min_frac, self.fixed_size, self.array_dim = min_frac, fixed_size, array_dim
+        self.schema = [image_field("image", max_height, max_width, channels), int_field("label")]
+        if array_dim:
+            self.schema.append(array_field("x", np.float32, (array_dim,)))
+
+    def __len__(self) -> int:
+        return self.num_samples
+
+    def dims_of(self, i: int) -> tuple[int, int]:
+        if self.fixed_size:
+            return self.max_height, self.max_width
+        r = Rng(stream_seed(self.seed, TAG_SYNTH, i, 1))
+        frac = self.min_frac + (1.0 - self.min_frac) * (r.below(1 << 20) / float(1 << 20))
+        if r.below(2):
+            return self.max_height, max(1, int(self.max_width * frac))
+        return max(1, int(self.max_height * frac)), self.max_width
+
+    def __getitem__(self, i: int) -> dict:
+        if not 0 <= i < self.num_samples:
+            raise IndexError(i)
+        r = Rng(stream_seed(self.seed, TAG_SYNTH, i))
+        label = r.below(self.num_classes)
+        h, w = self.dims_of(i)
+        g = np.random.default_rng([self.seed, i])
+        yy = np.arange(h, dtype=np.int32)[:, None, None]
+        xx = np.arange(w, dtype=np.int32)[None, :, None]
+        cc = np.arange(self.channels, dtype=np.int32)[None, None, :]
+        base = g.integers(0, 256, size=self.channels, dtype=np.int32)[None, None, :]
+        img = base + yy * (1 + cc) // 2 + xx * (3 - cc) // 2 + cc * 40
+        if self.noise:
+            img = img + g.integers(-self.noise, self.noise + 1, size=(h, w, self.channels), dtype=np.int32)
+        out = {"image": (img & 0xFF).astype(np.uint8), "label": label}
+        if self.array_dim:
+            out["x"] = g.standard_normal(self.array_dim, dtype=np.float32)
+        return out
 
 
 def write_raster(path, pixels) -> None:

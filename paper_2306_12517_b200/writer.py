@@ -14,11 +14,11 @@ Pages are assembled in memory and written whole.
 from __future__ import annotations
 
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
-from .codecs import CodecId, encode_image
+from .codecs import CodecId, JpegParams, encode_image
 from .errors import InvalidFile, SchemaMismatch, SourceError
 from .format import (
     DEFAULT_PAGE_SIZE, MIN_PAGE_SIZE, DatasetHeader, FieldKind, ImageCell, Region, VarBytesCell,
@@ -35,6 +35,7 @@ class WriterConfig:
     compress_probability: float = 0.0
     compress_codec: CodecId = CodecId.RLE
     seed: int = 0
+    jpeg: JpegParams = field(default_factory=JpegParams)   # used when compress_codec is JPEG
 
     def check(self) -> None:
         ps = self.page_size
@@ -138,7 +139,8 @@ def write_dataset(source, path, config: WriterConfig | None = None, schema=None)
                     cells.append(VarBytesCell(heap.put(data), len(data)) if data else VarBytesCell(0, 0))
                 else:
                     codec = config.compress_codec if draw.chance(config.compress_probability) else CodecId.RAW
-                    blob = encode_image(np.asarray(v), codec, max_height=f.max_height, max_width=f.max_width)
+                    blob = encode_image(np.asarray(v), codec, max_height=f.max_height, max_width=f.max_width,
+                                        jpeg=config.jpeg)
                     if blob.channels != f.channels:
                         raise SchemaMismatch(
                             f"sample {i} field {f.name!r}: {blob.channels} channels != {f.channels}")

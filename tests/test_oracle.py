@@ -169,3 +169,31 @@ def test_casts_match_numpy():
                          field, 8, 8, 3, 0, img.reshape(-1), 0)
     tb = torch.from_numpy(want).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(b16, tb)
+
+
+# ------------------------------------------------------- JPEG codec extension
+def test_jpeg_oracle_matches_pillow_goldens(golden):
+    """oracle/jpeg_oracle.c == Pillow/libjpeg-turbo, 0 LSB, on every golden case."""
+    import hashlib
+
+    cases = O.jpeg_golden_cases(golden)
+    assert len(cases) >= 100
+    for m, jpeg, px, sha in cases:
+        got = O.decode(m["h"], m["w"], m["c"], 3, jpeg)
+        if px is not None:
+            assert np.array_equal(got, px), m
+        else:
+            assert hashlib.sha256(got.tobytes()).hexdigest() == sha, m
+
+
+def test_jpeg_oracle_rejects_bad_streams(golden):
+    m, jpeg, _, _ = O.jpeg_golden_cases(golden)[20]
+    with pytest.raises(O.OracleError, match="SOI"):
+        O.decode(m["h"], m["w"], m["c"], 3, b"\x00\x01" + jpeg[2:])
+    with pytest.raises(O.OracleError, match="cell says"):
+        O.decode(m["h"] + 1, m["w"], m["c"], 3, jpeg)
+    prog = bytearray(jpeg)
+    i = prog.find(b"\xff\xc0")
+    prog[i + 1] = 0xC2
+    with pytest.raises(O.OracleError, match="progressive"):
+        O.decode(m["h"], m["w"], m["c"], 3, bytes(prog))
