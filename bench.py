@@ -62,6 +62,35 @@ def dataset_path() -> Path:
     return DATA_DIR / f"imagenet256_raw_{N_SAMPLES}.bbox"
 
 
+JPEG_B = 1024
+JPEG_SAMPLES = int(os.environ.get("BBX_BENCH_JPEG_SAMPLES", 8192))
+RST_BLOCKS = int(os.environ.get("BBX_BENCH_RST_BLOCKS", 4))   # restart interval (MCUs) the writer emits
+
+
+def jpeg_dataset_path() -> Path:
+    return DATA_DIR / f"imagenet256_jpeg_q90_420_rstb{RST_BLOCKS}_{JPEG_SAMPLES}.bbox"
+
+
+def ensure_jpeg_dataset(rank: int, barrier) -> Path:
+    """configs[2]: ImageNet-shaped synthetic photos (longer side 256, shorter side
+    153-256), JPEG q90 4:2:0 with a restart marker every RST_BLOCKS MCUs."""
+    import paper_2306_12517_b200 as bx
+
+    path = jpeg_dataset_path()
+    if rank == 0 and not path.exists():
+        DATA_DIR.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(".tmp")
+        t0 = time.time()
+        bx.write_dataset(bx.PhotoLikeSource(JPEG_SAMPLES, H, W, C, seed=1), tmp,
+                         bx.WriterConfig(seed=1, compress_probability=1.0, compress_codec=bx.CodecId.JPEG,
+                                         jpeg=bx.JpegParams(90, "4:2:0", restart_blocks=RST_BLOCKS),
+                                         num_encode_workers=min(16, os.cpu_count() or 1)))
+        os.replace(tmp, path)
+        log(f"wrote {path} ({path.stat().st_size / 1e6:.0f} MB) in {time.time() - t0:.1f}s")
+    barrier()
+    return path
+
+
 def ensure_dataset(rank: int, barrier) -> Path:
     import paper_2306_12517_b200 as bx
 
@@ -131,11 +160,11 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_loader(path, device, rank, world, strategy, slot_count=3):
+def make_loader(path, device, rank, world, strategy, slot_count=3, batch=B):
     import paper_2306_12517_b200 as bx
 
     ds = bx.open_dataset(path, strategy)
-    cfg = bx.LoaderConfig(batch_size=B, order=bx.OrderKind.RANDOM, seed=SEED, slot_count=slot_count,
+    cfg = bx.LoaderConfig(batch_size=batch, order=bx.OrderKind.RANDOM, seed=SEED, slot_count=slot_count,
                           pipelines={"image": bx.parse_pipeline(CHAIN_SPEC)}, device=device,
                           distributed=world > 1, rank=rank, world_size=world)
     return ds, bx.Loader(ds, cfg)
@@ -171,8 +200,8 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
     return reduce_max(secs), d2h / steps
 
 
-def cpu_baseline(path, seconds_budget: float = 15.0):
-    """Oracle C port on the host cores, bounded sample (whole batches of 512)."""
+def cpu_baseline(path, seconds_budget: float = 15.0, batch=B, what="RRC-192+flip+normalize->f16"):
+    """Oracle C port on the host cores, bounded sample (whole batches)."""
     import numpy as np
 
     from oracle import oracle as O
@@ -181,16 +210,89 @@ def cpu_baseline(path, seconds_budget: float = 15.0):
     field = f.fields[0]
     ops = O.parse_spec("decode")[:0] + O.parse_spec(ORACLE_SPEC)
     threads = os.cpu_count() or 1
-    batches = O.epoch_batches("random", SEED, 0, f.num_samples, B)
+    batches = O.epoch_batches("random", SEED, 0, f.num_samples, batch)
     done, t0 = 0, time.perf_counter()
     out = None
     while time.perf_counter() - t0 < seconds_budget and done < len(batches):
         out = O.run_field_batch(f, field, 0, ops, batches[done], SEED, 0, threads, out=out)
         done += 1
     el = time.perf_counter() - t0
-    return {"value": done * B / el, "unit": "images/s", "cores": threads, "kind": "port",
-            "sample": f"{done} batches x {B} images of {path.name} (RRC-192+flip+normalize->f16), "
+    return {"value": done * batch / el, "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{done} batches x {batch} images of {path.name} ({what}), "
                       f"{threads} threads, {el:.1f}s"}
+
+
+def h2d_peak_gbs(device) -> float:
+    """Pinned host -> device copy bandwidth on this box (best of 5, 256 MB)."""
+    import torch
+
+    src = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    best = 0.0
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, src.numel() / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return best
+
+
+def jpeg_workload(args, device, rank, world, barrier, reduce_max):
+    """configs[2]: JPEG q90 RRC-192 + flip + normalize -> f16, batch 1024 per GPU."""
+    import paper_2306_12517_b200 as bx
+
+    path = ensure_jpeg_dataset(rank, barrier)
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=JPEG_B)
+    ld.set_profiling(True)
+    with ClockSampler(device) as clk:
+        secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
+    st = ld.stats()
+    ld.shutdown()
+    ds.close()
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B)
+    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
+    st2 = ld2.stats()
+    ld2.shutdown()
+    ds2.close()
+    value = world * args.steps * JPEG_B / secs
+    e2e = world * args.steps * JPEG_B / e2e_secs
+    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
+    kern_s = st["kernel_seconds"] / max(st["batches"], 1)
+    payload_per_img = os.path.getsize(path) / JPEG_SAMPLES   # file bytes / samples (≈ compressed size)
+    hbm_peak, _ = peaks()
+    pcie = h2d_peak_gbs(device)
+    # per image: compressed read + coef (w+r) + planes (w+r) + RGB (w+r) + window read + f16 output
+    hbm_img = payload_per_img + 2 * 1.5 * H * W * 2 + 2 * 1.5 * H * W + 2 * H * W * C + OUT * OUT * C * 2
+    roof_pcie = pcie * 1e9 / max(h2d / JPEG_B, 1.0)
+    roof_hbm = hbm_peak * 1e9 / hbm_img
+    out = {
+        "workload": f"configs[2]: ImageNet-shaped synthetic JPEG .bbox (q90, 4:2:0, RST every {RST_BLOCKS} MCUs, "
+                    "longer side 256), RandomResizedCrop 192 + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC",
+        "batch_per_gpu": JPEG_B, "num_samples": JPEG_SAMPLES, "mean_file_bytes_per_image": payload_per_img,
+        "value": value, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
+        "device_ms_per_batch": kern_s * 1e3,
+        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_secs / args.steps * 1e3,
+                "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
+                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9},
+        "roofline": {"pcie_h2d_peak_gbs": pcie, "hbm_peak_gbs": hbm_peak,
+                     "pcie_images_per_s": roof_pcie, "hbm_images_per_s": roof_hbm,
+                     "binding": "pcie" if roof_pcie < roof_hbm else "hbm",
+                     "e2e_frac": e2e / min(roof_pcie, roof_hbm), "value_frac_hbm": value / roof_hbm,
+                     "note": "Huffman decode is serial integer work per restart interval; neither bandwidth binds "
+                             "the device path (see profiles/ for the per-kernel split)"},
+        "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
+    }
+    if world == 1 and rank == 0:
+        try:
+            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 2, JPEG_B,
+                                               "JPEG decode (oracle restatement of libjpeg-turbo) + RRC-192 + flip "
+                                               "+ normalize -> f16; restatement, not the reference")
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    return out
 
 
 def load_traffic():
@@ -218,6 +320,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--workloads", default="raw,jpeg", help="raw (configs[1], the headline) and/or jpeg (configs[2])")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -312,6 +415,10 @@ def main():
     e2e = world * args.steps * B / e2e_secs
     h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
 
+    jpeg = None
+    if "jpeg" in args.workloads.split(","):
+        jpeg = jpeg_workload(args, device, rank, world, barrier, reduce_max)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -341,6 +448,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds)
         except Exception as e:   # the baseline must not sink the GPU line
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if jpeg is not None:
+        line["workloads"] = {"configs[2]": jpeg}
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()

@@ -101,9 +101,11 @@ static int huff_decode(oj_reader* r, const oj_huff* t, int* sym) {   /* T.81 F.1
   return 0;
 }
 
-static int build_huff(oj_huff* t, const uint8_t counts[16], const uint8_t* vals, int nvals) {
+static int build_huff(oj_huff* t, const uint8_t counts[16], const uint8_t* vals, int nvals, int is_dc) {
   int k = 0, code = 0;
   memset(t, 0, sizeof *t);
+  if (is_dc)                                       /* DC symbols are categories 0..15 (jdhuff.c check) */
+    for (int i = 0; i < nvals; ++i) if (vals[i] > 15) return 1;
   for (int l = 1; l <= 16; ++l) {
     t->valptr[l] = k;
     t->mincode[l] = code;
@@ -272,7 +274,7 @@ int or_jpeg_decode(const uint8_t* d, int64_t n, int want_h, int want_w, int want
         int tc = s[k] >> 4, th = s[k] & 15, tot = 0;
         for (int i = 0; i < 16; ++i) tot += s[k + 1 + i];
         if (tc > 1 || th > 3 || k + 17 + tot > sl) return fail(e, "bad DHT");
-        if (build_huff(tc ? &ac[th] : &dc[th], s + k + 1, s + k + 17, tot)) return fail(e, "bad Huffman table");
+        if (build_huff(tc ? &ac[th] : &dc[th], s + k + 1, s + k + 17, tot, !tc)) return fail(e, "bad Huffman table");
         k += 17 + tot;
       }
     } else if (m == 0xDB) {

@@ -36,7 +36,8 @@ class JpegParams:
     """Writer-side JPEG settings (FFCV's RGBImageField(jpeg_quality=90) analogue)."""
     quality: int = 90
     subsampling: str = "4:2:0"     # "4:4:4" | "4:2:2" | "4:2:0"
-    restart_rows: int = 1          # DRI = this many MCU rows (0: no restart markers)
+    restart_rows: int = 0          # DRI = this many MCU rows (takes precedence when > 0)
+    restart_blocks: int = 4        # else DRI = this many MCUs (0 and rows 0: no restart markers)
 
 
 def encode_jpeg(px: np.ndarray, params: JpegParams | None = None) -> bytes:
@@ -53,8 +54,12 @@ def encode_jpeg(px: np.ndarray, params: JpegParams | None = None) -> bytes:
     kw = {"quality": int(params.quality)}
     if c == 3:
         kw["subsampling"] = params.subsampling
+    # Restart intervals are the device decoder's unit of parallelism (one
+    # thread each); 4 MCUs cost ~0.7% in file size at q90.
     if params.restart_rows:
         kw["restart_marker_rows"] = int(params.restart_rows)
+    elif params.restart_blocks:
+        kw["restart_marker_blocks"] = int(params.restart_blocks)
     bio = io.BytesIO()
     im.save(bio, "JPEG", **kw)
     return bio.getvalue()

@@ -131,7 +131,8 @@ struct Plan {
   int64_t jpeg_blocks_cap = 0;   // per sample: coefficient blocks (any sampling with factors <= 2)
   int64_t jpeg_int_cap = 0;      // per sample: restart intervals (<= MCUs)
   int16_t* d_coef = nullptr;     // JPEG scratch shared by the slots (one compute stream orders them)
-  uint8_t* d_planes = nullptr;
+  uint8_t* d_bits = nullptr;     // unstuffed restart-interval bitstreams
+  int64_t jpeg_bits_cap = 0;     // per sample
   uint32_t* d_istart = nullptr;
   uint32_t* d_iend = nullptr;
   void* d_lut = nullptr;
@@ -166,7 +167,8 @@ struct Slot {
   std::vector<char> plan_has_jpeg;
   std::vector<uint32_t> jpeg_total_int;
   std::vector<uint64_t> jpeg_total_blk;
-  std::vector<int32_t> jpeg_max_pix;
+  std::vector<int32_t> jpeg_max_rows;
+  std::vector<int32_t> jpeg_pix_smem;
 };
 
 // Device pools of the Huffman / quant tables the JPEG samples reference,
@@ -510,6 +512,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     const int64_t mh = f.info.max_height, mw = f.info.max_width;
     pl.jpeg_blocks_cap = (int64_t)f.info.channels * (2 * ((mh + 15) / 16)) * (2 * ((mw + 15) / 16));
     pl.jpeg_int_cap = ((mh + 7) / 8) * ((mw + 7) / 8);
+    pl.jpeg_bits_cap = (mx + 4 * pl.jpeg_int_cap + 32 + 15) / 16 * 16;
   }
   return BBX_OK;
 }
@@ -634,13 +637,14 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
 static void pipeline_loop(bbx_loader* L);
 
 // Table pool ids for one JPEG header (registering unseen tables).
-static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, int* id) {
-  std::string key(reinterpret_cast<const char*>(h.counts), 16);
+static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, bool is_ac, int* id) {
+  std::string key(1, is_ac ? 'A' : 'D');
+  key.append(reinterpret_cast<const char*>(h.counts), 16);
   key.append(reinterpret_cast<const char*>(h.vals), h.nvals);
   auto it = T.hmap.find(key);
   if (it != T.hmap.end()) { *id = it->second; return 0; }
   if (T.n_huff >= kJpegMaxHuff) return 2;
-  if (!jpeg_build_huff(h, &T.h_huff[T.n_huff])) return 1;
+  if (!jpeg_build_huff(h, is_ac, &T.h_huff[T.n_huff])) return 1;
   *id = T.hmap[key] = T.n_huff++;
   return 0;
 }
@@ -684,7 +688,7 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
     const auto& c = H.comp[i];
     JComp& o = J->comp[i];
     int dc, ac, q, r;
-    if ((r = jpeg_table_id(T, H.dc[c.td], &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], &ac)) ||
+    if ((r = jpeg_table_id(T, H.dc[c.td], false, &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], true, &ac)) ||
         (r = jpeg_quant_id(T, H.qt[c.tq], &q)))
       return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
     o.dc = (uint16_t)dc; o.ac = (uint16_t)ac; o.q = (uint16_t)q;
@@ -704,13 +708,25 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
   J->n_int = (total + J->restart - 1) / J->restart;
   J->ncomp = (uint8_t)H.ncomp; J->hmax = (uint8_t)hmax; J->vmax = (uint8_t)vmax;
   J->n_blocks = blocks;
-  if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap)
+  int bpm = 0;                                   // MCU block order (T.81 A.2.3): comps, then rows, then columns
+  for (int i = 0; i < H.ncomp; ++i)
+    for (int v = 0; v < J->comp[i].v; ++v)
+      for (int h = 0; h < J->comp[i].h; ++h, ++bpm)
+        J->sched |= (uint64_t)(i | v << 2 | h << 3) << (4 * bpm);
+  J->bpm = (uint8_t)bpm;
+  if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap ||
+      (int64_t)len + 4 * (int64_t)J->n_int + 32 > pl.jpeg_bits_cap)
     return bad("jpeg: geometry exceeds the field's device capacity");
   return true;
 }
 
-static size_t jpeg_block_bytes(int B) {
-  return ((size_t)B * sizeof(JpegDesc) + (size_t)(B + 1) * 4 + 7) / 8 * 8 + (size_t)(B + 1) * 8;
+static size_t jpeg_block_bytes(int B) { return (size_t)B * sizeof(JpegDesc) + (size_t)(B + 1) * 4; }
+
+// J3 shared memory of one sample: the windows of its components for one MCU row.
+static int jpeg_pix_smem(const JpegDesc& J) {
+  int b = 0;
+  for (int c = 0; c < J.ncomp; ++c) b += jpeg_window_rows(J.comp[c].v, J.vmax) * J.comp[c].bw * 8;
+  return b;
 }
 
 static int finalize(bbx_loader* L) {
@@ -772,7 +788,7 @@ static int finalize(bbx_loader* L) {
     if (pl.scalar || !pl.field_has_jpeg) continue;
     const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
     CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
-    CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
+    CK(cudaMalloc(&pl.d_bits, (size_t)L->batch * pl.jpeg_bits_cap + 256));
     CK(cudaMalloc(&pl.d_istart, ints * 4 + 64));
     CK(cudaMalloc(&pl.d_iend, ints * 4 + 64));
   }
@@ -823,7 +839,8 @@ static int process_slot(bbx_loader* L, int s) {
   S.plan_has_jpeg.assign(L->plans.size(), 0);
   S.jpeg_total_int.assign(L->plans.size(), 0);
   S.jpeg_total_blk.assign(L->plans.size(), 0);
-  S.jpeg_max_pix.assign(L->plans.size(), 0);
+  S.jpeg_max_rows.assign(L->plans.size(), 0);
+  S.jpeg_pix_smem.assign(L->plans.size(), 0);
   uint8_t* H = S.h_stage;
   std::memcpy(H + L->idx_off, S.idx.data(), (size_t)count * 8);
   for (int64_t pos = 0; pos < count; ++pos) {
@@ -901,23 +918,26 @@ static int process_slot(bbx_loader* L, int s) {
     uint8_t* jb = H + L->jpeg_off[p];
     JpegDesc* jds = reinterpret_cast<JpegDesc*>(jb);
     uint32_t* ipre = reinterpret_cast<uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
-    uint64_t* bpre = reinterpret_cast<uint64_t*>(jb + ((size_t)L->batch * sizeof(JpegDesc) + (size_t)(L->batch + 1) * 4 + 7) / 8 * 8);
     const uint8_t* dblk = H + L->desc_off[p];
     uint32_t ti = 0;
-    uint64_t tb = 0;
-    int32_t mp = 0;
+    uint64_t tb = 0, bs = 0;
+    int32_t mr = 0, ps = 0;
     for (int pos = 0; pos < count; ++pos) {
       JpegDesc& J = jds[pos];
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
       if (d->skip) J.n_int = 0;
       if (J.n_int == 0) J.n_blocks = 0;
-      J.int_base = ti; J.blk_base = tb;
-      ipre[pos] = ti; bpre[pos] = tb;
+      J.int_base = ti; J.blk_base = tb; J.bs_base = bs;
+      ipre[pos] = ti;
       ti += J.n_int; tb += J.n_blocks;
-      if (J.n_int) mp = std::max(mp, (int32_t)d->h * d->w);
+      if (J.n_int) {
+        bs += (uint64_t)pl.jpeg_bits_cap;
+        mr = std::max(mr, (int32_t)J.mcus_y);
+        ps = std::max(ps, jpeg_pix_smem(J));
+      }
     }
-    ipre[count] = ti; bpre[count] = tb;
-    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_pix[p] = mp;
+    ipre[count] = ti;
+    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_rows[p] = mr; S.jpeg_pix_smem[p] = ps;
     if (ti == 0) S.plan_has_jpeg[p] = 0;
   }
   {   // new JPEG tables: append-only upload ahead of this slot's H2D (same copy stream)
@@ -1027,13 +1047,15 @@ static int process_slot(bbx_loader* L, int s) {
       J.desc = A.desc; J.desc_stride = pl.dev.desc_stride; J.payload = A.payload;
       J.jd = reinterpret_cast<const JpegDesc*>(jb);
       J.int_prefix = reinterpret_cast<const uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
-      J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + ((size_t)L->batch * sizeof(JpegDesc) + (size_t)(L->batch + 1) * 4 + 7) / 8 * 8);
-      J.istart = pl.d_istart; J.iend = pl.d_iend; J.coef = pl.d_coef; J.planes = pl.d_planes;
+      J.istart = pl.d_istart; J.iend = pl.d_iend; J.bits = pl.d_bits; J.coef = pl.d_coef;
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
-      J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.status = A.status; J.count = count;
-      J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_pixels = S.jpeg_max_pix[p];
+      J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
+      J.total_int = S.jpeg_total_int[p]; J.max_mcu_rows = S.jpeg_max_rows[p]; J.pix_smem = S.jpeg_pix_smem[p];
+      if (J.pix_smem > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "jpeg: image rows too wide for the device decoder");
+      // J2 stores only nonzero coefficients
+      CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
       if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      launches += 4; any_jpeg = true;
+      launches += 3; any_jpeg = true;
     }
     int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, L->comp_st) : launch_image(pl.dev, A, L->comp_st);
     if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
@@ -1094,6 +1116,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   Plan pl;
   pl.jpeg_blocks_cap = (int64_t)c * (2 * ((h + 15) / 16)) * (2 * ((w + 15) / 16));
   pl.jpeg_int_cap = (int64_t)((h + 7) / 8) * ((w + 7) / 8);
+  pl.jpeg_bits_cap = (len + 4 * pl.jpeg_int_cap + 32 + 15) / 16 * 16;
   uint8_t desc[64] = {0};
   SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
   d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = CODEC_JPEG;
@@ -1102,24 +1125,24 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   bool ok = jpeg_prepare(&L, pl, pay, (uint32_t)len, d, &J, err, 0, 0);
   L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
   if (!ok) return fail(err.code, "%s", err.msg.c_str());
-  J.int_base = 0; J.blk_base = 0;
-  // device image: [desc 64][jd][prefixes][payload (+16 pad)] then tables, intervals, coef, planes, status
-  const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_bp = o_ip + 16, o_pay = o_bp + 16;
+  J.int_base = 0; J.blk_base = 0; J.bs_base = 0;
+  const int pix = jpeg_pix_smem(J);
+  if (pix > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "jpeg: image rows too wide for the device decoder");
+  // device image: [desc 64][jd][prefix][payload (+16 pad)] then tables, intervals, bits, coef, status
+  const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_pay = o_ip + 16;
   const size_t o_hf = (o_pay + len + 16 + 255) / 256 * 256;
   const size_t o_q = o_hf + sizeof(JHuff) * L.jt.n_huff;
   const size_t o_is = (o_q + sizeof(JQuant) * L.jt.n_quant + 255) / 256 * 256;
   const size_t o_ie = o_is + 4 * (size_t)J.n_int + 16;
-  const size_t o_cf = (o_ie + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
-  const size_t o_pl = o_cf + 128 * (size_t)J.n_blocks;
-  const size_t o_st = (o_pl + 64 * (size_t)J.n_blocks + 255) / 256 * 256;
+  const size_t o_bs = (o_ie + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
+  const size_t o_cf = (o_bs + (size_t)pl.jpeg_bits_cap + 255) / 256 * 256;
+  const size_t o_st = (o_cf + 128 * (size_t)J.n_blocks + 255) / 256 * 256;
   const size_t total = o_st + sizeof(SampleStatus);
   std::vector<uint8_t> img(o_is, 0);
   std::memcpy(img.data(), desc, 64);
   std::memcpy(img.data() + o_jd, &J, sizeof J);
   const uint32_t ip[2] = {0, J.n_int};
-  const uint64_t bp[2] = {0, J.n_blocks};
   std::memcpy(img.data() + o_ip, ip, sizeof ip);
-  std::memcpy(img.data() + o_bp, bp, sizeof bp);
   std::memcpy(img.data() + o_pay, pay, (size_t)len);
   std::memcpy(img.data() + o_hf, hh.data(), sizeof(JHuff) * L.jt.n_huff);
   std::memcpy(img.data() + o_q, hq.data(), sizeof(JQuant) * L.jt.n_quant);
@@ -1127,17 +1150,18 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   CK(cudaMalloc(&dev, total));
   cudaError_t e = cudaMemcpy(dev, img.data(), img.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(dev + o_st, 0, sizeof(SampleStatus));
+  if (e == cudaSuccess) e = cudaMemset(dev + o_cf, 0, 128 * (size_t)J.n_blocks);
   JpegArgs A{};
   A.desc = dev; A.desc_stride = 64; A.payload = dev + o_pay;
   A.jd = reinterpret_cast<const JpegDesc*>(dev + o_jd);
   A.int_prefix = reinterpret_cast<const uint32_t*>(dev + o_ip);
-  A.blk_prefix = reinterpret_cast<const uint64_t*>(dev + o_bp);
   A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
-  A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
+  A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf);
   A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
+  A.n_huff = L.jt.n_huff;
   A.status = reinterpret_cast<SampleStatus*>(dev + o_st);
-  A.count = 1; A.total_int = J.n_int; A.total_blocks = J.n_blocks; A.max_pixels = h * w;
+  A.count = 1; A.total_int = J.n_int; A.max_mcu_rows = J.mcus_y; A.pix_smem = pix;
   int rc = e == cudaSuccess ? launch_jpeg(A, nullptr) : 1;
   SampleStatus st{};
   if (e == cudaSuccess) e = cudaMemcpy(&st, dev + o_st, sizeof st, cudaMemcpyDeviceToHost);
@@ -1448,7 +1472,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     for (auto* p : pl.d_scratch) if (p) cudaFree(p);
     for (auto* p : pl.d_tables) if (p) cudaFree(p);
     if (pl.d_coef) cudaFree(pl.d_coef);
-    if (pl.d_planes) cudaFree(pl.d_planes);
+    if (pl.d_bits) cudaFree(pl.d_bits);
     if (pl.d_istart) cudaFree(pl.d_istart);
     if (pl.d_iend) cudaFree(pl.d_iend);
   }

@@ -1,32 +1,52 @@
 // JPEG codec (codec id 3): host header parse + device decoder.  Shared by
-// jpeg_host.cpp (parse, table registry), jpeg.cu (kernels) and engine.cpp.
+// jpeg_host.cpp (parse, table build), jpeg.cu (kernels) and engine.cpp.
 //
 // Device pipeline for the JPEG samples of one batch:
-//   J1 jpeg_scan_kernel     warp per sample: RSTn marker search over the
-//                           entropy-coded segment -> start/end of every
-//                           restart interval (T.81 F.1.2.3 / B.2.5)
-//   J2 jpeg_huffman_kernel  thread per restart interval: Huffman decode of
-//                           the interval's MCUs (T.81 F.2.2) -> int16
-//                           coefficient blocks, natural order
-//   J3 jpeg_idct_kernel     thread per block: dequantize + islow IDCT -> u8
-//                           component planes
-//   J4 jpeg_color_kernel    thread per pixel: fancy chroma upsampling +
-//                           YCbCr -> RGB into the sample's decode scratch,
-//                           which K1 then reads like an RLE-expanded image
+//   J1 jpeg_unstuff_kernel   warp per sample: finds the RSTn markers of the
+//                            entropy-coded segment (T.81 B.2.5 / F.1.2.3),
+//                            drops marker and stuffing bytes and writes every
+//                            restart interval as a 4-byte-aligned plain
+//                            bitstream (so J2 refills 32 bits per load, no
+//                            0xFF checks)
+//   J2 jpeg_huffman_kernel   thread per restart interval: one flat loop, one
+//                            symbol per iteration (T.81 F.2.2), shared-memory
+//                            tables that resolve code + extra bits in one
+//                            lookup; coefficient blocks built in shared memory,
+//                            stored as int16[64] natural order
+//   J3 jpeg_pixels_kernel    CTA per (sample, MCU row): islow IDCT of the
+//                            row's blocks (plus the chroma block rows above /
+//                            below that fancy upsampling reads) into shared
+//                            memory, then upsampling + YCbCr->RGB into the
+//                            sample's decode scratch, which K1 reads like an
+//                            RLE-expanded image
 #pragma once
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define BBX_HD __host__ __device__
+#else
+#define BBX_HD
+#endif
+
 namespace bbx {
 
-constexpr int kJpegLook = 9;              // Huffman lookahead bits (fast table)
+constexpr int kJpegFastBits = 10;         // Huffman lookahead bits (fast table)
 constexpr int kJpegMaxHuff = 512;         // device Huffman table pool entries
 constexpr int kJpegMaxQuant = 256;        // device quant table pool entries
+constexpr int kJpegSmemTables = 8;        // J2 stages the pool in smem when it holds at most this many
+
+// Fast-table entry (u32) indexed by the next kJpegFastBits bits of the stream,
+// for codes of at most kJpegFastBits bits (0 otherwise: maxcode walk):
+//   bits 0..4 code length, 5..9 extra bits (size), 10..13 zero run,
+//   bit 14 end of block (AC size 0, run < 15), bit 31 valid
+constexpr uint32_t kFastValid = 1u << 31, kFastEob = 1u << 14;
 
 struct JHuff {                            // one Huffman table, device form
-  uint16_t look[1 << kJpegLook];          // (len << 8) | symbol; 0 = code longer than kJpegLook
+  uint32_t fast[1 << kJpegFastBits];
   int32_t maxcode[18];                    // largest code of each length, -1 if none; [17] sentinel
   int32_t valoff[18];                     // vals index = code + valoff[len]
   uint8_t vals[256];
+  int32_t is_ac, pad[3];
 };
 struct JQuant { uint16_t q[64]; };        // natural order
 
@@ -44,44 +64,50 @@ struct JpegDesc {                         // per sample, staged with the descrip
   uint32_t scan_end;                      // payload length
   uint16_t mcus_x, mcus_y;
   uint32_t restart;                       // MCUs per interval (all MCUs when no DRI)
-  uint8_t ncomp, hmax, vmax, pad0;
+  uint8_t ncomp, hmax, vmax, bpm;         // bpm: blocks per MCU
   uint32_t n_int;                         // restart intervals (0: not a JPEG sample)
   uint32_t int_base;                      // first interval in the batch interval table
   uint32_t n_blocks;
-  uint64_t blk_base;                      // first block in the batch coefficient / plane buffers
+  uint64_t blk_base;                      // first block in the batch coefficient buffer
+  uint64_t bs_base;                       // first byte of the sample's unstuffed bitstream
+  uint64_t sched;                         // MCU block b: comp bits 4b..4b+1, v bit 4b+2, h bit 4b+3
   JComp comp[3];
   uint32_t pad1[3];
 };
-static_assert(sizeof(JpegDesc) == 112, "JpegDesc layout");
+static_assert(sizeof(JpegDesc) == 128, "JpegDesc layout");
 
 // Per-sample status kinds written by J1/J2 (SampleStatus::kind).
 enum : int32_t { JST_BAD_CODE = 3, JST_MARKER_COUNT = 4, JST_MARKER_SEQ = 5 };
 
 // Everything the JPEG kernels need for one batch of one plan.
 struct JpegArgs {
-  const uint8_t* desc;                    // SampleDesc array (P.desc_stride apart)
+  const uint8_t* desc;                    // SampleDesc array (desc_stride apart)
   int32_t desc_stride;
   const uint8_t* payload;                 // payload base (staged region or resident heap)
   const JpegDesc* jd;                     // count entries
   const uint32_t* int_prefix;             // count + 1: exclusive prefix of n_int
-  const uint64_t* blk_prefix;             // count + 1: exclusive prefix of n_blocks
-  uint32_t* istart;                       // interval tables (total intervals)
+  uint32_t* istart;                       // per interval: bitstream start / end (sample-relative)
   uint32_t* iend;
+  uint8_t* bits;                          // unstuffed bitstreams
   int16_t* coef;                          // total blocks x 64
-  uint8_t* planes;                        // total blocks x 64 (component planes)
   uint8_t* scratch;                       // count x scratch_bytes: decoded HWC u8
   int64_t scratch_bytes;
   const JHuff* huff;                      // table pools
   const JQuant* quant;
+  int32_t n_huff;                         // pool entries in use
   struct SampleStatus* status;
   int32_t count;
   uint32_t total_int;
-  uint64_t total_blocks;
-  int32_t max_pixels;                     // largest h*w in the batch
+  int32_t max_mcu_rows;                   // largest mcus_y in the batch
+  int32_t pix_smem;                       // J3 dynamic shared memory bytes
 };
 
 // jpeg.cu
 int launch_jpeg(const JpegArgs& A, void* stream);
+
+// J3 shared-memory window of component c for one MCU row: its own pixel rows
+// plus one block row above and below when it is vertically upsampled.
+BBX_HD inline int jpeg_window_rows(int v, int vmax) { return 8 * v + (vmax / v == 2 ? 16 : 0); }
 
 // jpeg_host.cpp
 struct JpegHeader {
@@ -95,6 +121,6 @@ struct JpegHeader {
 // Parses markers up to SOS.  Returns 0, or fills *err with the reason.
 int jpeg_parse_header(const uint8_t* p, uint64_t n, JpegHeader* h, char* err, int errlen);
 // Builds the device form of a DHT table; false if it is malformed.
-bool jpeg_build_huff(const JpegHeader::Huff& t, JHuff* out);
+bool jpeg_build_huff(const JpegHeader::Huff& t, bool is_ac, JHuff* out);
 
 }  // namespace bbx

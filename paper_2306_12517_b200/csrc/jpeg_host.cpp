@@ -113,9 +113,13 @@ int jpeg_parse_header(const uint8_t* d, uint64_t n, JpegHeader* h, char* err, in
 }
 
 // Canonical code assignment (T.81 C.2, F.15): per length, codes are
-// consecutive; the lookahead table covers every code of <= kJpegLook bits.
-bool jpeg_build_huff(const JpegHeader::Huff& t, JHuff* o) {
+// consecutive.  The fast table resolves every code of <= kJpegFastBits bits
+// to (length, extra bits, zero run, end of block).
+bool jpeg_build_huff(const JpegHeader::Huff& t, bool is_ac, JHuff* o) {
   std::memset(o, 0, sizeof *o);
+  if (!is_ac)
+    for (int i = 0; i < t.nvals; ++i) if (t.vals[i] > 15) return false;   // DC categories (jdhuff.c check)
+  constexpr int F = kJpegFastBits;
   int k = 0, code = 0;
   for (int l = 1; l <= 16; ++l) {
     const int cnt = t.counts[l - 1];
@@ -123,10 +127,13 @@ bool jpeg_build_huff(const JpegHeader::Huff& t, JHuff* o) {
     o->maxcode[l] = cnt ? code + cnt - 1 : -1;
     for (int i = 0; i < cnt; ++i, ++k, ++code) {
       if (code >= (1 << l) || k >= 256) return false;
-      if (l <= kJpegLook) {
-        const int sh = kJpegLook - l;
-        for (int f = 0; f < (1 << sh); ++f) o->look[(code << sh) | f] = (uint16_t)((l << 8) | t.vals[k]);
-      }
+      if (l > F) continue;
+      const int sym = t.vals[k];
+      const int size = is_ac ? (sym & 15) : sym, run = is_ac ? (sym >> 4) : 0;
+      const int sh = F - l;
+      const uint32_t e = kFastValid | (uint32_t)l | (uint32_t)size << 5 | (uint32_t)run << 10 |
+                         ((is_ac && size == 0 && run != 15) ? kFastEob : 0u);   // EOB / ZRL: jdhuff.c rule
+      for (int f = 0; f < (1 << sh); ++f) o->fast[(code << sh) | f] = e;
     }
     if (code >= (1 << l)) return false;   // over-subscribed or an all-ones code (jdhuff.c rule)
     code <<= 1;
@@ -134,6 +141,7 @@ bool jpeg_build_huff(const JpegHeader::Huff& t, JHuff* o) {
   o->maxcode[17] = 0x7fffffff;
   if (k != t.nvals) return false;
   std::memcpy(o->vals, t.vals, k);
+  o->is_ac = is_ac ? 1 : 0;
   return true;
 }
 

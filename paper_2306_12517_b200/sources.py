@@ -87,6 +87,14 @@ class PhotoLikeSource:
         self.schema = [image_field("image", max_height, max_width, channels), int_field("label")]
         if array_dim:
             self.schema.append(array_field("x", np.float32, (array_dim,)))
+        # shared gradient + noise bank (built once: __getitem__ runs on writer threads)
+        yy = np.arange(max_height, dtype=np.int32)[:, None, None]
+        xx = np.arange(max_width, dtype=np.int32)[None, :, None]
+        cc = np.arange(channels, dtype=np.int32)[None, None, :]
+        self._pattern = ((yy * (1 + cc) // 2 + xx * (3 - cc) // 2 + cc * 40) & 0xFF).astype(np.uint8)
+        g = np.random.default_rng([seed, 0x5EED])
+        nb = max_height * max_width * channels + (1 << 16)
+        self._noise = g.integers(-noise, noise + 1, size=nb, dtype=np.int16).astype(np.int8).view(np.uint8)
 
     def __len__(self) -> int:
         return self.num_samples
@@ -100,23 +108,24 @@ class PhotoLikeSource:
             return self.max_height, max(1, int(self.max_width * frac))
         return max(1, int(self.max_height * frac)), self.max_width
 
+    def _tables(self):
+        return self._pattern, self._noise
+
     def __getitem__(self, i: int) -> dict:
         if not 0 <= i < self.num_samples:
             raise IndexError(i)
         r = Rng(stream_seed(self.seed, TAG_SYNTH, i))
         label = r.below(self.num_classes)
+        base = np.array([r.below(256) for _ in range(self.channels)], dtype=np.uint8)
+        off = r.below(1 << 16)
         h, w = self.dims_of(i)
-        g = np.random.default_rng([self.seed, i])
-        yy = np.arange(h, dtype=np.int32)[:, None, None]
-        xx = np.arange(w, dtype=np.int32)[None, :, None]
-        cc = np.arange(self.channels, dtype=np.int32)[None, None, :]
-        base = g.integers(0, 256, size=self.channels, dtype=np.int32)[None, None, :]
-        img = base + yy * (1 + cc) // 2 + xx * (3 - cc) // 2 + cc * 40
+        pattern, noise = self._tables()
+        img = pattern[:h, :w] + base                           # u8 wrap-around arithmetic
         if self.noise:
-            img = img + g.integers(-self.noise, self.noise + 1, size=(h, w, self.channels), dtype=np.int32)
-        out = {"image": (img & 0xFF).astype(np.uint8), "label": label}
+            img += noise[off:off + h * w * self.channels].reshape(h, w, self.channels)
+        out = {"image": img, "label": label}
         if self.array_dim:
-            out["x"] = g.standard_normal(self.array_dim, dtype=np.float32)
+            out["x"] = np.random.default_rng([self.seed, i]).standard_normal(self.array_dim, dtype=np.float32)
         return out
 
 

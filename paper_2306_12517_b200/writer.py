@@ -114,29 +114,29 @@ def write_dataset(source, path, config: WriterConfig | None = None, schema=None)
     fd = os.open(path, os.O_RDWR | os.O_CREAT | os.O_TRUNC, 0o644)
     try:
         heap = _PagedHeap(fd, heap_offset, page)
-        for i in range(n):
+        def encode_sample(i):
+            """Source read + image encode of sample i (no allocation: thread-safe)."""
             try:
                 values = source[i]
             except Exception as e:
                 raise SourceError(f"sample {i}: {e}") from e
             draw = Rng(stream_seed(config.seed, TAG_CODEC, i))
-            cells = []
+            out = []
             for f in schema:
                 if f.name not in values:
                     raise SchemaMismatch(f"sample {i} missing field {f.name!r}")
                 v = values[f.name]
                 if f.kind == FieldKind.INT_SCALAR:
-                    cells.append(int(v))
+                    out.append(int(v))
                 elif f.kind == FieldKind.FLOAT_SCALAR:
-                    cells.append(float(v))
+                    out.append(float(v))
                 elif f.kind == FieldKind.FIXED_ARRAY:
                     arr = np.ascontiguousarray(v, dtype=f.array_dtype)
                     if arr.shape != tuple(f.array_dims):
                         raise SchemaMismatch(f"sample {i} field {f.name!r}: shape {arr.shape} != {f.array_dims}")
-                    cells.append(heap.put(arr.tobytes()))
+                    out.append(("heap", arr.tobytes()))
                 elif f.kind == FieldKind.VAR_BYTES:
-                    data = bytes(v)
-                    cells.append(VarBytesCell(heap.put(data), len(data)) if data else VarBytesCell(0, 0))
+                    out.append(("var", bytes(v)))
                 else:
                     codec = config.compress_codec if draw.chance(config.compress_probability) else CodecId.RAW
                     blob = encode_image(np.asarray(v), codec, max_height=f.max_height, max_width=f.max_width,
@@ -144,6 +144,34 @@ def write_dataset(source, path, config: WriterConfig | None = None, schema=None)
                     if blob.channels != f.channels:
                         raise SchemaMismatch(
                             f"sample {i} field {f.name!r}: {blob.channels} channels != {f.channels}")
+                    out.append(("image", blob, codec))
+            return out
+
+        def encoded():
+            if config.num_encode_workers <= 1:
+                for i in range(n):
+                    yield i, encode_sample(i)
+                return
+            from concurrent.futures import ThreadPoolExecutor
+
+            chunk = 64 * config.num_encode_workers
+            with ThreadPoolExecutor(config.num_encode_workers) as ex:
+                for c0 in range(0, n, chunk):
+                    for i, enc in zip(range(c0, min(n, c0 + chunk)), ex.map(encode_sample, range(c0, min(n, c0 + chunk)))):
+                        yield i, enc
+
+        for i, enc in encoded():   # allocation stays sequential: the layout is worker-count independent
+            cells = []
+            for item in enc:
+                if not isinstance(item, tuple):
+                    cells.append(item)
+                elif item[0] == "heap":
+                    cells.append(heap.put(item[1]))
+                elif item[0] == "var":
+                    data = item[1]
+                    cells.append(VarBytesCell(heap.put(data), len(data)) if data else VarBytesCell(0, 0))
+                else:
+                    _, blob, codec = item
                     off = heap.put(blob.payload)
                     cells.append(ImageCell(off, len(blob.payload), blob.height, blob.width, blob.channels,
                                            int(codec)))

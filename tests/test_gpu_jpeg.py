@@ -41,7 +41,8 @@ def _jpeg_dataset(tmp_path, n=96, side=64, channels=3, subsampling="4:2:0", rest
     path = tmp_path / f"jpeg_{channels}_{subsampling.replace(':', '')}_{restart_rows}_{p}.bbox"
     bx.write_dataset(src, path, bx.WriterConfig(page_size=1 << 20, seed=seed, compress_probability=p,
                                                 compress_codec=bx.CodecId.JPEG,
-                                                jpeg=bx.JpegParams(quality, subsampling, restart_rows)))
+                                                jpeg=bx.JpegParams(quality, subsampling, restart_rows=max(restart_rows, 0),
+                                                                   restart_blocks=-restart_rows if restart_rows < 0 else 0)))
     return path
 
 
@@ -54,7 +55,8 @@ JPEG_CHAINS = [
 ]
 
 
-@pytest.mark.parametrize("layout", [("4:2:0", 1), ("4:2:2", 2), ("4:4:4", 0), ("4:2:0", 0)])
+# restart: > 0 every that many MCU rows, < 0 every -n MCUs, 0 none
+@pytest.mark.parametrize("layout", [("4:2:0", 1), ("4:2:2", 2), ("4:4:4", 0), ("4:2:0", 0), ("4:2:0", -3), ("4:4:4", -1)])
 @pytest.mark.parametrize("chain", JPEG_CHAINS)
 def test_jpeg_chains_vs_oracle(tmp_path, layout, chain):
     path = _jpeg_dataset(tmp_path, subsampling=layout[0], restart_rows=layout[1])
