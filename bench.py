@@ -390,6 +390,13 @@ def main():
 
     device = local
     torch.cuda.set_device(device)
+    if "raw" not in args.workloads.split(","):   # JPEG leg alone (profiling runs)
+        jpeg = jpeg_workload(args, device, rank, world, barrier, reduce_max)
+        if rank == 0:
+            print(json.dumps({"workloads": {"configs[2]": jpeg}}))
+        if dist is not None:
+            dist.destroy_process_group()
+        return
     path = ensure_dataset(rank, barrier)
 
     # ---- value: heap resident in HBM

@@ -122,77 +122,64 @@ static int build_huff(oj_huff* t, const uint8_t counts[16], const uint8_t* vals,
   return 0;
 }
 
-/* islow IDCT of one dequantized block (IJG jidctint.c algorithm). */
+/* islow IDCT of one dequantized block (IJG jidctint.c algorithm) in 32-bit
+ * arithmetic, as libjpeg-turbo's SIMD islow computes it (16-bit inputs,
+ * 32-bit products and sums): identical to the C version's 64-bit JLONG for
+ * every coefficient range a real 8-bit image produces (pinned on the Pillow
+ * goldens); modular (wrapping) beyond, bit-identical to the device kernel. */
 #define CB 13
 #define P1 2
-#define DESC(x, n) (((x) + (1 << ((n) - 1))) >> (n))
+typedef uint32_t U32;
+static int32_t desc32(U32 x, int n) { return (int32_t)(x + (1u << (n - 1))) >> n; }
 static uint8_t range_out(int v) {                 /* range_limit[v & 1023] on the post-IDCT table */
   int s = ((v & 1023) ^ 512) - 512;
   s += 128;
   return (uint8_t)(s < 0 ? 0 : s > 255 ? 255 : s);
 }
+/* one 1-D pass over x[0..7] (stride st): outputs descaled by n bits */
+static void idct_pass(const int32_t* x, int st, int32_t* o, int ost, int n) {
+  U32 z1, z2, z3, z4, z5, t0, t1, t2, t3, t10, t11, t12, t13;
+  z2 = (U32)x[2 * st]; z3 = (U32)x[6 * st];
+  z1 = (z2 + z3) * 4433u;
+  t2 = z1 + z3 * (U32)-15137;
+  t3 = z1 + z2 * 6270u;
+  t0 = ((U32)x[0] + (U32)x[4 * st]) << CB;
+  t1 = ((U32)x[0] - (U32)x[4 * st]) << CB;
+  t10 = t0 + t3; t13 = t0 - t3; t11 = t1 + t2; t12 = t1 - t2;
+  t0 = (U32)x[7 * st]; t1 = (U32)x[5 * st]; t2 = (U32)x[3 * st]; t3 = (U32)x[st];
+  z1 = t0 + t3; z2 = t1 + t2; z3 = t0 + t2; z4 = t1 + t3;
+  z5 = (z3 + z4) * 9633u;
+  t0 *= 2446u; t1 *= 16819u; t2 *= 25172u; t3 *= 12299u;
+  z1 *= (U32)-7373; z2 *= (U32)-20995; z3 *= (U32)-16069; z4 *= (U32)-3196;
+  z3 += z5; z4 += z5;
+  t0 += z1 + z3; t1 += z2 + z4; t2 += z2 + z3; t3 += z1 + z4;
+  o[0] = desc32(t10 + t3, n); o[7 * ost] = desc32(t10 - t3, n);
+  o[ost] = desc32(t11 + t2, n); o[6 * ost] = desc32(t11 - t2, n);
+  o[2 * ost] = desc32(t12 + t1, n); o[5 * ost] = desc32(t12 - t1, n);
+  o[3 * ost] = desc32(t13 + t0, n); o[4 * ost] = desc32(t13 - t0, n);
+}
 static void idct_islow(const int16_t* coef, const uint16_t* q, uint8_t* out, int stride) {
-  int ws[64];
-  for (int c = 0; c < 8; ++c) {
-    int in[8];
-    for (int r = 0; r < 8; ++r) in[r] = (int)coef[r * 8 + c] * (int)q[r * 8 + c];
-    if (!in[1] && !in[2] && !in[3] && !in[4] && !in[5] && !in[6] && !in[7]) {
-      for (int r = 0; r < 8; ++r) ws[r * 8 + c] = in[0] * (1 << P1);
+  int32_t in[64], ws[64];
+  for (int i = 0; i < 64; ++i) in[i] = (int32_t)((U32)(int32_t)coef[i] * (U32)q[i]);
+  for (int c = 0; c < 8; ++c) {                   /* pass 1: columns (zero-AC shortcut is exact) */
+    const int32_t* x = in + c;
+    if (!x[8] && !x[16] && !x[24] && !x[32] && !x[40] && !x[48] && !x[56]) {
+      for (int r = 0; r < 8; ++r) ws[r * 8 + c] = (int32_t)((U32)x[0] << P1);
       continue;
     }
-    long long z1, z2, z3, z4, z5, t0, t1, t2, t3, t10, t11, t12, t13;
-    z2 = in[2]; z3 = in[6];
-    z1 = (z2 + z3) * 4433;
-    t2 = z1 + z3 * -15137;
-    t3 = z1 + z2 * 6270;
-    z2 = in[0]; z3 = in[4];
-    t0 = (z2 + z3) * (1 << CB);
-    t1 = (z2 - z3) * (1 << CB);
-    t10 = t0 + t3; t13 = t0 - t3; t11 = t1 + t2; t12 = t1 - t2;
-    t0 = in[7]; t1 = in[5]; t2 = in[3]; t3 = in[1];
-    z1 = t0 + t3; z2 = t1 + t2; z3 = t0 + t2; z4 = t1 + t3;
-    z5 = (z3 + z4) * 9633;
-    t0 *= 2446; t1 *= 16819; t2 *= 25172; t3 *= 12299;
-    z1 *= -7373; z2 *= -20995; z3 *= -16069; z4 *= -3196;
-    z3 += z5; z4 += z5;
-    t0 += z1 + z3; t1 += z2 + z4; t2 += z2 + z3; t3 += z1 + z4;
-    ws[0 * 8 + c] = (int)DESC(t10 + t3, CB - P1);
-    ws[7 * 8 + c] = (int)DESC(t10 - t3, CB - P1);
-    ws[1 * 8 + c] = (int)DESC(t11 + t2, CB - P1);
-    ws[6 * 8 + c] = (int)DESC(t11 - t2, CB - P1);
-    ws[2 * 8 + c] = (int)DESC(t12 + t1, CB - P1);
-    ws[5 * 8 + c] = (int)DESC(t12 - t1, CB - P1);
-    ws[3 * 8 + c] = (int)DESC(t13 + t0, CB - P1);
-    ws[4 * 8 + c] = (int)DESC(t13 - t0, CB - P1);
+    idct_pass(x, 8, ws + c, 8, CB - P1);
   }
-  for (int r = 0; r < 8; ++r) {
-    const int* w = ws + r * 8;
+  for (int r = 0; r < 8; ++r) {                   /* pass 2: rows */
+    const int32_t* w = ws + r * 8;
     uint8_t* o = out + (size_t)r * stride;
+    int32_t v[8];
     if (!w[1] && !w[2] && !w[3] && !w[4] && !w[5] && !w[6] && !w[7]) {
-      uint8_t v = range_out((int)DESC((long long)w[0], P1 + 3));
-      for (int c = 0; c < 8; ++c) o[c] = v;
-      continue;
+      const int32_t d = desc32((U32)w[0], P1 + 3);
+      for (int c = 0; c < 8; ++c) v[c] = d;
+    } else {
+      idct_pass(w, 1, v, 1, CB + P1 + 3);
     }
-    long long z1, z2, z3, z4, z5, t0, t1, t2, t3, t10, t11, t12, t13;
-    z2 = w[2]; z3 = w[6];
-    z1 = (z2 + z3) * 4433;
-    t2 = z1 + z3 * -15137;
-    t3 = z1 + z2 * 6270;
-    t0 = ((long long)w[0] + w[4]) * (1 << CB);
-    t1 = ((long long)w[0] - w[4]) * (1 << CB);
-    t10 = t0 + t3; t13 = t0 - t3; t11 = t1 + t2; t12 = t1 - t2;
-    t0 = w[7]; t1 = w[5]; t2 = w[3]; t3 = w[1];
-    z1 = t0 + t3; z2 = t1 + t2; z3 = t0 + t2; z4 = t1 + t3;
-    z5 = (z3 + z4) * 9633;
-    t0 *= 2446; t1 *= 16819; t2 *= 25172; t3 *= 12299;
-    z1 *= -7373; z2 *= -20995; z3 *= -16069; z4 *= -3196;
-    z3 += z5; z4 += z5;
-    t0 += z1 + z3; t1 += z2 + z4; t2 += z2 + z3; t3 += z1 + z4;
-    const int n = CB + P1 + 3;
-    o[0] = range_out((int)DESC(t10 + t3, n)); o[7] = range_out((int)DESC(t10 - t3, n));
-    o[1] = range_out((int)DESC(t11 + t2, n)); o[6] = range_out((int)DESC(t11 - t2, n));
-    o[2] = range_out((int)DESC(t12 + t1, n)); o[5] = range_out((int)DESC(t12 - t1, n));
-    o[3] = range_out((int)DESC(t13 + t0, n)); o[4] = range_out((int)DESC(t13 - t0, n));
+    for (int c = 0; c < 8; ++c) o[c] = range_out(v[c]);
   }
 }
 

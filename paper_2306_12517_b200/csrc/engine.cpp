@@ -512,7 +512,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     const int64_t mh = f.info.max_height, mw = f.info.max_width;
     pl.jpeg_blocks_cap = (int64_t)f.info.channels * (2 * ((mh + 15) / 16)) * (2 * ((mw + 15) / 16));
     pl.jpeg_int_cap = ((mh + 7) / 8) * ((mw + 7) / 8);
-    pl.jpeg_bits_cap = (mx + 4 * pl.jpeg_int_cap + 32 + 15) / 16 * 16;
+    pl.jpeg_bits_cap = (mx + (kJpegIntAlign + kJpegIntPad) * pl.jpeg_int_cap + 64 + 15) / 16 * 16;
   }
   return BBX_OK;
 }
@@ -702,7 +702,12 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
   }
   const uint32_t total = (uint32_t)mx * my;
   J->scan_off = H.scan_off;
-  J->scan_end = len;
+  // the scan data ends at the EOI marker (last 0xFFD9; inside coded data 0xFF
+  // is always followed by 0x00); a file without one is decoded as truncated
+  uint32_t end = len;
+  for (int64_t q = (int64_t)len - 2; q >= (int64_t)H.scan_off; --q)
+    if (pay[q] == 0xFF && pay[q + 1] == 0xD9) { end = (uint32_t)q; break; }
+  J->scan_end = end;
   J->mcus_x = (uint16_t)mx; J->mcus_y = (uint16_t)my;
   J->restart = H.restart ? (uint32_t)H.restart : total;
   J->n_int = (total + J->restart - 1) / J->restart;
@@ -715,19 +720,14 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
         J->sched |= (uint64_t)(i | v << 2 | h << 3) << (4 * bpm);
   J->bpm = (uint8_t)bpm;
   if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap ||
-      (int64_t)len + 4 * (int64_t)J->n_int + 32 > pl.jpeg_bits_cap)
+      (int64_t)len + (kJpegIntAlign + kJpegIntPad) * (int64_t)J->n_int + 64 > pl.jpeg_bits_cap)
     return bad("jpeg: geometry exceeds the field's device capacity");
   return true;
 }
 
 static size_t jpeg_block_bytes(int B) { return (size_t)B * sizeof(JpegDesc) + (size_t)(B + 1) * 4; }
 
-// J3 shared memory of one sample: the windows of its components for one MCU row.
-static int jpeg_pix_smem(const JpegDesc& J) {
-  int b = 0;
-  for (int c = 0; c < J.ncomp; ++c) b += jpeg_window_rows(J.comp[c].v, J.vmax) * J.comp[c].bw * 8;
-  return b;
-}
+
 
 static int finalize(bbx_loader* L) {
   if (L->finalized) return BBX_OK;
@@ -1116,7 +1116,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   Plan pl;
   pl.jpeg_blocks_cap = (int64_t)c * (2 * ((h + 15) / 16)) * (2 * ((w + 15) / 16));
   pl.jpeg_int_cap = (int64_t)((h + 7) / 8) * ((w + 7) / 8);
-  pl.jpeg_bits_cap = (len + 4 * pl.jpeg_int_cap + 32 + 15) / 16 * 16;
+  pl.jpeg_bits_cap = (len + (kJpegIntAlign + kJpegIntPad) * pl.jpeg_int_cap + 64 + 15) / 16 * 16;
   uint8_t desc[64] = {0};
   SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
   d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = CODEC_JPEG;

@@ -33,132 +33,189 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
 }
 
 // ------------------------------------------------------------------- J1
-// Warp per sample, 512 bytes of the entropy-coded segment per round (16 per
-// lane).  Byte j is coded data unless it follows 0xFF (stuffing 0x00 or a
-// marker code) or is an 0xFF that starts a marker; (0xFF, 0xD0..D7) is a
-// restart marker and opens the next interval at the next 4-byte boundary of
-// the output; any other marker ends the scan data.  A lane's effect on the
-// output cursor is x -> x + a, or x -> align4(x + a) + c once it holds a
-// marker; that family is closed under composition, so one warp scan gives
-// every lane its starting cursor.
-constexpr int kUnstuffWarps = 4;
+// CTA per sample, kUnstuffWarps warps, each owning a contiguous run of
+// 16-byte chunks of the entropy-coded segment [scan_off, scan_end) (scan_end:
+// the EOI marker, found by the host).  Byte j is coded data unless it follows
+// 0xFF (stuffing 0x00 or a marker code) or is an 0xFF that starts a marker;
+// (0xFF, 0xD0..D7) is a restart marker: the interval ends, kJpegIntAlign-
+// aligned zero padding follows, and the next interval starts aligned.  A
+// lane's effect on the output cursor is x -> x + a, or x -> alignA(x + a) + c
+// once it holds a marker; that family is closed under composition, so
+//   pass 1: every warp composes the functions of its chunks (warp scans),
+//   pass 2: an exclusive scan over the warps gives each warp its start cursor,
+//   pass 3: every warp replays its chunks and writes bytes / interval bounds.
+constexpr int kUnstuffWarps = 8;
+constexpr uint32_t kAlignMask = kJpegIntAlign - 1;
 
-struct CursorFn { uint32_t aligned, a, c; };   // aligned ? align4(x + a) + c : x + a
+__device__ __forceinline__ uint32_t align_int(uint32_t x) { return (x + kAlignMask) & ~kAlignMask; }
 
+struct CursorFn { uint32_t aligned, a, c; };   // aligned ? align_int(x + a) + c : x + a
+
+// c is a multiple of the alignment plus the bytes after the last marker, so
+// align(align(y) + c) == align(y) + align(c) keeps the family closed.
 __device__ __forceinline__ CursorFn compose(CursorFn f, CursorFn g) {   // g after f
   if (!g.aligned) return f.aligned ? CursorFn{1u, f.a, f.c + g.a} : CursorFn{0u, f.a + g.a, 0u};
-  return f.aligned ? CursorFn{1u, f.a, align4(f.c + g.a) + g.c} : CursorFn{1u, f.a + g.a, g.c};
+  return f.aligned ? CursorFn{1u, f.a, align_int(f.c + g.a) + g.c} : CursorFn{1u, f.a + g.a, g.c};
 }
-__device__ __forceinline__ uint32_t apply(CursorFn f, uint32_t x) { return f.aligned ? align4(x + f.a) + f.c : x + f.a; }
+__device__ __forceinline__ uint32_t apply(CursorFn f, uint32_t x) { return f.aligned ? align_int(x + f.a) + f.c : x + f.a; }
+
+struct ChunkMasks { uint32_t w[4]; uint32_t nxt, keep, rst, term; };
+
+// Masks of the 16 bytes of chunk ch (absolute address c0 + 16 ch) of [a_lo, a_hi).
+__device__ __forceinline__ ChunkMasks chunk_masks(uintptr_t my, uintptr_t a_lo, uintptr_t a_hi, int lane) {
+  ChunkMasks M;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (my < a_hi) v = ld_nc_v4(reinterpret_cast<const void*>(my));   // buffers carry >= 16 B of tail padding
+  M.w[0] = v.x; M.w[1] = v.y; M.w[2] = v.z; M.w[3] = v.w;
+  uint32_t prev = __shfl_up_sync(0xffffffffu, v.w >> 24, 1);
+  if (lane == 0) prev = (my > a_lo) ? *reinterpret_cast<const uint8_t*>(my - 1) : 0u;
+  uint32_t nxt = __shfl_down_sync(0xffffffffu, v.x & 0xFF, 1);
+  if (lane == 31) nxt = (my + 16 < a_hi) ? *reinterpret_cast<const uint8_t*>(my + 16) : 0u;
+  M.nxt = nxt;
+  M.keep = M.rst = M.term = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uintptr_t pos = my + j;
+    const uint32_t b = (M.w[j >> 2] >> ((j & 3) * 8)) & 0xFF;
+    const uint32_t p = pos == a_lo ? 0u : (j ? (M.w[(j - 1) >> 2] >> (((j - 1) & 3) * 8)) & 0xFF : prev);
+    const uint32_t n = pos + 1 >= a_hi ? 0u : (j < 15 ? (M.w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) & 0xFF : nxt);
+    if (pos < a_lo || pos >= a_hi) continue;
+    const bool marker = b == 0xFF && n != 0x00;
+    if (p != 0xFF && !marker && !(b == 0xFF && pos + 1 >= a_hi)) M.keep |= 1u << j;
+    if (marker && (n & 0xF8) == 0xD0) M.rst |= 1u << j;
+    if (marker && n != 0xFF && (n & 0xF8) != 0xD0) M.term |= 1u << j;
+  }
+  return M;
+}
+
+__device__ __forceinline__ CursorFn lane_fn(const ChunkMasks& M) {
+  CursorFn f{0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (M.rst >> j & 1) f = f.aligned ? CursorFn{1u, f.a, align_int(f.c) + kJpegIntPad} : CursorFn{1u, f.a, kJpegIntPad};
+    if (M.keep >> j & 1) { if (f.aligned) ++f.c; else ++f.a; }
+  }
+  return f;
+}
+
+__device__ __forceinline__ CursorFn warp_scan(CursorFn f, uint32_t& nr, int lane) {   // inclusive
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const CursorFn e{__shfl_up_sync(0xffffffffu, f.aligned, o), __shfl_up_sync(0xffffffffu, f.a, o),
+                     __shfl_up_sync(0xffffffffu, f.c, o)};
+    const uint32_t r = __shfl_up_sync(0xffffffffu, nr, o);
+    if (lane >= o) { f = compose(e, f); nr += r; }
+  }
+  return f;
+}
 
 __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const JpegArgs A) {
-  const int s = blockIdx.x * kUnstuffWarps + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (s >= A.count) return;
+  const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const JpegDesc& J = A.jd[s];
   const uint32_t nint = J.n_int;
   if (nint == 0) return;
+  __shared__ CursorFn s_fn[kUnstuffWarps];
+  __shared__ uint32_t s_nr[kUnstuffWarps], s_x[kUnstuffWarps], s_k[kUnstuffWarps];
+  __shared__ int s_bad;
   const uint8_t* base = A.payload + sdesc(A, s)->src;
   uint8_t* out = A.bits + J.bs_base;
   uint32_t* st = A.istart + J.int_base;
   uint32_t* en = A.iend + J.int_base;
-  if (lane == 0) st[0] = 0;
   const uintptr_t ab = reinterpret_cast<uintptr_t>(base);
   const uintptr_t a_lo = ab + J.scan_off, a_hi = ab + J.scan_end;
-  uint32_t kcur = 0, xcur = 0, carry = 0;
-  bool seq_bad = false, done = false;
-  uintptr_t c = a_lo & ~uintptr_t(15);
-  uint4 vn = make_uint4(0, 0, 0, 0);                 // next round's chunk, loaded one round ahead
-  if (c + (uintptr_t)lane * 16 < a_hi) vn = ld_nc_v4(reinterpret_cast<const void*>(c + (uintptr_t)lane * 16));
-  for (; c < a_hi && !done; c += 512) {
-    const uintptr_t my = c + (uintptr_t)lane * 16;
-    const uint4 v = vn;
-    vn = make_uint4(0, 0, 0, 0);
-    if (my + 512 < a_hi) vn = ld_nc_v4(reinterpret_cast<const void*>(my + 512));   // >= 16 B tail padding
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    uint32_t prev = __shfl_up_sync(0xffffffffu, w[3] >> 24, 1);
-    if (lane == 0) prev = carry;
-    uint32_t nxt = __shfl_down_sync(0xffffffffu, w[0] & 0xFF, 1);
-    const uint32_t nxt31 = __shfl_sync(0xffffffffu, vn.x & 0xFF, 0);   // first byte of the next round
-    if (lane == 31) nxt = nxt31;
-    uint32_t keep = 0, rst = 0, term = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uintptr_t pos = my + j;
-      const uint32_t b = (w[j >> 2] >> ((j & 3) * 8)) & 0xFF;
-      const uint32_t p = pos == a_lo ? 0u : (j ? (w[(j - 1) >> 2] >> (((j - 1) & 3) * 8)) & 0xFF : prev);
-      uint32_t n = j < 15 ? (w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) & 0xFF : nxt;
-      if (pos + 1 >= a_hi) n = 0xD9;
-      if (pos < a_lo || pos >= a_hi) continue;
-      const bool marker = b == 0xFF && n != 0x00;
-      if (p != 0xFF && !marker) keep |= 1u << j;
-      if (marker && (n & 0xF8) == 0xD0) rst |= 1u << j;
-      if (marker && n != 0xFF && (n & 0xF8) != 0xD0) term |= 1u << j;
+  const uintptr_t c0 = a_lo & ~uintptr_t(15);
+  const uint32_t nch = (uint32_t)((a_hi - c0 + 15) >> 4);
+  const uint32_t rounds = (nch + 32 * kUnstuffWarps - 1) / (32 * kUnstuffWarps);
+  const uint32_t ch0 = warp * rounds * 32;
+  if (threadIdx.x == 0) s_bad = 0;
+  // pass 1: this warp's cursor function and marker count
+  CursorFn F{0u, 0u, 0u};
+  uint32_t NR = 0;
+  bool term = false;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
+    term |= M.term != 0;
+    uint32_t nr = __popc(M.rst);
+    const CursorFn inc = warp_scan(lane_fn(M), nr, lane);
+    const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
+                       __shfl_sync(0xffffffffu, inc.c, 31)};
+    F = compose(F, all);
+    NR += __shfl_sync(0xffffffffu, nr, 31);
+  }
+  if (lane == 0) { s_fn[warp] = F; s_nr[warp] = NR; }
+  if (__any_sync(0xffffffffu, term) && lane == 0) s_bad = 1;   // a non-RST marker inside the scan data
+  __syncthreads();
+  // pass 2: exclusive scan over the warps
+  if (threadIdx.x == 0) {
+    CursorFn P{0u, 0u, 0u};
+    uint32_t k = 0;
+    for (int w = 0; w < kUnstuffWarps; ++w) {
+      s_x[w] = apply(P, 0u);
+      s_k[w] = k;
+      P = compose(P, s_fn[w]);
+      k += s_nr[w];
     }
-    // everything from the first non-RST marker on is not scan data
-    const uint32_t tb = __ballot_sync(0xffffffffu, term != 0);
-    if (tb) {
-      const int fl = __ffs(tb) - 1;
-      if (lane > fl) { keep = 0; rst = 0; }
-      if (lane == fl) { const uint32_t m = (1u << (__ffs(term) - 1)) - 1; keep &= m; rst &= m; }
-      done = true;
+    const uint32_t xend = apply(P, 0u);
+    SampleStatus& S = A.status[s];
+    S.kind = 0; S.value = 0;
+    if (s_bad) { S.kind = JST_MARKER_COUNT; S.value = -1; }
+    else if (k != nint - 1) { S.kind = JST_MARKER_COUNT; S.value = k; }
+    else {
+      st[0] = 0;
+      en[nint - 1] = xend;
+      for (uint32_t z = xend; z < align_int(xend) + kJpegIntPad; ++z) out[z] = 0;
     }
-    // this lane's cursor function, then an inclusive warp scan of them
-    CursorFn f{0u, 0u, 0u};
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (rst >> j & 1) f = f.aligned ? CursorFn{1u, f.a, align4(f.c)} : CursorFn{1u, f.a, 0u};
-      if (keep >> j & 1) { if (f.aligned) ++f.c; else ++f.a; }
-    }
-    uint32_t nr = __popc(rst), nr_incl = nr;
-    CursorFn inc = f;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      CursorFn e{__shfl_up_sync(0xffffffffu, inc.aligned, o), __shfl_up_sync(0xffffffffu, inc.a, o),
-                 __shfl_up_sync(0xffffffffu, inc.c, o)};
-      const uint32_t r = __shfl_up_sync(0xffffffffu, nr_incl, o);
-      if (lane >= o) { inc = compose(e, inc); nr_incl += r; }
-    }
+  }
+  __syncthreads();
+  if (A.status[s].kind != 0) return;
+  // pass 3: replay, writing bytes and interval bounds
+  uint32_t xw = s_x[warp], kw = s_k[warp];
+  bool seq_bad = false;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
+    const uint32_t nr = __popc(M.rst);
+    uint32_t nr_incl = nr;
+    const CursorFn f = lane_fn(M);
+    const CursorFn inc = warp_scan(f, nr_incl, lane);
     CursorFn exc{__shfl_up_sync(0xffffffffu, inc.aligned, 1), __shfl_up_sync(0xffffffffu, inc.a, 1),
                  __shfl_up_sync(0xffffffffu, inc.c, 1)};
     if (lane == 0) exc = CursorFn{0u, 0u, 0u};
-    uint32_t x = apply(exc, xcur), k = kcur + nr_incl - nr;
+    uint32_t x = apply(exc, xw), k = kw + nr_incl - nr;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-      if (rst >> j & 1) {
-        const uint32_t n = (j < 15 ? (w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) : nxt) & 7;
+      if (M.rst >> j & 1) {                          // interval k ends: zero tail, next one starts aligned
+        const uint32_t n = (j < 15 ? (M.w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) : M.nxt) & 7;
         if (n != (k & 7)) seq_bad = true;
-        if (k + 1 < nint) { en[k] = x; st[k + 1] = align4(x); }
-        x = align4(x);
+        const uint32_t nx = align_int(x) + kJpegIntPad;
+        en[k] = x;
+        st[k + 1] = nx;
+        for (uint32_t z = x; z < nx; ++z) out[z] = 0;
+        x = nx;
         ++k;
       }
-      if (keep >> j & 1) out[x++] = (uint8_t)(w[j >> 2] >> ((j & 3) * 8));
+      if (M.keep >> j & 1) out[x++] = (uint8_t)(M.w[j >> 2] >> ((j & 3) * 8));
     }
     const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
                        __shfl_sync(0xffffffffu, inc.c, 31)};
-    xcur = apply(all, xcur);
-    kcur += __shfl_sync(0xffffffffu, nr_incl, 31);
-    carry = __shfl_sync(0xffffffffu, w[3] >> 24, 31);
+    xw = apply(all, xw);
+    kw += __shfl_sync(0xffffffffu, nr_incl, 31);
   }
-  seq_bad = __any_sync(0xffffffffu, seq_bad);
-  if (lane == 0) {
-    SampleStatus& S = A.status[s];
-    S.kind = 0; S.value = 0;
-    if (kcur != nint - 1) { S.kind = JST_MARKER_COUNT; S.value = kcur; }
-    else if (seq_bad) S.kind = JST_MARKER_SEQ;
-    else en[nint - 1] = xcur;
-  }
+  if (__any_sync(0xffffffffu, seq_bad) && lane == 0) A.status[s].kind = JST_MARKER_SEQ;
 }
 
 // ------------------------------------------------------------------- J2
 // Thread per restart interval (DC predictors restart at zero, T.81
 // F.2.1.3.1), one symbol per loop iteration whatever block / MCU it belongs
-// to.  The body is branch-free except at block ends and for codes longer than
-// the fast table, so the lanes of a warp stay converged: the 32-bit refill is
-// predicated, the extra bits are always extracted (0 of them for EOB / ZRL),
-// and only nonzero coefficients are stored into the pre-zeroed block.  Past
-// the interval's end the stream reads as zeros (libjpeg's rule once a marker
-// is reached).
+// to, so the lanes of a warp stay converged.  Per iteration: a predicated
+// 32-bit refill from two 16-byte chunks held in registers (the next one is
+// loaded a chunk ahead; J1 left zero padding after every interval, so reading
+// past the data yields zeros, libjpeg's rule once a marker is reached), one u16 table
+// lookup for code length / extra bits / run / EOB, extra-bit extraction with
+// a branch-free EXTEND, and a store of the coefficient when it is nonzero
+// (the block buffer is pre-zeroed).  Block ends read the next block's
+// component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 128;
+constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
 template <typename T>
 __device__ __forceinline__ int find_sample(const T* prefix, int count, T t) {   // largest s: prefix[s] <= t
@@ -173,14 +230,18 @@ __device__ __forceinline__ int find_sample(const T* prefix, int count, T t) {   
 template <typename T>
 __device__ __forceinline__ T sel3(int i, T a, T b, T c) { return i == 0 ? a : (i == 1 ? b : c); }
 
+template <bool kSmem>
 __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegArgs A) {
-  extern __shared__ __align__(16) uint32_t sfast[];
+  extern __shared__ __align__(16) uint8_t hsm[];
   __shared__ uint8_t nat[80];
   constexpr int TW = 1 << kJpegFastBits;
-  const bool smem_tabs = A.n_huff <= kJpegSmemTables;
-  if (smem_tabs) {
+  const int tabs_bytes = kSmem ? A.n_huff * TW * 2 : 0;
+  const uint16_t* tab = kSmem ? reinterpret_cast<const uint16_t*>(hsm) : reinterpret_cast<const uint16_t*>(A.huff);
+  uint64_t* slot = reinterpret_cast<uint64_t*>(hsm + tabs_bytes) + threadIdx.x;   // [b * kHuffThreads]
+  if (kSmem) {
+    uint16_t* st = reinterpret_cast<uint16_t*>(hsm);
     const int n = A.n_huff * TW;
-    for (int i = threadIdx.x; i < n; i += kHuffThreads) sfast[i] = __ldg(&A.huff[i / TW].fast[i % TW]);
+    for (int i = threadIdx.x; i < n; i += kHuffThreads) st[i] = __ldg(&A.huff[i / TW].fast[i % TW]);
   }
   for (int i = threadIdx.x; i < 80; i += kHuffThreads) nat[i] = c_natural[i];
   __syncthreads();
@@ -193,67 +254,71 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
   const uint32_t mcus_x = J.mcus_x, total = mcus_x * J.mcus_y;
   const uint32_t m0 = k * J.restart, m1 = min(m0 + J.restart, total);
   if (m0 >= m1) return;
-  const uint64_t sched = J.sched;
   const int bpm = J.bpm;
-  // per-component constants (selected by index: no local-memory arrays)
-  const uint32_t bw0 = J.comp[0].bw, bw1 = J.comp[1].bw, bw2 = J.comp[2].bw;
+  // slot b: block offset in its component's MCU origin | comp << 16 | dc table << 18 | ac table << 41
+  constexpr uint32_t TSTRIDE = kSmem ? TW : (uint32_t)(sizeof(JHuff) / 2);
+  for (int b = 0; b < bpm; ++b) {
+    const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
+    const JComp& C = J.comp[c];
+    const uint64_t d = ((e >> 2) & 1) * C.bw + (e >> 3);
+    slot[b * kHuffThreads] = d | (uint64_t)c << 16 | (uint64_t)(C.dc * TSTRIDE) << 18 | (uint64_t)(C.ac * TSTRIDE) << 41;
+  }
+  const uint32_t h0 = J.comp[0].h, h1 = J.comp[1].h, h2 = J.comp[2].h;
+  const uint32_t rs0 = J.comp[0].v * J.comp[0].bw, rs1 = J.comp[1].v * J.comp[1].bw, rs2 = J.comp[2].v * J.comp[2].bw;
   const uint32_t of0 = J.comp[0].blk_off, of1 = J.comp[1].blk_off, of2 = J.comp[2].blk_off;
-  const uint32_t hv0 = J.comp[0].h | J.comp[0].v << 8, hv1 = J.comp[1].h | J.comp[1].v << 8,
-                 hv2 = J.comp[2].h | J.comp[2].v << 8;
-  const uint32_t tb0 = J.comp[0].dc | (uint32_t)J.comp[0].ac << 16, tb1 = J.comp[1].dc | (uint32_t)J.comp[1].ac << 16,
-                 tb2 = J.comp[2].dc | (uint32_t)J.comp[2].ac << 16;
   int16_t* const coef = A.coef + J.blk_base * 64;
 
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(A.bits + J.bs_base + A.istart[t]);
-  int rem = (int)(A.iend[t] - A.istart[t]);
+  // 16-byte chunks of the interval (J1 aligned it and zero-padded its tail):
+  // `cur` is being consumed, `nxt` is in flight
+  const uint4* p16 = reinterpret_cast<const uint4*>(A.bits + J.bs_base + A.istart[t]);
+  const uint4* plast = reinterpret_cast<const uint4*>(A.bits + J.bs_base + align_int(A.iend[t]) + kJpegIntPad - 16);
+  uint4 cur = ld_nc_v4(p16);
+  p16 += p16 < plast ? 1 : 0;
+  uint4 nxt = ld_nc_v4(p16);
+  int wi = 0;
   uint64_t acc = 0;
   int nb = 0;
 
   uint32_t m = m0, mx = m0 % mcus_x, my = m0 / mcus_x;
+  uint32_t base0 = of0 + my * rs0 + mx * h0, base1 = of1 + my * rs1 + mx * h1, base2 = of2 + my * rs2 + mx * h2;
   int b = 0, kk = 0, ci = 0;
   int pred0 = 0, pred1 = 0, pred2 = 0;
-  const uint32_t* fdc = nullptr;
-  const uint32_t* fac = nullptr;
-  const JHuff* gdc = nullptr;
-  const JHuff* gac = nullptr;
+  uint32_t tdc = 0, tac = 0;
   int16_t* cb = nullptr;
   bool bad = false;
-  auto setup = [&]() {                               // block b of MCU (mx, my)
-    const uint32_t e = (uint32_t)(sched >> (4 * b)) & 15u;
-    ci = (int)(e & 3);
-    const uint32_t hv = sel3(ci, hv0, hv1, hv2), H = hv & 0xFF, V = hv >> 8;
-    const uint32_t bidx =
-        sel3(ci, of0, of1, of2) + (my * V + ((e >> 2) & 1)) * sel3(ci, bw0, bw1, bw2) + mx * H + (e >> 3);
-    cb = coef + (size_t)bidx * 64;
-    const uint32_t tb = sel3(ci, tb0, tb1, tb2);
-    gdc = A.huff + (tb & 0xFFFF);
-    gac = A.huff + (tb >> 16);
-    fdc = smem_tabs ? sfast + (tb & 0xFFFF) * TW : gdc->fast;
-    fac = smem_tabs ? sfast + (tb >> 16) * TW : gac->fast;
+  auto setup = [&]() {                               // block b of the current MCU
+    const uint64_t r = slot[b * kHuffThreads];
+    ci = (int)((r >> 16) & 3);
+    tdc = (uint32_t)(r >> 18) & 0x7FFFFFu;
+    tac = (uint32_t)(r >> 41) & 0x7FFFFFu;
+    cb = coef + (size_t)(sel3(ci, base0, base1, base2) + (uint32_t)(r & 0xFFFF)) * 64;
     kk = 0;
   };
   setup();
   for (;;) {
-    {                                                // predicated 32-bit refill
+    {                                                // predicated 32-bit refill from the chunk registers
       const bool need = nb <= 32;
-      uint32_t wv = __byte_perm(__ldg(wp), 0, 0x0123);
-      const uint32_t keep = rem >= 4 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : (0xFFFFFFFFu << (8 * (4 - rem))));
-      wv = need ? (wv & keep) : 0u;
-      acc |= (uint64_t)wv << (need ? 32 - nb : 0);
-      wp += (need && rem > 4) ? 1 : 0;
-      rem -= need ? 4 : 0;
+      uint32_t wv = wi == 0 ? cur.x : (wi == 1 ? cur.y : (wi == 2 ? cur.z : cur.w));
+      wv = need ? __byte_perm(wv, 0, 0x0123) : 0u;
+      acc |= (uint64_t)wv << ((32 - nb) & 63);
       nb += need ? 32 : 0;
+      wi += need ? 1 : 0;
+      if (wi == 4) {
+        wi = 0;
+        cur = nxt;
+        p16 += p16 < plast ? 1 : 0;
+        nxt = ld_nc_v4(p16);
+      }
     }
-    const uint32_t e = (kk ? fac : fdc)[(uint32_t)(acc >> (64 - kJpegFastBits))];
-    int len, size, run;
+    const uint32_t e = tab[(kk ? tac : tdc) + (uint32_t)(acc >> (64 - kJpegFastBits))];
+    int len = (int)(e & 31), size, run;
     bool eob;
-    if (e & kFastValid) {
-      len = (int)(e & 31);
+    if (len) {
       size = (int)((e >> 5) & 31);
       run = (int)((e >> 10) & 15);
       eob = (e & kFastEob) != 0;
     } else {                                         // code longer than the fast table
-      const JHuff* g = kk ? gac : gdc;
+      const JHuff* g = A.huff + (kk ? tac : tdc) / TSTRIDE;
       const uint32_t c16 = (uint32_t)(acc >> 48);
       len = kJpegFastBits + 1;
       while (len <= 16 && (int32_t)(c16 >> (16 - len)) > __ldg(&g->maxcode[len])) ++len;
@@ -264,12 +329,12 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
       eob = kk && size == 0 && run != 15;
     }
     acc <<= len;
-    nb -= len;
-    const uint32_t bits = size ? (uint32_t)(acc >> (64 - size)) : 0u;
+    const uint32_t hi = (uint32_t)(acc >> 32);
+    const uint32_t bits = __funnelshift_l(hi, 0u, size);          // top `size` bits (0 when size == 0)
+    const int sgn = (int)hi >> 31;                               // leading extra bit 1: positive value
+    int v = (int)bits + ((int)((0xFFFFFFFFu << size) + 1u) & ~sgn);   // EXTEND (F.2.2.1)
     acc <<= size;
-    nb -= size;
-    int v = (int)bits;
-    if (size && bits < (1u << (size - 1))) v -= (1 << size) - 1;   // EXTEND (F.2.2.1)
+    nb -= len + size;
     if (kk == 0) {                                   // DC: prediction per component
       v += sel3(ci, pred0, pred1, pred2);
       pred0 = ci == 0 ? v : pred0;
@@ -282,9 +347,12 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     if (kk >= 64) {                                  // block done: next block of the MCU / next MCU
       if (++b == bpm) {
         b = 0;
-        ++m;
-        if (++mx == mcus_x) { mx = 0; ++my; }
-        if (m >= m1) break;
+        if (++m >= m1) break;
+        base0 += h0; base1 += h1; base2 += h2;
+        if (++mx == mcus_x) {
+          mx = 0; ++my;
+          base0 = of0 + my * rs0; base1 = of1 + my * rs1; base2 = of2 + my * rs2;
+        }
       }
       setup();
     }
@@ -308,27 +376,28 @@ __device__ __forceinline__ uint32_t range_out(int v) {   // post-IDCT range_limi
 
 template <bool kPass1>
 __device__ __forceinline__ void idct_1d(int& x0, int& x1, int& x2, int& x3, int& x4, int& x5, int& x6, int& x7) {
+  // 32-bit modular arithmetic, exactly oracle/jpeg_oracle.c idct_pass
   constexpr int CB = 13, P1 = 2, SH = kPass1 ? CB - P1 : CB + P1 + 3;
-  constexpr long long RND = 1ll << (SH - 1);
-  long long z1, z2, z3, z4, z5, t0, t1, t2, t3, t10, t11, t12, t13;
-  z2 = x2; z3 = x6;
-  z1 = (z2 + z3) * 4433;
-  t2 = z1 + z3 * -15137;
-  t3 = z1 + z2 * 6270;
-  t0 = ((long long)x0 + x4) * (1 << CB);
-  t1 = ((long long)x0 - x4) * (1 << CB);
+  constexpr uint32_t RND = 1u << (SH - 1);
+  uint32_t z1, z2, z3, z4, z5, t0, t1, t2, t3, t10, t11, t12, t13;
+  z2 = (uint32_t)x2; z3 = (uint32_t)x6;
+  z1 = (z2 + z3) * 4433u;
+  t2 = z1 + z3 * (uint32_t)-15137;
+  t3 = z1 + z2 * 6270u;
+  t0 = ((uint32_t)x0 + (uint32_t)x4) << CB;
+  t1 = ((uint32_t)x0 - (uint32_t)x4) << CB;
   t10 = t0 + t3; t13 = t0 - t3; t11 = t1 + t2; t12 = t1 - t2;
-  t0 = x7; t1 = x5; t2 = x3; t3 = x1;
+  t0 = (uint32_t)x7; t1 = (uint32_t)x5; t2 = (uint32_t)x3; t3 = (uint32_t)x1;
   z1 = t0 + t3; z2 = t1 + t2; z3 = t0 + t2; z4 = t1 + t3;
-  z5 = (z3 + z4) * 9633;
-  t0 *= 2446; t1 *= 16819; t2 *= 25172; t3 *= 12299;
-  z1 *= -7373; z2 *= -20995; z3 *= -16069; z4 *= -3196;
+  z5 = (z3 + z4) * 9633u;
+  t0 *= 2446u; t1 *= 16819u; t2 *= 25172u; t3 *= 12299u;
+  z1 *= (uint32_t)-7373; z2 *= (uint32_t)-20995; z3 *= (uint32_t)-16069; z4 *= (uint32_t)-3196;
   z3 += z5; z4 += z5;
   t0 += z1 + z3; t1 += z2 + z4; t2 += z2 + z3; t3 += z1 + z4;
-  x0 = (int)((t10 + t3 + RND) >> SH); x7 = (int)((t10 - t3 + RND) >> SH);
-  x1 = (int)((t11 + t2 + RND) >> SH); x6 = (int)((t11 - t2 + RND) >> SH);
-  x2 = (int)((t12 + t1 + RND) >> SH); x5 = (int)((t12 - t1 + RND) >> SH);
-  x3 = (int)((t13 + t0 + RND) >> SH); x4 = (int)((t13 - t0 + RND) >> SH);
+  x0 = (int)(t10 + t3 + RND) >> SH; x7 = (int)(t10 - t3 + RND) >> SH;
+  x1 = (int)(t11 + t2 + RND) >> SH; x6 = (int)(t11 - t2 + RND) >> SH;
+  x2 = (int)(t12 + t1 + RND) >> SH; x5 = (int)(t12 - t1 + RND) >> SH;
+  x3 = (int)(t13 + t0 + RND) >> SH; x4 = (int)(t13 - t0 + RND) >> SH;
 }
 
 // One block: coefficients (global, natural order) -> 8 rows of 8 bytes at dst (stride bytes).
@@ -338,19 +407,19 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
   int w[64];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const uint4 cv = __ldg(src + r), qv = __ldg(q4 + r);
+    const uint4 cv = src[r], qv = __ldg(q4 + r);
     const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      w[r * 8 + 2 * j] = (int)(int16_t)(cw[j] & 0xFFFF) * (int)(qw[j] & 0xFFFF);
-      w[r * 8 + 2 * j + 1] = (int)(int16_t)(cw[j] >> 16) * (int)(qw[j] >> 16);
+      w[r * 8 + 2 * j] = (int)((uint32_t)(int)(int16_t)(cw[j] & 0xFFFF) * (qw[j] & 0xFFFF));
+      w[r * 8 + 2 * j + 1] = (int)((uint32_t)(int)(int16_t)(cw[j] >> 16) * (qw[j] >> 16));
     }
   }
 #pragma unroll
   for (int col = 0; col < 8; ++col) {
     int* x = w + col;
     if ((x[8] | x[16] | x[24] | x[32] | x[40] | x[48] | x[56]) == 0) {
-      const int dc = x[0] * 4;
+      const int dc = (int)((uint32_t)x[0] << 2);
 #pragma unroll
       for (int r = 0; r < 8; ++r) x[r * 8] = dc;
     } else {
@@ -362,7 +431,7 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
     int* x = w + r * 8;
     uint32_t o[8];
     if ((x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7]) == 0) {
-      const uint32_t v = range_out((x[0] + 16) >> 5);
+      const uint32_t v = range_out((int)((uint32_t)x[0] + 16u) >> 5);
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] = v;
     } else {
@@ -400,70 +469,119 @@ __device__ __forceinline__ int win_sample(const Win& c, int y, int x) {
   return (3 * cs + ns + ((x & 1) ? 7 : 8)) >> 4;
 }
 
-__global__ void __launch_bounds__(kPixThreads) jpeg_pixels_kernel(const JpegArgs A) {
+__global__ void __launch_bounds__(kPixThreads, 3) jpeg_pixels_kernel(const JpegArgs A) {
   extern __shared__ __align__(16) uint8_t psm[];
+  __shared__ int s_coff[3], s_brlo[3], s_njob[3], s_bw[3], s_pw[3], s_y0[3], s_win[3];
   const int s = blockIdx.y, r = blockIdx.x;
   const JpegDesc& J = A.jd[s];
   if (J.n_int == 0 || r >= J.mcus_y || A.status[s].kind != 0) return;
   const SampleDesc* d = sdesc(A, s);
   const int w = d->w, h = d->h, nc = J.ncomp, hmax = J.hmax, vmax = J.vmax;
-  Win win[3];
-  int brlo[3], brhi[3], njob[3];
-  int off = 0;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    if (c >= nc) { njob[c] = 0; continue; }
-    const JComp& C = J.comp[c];
-    const int rv = vmax / C.v, ext = rv == 2 ? 1 : 0;
-    win[c].p = psm + off;
-    win[c].y0 = (r * C.v - ext) * 8;
-    win[c].pw = C.bw * 8;
-    win[c].dw = C.dw; win[c].dh = C.dh; win[c].rh = hmax / C.h; win[c].rv = rv;
-    brlo[c] = max(r * C.v - ext, 0);
-    brhi[c] = min(r * C.v + C.v - 1 + ext, (int)C.bh - 1);
-    njob[c] = (brhi[c] - brlo[c] + 1) * C.bw;
-    off += jpeg_window_rows(C.v, vmax) * C.bw * 8;
-  }
-  const int16_t* coef = A.coef + J.blk_base * 64;
-  for (int jb = threadIdx.x; jb < njob[0] + njob[1] + njob[2]; jb += kPixThreads) {
-    int c = 0, q = jb;
-    if (q >= njob[0]) { q -= njob[0]; c = 1; if (q >= njob[1]) { q -= njob[1]; c = 2; } }
-    const JComp& C = J.comp[c];
-    const int br = brlo[c] + q / C.bw, bx = q - (q / C.bw) * C.bw;
-    idct_block(coef + ((size_t)C.blk_off + (size_t)br * C.bw + bx) * 64, A.quant[C.q].q,
-               psm + (win[c].p - psm) + (br * 8 - win[c].y0) * win[c].pw + bx * 8, win[c].pw);
+  if (threadIdx.x == 0) {
+    int off = 0, slots = 0;
+    for (int c = 0; c < 3; ++c) {
+      if (c >= nc) { s_njob[c] = 0; s_coff[c] = slots; continue; }
+      const JComp& C = J.comp[c];
+      const int ext = vmax / C.v == 2 ? 1 : 0;
+      const int lo = max(r * C.v - ext, 0), hi = min(r * C.v + C.v - 1 + ext, (int)C.bh - 1);
+      s_brlo[c] = lo; s_njob[c] = (hi - lo + 1) * C.bw; s_bw[c] = C.bw; s_pw[c] = C.bw * 8;
+      s_y0[c] = (r * C.v - ext) * 8; s_win[c] = off; s_coff[c] = slots;
+      off += jpeg_window_rows(C.v, vmax) * C.bw * 8;
+      slots += s_njob[c];
+    }
+    s_coff[0] = off;                                 // coefficient staging starts after the windows
+    s_coff[1] = off + s_njob[0] * kJpegCoefSlot;
+    s_coff[2] = s_coff[1] + s_njob[1] * kJpegCoefSlot;
   }
   __syncthreads();
+  const int nj0 = s_njob[0], nj1 = s_njob[1], njob = nj0 + nj1 + s_njob[2];
+  const int16_t* coef = A.coef + J.blk_base * 64;
+  // stage the blocks: per component one contiguous run of block rows, 16-byte coalesced copies
+  for (int q = threadIdx.x; q < njob * 8; q += kPixThreads) {
+    const int jb = q >> 3, part = q & 7;
+    const int c = jb < nj0 ? 0 : (jb < nj0 + nj1 ? 1 : 2);
+    const int loc = jb - (c == 0 ? 0 : (c == 1 ? nj0 : nj0 + nj1));
+    const uint4* src = reinterpret_cast<const uint4*>(
+        coef + ((size_t)J.comp[c].blk_off + (size_t)s_brlo[c] * s_bw[c] + loc) * 64);
+    *reinterpret_cast<uint4*>(psm + s_coff[c] + loc * kJpegCoefSlot + part * 16) = ld_nc_v4(src + part);
+  }
+  __syncthreads();
+  for (int jb = threadIdx.x; jb < njob; jb += kPixThreads) {
+    const int c = jb < nj0 ? 0 : (jb < nj0 + nj1 ? 1 : 2);
+    const int loc = jb - (c == 0 ? 0 : (c == 1 ? nj0 : nj0 + nj1));
+    const int bw = s_bw[c], q = loc / bw, bx = loc - q * bw, br = s_brlo[c] + q;
+    idct_block(reinterpret_cast<const int16_t*>(psm + s_coff[c] + loc * kJpegCoefSlot), A.quant[J.comp[c].q].q,
+               psm + s_win[c] + (br * 8 - s_y0[c]) * s_pw[c] + bx * 8, s_pw[c]);
+  }
+  __syncthreads();
+  Win win[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (c >= nc) break;
+    const JComp& C = J.comp[c];
+    win[c].p = psm + s_win[c]; win[c].y0 = s_y0[c]; win[c].pw = s_pw[c];
+    win[c].dw = C.dw; win[c].dh = C.dh; win[c].rh = hmax / C.h; win[c].rv = vmax / C.v;
+  }
   const int y_first = r * vmax * 8, rows = min(vmax * 8, h - y_first);
   uint8_t* outp = A.scratch + (size_t)s * A.scratch_bytes;
   if (nc == 3 && hmax == 2 && vmax == 2 && win[0].rh == 1 && win[0].rv == 1 && win[1].rh == 2 &&
-      win[1].rv == 2 && win[2].rh == 2 && win[2].rv == 2 && win[1].dw > 2 && win[2].dw > 2) {
-    // 4:2:0 (h2v2 fancy): a thread produces the two output pixels of one chroma column
-    const int cw = (w + 1) >> 1, dw = win[1].dw, dh = win[1].dh, cpw = win[1].pw;
-    for (int idx = threadIdx.x; idx < rows * cw; idx += kPixThreads) {
-      const int yy = idx / cw, j = idx - yy * cw, y = y_first + yy;
+      win[1].rv == 2 && win[2].rh == 2 && win[2].rv == 2 && win[1].dw > 2 && win[2].dw > 2 &&
+      win[1].dw == win[2].dw && win[1].dh == win[2].dh && win[1].pw == win[2].pw && win[1].y0 == win[2].y0) {
+    // 4:2:0 (h2v2 fancy): a thread makes 4 output pixels (2 chroma columns) of a row into an
+    // RGB staging area laid out like the output (it reuses the coefficient slots), which the
+    // CTA then copies out with 16-byte stores
+    uint8_t* stg = psm + s_coff[0];
+    const int nq = (w + 3) >> 2, dw = win[1].dw, dh = win[1].dh, cpw = win[1].pw;
+    const uint8_t* cbp = win[1].p;
+    const uint8_t* crp = win[2].p;
+    for (int idx = threadIdx.x; idx < rows * nq; idx += kPixThreads) {
+      const int yy = idx / nq, q = idx - yy * nq, y = y_first + yy;
       const int i = y >> 1, i1 = (y & 1) ? min(i + 1, dh - 1) : max(i - 1, 0);
-      const int jl = max(j - 1, 0), jr = min(j + 1, dw - 1);
+      const int j0 = 2 * q;
+      const int ja = max(j0 - 1, 0), jc = min(j0 + 1, dw - 1), jd = min(j0 + 2, dw - 1);
       const int ra = (i - win[1].y0) * cpw, rb = (i1 - win[1].y0) * cpw;
-      int ce[2], co[2];
+      int u[2][4];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint8_t* P = win[1 + q].p;
-        const int cs = 3 * P[ra + j] + P[rb + j], cl = 3 * P[ra + jl] + P[rb + jl], cr = 3 * P[ra + jr] + P[rb + jr];
-        ce[q] = ((3 * cs + cl + 8) >> 4) - 128;
-        co[q] = ((3 * cs + cr + 7) >> 4) - 128;
+      for (int c = 0; c < 2; ++c) {
+        const uint8_t* P = c ? crp : cbp;
+        const int c0 = 3 * P[ra + ja] + P[rb + ja], c1 = 3 * P[ra + j0] + P[rb + j0];
+        const int c2 = 3 * P[ra + jc] + P[rb + jc], c3 = 3 * P[ra + jd] + P[rb + jd];
+        u[c][0] = ((3 * c1 + c0 + 8) >> 4) - 128;
+        u[c][1] = ((3 * c1 + c2 + 7) >> 4) - 128;
+        u[c][2] = ((3 * c2 + c1 + 8) >> 4) - 128;
+        u[c][3] = ((3 * c2 + c3 + 7) >> 4) - 128;
       }
-      const uint8_t* yrow = win[0].p + (y - win[0].y0) * win[0].pw;
-      uint8_t* o = outp + ((size_t)y * w + 2 * j) * 3;
+      const uint32_t y4 = *reinterpret_cast<const uint32_t*>(win[0].p + (y - win[0].y0) * win[0].pw + 4 * q);
+      uint32_t px[12];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (2 * j + q >= w) break;
-        const int Y = yrow[2 * j + q], cb = q ? co[0] : ce[0], cr = q ? co[1] : ce[1];
-        o[3 * q] = (uint8_t)min(max(Y + ((91881 * cr + 32768) >> 16), 0), 255);
-        o[3 * q + 1] = (uint8_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
-        o[3 * q + 2] = (uint8_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255);
+      for (int k = 0; k < 4; ++k) {
+        const int Y = (int)((y4 >> (8 * k)) & 0xFF), cb = u[0][k], cr = u[1][k];
+        px[3 * k] = (uint32_t)min(max(Y + ((91881 * cr + 32768) >> 16), 0), 255);
+        px[3 * k + 1] = (uint32_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
+        px[3 * k + 2] = (uint32_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255);
+      }
+      const int o = (yy * w + 4 * q) * 3;
+      if (4 * q + 4 <= w && (o & 3) == 0) {
+        uint32_t* o32 = reinterpret_cast<uint32_t*>(stg + o);
+        o32[0] = px[0] | px[1] << 8 | px[2] << 16 | px[3] << 24;
+        o32[1] = px[4] | px[5] << 8 | px[6] << 16 | px[7] << 24;
+        o32[2] = px[8] | px[9] << 8 | px[10] << 16 | px[11] << 24;
+      } else {
+        const int nv = min(4, w - 4 * q) * 3;
+#pragma unroll
+        for (int k = 0; k < 12; ++k) if (k < nv) stg[o + k] = (uint8_t)px[k];
       }
     }
+    __syncthreads();
+    const int nbytes = rows * w * 3;
+    uint8_t* g = outp + (size_t)y_first * w * 3;
+    int done = 0;
+    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+      done = nbytes & ~15;
+      for (int k = threadIdx.x * 16; k < done; k += kPixThreads * 16)
+        *reinterpret_cast<uint4*>(g + k) = *reinterpret_cast<const uint4*>(stg + k);
+    }
+    for (int k = done + threadIdx.x; k < nbytes; k += kPixThreads) g[k] = stg[k];
     return;
   }
   for (int idx = threadIdx.x; idx < rows * w; idx += kPixThreads) {
@@ -481,10 +599,17 @@ __global__ void __launch_bounds__(kPixThreads) jpeg_pixels_kernel(const JpegArgs
 int launch_jpeg(const JpegArgs& A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (A.count <= 0 || A.total_int == 0) return 0;
-  jpeg_unstuff_kernel<<<(A.count + kUnstuffWarps - 1) / kUnstuffWarps, 32 * kUnstuffWarps, 0, st>>>(A);
-  const int hsmem = A.n_huff <= kJpegSmemTables ? A.n_huff * (int)sizeof(JHuff::fast) : 0;
-  if (hsmem > 48 * 1024) cudaFuncSetAttribute(jpeg_huffman_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
-  jpeg_huffman_kernel<<<(A.total_int + kHuffThreads - 1) / kHuffThreads, kHuffThreads, hsmem, st>>>(A);
+  jpeg_unstuff_kernel<<<A.count, 32 * kUnstuffWarps, 0, st>>>(A);
+  const bool smem = A.n_huff <= kJpegSmemTables;
+  const int hsmem = (smem ? A.n_huff * (int)sizeof(JHuff::fast) : 0) + kMaxBpm * kHuffThreads * 8;
+  const unsigned hgrid = (A.total_int + kHuffThreads - 1) / kHuffThreads;
+  if (smem) {
+    cudaFuncSetAttribute(jpeg_huffman_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
+    jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A);
+  } else {
+    cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
+    jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A);
+  }
   if (A.pix_smem > 48 * 1024)
     cudaFuncSetAttribute(jpeg_pixels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.pix_smem);
   jpeg_pixels_kernel<<<dim3(A.max_mcu_rows, A.count), kPixThreads, A.pix_smem, st>>>(A);

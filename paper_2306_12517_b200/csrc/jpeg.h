@@ -6,8 +6,9 @@
 //                            entropy-coded segment (T.81 B.2.5 / F.1.2.3),
 //                            drops marker and stuffing bytes and writes every
 //                            restart interval as a 4-byte-aligned plain
-//                            bitstream (so J2 refills 32 bits per load, no
-//                            0xFF checks)
+//                            bitstream followed by kJpegIntPad zero bytes (so
+//                            J2 refills 32 bits per load, no 0xFF checks, no
+//                            end-of-data test)
 //   J2 jpeg_huffman_kernel   thread per restart interval: one flat loop, one
 //                            symbol per iteration (T.81 F.2.2), shared-memory
 //                            tables that resolve code + extra bits in one
@@ -30,19 +31,20 @@
 
 namespace bbx {
 
-constexpr int kJpegFastBits = 10;         // Huffman lookahead bits (fast table)
+constexpr int kJpegFastBits = 11;         // Huffman lookahead bits (fast table)
 constexpr int kJpegMaxHuff = 512;         // device Huffman table pool entries
 constexpr int kJpegMaxQuant = 256;        // device quant table pool entries
 constexpr int kJpegSmemTables = 8;        // J2 stages the pool in smem when it holds at most this many
+constexpr int kJpegIntAlign = 16;         // restart intervals start 16-byte aligned in the J1 output
+constexpr int kJpegIntPad = 32;           // zero bytes (at least) J1 writes after every interval
 
-// Fast-table entry (u32) indexed by the next kJpegFastBits bits of the stream,
-// for codes of at most kJpegFastBits bits (0 otherwise: maxcode walk):
-//   bits 0..4 code length, 5..9 extra bits (size), 10..13 zero run,
-//   bit 14 end of block (AC size 0, run < 15), bit 31 valid
-constexpr uint32_t kFastValid = 1u << 31, kFastEob = 1u << 14;
+// Fast-table entry (u16) indexed by the next kJpegFastBits bits of the stream:
+//   bits 0..4 code length (0: longer than kJpegFastBits -> maxcode walk),
+//   5..9 extra bits (size), 10..13 zero run, bit 14 end of block (AC size 0, run < 15)
+constexpr uint32_t kFastEob = 1u << 14;
 
 struct JHuff {                            // one Huffman table, device form
-  uint32_t fast[1 << kJpegFastBits];
+  uint16_t fast[1 << kJpegFastBits];
   int32_t maxcode[18];                    // largest code of each length, -1 if none; [17] sentinel
   int32_t valoff[18];                     // vals index = code + valoff[len]
   uint8_t vals[256];
@@ -105,9 +107,21 @@ struct JpegArgs {
 // jpeg.cu
 int launch_jpeg(const JpegArgs& A, void* stream);
 
-// J3 shared-memory window of component c for one MCU row: its own pixel rows
-// plus one block row above and below when it is vertically upsampled.
+// J3 shared memory for one MCU row: per component a pixel window (its own
+// rows plus one block row above and below when it is vertically upsampled)
+// and the staged coefficient blocks of those block rows (144-byte slots).
+constexpr int kJpegCoefSlot = 144;
 BBX_HD inline int jpeg_window_rows(int v, int vmax) { return 8 * v + (vmax / v == 2 ? 16 : 0); }
+BBX_HD inline int jpeg_pix_smem(const JpegDesc& J) {
+  int win = 0, slots = 0;
+  for (int c = 0; c < J.ncomp; ++c) {
+    const int rows = jpeg_window_rows(J.comp[c].v, J.vmax);
+    win += rows * J.comp[c].bw * 8;
+    slots += (rows / 8) * J.comp[c].bw * kJpegCoefSlot;
+  }
+  const int rgb = J.mcus_x * 8 * J.hmax * 8 * J.vmax * 3;   // RGB staging of one MCU row (reuses the slots)
+  return win + (slots > rgb ? slots : rgb);
+}
 
 // jpeg_host.cpp
 struct JpegHeader {

@@ -90,7 +90,8 @@ def target(name, sass):
 def kernel_mangle_guess(name):
     m = re.search(r"void bbx::(\w+)<(.*?)>\(", name)
     if not m:
-        return None
+        m = re.search(r"bbx::(\w+)\(", name)   # plain (non-template) kernel: _ZN3bbx<len><name>E...
+        return f"{len(m.group(1))}{m.group(1)}E" if m else None
     fn, args = m.group(1), [a.strip() for a in m.group(2).split(",")]
     enc = []
     for a in args:
