@@ -139,6 +139,8 @@ struct Plan {
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
   std::vector<uint32_t*> d_tables;   // per slot: K1 prologue tables
+  std::vector<JpegDesc> jcache;      // per sample, valid where jcached[i] (JPEG fields)
+  std::vector<uint8_t> jcached;
   uint64_t* d_col = nullptr;     // scalar column (num_samples x 8 B)
 };
 
@@ -180,7 +182,10 @@ struct JpegTables {
   JHuff* d_huff = nullptr;
   JQuant* d_quant = nullptr;
   int n_huff = 0, n_quant = 0, up_huff = 0, up_quant = 0;
-  std::unordered_map<std::string, int> hmap, qmap;
+  // content hash -> ids (several on a collision); raw bytes kept to verify
+  std::unordered_multimap<uint64_t, int> hmap, qmap;
+  std::vector<std::vector<uint8_t>> hkey, qkey;
+  std::mutex mu;                 // headers are parsed on the staging pool
 };
 
 }  // namespace bbx
@@ -200,6 +205,7 @@ struct bbx_loader {
   std::vector<size_t> desc_off;       // per plan, within a slot
   std::vector<size_t> jpeg_off;       // per plan with JPEG samples: JpegDesc[B] + prefixes, within a slot
   JpegTables jt;
+  bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
   size_t pay_base = 0;                // start of the compact payload region
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
@@ -636,25 +642,39 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
 
 static void pipeline_loop(bbx_loader* L);
 
-// Table pool ids for one JPEG header (registering unseen tables).
+// Table pool ids for one JPEG header (registering unseen tables).  Callers hold T.mu.
+static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 1469598103934665603ull) {
+  for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  return h;
+}
 static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, bool is_ac, int* id) {
-  std::string key(1, is_ac ? 'A' : 'D');
-  key.append(reinterpret_cast<const char*>(h.counts), 16);
-  key.append(reinterpret_cast<const char*>(h.vals), h.nvals);
-  auto it = T.hmap.find(key);
-  if (it != T.hmap.end()) { *id = it->second; return 0; }
+  uint8_t key[1 + 16 + 256];
+  key[0] = is_ac ? 'A' : 'D';
+  std::memcpy(key + 1, h.counts, 16);
+  std::memcpy(key + 17, h.vals, h.nvals);
+  const size_t n = 17 + h.nvals;
+  const uint64_t hv = fnv1a(key, n);
+  for (auto [it, end] = T.hmap.equal_range(hv); it != end; ++it) {
+    const auto& k = T.hkey[it->second];
+    if (k.size() == n && !std::memcmp(k.data(), key, n)) { *id = it->second; return 0; }
+  }
   if (T.n_huff >= kJpegMaxHuff) return 2;
   if (!jpeg_build_huff(h, is_ac, &T.h_huff[T.n_huff])) return 1;
-  *id = T.hmap[key] = T.n_huff++;
+  T.hkey.emplace_back(key, key + n);
+  T.hmap.emplace(hv, T.n_huff);
+  *id = T.n_huff++;
   return 0;
 }
 static int jpeg_quant_id(JpegTables& T, const JpegHeader::Quant& q, int* id) {
-  std::string key(reinterpret_cast<const char*>(q.q), sizeof q.q);
-  auto it = T.qmap.find(key);
-  if (it != T.qmap.end()) { *id = it->second; return 0; }
+  const uint8_t* key = reinterpret_cast<const uint8_t*>(q.q);
+  const uint64_t hv = fnv1a(key, sizeof q.q);
+  for (auto [it, end] = T.qmap.equal_range(hv); it != end; ++it)
+    if (!std::memcmp(T.qkey[it->second].data(), key, sizeof q.q)) { *id = it->second; return 0; }
   if (T.n_quant >= kJpegMaxQuant) return 2;
   std::memcpy(T.h_quant[T.n_quant].q, q.q, sizeof q.q);
-  *id = T.qmap[key] = T.n_quant++;
+  T.qkey.emplace_back(key, key + sizeof q.q);
+  T.qmap.emplace(hv, T.n_quant);
+  *id = T.n_quant++;
   return 0;
 }
 
@@ -688,9 +708,12 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
     const auto& c = H.comp[i];
     JComp& o = J->comp[i];
     int dc, ac, q, r;
-    if ((r = jpeg_table_id(T, H.dc[c.td], false, &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], true, &ac)) ||
-        (r = jpeg_quant_id(T, H.qt[c.tq], &q)))
-      return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
+    {
+      std::lock_guard<std::mutex> g(T.mu);
+      if ((r = jpeg_table_id(T, H.dc[c.td], false, &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], true, &ac)) ||
+          (r = jpeg_quant_id(T, H.qt[c.tq], &q)))
+        return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
+    }
     o.dc = (uint16_t)dc; o.ac = (uint16_t)ac; o.q = (uint16_t)q;
     o.h = (uint8_t)c.h; o.v = (uint8_t)c.v;
     o.bw = (uint16_t)(H.ncomp == 1 ? mx : mx * c.h);
@@ -786,6 +809,7 @@ static int finalize(bbx_loader* L) {
   }
   for (auto& pl : L->plans) {
     if (pl.scalar || !pl.field_has_jpeg) continue;
+    if (L->jpeg_cache) { pl.jcache.resize(L->ds->num_samples); pl.jcached.assign(L->ds->num_samples, 0); }
     const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
     CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
     CK(cudaMalloc(&pl.d_bits, (size_t)L->batch * pl.jpeg_bits_cap + 256));
@@ -858,6 +882,8 @@ static int process_slot(bbx_loader* L, int s) {
   // descriptors + payload plan (serial: ~100 ns per sample per field)
   struct Copy { const uint8_t* src; uint8_t* dst; uint32_t row_bytes, rows, src_stride; };
   std::vector<Copy> copies;
+  struct JParse { int plan; int pos; int64_t idx; uint64_t off; uint32_t len; };
+  std::vector<JParse> jparse;
   if (!resident) copies.reserve((size_t)count * L->plans.size());
   double t0 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // one compact payload region for every plan: [pay_base, cursor)
@@ -884,8 +910,9 @@ static int process_slot(bbx_loader* L, int s) {
       SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
       if (!ok) continue;
       if (d->codec == CODEC_RLE && ds->fields[pl.field_index].info.kind == 4) S.plan_has_rle[p] = 1;
-      if (image && d->codec == CODEC_JPEG) {
-        if (!jpeg_prepare(L, pl, ds->map + off, len, d, &jds[pos], S.herr, pos, (int)p)) continue;
+      if (image && d->codec == CODEC_JPEG) {   // header: from the cache, else parsed on the pool below
+        if (L->jpeg_cache && pl.jcached[i]) jds[pos] = pl.jcache[i];
+        else jparse.push_back({(int)p, pos, i, off, len});
         S.plan_has_jpeg[p] = 1;
       }
       if (resident) {
@@ -910,6 +937,22 @@ static int process_slot(bbx_loader* L, int s) {
       if (len) copies.push_back({ds->map + off, H + cursor, len, 1, len});
       cursor += ((size_t)len + 15) / 16 * 16;
     }
+  }
+  // JPEG headers not seen before: parse on the pool (tables registered under a mutex)
+  if (!jparse.empty()) {
+    std::vector<HostErr> jerr(jparse.size());
+    L->pool->parallel_for((int64_t)jparse.size(), [&](int64_t q) {
+      const JParse& j = jparse[q];
+      Plan& pl = L->plans[j.plan];
+      uint8_t* desc = H + L->desc_off[j.plan] + (size_t)j.pos * pl.dev.desc_stride;
+      JpegDesc* jd = reinterpret_cast<JpegDesc*>(H + L->jpeg_off[j.plan]) + j.pos;
+      if (jpeg_prepare(L, pl, ds->map + j.off, j.len, reinterpret_cast<SampleDesc*>(desc), jd, jerr[q], j.pos, j.plan)) {
+        if (L->jpeg_cache) { pl.jcache[j.idx] = *jd; pl.jcached[j.idx] = 1; }   // distinct samples: no race
+      }
+    });
+    for (const HostErr& e : jerr)
+      if (e.pos >= 0 && (S.herr.pos < 0 || e.pos < S.herr.pos || (e.pos == S.herr.pos && e.plan < S.herr.plan)))
+        S.herr = e;
   }
   // JPEG: interval / block prefixes of each plan's batch (J2/J3 thread maps)
   for (size_t p = 0; p < L->plans.size(); ++p) {
@@ -1265,6 +1308,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   L->slots.resize(slot_count);
   if (const char* e = std::getenv("BBX_WINDOW_STAGING")) L->window_staging = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_DMA")) L->dma_allowed = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BBX_JPEG_CACHE")) L->jpeg_cache = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   L->pool = std::make_unique<Pool>(nt);
