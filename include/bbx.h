@@ -183,7 +183,12 @@ void* bbx_loader_compute_stream(bbx_loader* ld);
 
 /* ------------------------------------------------------------- one image
  * codecs.decode_image (codecs.py:91-128) on device: decode one blob into a
- * caller-owned (h, w, c) u8 device buffer.  Synchronous; for tests/tools. */
+ * caller-owned (h, w, c) u8 device buffer.  Synchronous; for tests/tools.
+ * codec: the cell's codec byte (format.py:72) -- BBX_CODEC_RAW / _RLE /
+ * _SUBSAMPLE2 as codecs.py:25-28, plus BBX_CODEC_JPEG (this build's
+ * extension: baseline JFIF, 1 or 3 components, sampling factors <= 2,
+ * decoded bit-exactly as libjpeg-turbo's ISLOW + fancy-upsampling path). */
+enum { BBX_CODEC_RAW = 0, BBX_CODEC_RLE = 1, BBX_CODEC_SUBSAMPLE2 = 2, BBX_CODEC_JPEG = 3 };
 bbx_status bbx_decode_image(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host,
                             int64_t len, uint8_t* out_dev, int device);
 
