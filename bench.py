@@ -251,7 +251,7 @@ def jpeg_workload(args, device, rank, world, barrier, reduce_max):
     st = ld.stats()
     ld.shutdown()
     ds.close()
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B)
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B, slot_count=4)
     e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
     st2 = ld2.stats()
     ld2.shutdown()

@@ -703,6 +703,7 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
   const int mx = H.ncomp == 1 ? (H.width + 7) / 8 : (H.width + 8 * hmax - 1) / (8 * hmax);
   const int my = H.ncomp == 1 ? (H.height + 7) / 8 : (H.height + 8 * vmax - 1) / (8 * vmax);
   uint32_t blocks = 0;
+  int mcu_off = 0;
   JpegTables& T = L->jt;
   for (int i = 0; i < H.ncomp; ++i) {
     const auto& c = H.comp[i];
@@ -720,7 +721,8 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
     o.bh = (uint16_t)(H.ncomp == 1 ? my : my * c.v);
     o.dw = (uint16_t)(((int64_t)H.width * c.h + hmax - 1) / hmax);
     o.dh = (uint16_t)(((int64_t)H.height * c.v + vmax - 1) / vmax);
-    o.blk_off = blocks;
+    o.blk_off = (uint32_t)mcu_off;
+    mcu_off += H.ncomp == 1 ? 1 : c.h * c.v;
     blocks += (uint32_t)o.bw * o.bh;
   }
   const uint32_t total = (uint32_t)mx * my;
@@ -1093,6 +1095,7 @@ static int process_slot(bbx_loader* L, int s) {
       J.istart = pl.d_istart; J.iend = pl.d_iend; J.bits = pl.d_bits; J.coef = pl.d_coef;
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
       J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
+      J.coef_zeroed = 1;
       J.total_int = S.jpeg_total_int[p]; J.max_mcu_rows = S.jpeg_max_rows[p]; J.pix_smem = S.jpeg_pix_smem[p];
       if (J.pix_smem > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "jpeg: image rows too wide for the device decoder");
       // J2 stores only nonzero coefficients
@@ -1203,6 +1206,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
   A.n_huff = L.jt.n_huff;
+  A.coef_zeroed = 1;
   A.status = reinterpret_cast<SampleStatus*>(dev + o_st);
   A.count = 1; A.total_int = J.n_int; A.max_mcu_rows = J.mcus_y; A.pix_smem = pix;
   int rc = e == cudaSuccess ? launch_jpeg(A, nullptr) : 1;

@@ -68,7 +68,7 @@ __device__ __forceinline__ ChunkMasks chunk_masks(uintptr_t my, uintptr_t a_lo, 
   if (my < a_hi) v = ld_nc_v4(reinterpret_cast<const void*>(my));   // buffers carry >= 16 B of tail padding
   M.w[0] = v.x; M.w[1] = v.y; M.w[2] = v.z; M.w[3] = v.w;
   uint32_t prev = __shfl_up_sync(0xffffffffu, v.w >> 24, 1);
-  if (lane == 0) prev = (my > a_lo) ? *reinterpret_cast<const uint8_t*>(my - 1) : 0u;
+  if (lane == 0) prev = (my > a_lo && my <= a_hi) ? *reinterpret_cast<const uint8_t*>(my - 1) : 0u;
   uint32_t nxt = __shfl_down_sync(0xffffffffu, v.x & 0xFF, 1);
   if (lane == 31) nxt = (my + 16 < a_hi) ? *reinterpret_cast<const uint8_t*>(my + 16) : 0u;
   M.nxt = nxt;
@@ -231,133 +231,177 @@ template <typename T>
 __device__ __forceinline__ T sel3(int i, T a, T b, T c) { return i == 0 ? a : (i == 1 ? b : c); }
 
 template <bool kSmem>
-__global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegArgs A) {
+__global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegArgs A, uint32_t chunk) {
   extern __shared__ __align__(16) uint8_t hsm[];
   __shared__ uint8_t nat[80];
+  __shared__ uint32_t s_next;
   constexpr int TW = 1 << kJpegFastBits;
-  const int tabs_bytes = kSmem ? A.n_huff * TW * 2 : 0;
-  const uint16_t* tab = kSmem ? reinterpret_cast<const uint16_t*>(hsm) : reinterpret_cast<const uint16_t*>(A.huff);
-  uint64_t* slot = reinterpret_cast<uint64_t*>(hsm + tabs_bytes) + threadIdx.x;   // [b * kHuffThreads]
+  constexpr uint32_t TSTRIDE = kSmem ? TW : (uint32_t)(sizeof(JHuff) / 4);
+  const int tabs_bytes = kSmem ? A.n_huff * TW * 4 : 0;
+  const uint32_t* tab = kSmem ? reinterpret_cast<const uint32_t*>(hsm) : reinterpret_cast<const uint32_t*>(A.huff);
+  // long codes (12..16 bits): per table maxcode[12..16], valoff[12..16] (int32) and vals[256] in smem
+  constexpr int kSlowBytes = 10 * 4 + 256;
+  uint8_t* slow = hsm + tabs_bytes;
   if (kSmem) {
-    uint16_t* st = reinterpret_cast<uint16_t*>(hsm);
+    uint32_t* st = reinterpret_cast<uint32_t*>(hsm);
     const int n = A.n_huff * TW;
     for (int i = threadIdx.x; i < n; i += kHuffThreads) st[i] = __ldg(&A.huff[i / TW].fast[i % TW]);
+    for (int i = threadIdx.x; i < A.n_huff * kSlowBytes; i += kHuffThreads) {
+      const int tb = i / kSlowBytes, o = i % kSlowBytes;
+      const JHuff& H = A.huff[tb];
+      uint8_t v;
+      if (o < 20) { const int32_t m = H.maxcode[12 + o / 4]; v = (uint8_t)(m >> (8 * (o & 3))); }
+      else if (o < 40) { const int32_t m = H.valoff[12 + (o - 20) / 4]; v = (uint8_t)(m >> (8 * (o & 3))); }
+      else v = H.vals[o - 40];
+      slow[i] = v;
+    }
   }
   for (int i = threadIdx.x; i < 80; i += kHuffThreads) nat[i] = c_natural[i];
+  // this CTA's intervals [c0, c1): lanes start on the first kHuffThreads, then pull from s_next
+  const uint32_t c0 = blockIdx.x * chunk, c1 = min(c0 + chunk, A.total_int);
+  if (threadIdx.x == 0) s_next = c0 + kHuffThreads;
   __syncthreads();
-  const uint32_t t = blockIdx.x * kHuffThreads + threadIdx.x;
-  if (t >= A.total_int) return;
-  const int s = find_sample(A.int_prefix, A.count, t);
-  if (A.status[s].kind != 0) return;                 // J1 rejected the marker layout
-  const JpegDesc& J = A.jd[s];
-  const uint32_t k = t - J.int_base;
-  const uint32_t mcus_x = J.mcus_x, total = mcus_x * J.mcus_y;
-  const uint32_t m0 = k * J.restart, m1 = min(m0 + J.restart, total);
-  if (m0 >= m1) return;
-  const int bpm = J.bpm;
-  // slot b: block offset in its component's MCU origin | comp << 16 | dc table << 18 | ac table << 41
-  constexpr uint32_t TSTRIDE = kSmem ? TW : (uint32_t)(sizeof(JHuff) / 2);
-  for (int b = 0; b < bpm; ++b) {
-    const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
-    const JComp& C = J.comp[c];
-    const uint64_t d = ((e >> 2) & 1) * C.bw + (e >> 3);
-    slot[b * kHuffThreads] = d | (uint64_t)c << 16 | (uint64_t)(C.dc * TSTRIDE) << 18 | (uint64_t)(C.ac * TSTRIDE) << 41;
-  }
-  const uint32_t h0 = J.comp[0].h, h1 = J.comp[1].h, h2 = J.comp[2].h;
-  const uint32_t rs0 = J.comp[0].v * J.comp[0].bw, rs1 = J.comp[1].v * J.comp[1].bw, rs2 = J.comp[2].v * J.comp[2].bw;
-  const uint32_t of0 = J.comp[0].blk_off, of1 = J.comp[1].blk_off, of2 = J.comp[2].blk_off;
-  int16_t* const coef = A.coef + J.blk_base * 64;
 
-  // 16-byte chunks of the interval (J1 aligned it and zero-padded its tail):
-  // `cur` is being consumed, `nxt` is in flight
-  const uint4* p16 = reinterpret_cast<const uint4*>(A.bits + J.bs_base + A.istart[t]);
-  const uint4* plast = reinterpret_cast<const uint4*>(A.bits + J.bs_base + align_int(A.iend[t]) + kJpegIntPad - 16);
-  uint4 cur = ld_nc_v4(p16);
-  p16 += p16 < plast ? 1 : 0;
-  uint4 nxt = ld_nc_v4(p16);
-  int wi = 0;
+  // per-lane decoder state of the current restart interval
+  const uint4* p16 = nullptr;
+  const uint4* plast = nullptr;
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;          // next stream words; nxt = the chunk after them
+  uint4 nxt = make_uint4(0, 0, 0, 0);
   uint64_t acc = 0;
-  int nb = 0;
-
-  uint32_t m = m0, mx = m0 % mcus_x, my = m0 / mcus_x;
-  uint32_t base0 = of0 + my * rs0 + mx * h0, base1 = of1 + my * rs1 + mx * h1, base2 = of2 + my * rs2 + mx * h2;
-  int b = 0, kk = 0, ci = 0;
+  int nb = 0, wi = 0;
+  uint32_t m = 0, m1 = 0;                            // MCU counter / end
+  int b = 0, bpm = 1, kk = 0, ci = 0, s = 0;
+  uint32_t k = 0, sched = 0, tdc = 0, tac = 0;
+  uint64_t tabs = 0;                                 // dc / ac table ids of the components, 9 bits each
   int pred0 = 0, pred1 = 0, pred2 = 0;
-  uint32_t tdc = 0, tac = 0;
   int16_t* cb = nullptr;
-  bool bad = false;
-  auto setup = [&]() {                               // block b of the current MCU
-    const uint64_t r = slot[b * kHuffThreads];
-    ci = (int)((r >> 16) & 3);
-    tdc = (uint32_t)(r >> 18) & 0x7FFFFFu;
-    tac = (uint32_t)(r >> 41) & 0x7FFFFFu;
-    cb = coef + (size_t)(sel3(ci, base0, base1, base2) + (uint32_t)(r & 0xFFFF)) * 64;
-    kk = 0;
+
+  auto comp_tables = [&]() {                         // ci, tdc, tac of block b
+    ci = (int)((sched >> (2 * b)) & 3u);
+    const uint32_t ids = (uint32_t)(tabs >> (18 * ci));
+    tdc = (ids & 511u) * TSTRIDE;
+    tac = ((ids >> 9) & 511u) * TSTRIDE;
   };
-  setup();
-  for (;;) {
-    {                                                // predicated 32-bit refill from the chunk registers
+  // set up interval t; false when it has nothing to decode
+  auto start = [&](uint32_t t) -> bool {
+    s = find_sample(A.int_prefix, A.count, t);
+    if (A.status[s].kind != 0) return false;         // J1 rejected the marker layout
+    const JpegDesc& J = A.jd[s];
+    k = t - J.int_base;
+    const uint32_t total = (uint32_t)J.mcus_x * J.mcus_y;
+    m = k * J.restart;
+    m1 = min(m + J.restart, total);
+    if (m >= m1) return false;
+    bpm = J.bpm;
+    sched = 0;
+    for (int q = 0; q < bpm; ++q) sched |= ((uint32_t)(J.sched >> (4 * q)) & 3u) << (2 * q);
+    tabs = 0;
+    for (int c = 0; c < J.ncomp; ++c) tabs |= (uint64_t)(J.comp[c].dc | (uint32_t)J.comp[c].ac << 9) << (18 * c);
+    cb = A.coef + (J.blk_base + (uint64_t)m * bpm) * 64;
+    // 16-byte chunks of the interval (J1 aligned it and zero-padded its tail)
+    p16 = reinterpret_cast<const uint4*>(A.bits + J.bs_base + A.istart[t]);
+    plast = reinterpret_cast<const uint4*>(A.bits + J.bs_base + align_int(A.iend[t]) + kJpegIntPad - 16);
+    const uint4 c = ld_nc_v4(p16);
+    q0 = c.x; q1 = c.y; q2 = c.z; q3 = c.w;
+    p16 += p16 < plast ? 1 : 0;
+    nxt = ld_nc_v4(p16);
+    wi = 0; acc = 0; nb = 0;
+    b = 0; kk = 0;
+    pred0 = pred1 = pred2 = 0;
+    comp_tables();
+    return true;
+  };
+  auto acquire = [&](uint32_t t) -> bool {
+    for (;;) {
+      if (t >= c1) return false;
+      if (start(t)) return true;
+      t = atomicAdd(&s_next, 1u);
+    }
+  };
+  bool active = acquire(c0 + threadIdx.x);
+  while (__any_sync(0xffffffffu, active)) {
+    if (!active) continue;
+    {                                                // predicated 32-bit refill
       const bool need = nb <= 32;
-      uint32_t wv = wi == 0 ? cur.x : (wi == 1 ? cur.y : (wi == 2 ? cur.z : cur.w));
-      wv = need ? __byte_perm(wv, 0, 0x0123) : 0u;
+      const uint32_t wv = need ? __byte_perm(q0, 0, 0x0123) : 0u;
       acc |= (uint64_t)wv << ((32 - nb) & 63);
       nb += need ? 32 : 0;
       wi += need ? 1 : 0;
+      q0 = need ? q1 : q0; q1 = need ? q2 : q1; q2 = need ? q3 : q2;
       if (wi == 4) {
         wi = 0;
-        cur = nxt;
+        q0 = nxt.x; q1 = nxt.y; q2 = nxt.z; q3 = nxt.w;
         p16 += p16 < plast ? 1 : 0;
         nxt = ld_nc_v4(p16);
       }
     }
-    const uint32_t e = tab[(kk ? tac : tdc) + (uint32_t)(acc >> (64 - kJpegFastBits))];
-    int len = (int)(e & 31), size, run;
-    bool eob;
-    if (len) {
-      size = (int)((e >> 5) & 31);
-      run = (int)((e >> 10) & 15);
-      eob = (e & kFastEob) != 0;
-    } else {                                         // code longer than the fast table
-      const JHuff* g = A.huff + (kk ? tac : tdc) / TSTRIDE;
+    uint32_t e = tab[(kk ? tac : tdc) + (uint32_t)(acc >> (64 - kJpegFastBits))];
+    bool bad = false;
+    if (!(e & kFastValid)) {                         // code longer than the fast table (12..16 bits)
+      const uint32_t tid = (kk ? tac : tdc) / TSTRIDE;
       const uint32_t c16 = (uint32_t)(acc >> 48);
-      len = kJpegFastBits + 1;
-      while (len <= 16 && (int32_t)(c16 >> (16 - len)) > __ldg(&g->maxcode[len])) ++len;
-      if (len > 16) { bad = true; break; }
-      const int sym = __ldg(&g->vals[(c16 >> (16 - len)) + __ldg(&g->valoff[len])]);
-      size = kk ? (sym & 15) : sym;
-      run = kk ? (sym >> 4) : 0;
-      eob = kk && size == 0 && run != 15;
+      uint32_t hit = 0;
+      if (kSmem) {
+        const int32_t* mc = reinterpret_cast<const int32_t*>(slow + tid * kSlowBytes);
+#pragma unroll
+        for (int l = 12; l <= 16; ++l) hit |= ((int32_t)(c16 >> (16 - l)) <= mc[l - 12] ? 1u : 0u) << (l - 12);
+      } else {
+        const JHuff* g = A.huff + tid;
+#pragma unroll
+        for (int l = 12; l <= 16; ++l) hit |= ((int32_t)(c16 >> (16 - l)) <= __ldg(&g->maxcode[l]) ? 1u : 0u) << (l - 12);
+      }
+      int sym = 0, len = 16;
+      if (hit == 0) bad = true;
+      else {
+        len = 11 + __ffs(hit);
+        const int code = (int)(c16 >> (16 - len));
+        if (kSmem) {
+          const uint8_t* sb = slow + tid * kSlowBytes;
+          sym = sb[40 + code + reinterpret_cast<const int32_t*>(sb + 20)[len - 12]];
+        } else {
+          const JHuff* g = A.huff + tid;
+          sym = __ldg(&g->vals[code + __ldg(&g->valoff[len])]);
+        }
+      }
+      const int size = kk ? (sym & 15) : sym, run = kk ? (sym >> 4) : 0;
+      e = kFastValid | (uint32_t)len << 25 | (uint32_t)size << 16 | (uint32_t)run << 21 |
+          ((kk && size == 0 && run != 15) ? kFastEob : 0u);
     }
-    acc <<= len;
+    // common tail: consume the code (or code + extra bits), then any extra bits still pending
+    const int used = (int)((e >> 25) & 31);
+    acc <<= used;
+    const int size = (e & kFastFull) ? 0 : (int)((e >> 16) & 15);
     const uint32_t hi = (uint32_t)(acc >> 32);
-    const uint32_t bits = __funnelshift_l(hi, 0u, size);          // top `size` bits (0 when size == 0)
-    const int sgn = (int)hi >> 31;                               // leading extra bit 1: positive value
-    int v = (int)bits + ((int)((0xFFFFFFFFu << size) + 1u) & ~sgn);   // EXTEND (F.2.2.1)
+    const uint32_t bits = __funnelshift_l(hi, 0u, size);               // top `size` bits (0 when size == 0)
+    const int sgn = (int)hi >> 31;                                      // leading extra bit 1: positive
+    int v = (e & kFastFull) ? (int)(int16_t)(e & 0xFFFF)
+                            : (int)bits + ((int)((0xFFFFFFFFu << size) + 1u) & ~sgn);   // EXTEND (F.2.2.1)
     acc <<= size;
-    nb -= len + size;
+    nb -= used + size;
+    const int run = (int)((e >> 21) & 15);
     if (kk == 0) {                                   // DC: prediction per component
-      v += sel3(ci, pred0, pred1, pred2);
+      int p = ci == 0 ? pred0 : pred1;
+      p = ci == 2 ? pred2 : p;
+      v += p;
       pred0 = ci == 0 ? v : pred0;
       pred1 = ci == 1 ? v : pred1;
       pred2 = ci == 2 ? v : pred2;
     }
     const int pos = kk + run;
-    if (v != 0) cb[nat[pos]] = (int16_t)v;
-    kk = eob ? 64 : pos + 1;
-    if (kk >= 64) {                                  // block done: next block of the MCU / next MCU
-      if (++b == bpm) {
-        b = 0;
-        if (++m >= m1) break;
-        base0 += h0; base1 += h1; base2 += h2;
-        if (++mx == mcus_x) {
-          mx = 0; ++my;
-          base0 = of0 + my * rs0; base1 = of1 + my * rs1; base2 = of2 + my * rs2;
-        }
+    if (v != 0 && !bad) cb[nat[pos]] = (int16_t)v;
+    kk = (e & kFastEob) ? 64 : pos + 1;
+    if (kk >= 64 || bad) {                           // block done: blocks are stored in decode order
+      cb += 64;
+      kk = 0;
+      if (++b == bpm) { b = 0; ++m; }
+      if (bad || m >= m1) {
+        if (bad) { A.status[s].value = k; A.status[s].kind = JST_BAD_CODE; }
+        active = acquire(atomicAdd(&s_next, 1u));
+      } else {
+        comp_tables();
       }
-      setup();
     }
   }
-  if (bad) { A.status[s].value = k; A.status[s].kind = JST_BAD_CODE; }
 }
 
 // ------------------------------------------------------------------- J3
@@ -471,46 +515,51 @@ __device__ __forceinline__ int win_sample(const Win& c, int y, int x) {
 
 __global__ void __launch_bounds__(kPixThreads, 3) jpeg_pixels_kernel(const JpegArgs A) {
   extern __shared__ __align__(16) uint8_t psm[];
-  __shared__ int s_coff[3], s_brlo[3], s_njob[3], s_bw[3], s_pw[3], s_y0[3], s_win[3];
+  __shared__ int s_coff[3], s_brlo[3], s_njob[3], s_bw[3], s_pw[3], s_y0[3], s_win[3], s_vs[3], s_hs[3], s_boff[3];
   const int s = blockIdx.y, r = blockIdx.x;
   const JpegDesc& J = A.jd[s];
   if (J.n_int == 0 || r >= J.mcus_y || A.status[s].kind != 0) return;
   const SampleDesc* d = sdesc(A, s);
   const int w = d->w, h = d->h, nc = J.ncomp, hmax = J.hmax, vmax = J.vmax;
+  __shared__ int s_mrlo, s_nblk;
   if (threadIdx.x == 0) {
-    int off = 0, slots = 0;
+    int off = 0, ext_any = 0;
     for (int c = 0; c < 3; ++c) {
-      if (c >= nc) { s_njob[c] = 0; s_coff[c] = slots; continue; }
+      if (c >= nc) { s_njob[c] = 0; continue; }
       const JComp& C = J.comp[c];
       const int ext = vmax / C.v == 2 ? 1 : 0;
+      ext_any |= ext;
       const int lo = max(r * C.v - ext, 0), hi = min(r * C.v + C.v - 1 + ext, (int)C.bh - 1);
       s_brlo[c] = lo; s_njob[c] = (hi - lo + 1) * C.bw; s_bw[c] = C.bw; s_pw[c] = C.bw * 8;
-      s_y0[c] = (r * C.v - ext) * 8; s_win[c] = off; s_coff[c] = slots;
+      s_y0[c] = (r * C.v - ext) * 8; s_win[c] = off;
+      s_vs[c] = nc == 1 ? 0 : C.v - 1; s_hs[c] = nc == 1 ? 0 : C.h - 1; s_boff[c] = (int)C.blk_off;
       off += jpeg_window_rows(C.v, vmax) * C.bw * 8;
-      slots += s_njob[c];
     }
+    const int lo = max(r - ext_any, 0), hi = min(r + ext_any, (int)J.mcus_y - 1);
+    s_mrlo = lo;
+    s_nblk = (hi - lo + 1) * J.mcus_x * J.bpm;
     s_coff[0] = off;                                 // coefficient staging starts after the windows
-    s_coff[1] = off + s_njob[0] * kJpegCoefSlot;
-    s_coff[2] = s_coff[1] + s_njob[1] * kJpegCoefSlot;
   }
   __syncthreads();
   const int nj0 = s_njob[0], nj1 = s_njob[1], njob = nj0 + nj1 + s_njob[2];
-  const int16_t* coef = A.coef + J.blk_base * 64;
-  // stage the blocks: per component one contiguous run of block rows, 16-byte coalesced copies
-  for (int q = threadIdx.x; q < njob * 8; q += kPixThreads) {
-    const int jb = q >> 3, part = q & 7;
-    const int c = jb < nj0 ? 0 : (jb < nj0 + nj1 ? 1 : 2);
-    const int loc = jb - (c == 0 ? 0 : (c == 1 ? nj0 : nj0 + nj1));
-    const uint4* src = reinterpret_cast<const uint4*>(
-        coef + ((size_t)J.comp[c].blk_off + (size_t)s_brlo[c] * s_bw[c] + loc) * 64);
-    *reinterpret_cast<uint4*>(psm + s_coff[c] + loc * kJpegCoefSlot + part * 16) = ld_nc_v4(src + part);
+  const int bpm = J.bpm, mcus_x = J.mcus_x, mrlo = s_mrlo;
+  uint8_t* const slots = psm + s_coff[0];
+  // stage the MCU rows this row's IDCTs read (r, plus r-1 / r+1 when a component is
+  // vertically upsampled): contiguous in the MCU-ordered coefficient buffer
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(A.coef + (J.blk_base + (size_t)mrlo * mcus_x * bpm) * 64);
+    for (int q = threadIdx.x; q < s_nblk * 8; q += kPixThreads)
+      *reinterpret_cast<uint4*>(slots + (q >> 3) * kJpegCoefSlot + (q & 7) * 16) = ld_nc_v4(src + q);
   }
   __syncthreads();
+  // block (br, bx) of component c is block blk_off_c + (br % v) * h + bx % h of MCU (br / v, bx / h)
   for (int jb = threadIdx.x; jb < njob; jb += kPixThreads) {
     const int c = jb < nj0 ? 0 : (jb < nj0 + nj1 ? 1 : 2);
     const int loc = jb - (c == 0 ? 0 : (c == 1 ? nj0 : nj0 + nj1));
     const int bw = s_bw[c], q = loc / bw, bx = loc - q * bw, br = s_brlo[c] + q;
-    idct_block(reinterpret_cast<const int16_t*>(psm + s_coff[c] + loc * kJpegCoefSlot), A.quant[J.comp[c].q].q,
+    const int vs = s_vs[c], hs = s_hs[c];            // log2 of the sampling factors (0 or 1)
+    const int slot = (((br >> vs) - mrlo) * mcus_x + (bx >> hs)) * bpm + s_boff[c] + ((br & vs) << hs) + (bx & hs);
+    idct_block(reinterpret_cast<const int16_t*>(slots + slot * kJpegCoefSlot), A.quant[J.comp[c].q].q,
                psm + s_win[c] + (br * 8 - s_y0[c]) * s_pw[c] + bx * 8, s_pw[c]);
   }
   __syncthreads();
@@ -601,14 +650,19 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   if (A.count <= 0 || A.total_int == 0) return 0;
   jpeg_unstuff_kernel<<<A.count, 32 * kUnstuffWarps, 0, st>>>(A);
   const bool smem = A.n_huff <= kJpegSmemTables;
-  const int hsmem = (smem ? A.n_huff * (int)sizeof(JHuff::fast) : 0) + kMaxBpm * kHuffThreads * 8;
-  const unsigned hgrid = (A.total_int + kHuffThreads - 1) / kHuffThreads;
+  const int hsmem = smem ? A.n_huff * (int)sizeof(JHuff::fast) + (A.n_huff * (10 * 4 + 256) + 15) / 16 * 16 : 0;
+  // lanes pull intervals from a per-CTA queue: a few intervals per lane balance their
+  // unequal lengths once there are enough intervals to keep every SM busy
+  const uint32_t lanes = 148u * 4u * kHuffThreads;
+  const uint32_t per_lane = min(8u, max(1u, A.total_int / lanes));
+  const uint32_t chunk = per_lane * kHuffThreads;
+  const unsigned hgrid = (A.total_int + chunk - 1) / chunk;
   if (smem) {
     cudaFuncSetAttribute(jpeg_huffman_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
-    jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A);
+    jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
   } else {
     cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
-    jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A);
+    jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
   }
   if (A.pix_smem > 48 * 1024)
     cudaFuncSetAttribute(jpeg_pixels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.pix_smem);

@@ -38,13 +38,17 @@ constexpr int kJpegSmemTables = 8;        // J2 stages the pool in smem when it 
 constexpr int kJpegIntAlign = 16;         // restart intervals start 16-byte aligned in the J1 output
 constexpr int kJpegIntPad = 32;           // zero bytes (at least) J1 writes after every interval
 
-// Fast-table entry (u16) indexed by the next kJpegFastBits bits of the stream:
-//   bits 0..4 code length (0: longer than kJpegFastBits -> maxcode walk),
-//   5..9 extra bits (size), 10..13 zero run, bit 14 end of block (AC size 0, run < 15)
-constexpr uint32_t kFastEob = 1u << 14;
+// Fast-table entry (u32) indexed by the next kJpegFastBits bits of the stream:
+//   bit 31 valid (code <= kJpegFastBits bits; else the maxcode search),
+//   bit 30 full: code + extra bits fit, bits 0..15 hold the decoded value
+//          (EXTENDed coefficient, or the DC difference),
+//   bits 25..29 bits to consume (full: code + extra; else the code only),
+//   bits 21..24 zero run, bit 20 end of block (AC size 0, run < 15),
+//   bits 16..19 extra bits still to read (entries that are not full)
+constexpr uint32_t kFastValid = 1u << 31, kFastFull = 1u << 30, kFastEob = 1u << 20;
 
 struct JHuff {                            // one Huffman table, device form
-  uint16_t fast[1 << kJpegFastBits];
+  uint32_t fast[1 << kJpegFastBits];
   int32_t maxcode[18];                    // largest code of each length, -1 if none; [17] sentinel
   int32_t valoff[18];                     // vals index = code + valoff[len]
   uint8_t vals[256];
@@ -57,7 +61,7 @@ struct JComp {
   uint8_t h, v;                           // sampling factors (1 or 2; 1 for single-component files)
   uint16_t bw, bh;                        // coded blocks per row / column
   uint16_t dw, dh;                        // downsampled width / height (jdsample edge rule)
-  uint32_t blk_off;                       // first block, relative to the sample's block base
+  uint32_t blk_off;                       // offset of this component's first block inside an MCU
 };
 static_assert(sizeof(JComp) == 20, "JComp layout");
 
@@ -70,7 +74,8 @@ struct JpegDesc {                         // per sample, staged with the descrip
   uint32_t n_int;                         // restart intervals (0: not a JPEG sample)
   uint32_t int_base;                      // first interval in the batch interval table
   uint32_t n_blocks;
-  uint64_t blk_base;                      // first block in the batch coefficient buffer
+  uint64_t blk_base;                      // first block in the batch coefficient buffer (MCU order:
+                                          // block b of MCU m at blk_base + m * bpm + b)
   uint64_t bs_base;                       // first byte of the sample's unstuffed bitstream
   uint64_t sched;                         // MCU block b: comp bits 4b..4b+1, v bit 4b+2, h bit 4b+3
   JComp comp[3];
@@ -97,6 +102,7 @@ struct JpegArgs {
   const JHuff* huff;                      // table pools
   const JQuant* quant;
   int32_t n_huff;                         // pool entries in use
+  int32_t coef_zeroed;                    // coef holds zeros where J2 stores nothing
   struct SampleStatus* status;
   int32_t count;
   uint32_t total_int;
@@ -109,16 +115,17 @@ int launch_jpeg(const JpegArgs& A, void* stream);
 
 // J3 shared memory for one MCU row: per component a pixel window (its own
 // rows plus one block row above and below when it is vertically upsampled)
-// and the staged coefficient blocks of those block rows (144-byte slots).
+// and the staged coefficient blocks of the MCU rows those come from
+// (144-byte slots; reused as the RGB staging of the row).
 constexpr int kJpegCoefSlot = 144;
 BBX_HD inline int jpeg_window_rows(int v, int vmax) { return 8 * v + (vmax / v == 2 ? 16 : 0); }
 BBX_HD inline int jpeg_pix_smem(const JpegDesc& J) {
-  int win = 0, slots = 0;
+  int win = 0, ext = 0;
   for (int c = 0; c < J.ncomp; ++c) {
-    const int rows = jpeg_window_rows(J.comp[c].v, J.vmax);
-    win += rows * J.comp[c].bw * 8;
-    slots += (rows / 8) * J.comp[c].bw * kJpegCoefSlot;
+    win += jpeg_window_rows(J.comp[c].v, J.vmax) * J.comp[c].bw * 8;
+    ext |= J.vmax / J.comp[c].v == 2 ? 1 : 0;
   }
+  const int slots = (1 + 2 * ext) * J.mcus_x * J.bpm * kJpegCoefSlot;   // staged MCU rows
   const int rgb = J.mcus_x * 8 * J.hmax * 8 * J.vmax * 3;   // RGB staging of one MCU row (reuses the slots)
   return win + (slots > rgb ? slots : rgb);
 }

@@ -131,9 +131,18 @@ bool jpeg_build_huff(const JpegHeader::Huff& t, bool is_ac, JHuff* o) {
       const int sym = t.vals[k];
       const int size = is_ac ? (sym & 15) : sym, run = is_ac ? (sym >> 4) : 0;
       const int sh = F - l;
-      const uint16_t e = (uint16_t)((uint32_t)l | (uint32_t)size << 5 | (uint32_t)run << 10 |
-                                    ((is_ac && size == 0 && run != 15) ? kFastEob : 0u));   // EOB / ZRL: jdhuff.c
-      for (int f = 0; f < (1 << sh); ++f) o->fast[(code << sh) | f] = e;
+      const bool eob = is_ac && size == 0 && run != 15;           // EOB / ZRL: jdhuff.c rule
+      for (int f = 0; f < (1 << sh); ++f) {
+        uint32_t e = kFastValid | (uint32_t)run << 21 | (eob ? kFastEob : 0u);
+        if (l + size <= F) {                                        // value fits: decode it here
+          const int bits = size ? (f >> (sh - size)) & ((1 << size) - 1) : 0;
+          const int v = size ? (bits < (1 << (size - 1)) ? bits - (1 << size) + 1 : bits) : 0;
+          e |= kFastFull | (uint32_t)(l + size) << 25 | (uint32_t)(uint16_t)(int16_t)v;
+        } else {
+          e |= (uint32_t)l << 25 | (uint32_t)size << 16;
+        }
+        o->fast[(code << sh) | f] = e;
+      }
     }
     if (code >= (1 << l)) return false;   // over-subscribed or an all-ones code (jdhuff.c rule)
     code <<= 1;
