@@ -132,6 +132,7 @@ struct Plan {
   int64_t jpeg_int_cap = 0;      // per sample: restart intervals (<= MCUs)
   int16_t* d_coef = nullptr;     // JPEG scratch shared by the slots (one compute stream orders them)
   uint8_t* d_bits = nullptr;     // unstuffed restart-interval bitstreams
+  uint8_t* d_planes = nullptr;   // IDCT output: component planes
   int64_t jpeg_bits_cap = 0;     // per sample
   uint32_t* d_istart = nullptr;
   uint32_t* d_iend = nullptr;
@@ -169,8 +170,7 @@ struct Slot {
   std::vector<char> plan_has_jpeg;
   std::vector<uint32_t> jpeg_total_int;
   std::vector<uint64_t> jpeg_total_blk;
-  std::vector<int32_t> jpeg_max_rows;
-  std::vector<int32_t> jpeg_pix_smem;
+  std::vector<int32_t> jpeg_max_quads;
 };
 
 // Device pools of the Huffman / quant tables the JPEG samples reference,
@@ -723,6 +723,7 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
     o.dh = (uint16_t)(((int64_t)H.height * c.v + vmax - 1) / vmax);
     o.blk_off = (uint32_t)mcu_off;
     mcu_off += H.ncomp == 1 ? 1 : c.h * c.v;
+    J->plane_blk[i] = blocks;
     blocks += (uint32_t)o.bw * o.bh;
   }
   const uint32_t total = (uint32_t)mx * my;
@@ -750,7 +751,10 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
   return true;
 }
 
-static size_t jpeg_block_bytes(int B) { return (size_t)B * sizeof(JpegDesc) + (size_t)(B + 1) * 4; }
+// staged per JPEG plan: JpegDesc[B] | u32 interval prefix[B+1] | u64 block prefix[B+1]
+static size_t jpeg_iprefix_off(int B) { return (size_t)B * sizeof(JpegDesc); }
+static size_t jpeg_bprefix_off(int B) { return (jpeg_iprefix_off(B) + (size_t)(B + 1) * 4 + 7) / 8 * 8; }
+static size_t jpeg_block_bytes(int B) { return jpeg_bprefix_off(B) + (size_t)(B + 1) * 8; }
 
 
 
@@ -815,6 +819,7 @@ static int finalize(bbx_loader* L) {
     const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
     CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
     CK(cudaMalloc(&pl.d_bits, (size_t)L->batch * pl.jpeg_bits_cap + 256));
+    CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
     CK(cudaMalloc(&pl.d_istart, ints * 4 + 64));
     CK(cudaMalloc(&pl.d_iend, ints * 4 + 64));
   }
@@ -865,8 +870,7 @@ static int process_slot(bbx_loader* L, int s) {
   S.plan_has_jpeg.assign(L->plans.size(), 0);
   S.jpeg_total_int.assign(L->plans.size(), 0);
   S.jpeg_total_blk.assign(L->plans.size(), 0);
-  S.jpeg_max_rows.assign(L->plans.size(), 0);
-  S.jpeg_pix_smem.assign(L->plans.size(), 0);
+  S.jpeg_max_quads.assign(L->plans.size(), 0);
   uint8_t* H = S.h_stage;
   std::memcpy(H + L->idx_off, S.idx.data(), (size_t)count * 8);
   for (int64_t pos = 0; pos < count; ++pos) {
@@ -962,27 +966,27 @@ static int process_slot(bbx_loader* L, int s) {
     const Plan& pl = L->plans[p];
     uint8_t* jb = H + L->jpeg_off[p];
     JpegDesc* jds = reinterpret_cast<JpegDesc*>(jb);
-    uint32_t* ipre = reinterpret_cast<uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
+    uint32_t* ipre = reinterpret_cast<uint32_t*>(jb + jpeg_iprefix_off(L->batch));
+    uint64_t* bpre = reinterpret_cast<uint64_t*>(jb + jpeg_bprefix_off(L->batch));
     const uint8_t* dblk = H + L->desc_off[p];
     uint32_t ti = 0;
     uint64_t tb = 0, bs = 0;
-    int32_t mr = 0, ps = 0;
+    int32_t mq = 0;
     for (int pos = 0; pos < count; ++pos) {
       JpegDesc& J = jds[pos];
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
       if (d->skip) J.n_int = 0;
       if (J.n_int == 0) J.n_blocks = 0;
       J.int_base = ti; J.blk_base = tb; J.bs_base = bs;
-      ipre[pos] = ti;
+      ipre[pos] = ti; bpre[pos] = tb;
       ti += J.n_int; tb += J.n_blocks;
       if (J.n_int) {
         bs += (uint64_t)pl.jpeg_bits_cap;
-        mr = std::max(mr, (int32_t)J.mcus_y);
-        ps = std::max(ps, jpeg_pix_smem(J));
+        mq = std::max(mq, (int32_t)d->h);
       }
     }
-    ipre[count] = ti;
-    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_rows[p] = mr; S.jpeg_pix_smem[p] = ps;
+    ipre[count] = ti; bpre[count] = tb;
+    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_quads[p] = mq;
     if (ti == 0) S.plan_has_jpeg[p] = 0;
   }
   {   // new JPEG tables: append-only upload ahead of this slot's H2D (same copy stream)
@@ -1091,17 +1095,17 @@ static int process_slot(bbx_loader* L, int s) {
       const uint8_t* jb = S.d_stage + L->jpeg_off[p];
       J.desc = A.desc; J.desc_stride = pl.dev.desc_stride; J.payload = A.payload;
       J.jd = reinterpret_cast<const JpegDesc*>(jb);
-      J.int_prefix = reinterpret_cast<const uint32_t*>(jb + (size_t)L->batch * sizeof(JpegDesc));
-      J.istart = pl.d_istart; J.iend = pl.d_iend; J.bits = pl.d_bits; J.coef = pl.d_coef;
+      J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
+      J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
+      J.istart = pl.d_istart; J.iend = pl.d_iend; J.bits = pl.d_bits; J.coef = pl.d_coef; J.planes = pl.d_planes;
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
       J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
       J.coef_zeroed = 1;
-      J.total_int = S.jpeg_total_int[p]; J.max_mcu_rows = S.jpeg_max_rows[p]; J.pix_smem = S.jpeg_pix_smem[p];
-      if (J.pix_smem > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "jpeg: image rows too wide for the device decoder");
+      J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
       // J2 stores only nonzero coefficients
       CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
       if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      launches += 3; any_jpeg = true;
+      launches += 4; any_jpeg = true;
     }
     int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, L->comp_st) : launch_image(pl.dev, A, L->comp_st);
     if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
@@ -1172,23 +1176,24 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
   if (!ok) return fail(err.code, "%s", err.msg.c_str());
   J.int_base = 0; J.blk_base = 0; J.bs_base = 0;
-  const int pix = jpeg_pix_smem(J);
-  if (pix > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "jpeg: image rows too wide for the device decoder");
-  // device image: [desc 64][jd][prefix][payload (+16 pad)] then tables, intervals, bits, coef, status
-  const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_pay = o_ip + 16;
+  // device image: [desc 64][jd][prefixes][payload (+16 pad)] then tables, intervals, bits, coef, planes, status
+  const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_bp = o_ip + 16, o_pay = o_bp + 16;
   const size_t o_hf = (o_pay + len + 16 + 255) / 256 * 256;
   const size_t o_q = o_hf + sizeof(JHuff) * L.jt.n_huff;
   const size_t o_is = (o_q + sizeof(JQuant) * L.jt.n_quant + 255) / 256 * 256;
   const size_t o_ie = o_is + 4 * (size_t)J.n_int + 16;
   const size_t o_bs = (o_ie + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
   const size_t o_cf = (o_bs + (size_t)pl.jpeg_bits_cap + 255) / 256 * 256;
-  const size_t o_st = (o_cf + 128 * (size_t)J.n_blocks + 255) / 256 * 256;
+  const size_t o_pl = (o_cf + 128 * (size_t)J.n_blocks + 255) / 256 * 256;
+  const size_t o_st = (o_pl + 64 * (size_t)J.n_blocks + 255) / 256 * 256;
   const size_t total = o_st + sizeof(SampleStatus);
   std::vector<uint8_t> img(o_is, 0);
   std::memcpy(img.data(), desc, 64);
   std::memcpy(img.data() + o_jd, &J, sizeof J);
   const uint32_t ip[2] = {0, J.n_int};
+  const uint64_t bp[2] = {0, J.n_blocks};
   std::memcpy(img.data() + o_ip, ip, sizeof ip);
+  std::memcpy(img.data() + o_bp, bp, sizeof bp);
   std::memcpy(img.data() + o_pay, pay, (size_t)len);
   std::memcpy(img.data() + o_hf, hh.data(), sizeof(JHuff) * L.jt.n_huff);
   std::memcpy(img.data() + o_q, hq.data(), sizeof(JQuant) * L.jt.n_quant);
@@ -1201,14 +1206,15 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   A.desc = dev; A.desc_stride = 64; A.payload = dev + o_pay;
   A.jd = reinterpret_cast<const JpegDesc*>(dev + o_jd);
   A.int_prefix = reinterpret_cast<const uint32_t*>(dev + o_ip);
+  A.blk_prefix = reinterpret_cast<const uint64_t*>(dev + o_bp);
   A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
-  A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf);
+  A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
   A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
   A.n_huff = L.jt.n_huff;
   A.coef_zeroed = 1;
   A.status = reinterpret_cast<SampleStatus*>(dev + o_st);
-  A.count = 1; A.total_int = J.n_int; A.max_mcu_rows = J.mcus_y; A.pix_smem = pix;
+  A.count = 1; A.total_int = J.n_int; A.total_blocks = J.n_blocks; A.max_quads = h;
   int rc = e == cudaSuccess ? launch_jpeg(A, nullptr) : 1;
   SampleStatus st{};
   if (e == cudaSuccess) e = cudaMemcpy(&st, dev + o_st, sizeof st, cudaMemcpyDeviceToHost);
@@ -1521,6 +1527,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     for (auto* p : pl.d_tables) if (p) cudaFree(p);
     if (pl.d_coef) cudaFree(pl.d_coef);
     if (pl.d_bits) cudaFree(pl.d_bits);
+    if (pl.d_planes) cudaFree(pl.d_planes);
     if (pl.d_istart) cudaFree(pl.d_istart);
     if (pl.d_iend) cudaFree(pl.d_iend);
   }

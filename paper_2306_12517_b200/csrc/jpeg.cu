@@ -451,7 +451,7 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
   int w[64];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const uint4 cv = src[r], qv = __ldg(q4 + r);
+    const uint4 cv = ld_nc_v4(src + r), qv = __ldg(q4 + r);
     const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -488,13 +488,38 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
   }
 }
 
-struct Win {                       // one component's shared-memory window for an MCU row
+// J3: thread per block, blocks taken in the coefficient buffer's MCU order.
+constexpr int kIdctThreads = 128;
+
+__global__ void __launch_bounds__(kIdctThreads) jpeg_idct_kernel(const JpegArgs A) {
+  const uint64_t g = (uint64_t)blockIdx.x * kIdctThreads + threadIdx.x;
+  if (g >= A.total_blocks) return;
+  const int s = find_sample(A.blk_prefix, A.count, g);
+  const JpegDesc& J = A.jd[s];
+  if (A.status[s].kind != 0) return;
+  const uint32_t rel = (uint32_t)(g - J.blk_base), bpm = J.bpm;
+  const uint32_t m = rel / bpm, b = rel - m * bpm;
+  const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
+  const JComp& C = J.comp[c];
+  const uint32_t my = m / J.mcus_x, mx = m - my * J.mcus_x;
+  const uint32_t V = J.ncomp == 1 ? 1 : C.v, H = J.ncomp == 1 ? 1 : C.h;
+  const uint32_t by = my * V + ((e >> 2) & 1), bx = mx * H + (e >> 3), pw = (uint32_t)C.bw * 8;
+  uint8_t* plane = A.planes + (J.blk_base + J.plane_blk[c]) * 64;
+  idct_block(A.coef + g * 64, A.quant[C.q].q, plane + (size_t)by * 8 * pw + bx * 8, (int)pw);
+}
+
+// J4: thread per 4 output pixels of one row.  libjpeg's fancy upsampling
+// (h2v1 / h1v2 / h2v2 triangle filters with edge replication; box when the
+// downsampled width is <= 2) and JFIF YCbCr -> RGB in 16-bit fixed point.
+constexpr int kColorThreads = 256;
+
+struct Plane {
   const uint8_t* p;
-  int y0, pw, dw, dh, rh, rv;      // plane row of window row 0, row pitch, downsampled dims, up ratios
+  int pw, dw, dh, rh, rv;          // row pitch, downsampled dims, upsampling ratios
 };
 
-__device__ __forceinline__ int win_sample(const Win& c, int y, int x) {
-  auto at = [&](int yy, int xx) { return (int)c.p[(yy - c.y0) * c.pw + xx]; };
+__device__ __forceinline__ int plane_sample(const Plane& c, int y, int x) {
+  auto at = [&](int yy, int xx) { return (int)__ldg(c.p + (size_t)yy * c.pw + xx); };
   if (c.rh == 1 && c.rv == 1) return at(y, x);
   const bool fancy_w = c.dw > 2;
   if (c.rv == 1) {                                  // h2v1
@@ -513,135 +538,129 @@ __device__ __forceinline__ int win_sample(const Win& c, int y, int x) {
   return (3 * cs + ns + ((x & 1) ? 7 : 8)) >> 4;
 }
 
-__global__ void __launch_bounds__(kPixThreads, 3) jpeg_pixels_kernel(const JpegArgs A) {
-  extern __shared__ __align__(16) uint8_t psm[];
-  __shared__ int s_coff[3], s_brlo[3], s_njob[3], s_bw[3], s_pw[3], s_y0[3], s_win[3], s_vs[3], s_hs[3], s_boff[3];
-  const int s = blockIdx.y, r = blockIdx.x;
+__device__ __forceinline__ uint32_t ycc_r(int Y, int cr) { return (uint32_t)min(max(Y + ((91881 * cr + 32768) >> 16), 0), 255); }
+__device__ __forceinline__ uint32_t ycc_g(int Y, int cb, int cr) {
+  return (uint32_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
+}
+__device__ __forceinline__ uint32_t ycc_b(int Y, int cb) { return (uint32_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255); }
+
+template <int N>
+__device__ __forceinline__ void store_px(uint8_t* o, const uint32_t (&px)[N], int n) {   // first n bytes, packed
+  const uintptr_t a = reinterpret_cast<uintptr_t>(o);
+  if (n == N && (a & 7) == 0 && (N & 7) == 0) {
+#pragma unroll
+    for (int k = 0; k < N; k += 8)
+      *reinterpret_cast<uint2*>(o + k) =
+          make_uint2(px[k] | px[k + 1] << 8 | px[k + 2] << 16 | px[k + 3] << 24,
+                     px[k + 4] | px[k + 5] << 8 | px[k + 6] << 16 | px[k + 7] << 24);
+  } else if (n == N && (a & 3) == 0 && (N & 3) == 0) {
+#pragma unroll
+    for (int k = 0; k < N; k += 4)
+      *reinterpret_cast<uint32_t*>(o + k) = px[k] | px[k + 1] << 8 | px[k + 2] << 16 | px[k + 3] << 24;
+  } else {
+#pragma unroll
+    for (int k = 0; k < N; ++k) if (k < n) o[k] = (uint8_t)px[k];
+  }
+}
+
+// J4: CTA per (sample, band of kColorRows rows); a thread produces 8 output
+// pixels of one row per step (4:2:0 fast path: one 8-byte luma load and, per
+// chroma plane and row, one 4-byte load plus the two edge-clamped
+// neighbours); any other layout goes per pixel through plane_sample.
+constexpr int kColorRows = 16;
+
+__global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArgs A) {
+  const int s = blockIdx.y;
+  __shared__ Plane sP[3];
+  __shared__ int s_ok, s_fast;
   const JpegDesc& J = A.jd[s];
-  if (J.n_int == 0 || r >= J.mcus_y || A.status[s].kind != 0) return;
   const SampleDesc* d = sdesc(A, s);
-  const int w = d->w, h = d->h, nc = J.ncomp, hmax = J.hmax, vmax = J.vmax;
-  __shared__ int s_mrlo, s_nblk;
+  const int w = d->w, h = d->h, nc = J.ncomp;
+  const int y_lo = blockIdx.x * kColorRows, y_hi = min(y_lo + kColorRows, h);
   if (threadIdx.x == 0) {
-    int off = 0, ext_any = 0;
-    for (int c = 0; c < 3; ++c) {
-      if (c >= nc) { s_njob[c] = 0; continue; }
+    s_ok = J.n_int != 0 && A.status[s].kind == 0 && y_lo < h;
+    const uint8_t* planes = A.planes + J.blk_base * 64;
+    for (int c = 0; c < nc; ++c) {
       const JComp& C = J.comp[c];
-      const int ext = vmax / C.v == 2 ? 1 : 0;
-      ext_any |= ext;
-      const int lo = max(r * C.v - ext, 0), hi = min(r * C.v + C.v - 1 + ext, (int)C.bh - 1);
-      s_brlo[c] = lo; s_njob[c] = (hi - lo + 1) * C.bw; s_bw[c] = C.bw; s_pw[c] = C.bw * 8;
-      s_y0[c] = (r * C.v - ext) * 8; s_win[c] = off;
-      s_vs[c] = nc == 1 ? 0 : C.v - 1; s_hs[c] = nc == 1 ? 0 : C.h - 1; s_boff[c] = (int)C.blk_off;
-      off += jpeg_window_rows(C.v, vmax) * C.bw * 8;
+      sP[c].p = planes + (size_t)J.plane_blk[c] * 64;
+      sP[c].pw = C.bw * 8; sP[c].dw = C.dw; sP[c].dh = C.dh; sP[c].rh = J.hmax / C.h; sP[c].rv = J.vmax / C.v;
     }
-    const int lo = max(r - ext_any, 0), hi = min(r + ext_any, (int)J.mcus_y - 1);
-    s_mrlo = lo;
-    s_nblk = (hi - lo + 1) * J.mcus_x * J.bpm;
-    s_coff[0] = off;                                 // coefficient staging starts after the windows
+    s_fast = nc == 3 && sP[0].rh == 1 && sP[0].rv == 1 && sP[1].rh == 2 && sP[1].rv == 2 && sP[2].rh == 2 &&
+             sP[2].rv == 2 && sP[1].dw > 2 && sP[2].dw > 2 && sP[1].dw == sP[2].dw && sP[1].dh == sP[2].dh &&
+             sP[1].pw == sP[2].pw;
   }
   __syncthreads();
-  const int nj0 = s_njob[0], nj1 = s_njob[1], njob = nj0 + nj1 + s_njob[2];
-  const int bpm = J.bpm, mcus_x = J.mcus_x, mrlo = s_mrlo;
-  uint8_t* const slots = psm + s_coff[0];
-  // stage the MCU rows this row's IDCTs read (r, plus r-1 / r+1 when a component is
-  // vertically upsampled): contiguous in the MCU-ordered coefficient buffer
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(A.coef + (J.blk_base + (size_t)mrlo * mcus_x * bpm) * 64);
-    for (int q = threadIdx.x; q < s_nblk * 8; q += kPixThreads)
-      *reinterpret_cast<uint4*>(slots + (q >> 3) * kJpegCoefSlot + (q & 7) * 16) = ld_nc_v4(src + q);
-  }
-  __syncthreads();
-  // block (br, bx) of component c is block blk_off_c + (br % v) * h + bx % h of MCU (br / v, bx / h)
-  for (int jb = threadIdx.x; jb < njob; jb += kPixThreads) {
-    const int c = jb < nj0 ? 0 : (jb < nj0 + nj1 ? 1 : 2);
-    const int loc = jb - (c == 0 ? 0 : (c == 1 ? nj0 : nj0 + nj1));
-    const int bw = s_bw[c], q = loc / bw, bx = loc - q * bw, br = s_brlo[c] + q;
-    const int vs = s_vs[c], hs = s_hs[c];            // log2 of the sampling factors (0 or 1)
-    const int slot = (((br >> vs) - mrlo) * mcus_x + (bx >> hs)) * bpm + s_boff[c] + ((br & vs) << hs) + (bx & hs);
-    idct_block(reinterpret_cast<const int16_t*>(slots + slot * kJpegCoefSlot), A.quant[J.comp[c].q].q,
-               psm + s_win[c] + (br * 8 - s_y0[c]) * s_pw[c] + bx * 8, s_pw[c]);
-  }
-  __syncthreads();
-  Win win[3];
+  if (!s_ok) return;
+  const int no = (w + 7) >> 3, n = (y_hi - y_lo) * no;
+  uint8_t* const out = A.scratch + (size_t)s * A.scratch_bytes;
+  if (nc == 1) {
+    const Plane P0 = sP[0];
+    for (int t = threadIdx.x; t < n; t += kColorThreads) {
+      const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+      uint32_t px[8];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    if (c >= nc) break;
-    const JComp& C = J.comp[c];
-    win[c].p = psm + s_win[c]; win[c].y0 = s_y0[c]; win[c].pw = s_pw[c];
-    win[c].dw = C.dw; win[c].dh = C.dh; win[c].rh = hmax / C.h; win[c].rv = vmax / C.v;
-  }
-  const int y_first = r * vmax * 8, rows = min(vmax * 8, h - y_first);
-  uint8_t* outp = A.scratch + (size_t)s * A.scratch_bytes;
-  if (nc == 3 && hmax == 2 && vmax == 2 && win[0].rh == 1 && win[0].rv == 1 && win[1].rh == 2 &&
-      win[1].rv == 2 && win[2].rh == 2 && win[2].rv == 2 && win[1].dw > 2 && win[2].dw > 2 &&
-      win[1].dw == win[2].dw && win[1].dh == win[2].dh && win[1].pw == win[2].pw && win[1].y0 == win[2].y0) {
-    // 4:2:0 (h2v2 fancy): a thread makes 4 output pixels (2 chroma columns) of a row into an
-    // RGB staging area laid out like the output (it reuses the coefficient slots), which the
-    // CTA then copies out with 16-byte stores
-    uint8_t* stg = psm + s_coff[0];
-    const int nq = (w + 3) >> 2, dw = win[1].dw, dh = win[1].dh, cpw = win[1].pw;
-    const uint8_t* cbp = win[1].p;
-    const uint8_t* crp = win[2].p;
-    for (int idx = threadIdx.x; idx < rows * nq; idx += kPixThreads) {
-      const int yy = idx / nq, q = idx - yy * nq, y = y_first + yy;
-      const int i = y >> 1, i1 = (y & 1) ? min(i + 1, dh - 1) : max(i - 1, 0);
-      const int j0 = 2 * q;
-      const int ja = max(j0 - 1, 0), jc = min(j0 + 1, dw - 1), jd = min(j0 + 2, dw - 1);
-      const int ra = (i - win[1].y0) * cpw, rb = (i1 - win[1].y0) * cpw;
-      int u[2][4];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const uint8_t* P = c ? crp : cbp;
-        const int c0 = 3 * P[ra + ja] + P[rb + ja], c1 = 3 * P[ra + j0] + P[rb + j0];
-        const int c2 = 3 * P[ra + jc] + P[rb + jc], c3 = 3 * P[ra + jd] + P[rb + jd];
-        u[c][0] = ((3 * c1 + c0 + 8) >> 4) - 128;
-        u[c][1] = ((3 * c1 + c2 + 7) >> 4) - 128;
-        u[c][2] = ((3 * c2 + c1 + 8) >> 4) - 128;
-        u[c][3] = ((3 * c2 + c3 + 7) >> 4) - 128;
-      }
-      const uint32_t y4 = *reinterpret_cast<const uint32_t*>(win[0].p + (y - win[0].y0) * win[0].pw + 4 * q);
-      uint32_t px[12];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int Y = (int)((y4 >> (8 * k)) & 0xFF), cb = u[0][k], cr = u[1][k];
-        px[3 * k] = (uint32_t)min(max(Y + ((91881 * cr + 32768) >> 16), 0), 255);
-        px[3 * k + 1] = (uint32_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
-        px[3 * k + 2] = (uint32_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255);
-      }
-      const int o = (yy * w + 4 * q) * 3;
-      if (4 * q + 4 <= w && (o & 3) == 0) {
-        uint32_t* o32 = reinterpret_cast<uint32_t*>(stg + o);
-        o32[0] = px[0] | px[1] << 8 | px[2] << 16 | px[3] << 24;
-        o32[1] = px[4] | px[5] << 8 | px[6] << 16 | px[7] << 24;
-        o32[2] = px[8] | px[9] << 8 | px[10] << 16 | px[11] << 24;
-      } else {
-        const int nv = min(4, w - 4 * q) * 3;
-#pragma unroll
-        for (int k = 0; k < 12; ++k) if (k < nv) stg[o + k] = (uint8_t)px[k];
-      }
+      for (int k = 0; k < 8; ++k) px[k] = (uint32_t)plane_sample(P0, y, min(x0 + k, w - 1));
+      store_px(out + (size_t)y * w + x0, px, min(8, w - x0));
     }
-    __syncthreads();
-    const int nbytes = rows * w * 3;
-    uint8_t* g = outp + (size_t)y_first * w * 3;
-    int done = 0;
-    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
-      done = nbytes & ~15;
-      for (int k = threadIdx.x * 16; k < done; k += kPixThreads * 16)
-        *reinterpret_cast<uint4*>(g + k) = *reinterpret_cast<const uint4*>(stg + k);
-    }
-    for (int k = done + threadIdx.x; k < nbytes; k += kPixThreads) g[k] = stg[k];
     return;
   }
-  for (int idx = threadIdx.x; idx < rows * w; idx += kPixThreads) {
-    const int yy = idx / w, x = idx - yy * w, y = y_first + yy;
-    const int Y = win_sample(win[0], y, x);
-    if (nc == 1) { outp[(size_t)y * w + x] = (uint8_t)Y; continue; }
-    const int cb = win_sample(win[1], y, x) - 128, cr = win_sample(win[2], y, x) - 128;
-    uint8_t* o = outp + ((size_t)y * w + x) * 3;
-    o[0] = (uint8_t)min(max(Y + ((91881 * cr + 32768) >> 16), 0), 255);
-    o[1] = (uint8_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
-    o[2] = (uint8_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255);
+  if (s_fast) {                                      // 4:2:0 fancy (h2v2)
+    const uint8_t* yp = sP[0].p;
+    const uint8_t* cbp = sP[1].p;
+    const uint8_t* crp = sP[2].p;
+    const int ypw = sP[0].pw, cpw = sP[1].pw, dw = sP[1].dw, dh = sP[1].dh;
+    for (int t = threadIdx.x; t < n; t += kColorThreads) {
+      const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+      const uint2 y8 = __ldg(reinterpret_cast<const uint2*>(yp + (size_t)y * ypw + x0));
+      const int i = y >> 1, i1 = (y & 1) ? min(i + 1, dh - 1) : max(i - 1, 0), j0 = 4 * q;
+      const int ja = max(j0 - 1, 0), je = min(j0 + 4, dw - 1);
+      int u[2][8];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {                  // chroma columns j0-1 .. j0+4 (edge-clamped)
+        const uint8_t* ra = (c ? crp : cbp) + (size_t)i * cpw;
+        const uint8_t* rb = (c ? crp : cbp) + (size_t)i1 * cpw;
+        int cs[6];
+        cs[0] = 3 * __ldg(ra + ja) + __ldg(rb + ja);
+        cs[5] = 3 * __ldg(ra + je) + __ldg(rb + je);
+        if (j0 + 4 <= dw) {
+          const uint32_t a4 = __ldg(reinterpret_cast<const uint32_t*>(ra + j0));
+          const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(rb + j0));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cs[1 + k] = 3 * (int)((a4 >> (8 * k)) & 0xFF) + (int)((b4 >> (8 * k)) & 0xFF);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int jj = min(j0 + k, dw - 1);
+            cs[1 + k] = 3 * __ldg(ra + jj) + __ldg(rb + jj);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          u[c][2 * k] = ((3 * cs[1 + k] + cs[k] + 8) >> 4) - 128;
+          u[c][2 * k + 1] = ((3 * cs[1 + k] + cs[2 + k] + 7) >> 4) - 128;
+        }
+      }
+      uint32_t px[24];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int Y = (int)(((k < 4 ? y8.x : y8.y) >> (8 * (k & 3))) & 0xFF), cb = u[0][k], cr = u[1][k];
+        px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
+      }
+      store_px(out + ((size_t)y * w + x0) * 3, px, 3 * min(8, w - x0));
+    }
+    return;
+  }
+  const Plane P0 = sP[0], P1 = sP[1], P2 = sP[2];
+  for (int t = threadIdx.x; t < n; t += kColorThreads) {
+    const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+    uint32_t px[24];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int x = min(x0 + k, w - 1);
+      const int Y = plane_sample(P0, y, x), cb = plane_sample(P1, y, x) - 128, cr = plane_sample(P2, y, x) - 128;
+      px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
+    }
+    store_px(out + ((size_t)y * w + x0) * 3, px, 3 * min(8, w - x0));
   }
 }
 
@@ -664,9 +683,8 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
     cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
     jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
   }
-  if (A.pix_smem > 48 * 1024)
-    cudaFuncSetAttribute(jpeg_pixels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, A.pix_smem);
-  jpeg_pixels_kernel<<<dim3(A.max_mcu_rows, A.count), kPixThreads, A.pix_smem, st>>>(A);
+  jpeg_idct_kernel<<<(unsigned)((A.total_blocks + kIdctThreads - 1) / kIdctThreads), kIdctThreads, 0, st>>>(A);
+  jpeg_color_kernel<<<dim3((A.max_quads + kColorRows - 1) / kColorRows, A.count), kColorThreads, 0, st>>>(A);
   return cudaGetLastError() != cudaSuccess;
 }
 

@@ -14,12 +14,11 @@
 //                            tables that resolve code + extra bits in one
 //                            lookup; coefficient blocks built in shared memory,
 //                            stored as int16[64] natural order
-//   J3 jpeg_pixels_kernel    CTA per (sample, MCU row): islow IDCT of the
-//                            row's blocks (plus the chroma block rows above /
-//                            below that fancy upsampling reads) into shared
-//                            memory, then upsampling + YCbCr->RGB into the
-//                            sample's decode scratch, which K1 reads like an
-//                            RLE-expanded image
+//   J3 jpeg_idct_kernel      thread per 8x8 block: dequantize + islow IDCT in
+//                            registers -> u8 component planes
+//   J4 jpeg_color_kernel     thread per 8 output pixels: fancy chroma
+//                            upsampling + YCbCr->RGB into the sample's decode
+//                            scratch, which K1 reads like an RLE-expanded image
 #pragma once
 #include <cstdint>
 
@@ -79,7 +78,7 @@ struct JpegDesc {                         // per sample, staged with the descrip
   uint64_t bs_base;                       // first byte of the sample's unstuffed bitstream
   uint64_t sched;                         // MCU block b: comp bits 4b..4b+1, v bit 4b+2, h bit 4b+3
   JComp comp[3];
-  uint32_t pad1[3];
+  uint32_t plane_blk[3];                  // component c's pixel plane starts plane_blk[c] blocks into the sample's planes
 };
 static_assert(sizeof(JpegDesc) == 128, "JpegDesc layout");
 
@@ -93,6 +92,8 @@ struct JpegArgs {
   const uint8_t* payload;                 // payload base (staged region or resident heap)
   const JpegDesc* jd;                     // count entries
   const uint32_t* int_prefix;             // count + 1: exclusive prefix of n_int
+  const uint64_t* blk_prefix;             // count + 1: exclusive prefix of n_blocks
+  uint8_t* planes;                        // total blocks x 64: component planes (J3 -> J4)
   uint32_t* istart;                       // per interval: bitstream start / end (sample-relative)
   uint32_t* iend;
   uint8_t* bits;                          // unstuffed bitstreams
@@ -106,29 +107,12 @@ struct JpegArgs {
   struct SampleStatus* status;
   int32_t count;
   uint32_t total_int;
-  int32_t max_mcu_rows;                   // largest mcus_y in the batch
-  int32_t pix_smem;                       // J3 dynamic shared memory bytes
+  uint64_t total_blocks;
+  int32_t max_quads;                      // largest image height in the batch (J4 grid: bands of rows)
 };
 
 // jpeg.cu
 int launch_jpeg(const JpegArgs& A, void* stream);
-
-// J3 shared memory for one MCU row: per component a pixel window (its own
-// rows plus one block row above and below when it is vertically upsampled)
-// and the staged coefficient blocks of the MCU rows those come from
-// (144-byte slots; reused as the RGB staging of the row).
-constexpr int kJpegCoefSlot = 144;
-BBX_HD inline int jpeg_window_rows(int v, int vmax) { return 8 * v + (vmax / v == 2 ? 16 : 0); }
-BBX_HD inline int jpeg_pix_smem(const JpegDesc& J) {
-  int win = 0, ext = 0;
-  for (int c = 0; c < J.ncomp; ++c) {
-    win += jpeg_window_rows(J.comp[c].v, J.vmax) * J.comp[c].bw * 8;
-    ext |= J.vmax / J.comp[c].v == 2 ? 1 : 0;
-  }
-  const int slots = (1 + 2 * ext) * J.mcus_x * J.bpm * kJpegCoefSlot;   // staged MCU rows
-  const int rgb = J.mcus_x * 8 * J.hmax * 8 * J.vmax * 3;   // RGB staging of one MCU row (reuses the slots)
-  return win + (slots > rgb ? slots : rgb);
-}
 
 // jpeg_host.cpp
 struct JpegHeader {
