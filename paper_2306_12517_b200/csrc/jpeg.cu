@@ -61,7 +61,11 @@ __device__ __forceinline__ uint32_t apply(CursorFn f, uint32_t x) { return f.ali
 
 struct ChunkMasks { uint32_t w[4]; uint32_t nxt, keep, rst, term; };
 
-// Masks of the 16 bytes of chunk ch (absolute address c0 + 16 ch) of [a_lo, a_hi).
+// 4-bit mask of the bytes of w that __vcmpeq4 flagged (0xFF per equal byte).
+__device__ __forceinline__ uint32_t byte_bits(uint32_t eq) { return ((eq & 0x01010101u) * 0x10204080u) >> 28; }
+
+// Masks of the 16 bytes at `my` (16-byte aligned) restricted to [a_lo, a_hi),
+// byte-parallel (SWAR): data bytes to keep, RST markers, other markers.
 __device__ __forceinline__ ChunkMasks chunk_masks(uintptr_t my, uintptr_t a_lo, uintptr_t a_hi, int lane) {
   ChunkMasks M;
   uint4 v = make_uint4(0, 0, 0, 0);
@@ -72,23 +76,32 @@ __device__ __forceinline__ ChunkMasks chunk_masks(uintptr_t my, uintptr_t a_lo, 
   uint32_t nxt = __shfl_down_sync(0xffffffffu, v.x & 0xFF, 1);
   if (lane == 31) nxt = (my + 16 < a_hi) ? *reinterpret_cast<const uint8_t*>(my + 16) : 0u;
   M.nxt = nxt;
-  M.keep = M.rst = M.term = 0;
+  uint32_t ff = 0, z = 0, rs = 0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const uintptr_t pos = my + j;
-    const uint32_t b = (M.w[j >> 2] >> ((j & 3) * 8)) & 0xFF;
-    const uint32_t p = pos == a_lo ? 0u : (j ? (M.w[(j - 1) >> 2] >> (((j - 1) & 3) * 8)) & 0xFF : prev);
-    const uint32_t n = pos + 1 >= a_hi ? 0u : (j < 15 ? (M.w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) & 0xFF : nxt);
-    if (pos < a_lo || pos >= a_hi) continue;
-    const bool marker = b == 0xFF && n != 0x00;
-    if (p != 0xFF && !marker && !(b == 0xFF && pos + 1 >= a_hi)) M.keep |= 1u << j;
-    if (marker && (n & 0xF8) == 0xD0) M.rst |= 1u << j;
-    if (marker && n != 0xFF && (n & 0xF8) != 0xD0) M.term |= 1u << j;
+  for (int q = 0; q < 4; ++q) {
+    ff |= byte_bits(__vcmpeq4(M.w[q], 0xFFFFFFFFu)) << (4 * q);
+    z |= byte_bits(__vcmpeq4(M.w[q], 0u)) << (4 * q);
+    rs |= byte_bits(__vcmpeq4(M.w[q] & 0xF8F8F8F8u, 0xD0D0D0D0u)) << (4 * q);
   }
+  // bytes of this chunk inside [a_lo, a_hi); the first has no predecessor, the last no successor
+  const int lo = my >= a_lo ? 0 : (int)min((uintptr_t)16, a_lo - my);
+  const int hi = my >= a_hi ? 0 : (int)min((uintptr_t)16, a_hi - my);
+  const uint32_t inr = lo < hi ? ((0xFFFFu >> (16 - hi)) & (0xFFFFu << lo)) : 0u;
+  const uint32_t first = (my <= a_lo && a_lo < my + 16) ? 1u << (a_lo - my) : 0u;
+  const uint32_t last = (a_hi > my && a_hi <= my + 16) ? 1u << (a_hi - 1 - my) : 0u;
+  const uint32_t prev_ff = ((ff << 1) | (prev == 0xFF ? 1u : 0u)) & ~first;
+  const uint32_t next_z = (z >> 1) | (nxt == 0 ? 0x8000u : 0u) | last;
+  const uint32_t next_rs = ((rs >> 1) | ((nxt & 0xF8) == 0xD0 ? 0x8000u : 0u)) & ~last;
+  const uint32_t next_ff = ((ff >> 1) | (nxt == 0xFF ? 0x8000u : 0u)) & ~last;
+  const uint32_t marker = ff & ~next_z;
+  M.keep = inr & ~prev_ff & ~marker & ~(ff & last);   // a trailing 0xFF is a fill byte
+  M.rst = inr & marker & next_rs;
+  M.term = inr & marker & ~next_ff & ~next_rs;
   return M;
 }
 
 __device__ __forceinline__ CursorFn lane_fn(const ChunkMasks& M) {
+  if (M.rst == 0) return CursorFn{0u, (uint32_t)__popc(M.keep), 0u};
   CursorFn f{0u, 0u, 0u};
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -567,7 +580,7 @@ __device__ __forceinline__ void store_px(uint8_t* o, const uint32_t (&px)[N], in
 // pixels of one row per step (4:2:0 fast path: one 8-byte luma load and, per
 // chroma plane and row, one 4-byte load plus the two edge-clamped
 // neighbours); any other layout goes per pixel through plane_sample.
-constexpr int kColorRows = 16;
+constexpr int kColorRows = 64;
 
 __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArgs A) {
   const int s = blockIdx.y;
