@@ -442,8 +442,11 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     }
     // C <= 4: the whole value chain u8 -> output is a 256-entry table per
     // channel, built on the host with the reference's exact arithmetic.
+    // value chain on a u8 input: a 256-entry table per channel (one smem load per
+    // element), or arithmetic (BBX_VALUE_ALU=1: the divide-free form when proven exact)
+    const bool alu = std::getenv("BBX_VALUE_ALU") && std::atoi(std::getenv("BBX_VALUE_ALU")) != 0;
     P.value_mode = !has_values ? VAL_COPY
-                 : C <= 4 ? VAL_LUT
+                 : (C <= 4 && !alu) ? VAL_LUT
                  : verify_fma_normalize(P, C) ? VAL_FMA : VAL_DIRECT;
     if (P.value_mode == VAL_COPY && out_dt != BBX_U8) return fail(BBX_SPEC_MISMATCH, "unexpected output dtype");
     // tile height: 16 rows, shrunk until the smem layout allows 4 CTAs per SM
