@@ -74,6 +74,9 @@ struct PlanDev {
   // streaming K1: a CTA walks band_rows output rows in groups of grp_rows,
   // source rows pass through an ns-row cp.async ring and an nh-row H ring
   int32_t stream, band_rows, grp_rows, ns_ring, nh_ring, bands_per_sample;
+  // column-walker K1 (bilinear, 3 channels): a thread per output column walks the
+  // tile's rows; no horizontal-pass buffer, so tiles are taller and CTAs smaller
+  int32_t cw, cw_smem;
   StreamLayout sl;
   SmemLayout lay;
 };
@@ -126,5 +129,6 @@ int image_smem_bytes(const PlanDev& P);
 SmemLayout img_layout_host(const PlanDev& P);
 int image_tab_stride(const PlanDev& P);
 StreamLayout stream_layout_host(const PlanDev& P);
+int cw_smem_host(const PlanDev& P);
 
 }  // namespace bbx

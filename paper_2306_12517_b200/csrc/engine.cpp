@@ -482,6 +482,19 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     P.h_tpc = std::max(1, kThreads / W);
     P.tab_stride = image_tab_stride(P);
     plan_stream(P, f);
+    // column-walker K1 for 3-channel bilinear decoders (BBX_CW=0 keeps the tile kernel)
+    P.cw = 0;
+    const char* cwe = std::getenv("BBX_CW");
+    if (P.src_kind == SRC_RESAMPLE && C == 3 && !P.stream && !(cwe && std::atoi(cwe) == 0)) {
+      PlanDev Q = P;
+      Q.rows_per_tile = std::min(16, H);
+      if (const char* e = std::getenv("BBX_CW_ROWS")) Q.rows_per_tile = std::max(1, std::min(std::atoi(e), H));
+      Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
+      Q.lay = img_layout_host(Q);
+      Q.tab_stride = image_tab_stride(Q);
+      Q.cw_smem = cw_smem_host(Q);
+      if (Q.cw_smem <= 100 * 1024) { P = Q; P.cw = 1; }
+    }
     if ((W + 3 * H) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "output too large for the device plan");
   }
   if (P.value_mode == VAL_LUT) {   // exact u8 -> output table (pipeline.py:158-160 arithmetic)

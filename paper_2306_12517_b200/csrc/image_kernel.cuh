@@ -733,9 +733,138 @@ __global__ void __launch_bounds__(kThreads, 4) image_stream_kernel(const PlanDev
   cp_async_wait<0>();
 }
 
+// ------------------------------------------------------- K1 (column walker)
+// Bilinear decoders, 3 channels.  grid = (tiles_per_sample, count); a tile is
+// rows_per_tile output rows.  After the tile's source rows are staged (as K1),
+// thread x owns output column x and walks the rows: the 2-tap horizontal sums
+// of a source row are computed in registers when a row first appears (and kept
+// for the next output row that reuses it), then the vertical blend, the value
+// table and the store.  Same integer arithmetic as image_kernel (bit-identical).
+__host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }
+__host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
+__host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
+  return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
+}
+__host__ __device__ inline int cw_meta_off(const PlanDev& P) { return cw_lut_bytes(P); }
+__host__ __device__ inline int cw_src_off(const PlanDev& P) {
+  return cw_meta_off(P) + align_up((2 * cw_nslot(P) + 3 * P.rows_per_tile) * 4, 16);
+}
+__host__ __device__ inline int cw_smem_bytes(const PlanDev& P) { return cw_src_off(P) + cw_nslot(P) * cw_span_pad(P); }
+
+template <typename OutT, int kVal>
+__global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
+  constexpr int C = 3;
+  const int s = blockIdx.y;
+  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+  if (d->skip) return;
+  const int tile = blockIdx.x, r0 = tile * P.rows_per_tile;
+  const int R = min(P.rows_per_tile, P.out_h - r0);
+  if (R <= 0) return;
+  const int OW = P.out_w, tid = threadIdx.x, nslot = cw_nslot(P), span_pad = cw_span_pad(P);
+  const SrcRows S = src_rows_of(P, A, d, s);
+  extern __shared__ __align__(16) uint8_t smem[];
+  OutT* lut = reinterpret_cast<OutT*>(smem);
+  int* slot_row = reinterpret_cast<int*>(smem + cw_meta_off(P));
+  int* s_shift = slot_row + nslot;
+  int* row_a = s_shift + nslot;                   // row_a[R], row_b[R], row_wy[R]
+  int* row_b = row_a + P.rows_per_tile;
+  int* row_wy = row_b + P.rows_per_tile;
+  uint8_t* srcbuf = smem + cw_src_off(P);
+
+  const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
+  const int col_lo = (int)T[0], col_hi = (int)T[1];
+  const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+  const uint32_t* M = T + 4 + tab_owp(P) + (size_t)tile * tab_tm(P);
+  const int nvalid = (int)M[0];
+  if (tid < nslot) { slot_row[tid] = (int)M[1 + tid]; s_shift[tid] = 0; }
+  if (tid < 3 * P.rows_per_tile) row_a[tid] = (int)M[1 + nslot + tid];
+  if constexpr (kVal == VAL_LUT) {
+    const uint4* g = reinterpret_cast<const uint4*>(A.lut);
+    uint4* l4 = reinterpret_cast<uint4*>(lut);
+    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += kThreads) l4[i] = g[i];
+  }
+  __syncthreads();
+  {   // stage source row segments (warp per slot, 16-byte vectors)
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int j = warp; j < nvalid; j += kThreads / 32) {
+      const int srow = slot_row[j];
+      if (srow < 0 || span_bytes == 0) continue;
+      const uint8_t* src = S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C;
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
+      const int shift = (int)(a - a0), n16 = (shift + span_bytes + 15) >> 4;
+      uint8_t* dst = srcbuf + (size_t)j * span_pad;
+      const uint8_t* s0 = reinterpret_cast<const uint8_t*>(a0);
+      for (int c = lane; c < n16; c += 32) *reinterpret_cast<uint4*>(dst + 16 * c) = ld_nc_v4(s0 + 16 * c);
+      if (lane == 0) s_shift[j] = shift;
+    }
+  }
+  __syncthreads();
+  OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * OW * C;
+  for (int ox = tid; ox < OW; ox += kThreads) {
+    const uint32_t e = __ldg(T + 4 + ox);
+    const int off0 = (int)(e & 0xFFFFu), off1 = (e >> 28) ? off0 : off0 + C;
+    const uint32_t w1 = (e >> 16) & 0xFFFu, w0 = 2048u - w1;
+    int k0 = -1, k1 = -1;                          // slots whose sums are cached in h0 / h1
+    uint32_t h0[C], h1[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) { h0[k] = 0; h1[k] = 0; }
+    auto hsum = [&](int j, uint32_t* hv) {
+      const uint8_t* row = srcbuf + j * span_pad + s_shift[j];
+#pragma unroll
+      for (int k = 0; k < C; ++k) hv[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+    };
+    for (int r = 0; r < R; ++r) {
+      const int a = row_a[r], b = row_b[r];
+      const uint32_t wy1 = (uint32_t)row_wy[r], wy0 = 2048u - wy1;
+      uint32_t ta[C], tb[C];
+      // a and b only move forward: reuse the previous row's sums where they match
+      if (a == k0) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) ta[k] = h0[k];
+      } else if (a == k1) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) ta[k] = h1[k];
+      } else {
+        hsum(a, ta);
+      }
+      if (b == a) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) tb[k] = ta[k];
+      } else if (b == k1) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) tb[k] = h1[k];
+      } else {
+        hsum(b, tb);
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k) { h0[k] = ta[k]; h1[k] = tb[k]; }
+      k0 = a; k1 = b;
+      OutT* o = out + ((size_t)r * OW + ox) * C;
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const uint32_t v = (wy0 * ta[k] + wy1 * tb[k] + (1u << 21)) >> 22;
+        if constexpr (kVal == VAL_LUT) o[k] = lut[k * 256 + v];
+        else o[k] = value_generic<OutT, kVal>(P, v, k);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ K1 dispatch
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
+  if constexpr (kRes && kC == 3) {
+    if (P.cw) {
+      auto pk = sample_tables_kernel<kRes>;
+      int tsm = (P.out_w + 3 * P.out_h) * 4;
+      if (tsm > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
+      pk<<<A.count, kThreads, tsm, st>>>(P, A);
+      auto k = image_cw_kernel<OutT, kVal == VAL_LUT ? VAL_LUT : kVal>;
+      if (P.cw_smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.cw_smem);
+      k<<<dim3(P.tiles_per_sample, A.count), kThreads, P.cw_smem, st>>>(P, A);
+      return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
+  }
   if (P.stream) {
     auto k = image_stream_kernel<OutT, kRes, kVal, kC, kVec>;
     const int smem = P.sl.total;
