@@ -76,7 +76,8 @@ struct PlanDev {
   int32_t stream, band_rows, grp_rows, ns_ring, nh_ring, bands_per_sample;
   // column-walker K1 (bilinear, 3 channels): a thread per output column walks the
   // tile's rows; no horizontal-pass buffer, so tiles are taller and CTAs smaller
-  int32_t cw, cw_smem;
+  int32_t cw, cw_smem, cw_npair, cw_groups;
+  uint32_t cw_magic;                       // ceil(2^32 / cw_npair) when exact for every item index
   StreamLayout sl;
   SmemLayout lay;
 };

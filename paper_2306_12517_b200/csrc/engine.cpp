@@ -493,6 +493,11 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       Q.lay = img_layout_host(Q);
       Q.tab_stride = image_tab_stride(Q);
       Q.cw_smem = cw_smem_host(Q);
+      Q.cw_npair = (W + 1) / 2;
+      Q.cw_groups = std::max(1, std::min(Q.rows_per_tile, kThreads / Q.cw_npair));
+      const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
+      Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
+                       ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
       if (Q.cw_smem <= 100 * 1024) { P = Q; P.cw = 1; }
     }
     if ((W + 3 * H) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "output too large for the device plan");

@@ -800,52 +800,86 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
   }
   __syncthreads();
   OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * OW * C;
-  for (int ox = tid; ox < OW; ox += kThreads) {
-    const uint32_t e = __ldg(T + 4 + ox);
-    const int off0 = (int)(e & 0xFFFFu), off1 = (e >> 28) ? off0 : off0 + C;
-    const uint32_t w1 = (e >> 16) & 0xFFFu, w0 = 2048u - w1;
-    int k0 = -1, k1 = -1;                          // slots whose sums are cached in h0 / h1
-    uint32_t h0[C], h1[C];
+  // a thread owns 2 adjacent output columns (3 packed 32-bit stores for 16-bit
+  // outputs) and a contiguous run of the tile's rows
+  constexpr int NP = 2;
+  const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
+  const int rg = (R + groups - 1) / groups;
+  for (int item = tid; item < npair * groups; item += kThreads) {
+    const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
+    const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
+    const int ox0 = pr * NP;
+    int off0[NP], off1[NP];
+    uint32_t w0[NP], w1[NP];
 #pragma unroll
-    for (int k = 0; k < C; ++k) { h0[k] = 0; h1[k] = 0; }
+    for (int q = 0; q < NP; ++q) {
+      const uint32_t e = __ldg(T + 4 + min(ox0 + q, OW - 1));
+      off0[q] = (int)(e & 0xFFFFu);
+      off1[q] = (e >> 28) ? off0[q] : off0[q] + C;
+      w1[q] = (e >> 16) & 0xFFFu;
+      w0[q] = 2048u - w1[q];
+    }
+    int k0 = -1, k1 = -1;                          // slots whose sums are cached in h0 / h1
+    uint32_t h0[NP * C], h1[NP * C];
+#pragma unroll
+    for (int k = 0; k < NP * C; ++k) { h0[k] = 0; h1[k] = 0; }
     auto hsum = [&](int j, uint32_t* hv) {
       const uint8_t* row = srcbuf + j * span_pad + s_shift[j];
 #pragma unroll
-      for (int k = 0; k < C; ++k) hv[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int k = 0; k < C; ++k) hv[q * C + k] = w0[q] * row[off0[q] + k] + w1[q] * row[off1[q] + k];
     };
-    for (int r = 0; r < R; ++r) {
+    const bool full = ox0 + NP <= OW;
+    for (int r = ra0; r < ra1; ++r) {
       const int a = row_a[r], b = row_b[r];
       const uint32_t wy1 = (uint32_t)row_wy[r], wy0 = 2048u - wy1;
-      uint32_t ta[C], tb[C];
+      uint32_t ta[NP * C], tb[NP * C];
       // a and b only move forward: reuse the previous row's sums where they match
       if (a == k0) {
 #pragma unroll
-        for (int k = 0; k < C; ++k) ta[k] = h0[k];
+        for (int k = 0; k < NP * C; ++k) ta[k] = h0[k];
       } else if (a == k1) {
 #pragma unroll
-        for (int k = 0; k < C; ++k) ta[k] = h1[k];
+        for (int k = 0; k < NP * C; ++k) ta[k] = h1[k];
       } else {
         hsum(a, ta);
       }
       if (b == a) {
 #pragma unroll
-        for (int k = 0; k < C; ++k) tb[k] = ta[k];
+        for (int k = 0; k < NP * C; ++k) tb[k] = ta[k];
       } else if (b == k1) {
 #pragma unroll
-        for (int k = 0; k < C; ++k) tb[k] = h1[k];
+        for (int k = 0; k < NP * C; ++k) tb[k] = h1[k];
       } else {
         hsum(b, tb);
       }
 #pragma unroll
-      for (int k = 0; k < C; ++k) { h0[k] = ta[k]; h1[k] = tb[k]; }
+      for (int k = 0; k < NP * C; ++k) { h0[k] = ta[k]; h1[k] = tb[k]; }
       k0 = a; k1 = b;
-      OutT* o = out + ((size_t)r * OW + ox) * C;
+      OutT v[NP * C];
 #pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const uint32_t v = (wy0 * ta[k] + wy1 * tb[k] + (1u << 21)) >> 22;
-        if constexpr (kVal == VAL_LUT) o[k] = lut[k * 256 + v];
-        else o[k] = value_generic<OutT, kVal>(P, v, k);
+      for (int k = 0; k < NP * C; ++k) {
+        const uint32_t u = (wy0 * ta[k] + wy1 * tb[k] + (1u << 21)) >> 22;
+        if constexpr (kVal == VAL_LUT) v[k] = lut[(k % C) * 256 + u];
+        else v[k] = value_generic<OutT, kVal>(P, u, k % C);
       }
+      OutT* o = out + ((size_t)r * OW + ox0) * C;
+      if constexpr (sizeof(OutT) == 2) {
+        if (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+          uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+          for (int k = 0; k < NP * C / 2; ++k) {
+            uint16_t lo, hi;
+            memcpy(&lo, &v[2 * k], 2);
+            memcpy(&hi, &v[2 * k + 1], 2);
+            o32[k] = (uint32_t)lo | (uint32_t)hi << 16;
+          }
+          continue;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NP * C; ++k) if (full || k < C) o[k] = v[k];
     }
   }
 }
