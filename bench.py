@@ -64,24 +64,28 @@ def dataset_path() -> Path:
 
 JPEG_B = 1024
 JPEG_SAMPLES = int(os.environ.get("BBX_BENCH_JPEG_SAMPLES", 8192))
-RST_BLOCKS = int(os.environ.get("BBX_BENCH_RST_BLOCKS", 4))   # restart interval (MCUs) the writer emits
+RST_BLOCKS = int(os.environ.get("BBX_BENCH_RST_BLOCKS", 2))   # restart interval (MCUs) the writer emits
+ND = int(os.environ.get("BBX_BENCH_ND", 50000))               # configs[4] float32 NDArray length (paper: d = 50,000)
+VAL_SPEC = f"center:224,224,{224 / 256}|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}/f16"
 
 
 def jpeg_dataset_path() -> Path:
     return DATA_DIR / f"imagenet256_jpeg_q90_420_rstb{RST_BLOCKS}_{JPEG_SAMPLES}.bbox"
 
 
-def ensure_jpeg_dataset(rank: int, barrier) -> Path:
-    """configs[2]: ImageNet-shaped synthetic photos (longer side 256, shorter side
-    153-256), JPEG q90 4:2:0 with a restart marker every RST_BLOCKS MCUs."""
+def ensure_jpeg_dataset(rank: int, barrier, nd: int = 0) -> Path:
+    """configs[2..4]: ImageNet-shaped synthetic photos (longer side 256, shorter side
+    153-256), JPEG q90 4:2:0 with a restart marker every RST_BLOCKS MCUs; with
+    `nd`, plus the float32 NDArray field "x" of that length (configs[4])."""
     import paper_2306_12517_b200 as bx
 
-    path = jpeg_dataset_path()
+    path = jpeg_dataset_path() if not nd else jpeg_dataset_path().with_name(
+        jpeg_dataset_path().stem + f"_nd{nd}.bbox")
     if rank == 0 and not path.exists():
         DATA_DIR.mkdir(parents=True, exist_ok=True)
         tmp = path.with_suffix(".tmp")
         t0 = time.time()
-        bx.write_dataset(bx.PhotoLikeSource(JPEG_SAMPLES, H, W, C, seed=1), tmp,
+        bx.write_dataset(bx.PhotoLikeSource(JPEG_SAMPLES, H, W, C, seed=1, array_dim=nd), tmp,
                          bx.WriterConfig(seed=1, compress_probability=1.0, compress_codec=bx.CodecId.JPEG,
                                          jpeg=bx.JpegParams(90, "4:2:0", restart_blocks=RST_BLOCKS),
                                          num_encode_workers=min(16, os.cpu_count() or 1)))
@@ -160,12 +164,12 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_loader(path, device, rank, world, strategy, slot_count=3, batch=B):
+def make_loader(path, device, rank, world, strategy, slot_count=3, batch=B, chain=CHAIN_SPEC, order="random"):
     import paper_2306_12517_b200 as bx
 
     ds = bx.open_dataset(path, strategy)
-    cfg = bx.LoaderConfig(batch_size=batch, order=bx.OrderKind.RANDOM, seed=SEED, slot_count=slot_count,
-                          pipelines={"image": bx.parse_pipeline(CHAIN_SPEC)}, device=device,
+    cfg = bx.LoaderConfig(batch_size=batch, order=bx.OrderKind(order), seed=SEED, slot_count=slot_count,
+                          pipelines={"image": bx.parse_pipeline(chain)}, device=device,
                           distributed=world > 1, rank=rank, world_size=world)
     return ds, bx.Loader(ds, cfg)
 
@@ -200,7 +204,8 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
     return reduce_max(secs), d2h / steps
 
 
-def cpu_baseline(path, seconds_budget: float = 15.0, batch=B, what="RRC-192+flip+normalize->f16"):
+def cpu_baseline(path, seconds_budget: float = 15.0, batch=B, what="RRC-192+flip+normalize->f16",
+                 spec=None, order="random"):
     """Oracle C port on the host cores, bounded sample (whole batches)."""
     import numpy as np
 
@@ -208,9 +213,10 @@ def cpu_baseline(path, seconds_budget: float = 15.0, batch=B, what="RRC-192+flip
 
     f = O.OracleFile(path)
     field = f.fields[0]
-    ops = O.parse_spec("decode")[:0] + O.parse_spec(ORACLE_SPEC)
+    ops = O.parse_spec(spec or ORACLE_SPEC)
     threads = os.cpu_count() or 1
-    batches = O.epoch_batches("random", SEED, 0, f.num_samples, batch)
+    page_map = [f.primary_page(i) for i in range(f.num_samples)] if order == "quasi-random" else None
+    batches = O.epoch_batches(order, SEED, 0, f.num_samples, batch, page_map)
     done, t0 = 0, time.perf_counter()
     out = None
     while time.perf_counter() - t0 < seconds_budget and done < len(batches):
@@ -239,19 +245,38 @@ def h2d_peak_gbs(device) -> float:
     return best
 
 
-def jpeg_workload(args, device, rank, world, barrier, reduce_max):
-    """configs[2]: JPEG q90 RRC-192 + flip + normalize -> f16, batch 1024 per GPU."""
+def oracle_spec(spec: str) -> str:
+    return spec.replace("/f16", "|cast:f16")
+
+
+JPEG_LEGS = {
+    "jpeg": ("configs[2]", "RandomResizedCrop 192 + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC, random order",
+             CHAIN_SPEC, "random", 0),
+    "val": ("configs[3]", "validation path: CenterCrop 224 (ratio 224/256) + NormalizeImage(ImageNet) -> f16 NHWC, "
+                          "sequential order", VAL_SPEC, "sequential", 0),
+    "ndarray": ("configs[4]", "QUASI_RANDOM order (distributed=True sharding under torchrun) RRC-192 + flip + "
+                              "normalize -> f16, plus a float32 NDArray field of the sparse-regression case study",
+                CHAIN_SPEC, "quasi-random", ND),
+}
+
+
+def jpeg_workload(args, device, rank, world, barrier, reduce_max, leg="jpeg"):
+    """configs[2..4] on the synthetic JPEG .bbox, batch 1024 per GPU: `value` with the
+    compressed heap resident in HBM, `e2e` staging every batch from host RAM."""
     import paper_2306_12517_b200 as bx
 
-    path = ensure_jpeg_dataset(rank, barrier)
-    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=JPEG_B)
+    name, desc, chain, order, nd = JPEG_LEGS[leg]
+    path = ensure_jpeg_dataset(rank, barrier, nd)
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=JPEG_B, chain=chain,
+                         order=order)
     ld.set_profiling(True)
     with ClockSampler(device) as clk:
         secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
     st = ld.stats()
     ld.shutdown()
     ds.close()
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B, slot_count=4)
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B, slot_count=4, chain=chain,
+                           order=order)
     e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
     st2 = ld2.stats()
     ld2.shutdown()
@@ -260,17 +285,19 @@ def jpeg_workload(args, device, rank, world, barrier, reduce_max):
     e2e = world * args.steps * JPEG_B / e2e_secs
     h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
     kern_s = st["kernel_seconds"] / max(st["batches"], 1)
-    payload_per_img = os.path.getsize(path) / JPEG_SAMPLES   # file bytes / samples (≈ compressed size)
+    h2d_img = h2d / JPEG_B
     hbm_peak, _ = peaks()
     pcie = h2d_peak_gbs(device)
-    # per image: compressed read + coef (w+r) + planes (w+r) + RGB (w+r) + window read + f16 output
-    hbm_img = payload_per_img + 2 * 1.5 * H * W * 2 + 2 * 1.5 * H * W + 2 * H * W * C + OUT * OUT * C * 2
-    roof_pcie = pcie * 1e9 / max(h2d / JPEG_B, 1.0)
+    out_px = 224 * 224 if leg == "val" else OUT * OUT
+    # per image: compressed read + unstuffed bits (w+r) + coef (w+r) + planes (w+r) + RGB (w+r) + output (+ array)
+    comp = h2d_img - 4 * nd
+    hbm_img = comp * 3 + 2 * 1.5 * H * W * 2 + 2 * 1.5 * H * W + 2 * H * W * C + out_px * C * 2 + 2 * 4 * nd
+    roof_pcie = pcie * 1e9 / max(h2d_img, 1.0)
     roof_hbm = hbm_peak * 1e9 / hbm_img
     out = {
-        "workload": f"configs[2]: ImageNet-shaped synthetic JPEG .bbox (q90, 4:2:0, RST every {RST_BLOCKS} MCUs, "
-                    "longer side 256), RandomResizedCrop 192 + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC",
-        "batch_per_gpu": JPEG_B, "num_samples": JPEG_SAMPLES, "mean_file_bytes_per_image": payload_per_img,
+        "workload": f"{name}: ImageNet-shaped synthetic JPEG .bbox (q90, 4:2:0, RST every {RST_BLOCKS} MCUs, longer "
+                    f"side 256){f', + float32 NDArray d={nd}' if nd else ''}; {desc}",
+        "batch_per_gpu": JPEG_B, "num_samples": JPEG_SAMPLES, "h2d_bytes_per_image": h2d_img,
         "value": value, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
         "device_ms_per_batch": kern_s * 1e3,
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -282,14 +309,14 @@ def jpeg_workload(args, device, rank, world, barrier, reduce_max):
                      "binding": "pcie" if roof_pcie < roof_hbm else "hbm",
                      "e2e_frac": e2e / min(roof_pcie, roof_hbm), "value_frac_hbm": value / roof_hbm,
                      "note": "Huffman decode is serial integer work per restart interval; neither bandwidth binds "
-                             "the device path (see profiles/ for the per-kernel split)"},
+                             "the device path (profiles/ has the per-kernel split)"},
         "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
     }
     if world == 1 and rank == 0:
         try:
-            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 2, JPEG_B,
-                                               "JPEG decode (oracle restatement of libjpeg-turbo) + RRC-192 + flip "
-                                               "+ normalize -> f16; restatement, not the reference")
+            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 3, JPEG_B,
+                                               "JPEG decode (oracle restatement of libjpeg-turbo) + the same chain; "
+                                               "restatement, not the reference", spec=oracle_spec(chain), order=order)
         except Exception as e:
             out["cpu_baseline"] = {"value": None, "error": str(e)}
     return out
@@ -320,7 +347,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--workloads", default="raw,jpeg", help="raw (configs[1], the headline) and/or jpeg (configs[2])")
+    ap.add_argument("--workloads", default="raw,jpeg,val,ndarray",
+                    help="raw (configs[1], the headline), jpeg (configs[2]), val (configs[3]), ndarray (configs[4])")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -390,10 +418,11 @@ def main():
 
     device = local
     torch.cuda.set_device(device)
-    if "raw" not in args.workloads.split(","):   # JPEG leg alone (profiling runs)
-        jpeg = jpeg_workload(args, device, rank, world, barrier, reduce_max)
+    legs = [w for w in args.workloads.split(",") if w in JPEG_LEGS]
+    if "raw" not in args.workloads.split(","):   # JPEG legs alone (profiling runs)
+        res = {JPEG_LEGS[w][0]: jpeg_workload(args, device, rank, world, barrier, reduce_max, w) for w in legs}
         if rank == 0:
-            print(json.dumps({"workloads": {"configs[2]": jpeg}}))
+            print(json.dumps({"workloads": res}))
         if dist is not None:
             dist.destroy_process_group()
         return
@@ -422,9 +451,7 @@ def main():
     e2e = world * args.steps * B / e2e_secs
     h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
 
-    jpeg = None
-    if "jpeg" in args.workloads.split(","):
-        jpeg = jpeg_workload(args, device, rank, world, barrier, reduce_max)
+    jpeg = {JPEG_LEGS[w][0]: jpeg_workload(args, device, rank, world, barrier, reduce_max, w) for w in legs} or None
 
     if rank != 0:
         if dist is not None:
@@ -456,7 +483,7 @@ def main():
         except Exception as e:   # the baseline must not sink the GPU line
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if jpeg is not None:
-        line["workloads"] = {"configs[2]": jpeg}
+        line["workloads"] = jpeg
     print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
