@@ -50,37 +50,45 @@ Pool::~Pool() {
   cv_.notify_all();
   for (auto& t : workers_) t.join();
 }
+void Pool::work(Job& job) {
+  for (int64_t i; (i = job.next.fetch_add(1)) < job.n;) {
+    (*job.fn)(i);
+    if (job.done.fetch_add(1) + 1 == job.n) {
+      std::lock_guard<std::mutex> g(mu_);
+      done_cv_.notify_all();
+    }
+  }
+}
 void Pool::run() {
   uint64_t seen = 0;
   for (;;) {
-    const std::function<void(int64_t)>* fn;
-    int64_t n;
+    std::shared_ptr<Job> job;
     {
       std::unique_lock<std::mutex> lk(mu_);
       cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
       if (stop_) return;
       seen = gen_;
-      fn = fn_; n = n_;
-      ++active_;
+      job = job_;
     }
-    for (int64_t i; (i = next_.fetch_add(1)) < n;) (*fn)(i);
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      if (--active_ == 0) done_cv_.notify_all();
-    }
+    if (job) work(*job);
   }
 }
 void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
   if (n <= 0) return;
   if (workers_.empty() || n == 1) { for (int64_t i = 0; i < n; ++i) fn(i); return; }
+  auto job = std::make_shared<Job>();
+  job->fn = &fn;
+  job->n = n;
   {
     std::lock_guard<std::mutex> g(mu_);
-    fn_ = &fn; n_ = n; next_.store(0); ++gen_;
+    job_ = job;
+    ++gen_;
   }
   cv_.notify_all();
-  for (int64_t i; (i = next_.fetch_add(1)) < n;) fn(i);
+  work(*job);
   std::unique_lock<std::mutex> lk(mu_);
-  done_cv_.wait(lk, [&] { return active_ == 0 && next_.load() >= n; });
+  done_cv_.wait(lk, [&] { return job->done.load() >= n; });
+  if (job_ == job) job_.reset();
 }
 
 // -------------------------------------------------------------------- plan

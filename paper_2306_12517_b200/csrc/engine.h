@@ -116,14 +116,20 @@ class Pool {
   int size() const { return (int)workers_.size() + 1; }
 
  private:
+  // One parallel_for call.  Each call owns its counters, so a worker that wakes
+  // late for an earlier call can neither run that call's function again nor
+  // claim indices of the next call (workers hold a shared_ptr to the job).
+  struct Job {
+    const std::function<void(int64_t)>* fn = nullptr;
+    int64_t n = 0;
+    std::atomic<int64_t> next{0}, done{0};
+  };
   void run();
+  void work(Job& job);
   std::vector<std::thread> workers_;
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
-  const std::function<void(int64_t)>* fn_ = nullptr;
-  int64_t n_ = 0;
-  std::atomic<int64_t> next_{0};
-  int active_ = 0;
+  std::shared_ptr<Job> job_;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
