@@ -214,6 +214,7 @@ struct bbx_loader {
   std::vector<size_t> jpeg_off;       // per plan with JPEG samples: JpegDesc[B] + prefixes, within a slot
   JpegTables jt;
   bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
+  bool jpeg_roi = true;               // decode only the MCUs a sample's chain reads (BBX_JPEG_ROI=0: whole image)
   size_t pay_base = 0;                // start of the compact payload region
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
@@ -1006,6 +1007,13 @@ static int process_slot(bbx_loader* L, int s) {
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
       if (d->skip) J.n_int = 0;
       if (J.n_int == 0) J.n_blocks = 0;
+      if (J.n_int) {   // region of interest: the pixels this sample's chain reads
+        int y0, y1, x0, x1;
+        read_window(pl.dev, d, reinterpret_cast<const int32_t*>(dblk + (size_t)pos * pl.dev.desc_stride + kDescHeader),
+                    &y0, &y1, &x0, &x1);
+        if (!L->jpeg_roi) { y0 = 0; y1 = d->h; x0 = 0; x1 = d->w; }
+        J.win[0] = (uint16_t)y0; J.win[1] = (uint16_t)y1; J.win[2] = (uint16_t)x0; J.win[3] = (uint16_t)x1;
+      }
       J.int_base = ti; J.blk_base = tb; J.bs_base = bs;
       ipre[pos] = ti; bpre[pos] = tb;
       ti += J.n_int; tb += J.n_blocks;
@@ -1205,6 +1213,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
   if (!ok) return fail(err.code, "%s", err.msg.c_str());
   J.int_base = 0; J.blk_base = 0; J.bs_base = 0;
+  J.win[0] = 0; J.win[1] = (uint16_t)h; J.win[2] = 0; J.win[3] = (uint16_t)w;
   // device image: [desc 64][jd][prefixes][payload (+16 pad)] then tables, intervals, bits, coef, planes, status
   const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_bp = o_ip + 16, o_pay = o_bp + 16;
   const size_t o_hf = (o_pay + len + 16 + 255) / 256 * 256;
@@ -1348,6 +1357,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (const char* e = std::getenv("BBX_WINDOW_STAGING")) L->window_staging = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_DMA")) L->dma_allowed = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_JPEG_CACHE")) L->jpeg_cache = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BBX_JPEG_ROI")) L->jpeg_roi = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   L->pool = std::make_unique<Pool>(nt);

@@ -305,6 +305,12 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     m = k * J.restart;
     m1 = min(m + J.restart, total);
     if (m >= m1) return false;
+    {                                                // region of interest (conservative across row wraps)
+      const McuRect R = jpeg_mcu_rect(J);
+      const uint32_t mx = J.mcus_x, ra = m / mx, rb = (m1 - 1) / mx;
+      if ((int)rb < R.y0 || (int)ra >= R.y1) return false;
+      if (ra == rb && ((int)((m1 - 1) % mx) < R.x0 || (int)(m % mx) >= R.x1)) return false;
+    }
     bpm = J.bpm;
     sched = 0;
     for (int q = 0; q < bpm; ++q) sched |= ((uint32_t)(J.sched >> (4 * q)) & 3u) << (2 * q);
@@ -515,6 +521,8 @@ __global__ void __launch_bounds__(kIdctThreads) jpeg_idct_kernel(const JpegArgs 
   const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
   const JComp& C = J.comp[c];
   const uint32_t my = m / J.mcus_x, mx = m - my * J.mcus_x;
+  const McuRect R = jpeg_mcu_rect(J);
+  if ((int)mx < R.x0 || (int)mx >= R.x1 || (int)my < R.y0 || (int)my >= R.y1) return;
   const uint32_t V = J.ncomp == 1 ? 1 : C.v, H = J.ncomp == 1 ? 1 : C.h;
   const uint32_t by = my * V + ((e >> 2) & 1), bx = mx * H + (e >> 3), pw = (uint32_t)C.bw * 8;
   uint8_t* plane = A.planes + (J.blk_base + J.plane_blk[c]) * 64;
@@ -588,10 +596,11 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
   __shared__ int s_ok, s_fast;
   const JpegDesc& J = A.jd[s];
   const SampleDesc* d = sdesc(A, s);
-  const int w = d->w, h = d->h, nc = J.ncomp;
-  const int y_lo = blockIdx.x * kColorRows, y_hi = min(y_lo + kColorRows, h);
+  const int w = d->w, nc = J.ncomp;
+  const int y_lo = max((int)blockIdx.x * kColorRows, (int)J.win[0]);
+  const int y_hi = min((int)(blockIdx.x + 1) * kColorRows, (int)J.win[1]);
   if (threadIdx.x == 0) {
-    s_ok = J.n_int != 0 && A.status[s].kind == 0 && y_lo < h;
+    s_ok = J.n_int != 0 && A.status[s].kind == 0 && y_lo < y_hi && J.win[2] < J.win[3];
     const uint8_t* planes = A.planes + J.blk_base * 64;
     for (int c = 0; c < nc; ++c) {
       const JComp& C = J.comp[c];
@@ -604,12 +613,13 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
   }
   __syncthreads();
   if (!s_ok) return;
-  const int no = (w + 7) >> 3, n = (y_hi - y_lo) * no;
+  // octets covering the window's columns (their extra pixels lie inside the decoded MCUs)
+  const int q_lo = J.win[2] >> 3, no = ((J.win[3] + 7) >> 3) - q_lo, n = (y_hi - y_lo) * no;
   uint8_t* const out = A.scratch + (size_t)s * A.scratch_bytes;
   if (nc == 1) {
     const Plane P0 = sP[0];
     for (int t = threadIdx.x; t < n; t += kColorThreads) {
-      const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+      const int yy = t / no, q = t - yy * no + q_lo, y = y_lo + yy, x0 = 8 * q;
       uint32_t px[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) px[k] = (uint32_t)plane_sample(P0, y, min(x0 + k, w - 1));
@@ -623,7 +633,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
     const uint8_t* crp = sP[2].p;
     const int ypw = sP[0].pw, cpw = sP[1].pw, dw = sP[1].dw, dh = sP[1].dh;
     for (int t = threadIdx.x; t < n; t += kColorThreads) {
-      const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+      const int yy = t / no, q = t - yy * no + q_lo, y = y_lo + yy, x0 = 8 * q;
       const uint2 y8 = __ldg(reinterpret_cast<const uint2*>(yp + (size_t)y * ypw + x0));
       const int i = y >> 1, i1 = (y & 1) ? min(i + 1, dh - 1) : max(i - 1, 0), j0 = 4 * q;
       const int ja = max(j0 - 1, 0), je = min(j0 + 4, dw - 1);
@@ -665,7 +675,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
   }
   const Plane P0 = sP[0], P1 = sP[1], P2 = sP[2];
   for (int t = threadIdx.x; t < n; t += kColorThreads) {
-    const int yy = t / no, q = t - yy * no, y = y_lo + yy, x0 = 8 * q;
+    const int yy = t / no, q = t - yy * no + q_lo, y = y_lo + yy, x0 = 8 * q;
     uint32_t px[24];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {

@@ -79,8 +79,25 @@ struct JpegDesc {                         // per sample, staged with the descrip
   uint64_t sched;                         // MCU block b: comp bits 4b..4b+1, v bit 4b+2, h bit 4b+3
   JComp comp[3];
   uint32_t plane_blk[3];                  // component c's pixel plane starts plane_blk[c] blocks into the sample's planes
+  uint16_t win[4];                        // pixels the chain reads: rows [win[0], win[1]) x cols [win[2], win[3])
 };
-static_assert(sizeof(JpegDesc) == 128, "JpegDesc layout");
+static_assert(sizeof(JpegDesc) == 136, "JpegDesc layout");
+
+// MCUs whose pixels (or, through fancy upsampling, whose chroma neighbours) the
+// chain reads: the window's MCU rectangle grown by one MCU on every side.
+// Restart intervals entirely outside it are not decoded (their DC predictors
+// restart, so nothing else depends on them), nor are its blocks inverse-DCT'd.
+struct McuRect { int x0, x1, y0, y1; };
+BBX_HD inline McuRect jpeg_mcu_rect(const JpegDesc& J) {
+  const int mw = J.ncomp == 1 ? 8 : 8 * J.hmax, mh = J.ncomp == 1 ? 8 : 8 * J.vmax;
+  McuRect r{0, 0, 0, 0};
+  if (J.win[0] >= J.win[1] || J.win[2] >= J.win[3]) return r;
+  r.y0 = J.win[0] / mh - 1; if (r.y0 < 0) r.y0 = 0;
+  r.y1 = (J.win[1] - 1) / mh + 2; if (r.y1 > J.mcus_y) r.y1 = J.mcus_y;
+  r.x0 = J.win[2] / mw - 1; if (r.x0 < 0) r.x0 = 0;
+  r.x1 = (J.win[3] - 1) / mw + 2; if (r.x1 > J.mcus_x) r.x1 = J.mcus_x;
+  return r;
+}
 
 // Per-sample status kinds written by J1/J2 (SampleStatus::kind).
 enum : int32_t { JST_BAD_CODE = 3, JST_MARKER_COUNT = 4, JST_MARKER_SEQ = 5 };
