@@ -521,10 +521,9 @@ __global__ void __launch_bounds__(kIdctThreads) jpeg_idct_kernel(const JpegArgs 
   const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
   const JComp& C = J.comp[c];
   const uint32_t my = m / J.mcus_x, mx = m - my * J.mcus_x;
-  const McuRect R = jpeg_mcu_rect(J);
-  if ((int)mx < R.x0 || (int)mx >= R.x1 || (int)my < R.y0 || (int)my >= R.y1) return;
   const uint32_t V = J.ncomp == 1 ? 1 : C.v, H = J.ncomp == 1 ? 1 : C.h;
   const uint32_t by = my * V + ((e >> 2) & 1), bx = mx * H + (e >> 3), pw = (uint32_t)C.bw * 8;
+  if (!jpeg_block_needed(J, (int)c, (int)by, (int)bx)) return;
   uint8_t* plane = A.planes + (J.blk_base + J.plane_blk[c]) * 64;
   idct_block(A.coef + g * 64, A.quant[C.q].q, plane + (size_t)by * 8 * pw + bx * 8, (int)pw);
 }

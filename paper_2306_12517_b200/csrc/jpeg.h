@@ -83,19 +83,45 @@ struct JpegDesc {                         // per sample, staged with the descrip
 };
 static_assert(sizeof(JpegDesc) == 136, "JpegDesc layout");
 
-// MCUs whose pixels (or, through fancy upsampling, whose chroma neighbours) the
-// chain reads: the window's MCU rectangle grown by one MCU on every side.
-// Restart intervals entirely outside it are not decoded (their DC predictors
-// restart, so nothing else depends on them), nor are its blocks inverse-DCT'd.
-struct McuRect { int x0, x1, y0, y1; };
+// Region of interest.  Component c's samples the chain needs: the window's rows
+// / columns scaled to the component (plus one on each side when it is
+// upsampled 2x: fancy upsampling reads the neighbouring row / column), i.e.
+// blocks [lo / 8, hi / 8] of that component.  Restart intervals whose MCUs hold
+// none of them are not decoded (DC predictors restart per interval, so nothing
+// else depends on them), and their blocks are not inverse-DCT'd.
+struct CompSpan { int lo, hi; };                 // inclusive sample range, lo > hi: empty
+BBX_HD inline CompSpan jpeg_comp_span(int p0, int p1, int f, int fmax, int dn) {
+  CompSpan r{0, -1};
+  if (p0 >= p1) return r;
+  const int up = fmax / f == 2 ? 1 : 0;
+  r.lo = (p0 * f) / fmax - up; if (r.lo < 0) r.lo = 0;
+  r.hi = ((p1 - 1) * f) / fmax + up; if (r.hi > dn - 1) r.hi = dn - 1;
+  return r;
+}
+// block (by, bx) of component c needed?
+BBX_HD inline bool jpeg_block_needed(const JpegDesc& J, int c, int by, int bx) {
+  const JComp& C = J.comp[c];
+  const int v = J.ncomp == 1 ? 1 : C.v, h = J.ncomp == 1 ? 1 : C.h;
+  const int vm = J.ncomp == 1 ? 1 : J.vmax, hm = J.ncomp == 1 ? 1 : J.hmax;
+  const CompSpan ys = jpeg_comp_span(J.win[0], J.win[1], v, vm, C.dh), xs = jpeg_comp_span(J.win[2], J.win[3], h, hm, C.dw);
+  return by >= ys.lo / 8 && by <= ys.hi / 8 && bx >= xs.lo / 8 && bx <= xs.hi / 8;
+}
+struct McuRect { int x0, x1, y0, y1; };          // half-open MCU ranges
 BBX_HD inline McuRect jpeg_mcu_rect(const JpegDesc& J) {
-  const int mw = J.ncomp == 1 ? 8 : 8 * J.hmax, mh = J.ncomp == 1 ? 8 : 8 * J.vmax;
-  McuRect r{0, 0, 0, 0};
-  if (J.win[0] >= J.win[1] || J.win[2] >= J.win[3]) return r;
-  r.y0 = J.win[0] / mh - 1; if (r.y0 < 0) r.y0 = 0;
-  r.y1 = (J.win[1] - 1) / mh + 2; if (r.y1 > J.mcus_y) r.y1 = J.mcus_y;
-  r.x0 = J.win[2] / mw - 1; if (r.x0 < 0) r.x0 = 0;
-  r.x1 = (J.win[3] - 1) / mw + 2; if (r.x1 > J.mcus_x) r.x1 = J.mcus_x;
+  McuRect r{1 << 30, 0, 1 << 30, 0};
+  for (int c = 0; c < J.ncomp; ++c) {
+    const JComp& C = J.comp[c];
+    const int v = J.ncomp == 1 ? 1 : C.v, h = J.ncomp == 1 ? 1 : C.h;
+    const int vm = J.ncomp == 1 ? 1 : J.vmax, hm = J.ncomp == 1 ? 1 : J.hmax;
+    const CompSpan ys = jpeg_comp_span(J.win[0], J.win[1], v, vm, C.dh), xs = jpeg_comp_span(J.win[2], J.win[3], h, hm, C.dw);
+    if (ys.lo > ys.hi || xs.lo > xs.hi) continue;
+    const int y0 = ys.lo / (8 * v), y1 = ys.hi / (8 * v) + 1, x0 = xs.lo / (8 * h), x1 = xs.hi / (8 * h) + 1;
+    if (y0 < r.y0) r.y0 = y0;
+    if (y1 > r.y1) r.y1 = y1;
+    if (x0 < r.x0) r.x0 = x0;
+    if (x1 > r.x1) r.x1 = x1;
+  }
+  if (r.y0 >= r.y1 || r.x0 >= r.x1) r = McuRect{0, 0, 0, 0};
   return r;
 }
 
