@@ -36,11 +36,6 @@ struct SmemLayout {
   int32_t xt_off, meta_off, src_off, h_off, total;
 };
 
-// Shared-memory layout of the streaming K1 (one CTA = one band of output rows).
-struct StreamLayout {
-  int32_t xt_off, rows_off, grp_off, shift_off, lut_off, src_off, h_off, total;
-};
-
 // Everything the kernels need about one compiled chain; passed by value.
 struct PlanDev {
   int32_t src_kind;
@@ -71,14 +66,10 @@ struct PlanDev {
   uint32_t linx_magic, liny_magic;         // for 2*canvas_w / 2*canvas_h (bilinear axes), 0 = use /
   int32_t h_tpc;                           // horizontal pass: threads per output column
   int32_t tab_stride;                      // K1 prologue table words per sample
-  // streaming K1: a CTA walks band_rows output rows in groups of grp_rows,
-  // source rows pass through an ns-row cp.async ring and an nh-row H ring
-  int32_t stream, band_rows, grp_rows, ns_ring, nh_ring, bands_per_sample;
   // column-walker K1 (bilinear, 3 channels): a thread per output column walks the
   // tile's rows; no horizontal-pass buffer, so tiles are taller and CTAs smaller
   int32_t cw, cw_smem, cw_npair, cw_groups;
   uint32_t cw_magic;                       // ceil(2^32 / cw_npair) when exact for every item index
-  StreamLayout sl;
   SmemLayout lay;
 };
 
@@ -129,7 +120,6 @@ int launch_scalar_gather(const ScalarArgs& S, void* stream);
 int image_smem_bytes(const PlanDev& P);
 SmemLayout img_layout_host(const PlanDev& P);
 int image_tab_stride(const PlanDev& P);
-StreamLayout stream_layout_host(const PlanDev& P);
 int cw_smem_host(const PlanDev& P);
 
 }  // namespace bbx

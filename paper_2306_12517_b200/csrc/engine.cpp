@@ -265,63 +265,6 @@ static void host_lin_axis(int o, int out_n, int in_n, int* i0, int* i1) {
   *i0 = (int)q; *i1 = (int)q + 1;
 }
 
-// Streaming-K1 feasibility and ring sizes: the worst case, over every sample
-// the plan can see, of the source rows one group of G output rows spans and
-// of the step of the last source row from one group to the next.
-static void plan_stream(PlanDev& P, const Field& f) {
-  P.stream = 0;
-  // Opt-in until the streaming variant is parity-green on the GPU (round-1
-  // run: 27 mismatching parity cases + an illegal access); the tile K1 is the default.
-  const char* en = std::getenv("BBX_STREAM");
-  if (!en || std::atoi(en) == 0) return;
-  const int H = P.out_h;
-  int band = 32;
-  if (const char* e = std::getenv("BBX_BAND_ROWS")) band = std::max(1, std::atoi(e));
-  for (int G : {8, 4, 2}) {
-    int max_span = 1, max_step = 1;
-    auto scan = [&](auto&& ymap_lo, auto&& ymap_hi) {
-      int prev_hi = -1;
-      for (int r0 = 0; r0 < H; r0 += G) {
-        if (r0 % band == 0) prev_hi = -1;   // a band starts from scratch
-        const int rl = std::min(r0 + G, H) - 1;
-        const int lo = ymap_lo(r0), hi = ymap_hi(rl);
-        max_span = std::max(max_span, hi - lo + 1);
-        if (prev_hi >= 0) max_step = std::max(max_step, hi - prev_hi);
-        prev_hi = hi;
-      }
-    };
-    if (P.src_kind == SRC_RESAMPLE) {
-      // the window height ch varies per sample: check every possible value
-      const int maxh = f.info.max_height;
-      if ((int64_t)maxh * H > 40000000) return;
-      for (int ch = 1; ch <= maxh; ++ch) {
-        auto y_of = [&](int r, bool tap1) {
-          int32_t prm[64] = {0};
-          int cy = host_back_y(P, prm, r), y0, y1;
-          host_lin_axis(cy, P.canvas_h, ch, &y0, &y1);
-          return tap1 ? y1 : y0;
-        };
-        scan([&](int r) { return y_of(r, false); }, [&](int r) { return y_of(r, true); });
-      }
-    } else {
-      int32_t prm[64] = {0};
-      auto y_of = [&](int r) { return host_back_y(P, prm, r); };
-      scan(y_of, y_of);
-    }
-    const int ns = std::max(2 * max_step, max_span + max_step) + 1, nh = max_span;
-    if (ns > 64 || nh > 64 || G > 64) continue;
-    P.grp_rows = G;
-    P.band_rows = std::max(G, band / G * G);
-    P.ns_ring = ns;
-    P.nh_ring = nh;
-    P.bands_per_sample = (H + P.band_rows - 1) / P.band_rows;
-    P.sl = stream_layout_host(P);
-    if (P.sl.total > 110 * 1024) continue;
-    P.stream = 1;
-    return;
-  }
-}
-
 static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n_ops, Plan& pl) {
   const bbx_dataset* ds = L->ds;
   if (field_index < 0 || field_index >= (int)ds->fields.size())
@@ -490,11 +433,10 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     P.lay = img_layout_host(P);
     P.h_tpc = std::max(1, kThreads / W);
     P.tab_stride = image_tab_stride(P);
-    plan_stream(P, f);
     // column-walker K1 for 3-channel bilinear decoders (BBX_CW=0 keeps the tile kernel)
     P.cw = 0;
     const char* cwe = std::getenv("BBX_CW");
-    if (P.src_kind == SRC_RESAMPLE && C == 3 && !P.stream && !(cwe && std::atoi(cwe) == 0)) {
+    if (P.src_kind == SRC_RESAMPLE && C == 3 && !(cwe && std::atoi(cwe) == 0)) {
       PlanDev Q = P;
       Q.rows_per_tile = std::min(16, H);
       if (const char* e = std::getenv("BBX_CW_ROWS")) Q.rows_per_tile = std::max(1, std::min(std::atoi(e), H));
@@ -1160,7 +1102,7 @@ static int process_slot(bbx_loader* L, int s) {
       }
     }
     if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.stream) ? 1 : 2;   // tile K1 = prologue + tiles
+    launches += pl.dev.src_kind == SRC_ARRAY ? 1 : 2;   // K1 = prologue + tiles
   }
   if (prof) CK(cudaEventRecord(S.k1, L->comp_st));
   S.timed = prof;

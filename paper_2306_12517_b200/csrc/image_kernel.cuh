@@ -514,225 +514,6 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
         reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * rowlen, lut, tid);
 }
 
-// ------------------------------------------------------------ K1 (streaming)
-__host__ __device__ inline StreamLayout stream_layout(const PlanDev& P) {
-  StreamLayout L;
-  const bool res = P.src_kind == SRC_RESAMPLE;
-  const int span_pad = align_up(P.src_row_w * P.channels, 16) + 32;
-  const int hrow_pad = align_up(P.out_w * P.channels * (res ? 4 : 1), 16) + 16;
-  const int ngrp = (P.band_rows + P.grp_rows - 1) / P.grp_rows;
-  L.xt_off = 0;
-  L.rows_off = align_up(P.out_w * 4, 16);                           // ra, rb, wy: band_rows each
-  L.grp_off = L.rows_off + align_up(3 * P.band_rows * 4, 16);        // glo, ghi: ngrp each
-  L.shift_off = L.grp_off + align_up(2 * ngrp * 4, 16);              // per source-ring slot
-  L.lut_off = L.shift_off + align_up(P.ns_ring * 4, 16);
-  const int lut = P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
-  L.src_off = L.lut_off + lut;
-  L.h_off = L.src_off + P.ns_ring * span_pad;
-  L.total = L.h_off + P.nh_ring * hrow_pad;
-  return L;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-  unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// grid = (bands_per_sample, count).  A CTA owns output rows [R0, R1) of one
-// sample and walks them in groups of G rows.  The source rows a group needs
-// form a contiguous, monotone range; they are fetched one group ahead with
-// cp.async into a ring (slot = row % NS), horizontally resampled once into a
-// second ring (slot = row % NH), and consumed by the vertical pass, so each
-// source row crosses HBM->SM once and the fetch of group g+1 overlaps the
-// arithmetic of group g.  Ring sizes come from the plan's worst-case row
-// steps (engine.cpp: plan_stream).
-template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
-__global__ void __launch_bounds__(kThreads, 4) image_stream_kernel(const PlanDev P, const LaunchArgs A) {
-  const int s = blockIdx.y;
-  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-  if (d->skip) return;
-  const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
-  const int C = kC > 0 ? kC : P.channels;
-  const int OW = P.out_w, OH = P.out_h, rowlen = OW * C, h = d->h, w = d->w, tid = threadIdx.x;
-  const int R0 = blockIdx.x * P.band_rows, R1 = min(OH, R0 + P.band_rows);
-  if (R0 >= R1) return;
-  const int NB = R1 - R0, G = P.grp_rows, ngrp = (NB + G - 1) / G;
-  const int NS = P.ns_ring, NH = P.nh_ring;
-  const SrcRows S = src_rows_of(P, A, d, s);
-  const int sh = S.sh;
-  const int span_pad = align_up(P.src_row_w * C, 16) + 32;
-  const int hrow_pad = align_up(OW * C * (kRes ? 4 : 1), 16) + 16;
-
-  extern __shared__ __align__(16) uint8_t smem[];
-  const StreamLayout& L = P.sl;
-  uint32_t* xt = reinterpret_cast<uint32_t*>(smem + L.xt_off);
-  int* xraw = reinterpret_cast<int*>(xt);
-  int* ya = reinterpret_cast<int*>(smem + L.rows_off);   // source row (>> sh) of tap 0, -1 = zero row
-  int* yb = ya + P.band_rows;                            // tap 1 (bilinear)
-  int* wyv = yb + P.band_rows;
-  int* glo = reinterpret_cast<int*>(smem + L.grp_off);   // per group: first / last source row (-1: none)
-  int* ghi = glo + ngrp;
-  int* shift = reinterpret_cast<int*>(smem + L.shift_off);
-  OutT* lut = reinterpret_cast<OutT*>(smem + L.lut_off);
-  uint8_t* srcring = smem + L.src_off;
-  uint8_t* hring = smem + L.h_off;
-  __shared__ int s_clo, s_chi;
-  __shared__ int hra[64], hrb[64];   // per output row of the current group: H-ring rows
-  __shared__ int hsrc[64], hdst[64]; // per source row H-passed by the current group: ring offsets
-
-  const int top = kRes ? prm[0] : 0, left = kRes ? prm[1] : 0, ch = kRes ? prm[2] : 0, cw = kRes ? prm[3] : 0;
-  // ---- A: geometry of this band
-  for (int ox = tid; ox < OW; ox += kThreads) xraw[ox] = back_x(P, prm, ox);
-  for (int r = tid; r < NB; r += kThreads) {
-    if constexpr (kRes) {
-      int cy = back_y(P, prm, R0 + r), y0, y1, wy;
-      lin_axis(cy, P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
-      ya[r] = (top + y0) >> sh; yb[r] = (top + y1) >> sh; wyv[r] = wy;
-    } else {
-      int cy = back_y(P, prm, R0 + r);
-      ya[r] = cy < h ? (cy >> sh) : -1;
-    }
-  }
-  if constexpr (kVal == VAL_LUT) {
-    const uint4* g = reinterpret_cast<const uint4*>(A.lut);
-    uint4* l4 = reinterpret_cast<uint4*>(lut);
-    const int n16 = C * 256 * (int)sizeof(OutT) / 16;
-    for (int i = tid; i < n16; i += kThreads) l4[i] = g[i];
-  }
-  __syncthreads();
-  if (tid == 0) {   // composed maps are monotone: the end columns span the source columns
-    int xa = xraw[0], xb = xraw[OW - 1], clo, chi;
-    if constexpr (kRes) {
-      int a0, a1, aw, b0, b1, bw;
-      lin_axis(min(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, a0, a1, aw);
-      lin_axis(max(xa, xb), P.canvas_w, cw, P.lin32, P.linx_magic, b0, b1, bw);
-      clo = (left + a0) >> sh; chi = (left + b1) >> sh;
-    } else {
-      clo = min(xa, xb) >> sh; chi = min(max(xa, xb), w - 1) >> sh;
-    }
-    s_clo = clo; s_chi = chi;
-  }
-  for (int g = tid; g < ngrp; g += kThreads) {
-    const int rf = g * G, rl = min(rf + G, NB) - 1;
-    int lo = ya[rf], hi;
-    if constexpr (kRes) {
-      hi = yb[rl];
-    } else {
-      hi = -1;
-      for (int r = rl; r >= rf; --r) if (ya[r] >= 0) { hi = ya[r]; break; }
-      if (lo < 0) hi = -1;
-    }
-    glo[g] = lo; ghi[g] = hi;
-  }
-  __syncthreads();
-  const int col_lo = s_clo;
-  const int span_bytes = s_chi >= col_lo ? (s_chi - col_lo + 1) * C : 0;
-  for (int ox = tid; ox < OW; ox += kThreads) {
-    const int cx = xraw[ox];
-    if constexpr (kRes) {
-      int x0, x1, wx;
-      lin_axis(cx, P.canvas_w, cw, P.lin32, P.linx_magic, x0, x1, wx);
-      int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
-      xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
-    } else {
-      xt[ox] = cx < w ? (uint32_t)(((cx >> sh) - col_lo) * C) : 0xFFFFFFFFu;
-    }
-  }
-
-  const int lane = tid & 31, warp = tid >> 5;
-  // issue the cp.async copies of source rows [y0, y1] (warp per row)
-  auto fetch = [&](int y0, int y1) {
-    if (span_bytes == 0) return;
-    for (int y = y0 + warp; y <= y1; y += kThreads / 32) {
-      const int slot = y % NS;
-      const uint8_t* src = S.base + (int64_t)y * S.rstride + (int64_t)col_lo * C;
-      uintptr_t a = reinterpret_cast<uintptr_t>(src);
-      uintptr_t a0 = a & ~(uintptr_t)15;
-      const int sft = (int)(a - a0);
-      const int n16 = (sft + span_bytes + 15) >> 4;
-      uint8_t* dst = srcring + (size_t)slot * span_pad;
-      const uint8_t* s0 = reinterpret_cast<const uint8_t*>(a0);
-      for (int c = lane; c < n16; c += 32) cp_async16(dst + 16 * c, s0 + 16 * c);
-      if (lane == 0) shift[slot] = sft;
-    }
-  };
-  int fetched = -1, hdone = -1;
-  {
-    const int lo = glo[0], hi = ghi[0];
-    if (hi >= 0) { fetch(lo, hi); fetched = hi; hdone = lo - 1; }
-  }
-  cp_async_commit();
-  OutT* out_band = reinterpret_cast<OutT*>(A.out) + ((size_t)s * OH + R0) * rowlen;
-
-  for (int g = 0; g < ngrp; ++g) {
-    // prefetch the next group's new rows (one group ahead)
-    if (g + 1 < ngrp) {
-      const int hi1 = ghi[g + 1];
-      if (hi1 > fetched) {
-        const int from = max(fetched + 1, glo[g + 1]);
-        fetch(from, hi1);
-        fetched = hi1;
-        if (hdone < 0) hdone = from - 1;
-      }
-    }
-    cp_async_commit();
-    cp_async_wait<1>();          // everything but the newest group has landed
-    const int rf = g * G, R = min(G, NB - rf);
-    const int hi = ghi[g];
-    const int first = max(hdone + 1, glo[g]);
-    const int nrows = hi >= first ? hi - first + 1 : 0;
-    if (tid < R) {
-      const int r = rf + tid;
-      hra[tid] = ya[r] >= 0 ? ya[r] % NH : -1;
-      if constexpr (kRes) hrb[tid] = yb[r] % NH;
-    }
-    if (tid < nrows) {           // ring addresses of the rows this group H-passes
-      const int y = first + tid, slot = y % NS;
-      hsrc[tid] = slot * span_pad + shift[slot];
-      hdst[tid] = (y % NH) * hrow_pad;
-    }
-    __syncthreads();
-    // ---- H: source rows (hdone, ghi[g]] -> H ring; thread per (row, column)
-    if (nrows > 0) {
-      const int total = nrows * OW;
-      for (int idx = tid; idx < total; idx += kThreads) {
-        const int j = P.ow_magic ? (int)fast_div((uint32_t)idx, P.ow_magic) : idx / OW;
-        const int ox = idx - j * OW;
-        const uint8_t* row = srcring + hsrc[j];
-        const uint32_t e = xt[ox];
-        if constexpr (kRes) {
-          uint32_t* hr = reinterpret_cast<uint32_t*>(hring + hdst[j]) + ox * C;
-          const int off0 = (int)(e & 0xFFFFu), wx = (int)((e >> 16) & 0xFFFu);
-          const int off1 = (e >> 28) ? off0 : off0 + C;
-          const uint32_t w0 = 2048u - (uint32_t)wx, w1 = (uint32_t)wx;
-#pragma unroll
-          for (int k = 0; k < (kC > 0 ? kC : 1); ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
-          if constexpr (kC == 0)
-            for (int k = 1; k < C; ++k) hr[k] = w0 * row[off0 + k] + w1 * row[off1 + k];
-        } else {
-          uint8_t* hr = hring + hdst[j] + ox * C;
-          const bool pad = e == 0xFFFFFFFFu;
-          const uint32_t eo = pad ? 0u : e;
-#pragma unroll
-          for (int k = 0; k < (kC > 0 ? kC : 1); ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
-          if constexpr (kC == 0)
-            for (int k = 1; k < C; ++k) { uint8_t v = row[eo + k]; hr[k] = pad ? 0 : v; }
-        }
-      }
-      hdone = hi;
-    }
-    __syncthreads();
-    // ---- V: this group's output rows
-    vpass<OutT, kRes, kVal, kC, kVec>(P, hring, hrow_pad, hra, hrb, wyv + rf, R, out_band + (size_t)rf * rowlen, lut,
-                                      tid);
-    __syncthreads();             // hra/hrb and the H ring are rewritten next iteration
-  }
-  cp_async_wait<0>();
-}
-
 // ------------------------------------------------------- K1 (column walker)
 // Bilinear decoders, 3 channels.  grid = (tiles_per_sample, count); a tile is
 // rows_per_tile output rows.  After the tile's source rows are staged (as K1),
@@ -898,13 +679,6 @@ static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) 
       k<<<dim3(P.tiles_per_sample, A.count), kThreads, P.cw_smem, st>>>(P, A);
       return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
-  }
-  if (P.stream) {
-    auto k = image_stream_kernel<OutT, kRes, kVal, kC, kVec>;
-    const int smem = P.sl.total;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<dim3(P.bands_per_sample, A.count), kThreads, smem, st>>>(P, A);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
   }
   {   // prologue: per-sample geometry tables
     auto pk = sample_tables_kernel<kRes>;

@@ -424,13 +424,8 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
 }
 
 // ------------------------------------------------------------------- J3
-// CTA per (sample, MCU row).  Phase 1: one thread per 8x8 block, dequantize +
-// islow IDCT (13-bit constants, 2 pass-1 bits) in registers, rows into the
-// component's shared-memory window.  Phase 2: one thread per output pixel:
-// libjpeg's fancy upsampling (h2v1 / h1v2 / h2v2 triangle filters with edge
-// replication; box when the downsampled width is <= 2) and JFIF YCbCr -> RGB
-// in 16-bit fixed point, into the decode scratch (HWC, row stride w*C).
-constexpr int kPixThreads = 256;
+// Dequantize + islow IDCT (13-bit constants, 2 pass-1 bits, 32-bit modular
+// arithmetic as oracle/jpeg_oracle.c) of one 8x8 block in registers.
 
 __device__ __forceinline__ uint32_t range_out(int v) {   // post-IDCT range_limit[v & 1023]
   int s = ((v & 1023) ^ 512) - 512 + 128;

@@ -160,7 +160,6 @@ __global__ void __launch_bounds__(kThreads) array_kernel(const PlanDev P, const 
 int image_smem_bytes(const PlanDev& P) { return img_layout(P).total; }
 SmemLayout img_layout_host(const PlanDev& P) { return img_layout(P); }
 int image_tab_stride(const PlanDev& P) { return tab_stride(P); }
-StreamLayout stream_layout_host(const PlanDev& P) { return stream_layout(P); }
 int cw_smem_host(const PlanDev& P) { return cw_smem_bytes(P); }
 
 int launch_image(const PlanDev& P, const LaunchArgs& A, void* stream) {
