@@ -173,7 +173,13 @@ typedef struct {
   int64_t kernel_timed;       /* kernel launches that were timed */
   int64_t kernel_bytes;       /* algorithmic bytes of the timed launches */
   int64_t dma_batches;        /* batches whose payloads the copy engine read from the registered mmap */
+  int64_t zero_copy_bytes;    /* payload bytes kernels read straight from pinned host memory over PCIe */
 } bbx_loader_stats;
+/* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
+ * RLE / JPEG fields, kernels read each sample's payload window straight from
+ * host memory over PCIe -- no CPU gather, no staging copy.  Call before the
+ * first submit; ignored when the plan cannot use it. */
+bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
 /* Turn per-launch CUDA-event timing of the transform kernels on/off. */
 bbx_status bbx_loader_set_profiling(bbx_loader* ld, int enabled);
 bbx_status bbx_loader_get_stats(const bbx_loader* ld, bbx_loader_stats* out);

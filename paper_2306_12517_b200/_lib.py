@@ -41,7 +41,7 @@ class LoaderStats(ctypes.Structure):
     _fields_ = [("batches", c_i64), ("samples", c_i64), ("h2d_bytes", c_i64), ("d2h_bytes", c_i64),
                 ("kernel_launches", c_i64), ("stage_seconds", c_dbl), ("wait_seconds", c_dbl),
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
-                ("dma_batches", c_i64)]
+                ("dma_batches", c_i64), ("zero_copy_bytes", c_i64)]
 
 
 # bbx_status -> exception class (errors.py:4-57)
@@ -101,6 +101,7 @@ def lib():
         "bbx_loader_reset_stats": (c_i32, [c_vp]),
         "bbx_loader_compute_stream": (c_vp, [c_vp]),
         "bbx_loader_set_profiling": (c_i32, [c_vp, ctypes.c_int]),
+        "bbx_loader_set_zero_copy": (c_i32, [c_vp, ctypes.c_int]),
         "bbx_decode_image": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -117,7 +118,8 @@ EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_cl
             "bbx_epoch_order", "bbx_loader_create", "bbx_loader_destroy", "bbx_loader_add_field",
             "bbx_loader_add_scalar", "bbx_loader_bind", "bbx_loader_submit", "bbx_loader_wait",
             "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",
-            "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling", "bbx_decode_image")
+            "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling",
+            "bbx_loader_set_zero_copy", "bbx_decode_image")
 
 
 def last_error() -> str:

@@ -215,6 +215,9 @@ struct bbx_loader {
   JpegTables jt;
   bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
   bool jpeg_roi = true;               // decode only the MCUs a sample's chain reads (BBX_JPEG_ROI=0: whole image)
+  bool zero_copy = false;             // requested: kernels read payloads from the pinned host heap
+  const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
+  bool zc = false;                    // payload_dev is host memory (zero-copy)
   size_t pay_base = 0;                // start of the compact payload region
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
@@ -755,7 +758,11 @@ static int finalize(bbx_loader* L) {
     off = (off + 255) / 256 * 256;
   }
   L->desc_bytes = off;
-  bool resident = L->ds->d_heap != nullptr;
+  bool codec_stage = false;           // RLE / JPEG payloads are expanded from a staged copy
+  for (const auto& pl : L->plans) codec_stage |= !pl.scalar && (pl.field_has_rle || pl.field_has_jpeg);
+  L->zc = !L->ds->d_heap && L->zero_copy && L->ds->h_heap_dev && !codec_stage;
+  L->payload_dev = L->ds->d_heap ? L->ds->d_heap : (L->zc ? L->ds->h_heap_dev : nullptr);
+  bool resident = L->payload_dev != nullptr;
   L->pay_base = off;
   for (size_t p = 0; p < L->plans.size(); ++p) {   // capacity: every sample's whole payload
     if (L->plans[p].scalar || resident) continue;
@@ -833,8 +840,9 @@ static int process_slot(bbx_loader* L, int s) {
   Slot& S = L->slots[s];
   const bbx_dataset* ds = L->ds;
   const int count = S.count;
-  const bool resident = ds->d_heap != nullptr;
+  const bool resident = L->payload_dev != nullptr;   // HBM heap or zero-copy: no payload staging
   CK(cudaSetDevice(L->device));
+  int64_t zc_bytes = 0;
   // the pinned slot may still be the source of the previous H2D
   if (S.used) CK(cudaEventSynchronize(S.h2d_done));
   S.herr = HostErr{};
@@ -895,6 +903,15 @@ static int process_slot(bbx_loader* L, int s) {
       }
       if (resident) {
         d->src = off;                                   // absolute file offset; base = heap - heap_offset
+        if (L->zc) {                                    // bytes the kernels will pull over PCIe
+          if (image && d->codec == CODEC_RAW) {
+            int y0, y1, x0, x1;
+            read_window(pl.dev, d, reinterpret_cast<const int32_t*>(desc + kDescHeader), &y0, &y1, &x0, &x1);
+            zc_bytes += (int64_t)(y1 - y0) * (x1 - x0) * d->c;
+          } else {
+            zc_bytes += len;
+          }
+        }
         continue;
       }
       d->src = cursor - pay_base;                       // relative to the payload region
@@ -1057,7 +1074,7 @@ static int process_slot(bbx_loader* L, int s) {
     }
     LaunchArgs A{};
     A.desc = S.d_stage + L->desc_off[p];
-    A.payload = resident ? (const uint8_t*)(ds->d_heap - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
+    A.payload = resident ? (const uint8_t*)(L->payload_dev - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
     A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
     A.tables = pl.d_tables.empty() ? nullptr : pl.d_tables[s];
     A.lut = pl.d_lut;
@@ -1128,6 +1145,7 @@ static int process_slot(bbx_loader* L, int s) {
     L->stats.kernel_launches += launches;
     L->stats.stage_seconds += t1 - t0;
     L->stats.dma_batches += dma_done ? 1 : 0;
+    L->stats.zero_copy_bytes += zc_bytes;
   }
   return BBX_OK;
 }
@@ -1519,6 +1537,13 @@ void bbx_loader_destroy(bbx_loader* L) {
   if (L->copy_st) cudaStreamDestroy(L->copy_st);
   if (L->comp_st) cudaStreamDestroy(L->comp_st);
   delete L;
+}
+
+bbx_status bbx_loader_set_zero_copy(bbx_loader* L, int enabled) {
+  if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
+  L->zero_copy = enabled != 0;
+  return BBX_OK;
 }
 
 bbx_status bbx_loader_get_stats(const bbx_loader* L, bbx_loader_stats* out) {

@@ -80,6 +80,7 @@ struct bbx_dataset {
   uint8_t* d_heap = nullptr;   // device copy of [heap_offset, alloc_table_offset)
   bool host_registered = false; // the mmap is page-locked for DMA (cudaHostRegister)
   uint8_t* h_heap = nullptr;     // pinned host copy of the heap (bbx_dataset_pin_host)
+  uint8_t* h_heap_dev = nullptr; // its device-mapped address (zero-copy reads over PCIe)
   // DMA-able host address of file offset o: dma_base + o (registered mmap or pinned copy)
   const uint8_t* dma_base() const { return h_heap ? h_heap - heap_offset : (host_registered ? map : nullptr); }
   std::mutex reg_mu;

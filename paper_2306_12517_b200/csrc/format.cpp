@@ -163,7 +163,7 @@ int dataset_pin_host(bbx_dataset* ds, int threads) {
   if (ds->h_heap) return BBX_OK;
   size_t heap = (size_t)(ds->alloc_table_offset - ds->heap_offset);
   uint8_t* h = nullptr;
-  CK(cudaHostAlloc(&h, heap + 256, cudaHostAllocPortable));
+  CK(cudaHostAlloc(&h, heap + 256, cudaHostAllocPortable | cudaHostAllocMapped));
   std::memset(h + heap, 0, 256);
   const size_t chunk = 64ull << 20;
   const size_t nchunks = (heap + chunk - 1) / chunk;
@@ -179,6 +179,9 @@ int dataset_pin_host(bbx_dataset* ds, int threads) {
     });
   for (auto& t : th) t.join();
   ds->h_heap = h;
+  void* dp = nullptr;
+  if (cudaHostGetDevicePointer(&dp, h, 0) == cudaSuccess) ds->h_heap_dev = static_cast<uint8_t*>(dp);
+  else cudaGetLastError();
   return BBX_OK;
 }
 

@@ -223,6 +223,8 @@ class Loader:
         _lib.check(L.bbx_loader_create(self.dataset.handle, self.device, config.batch_size, config.slot_count,
                                        config.staging_threads, ctypes.byref(h)))
         self._handle = h
+        if isinstance(strategy, OsCache) and getattr(strategy, "zero_copy", False):
+            _lib.check(L.bbx_loader_set_zero_copy(h, 1))
         field_index = {f.name: i for i, f in enumerate(schema)}
         self._field_index = field_index
         pipelines = dict(config.pipelines or {})

@@ -41,12 +41,17 @@ class OsCache:
     Measured on B200 (profiles/): the pooled CPU gather + one contiguous H2D
     is faster for windowed RAW batches (460k vs 163k img/s), so the default
     (None/False) gathers; True opts in (e.g. when host cores are scarce).
+
+    zero_copy: with pinned=True, kernels read each sample's payload window
+    straight from the pinned host heap over PCIe (no CPU gather, no staging
+    copy).  RAW / SUBSAMPLE2 / array fields only; RLE / JPEG fields stage.
     """
 
     PIN_HOST_RAM_FRACTION = 0.2
 
-    def __init__(self, pinned: bool | None = None):
-        self.pinned = pinned
+    def __init__(self, pinned: bool | None = None, zero_copy: bool = False):
+        self.pinned = pinned or zero_copy
+        self.zero_copy = zero_copy
 
 
 @dataclass
