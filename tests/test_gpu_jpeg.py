@@ -174,3 +174,32 @@ def test_repeated_epochs_are_deterministic(tmp_path):
         assert_same(run_gpu(path, 8, "quasi-random", seed=9, epoch=1, pipelines={"image": chain}), ref)
     for i, (_, arrs) in enumerate(ref):
         assert np.array_equal(arrs["x"], np.stack([src[j]["x"] for j in ref[i][0]]))
+
+
+def test_unsupported_jpeg_processes_raise_at_their_position(tmp_path):
+    """A progressive JPEG cell (SOF2) and a non-JPEG payload in a JPEG field are
+    rejected host-side with CorruptPayload at the sample's position; the oracle
+    rejects the same bytes."""
+    import io
+
+    from PIL import Image
+
+    src = bx.PhotoLikeSource(10, 40, 40, 3, seed=6, fixed_size=True)
+    path = tmp_path / "p.bbox"
+    bx.write_dataset(src, path, bx.WriterConfig(page_size=1 << 16, seed=6, compress_probability=1.0,
+                                                compress_codec=bx.CodecId.JPEG))
+    raw = bytearray(path.read_bytes())
+    c = _cell(path, 6)
+    bio = io.BytesIO()
+    Image.fromarray(src[6]["image"]).save(bio, "JPEG", quality=90, progressive=True)
+    prog = bio.getvalue()
+    assert len(prog) <= c["length"]
+    raw[c["offset"]:c["offset"] + len(prog)] = prog
+    bad = tmp_path / "prog.bbox"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(O.OracleError, match="progressive"):
+        O.decode(c["h"], c["w"], c["c"], 3, prog)
+    for bs in (4, 5):
+        seen, err = _first_error(bad, bs)
+        assert "progressive" in err, err
+        assert seen == list(range(6 // bs * bs))
