@@ -409,6 +409,20 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     const int pos = kk + run;
     if (v != 0 && !bad) cb[nat[pos]] = (int16_t)v;
     kk = (e & kFastEob) ? 64 : pos + 1;
+    // a second AC symbol in the same iteration when the block continues, the bit
+    // buffer certainly holds it (>= 27 bits) and its code + value resolve in the
+    // fast table; otherwise it is left for the next iteration
+    if (kk < 64 && !bad && nb >= 27) {
+      const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
+      if ((e2 & (kFastValid | kFastFull)) == (kFastValid | kFastFull)) {
+        acc <<= (e2 >> 25) & 31;
+        nb -= (int)((e2 >> 25) & 31);
+        const int pos2 = kk + (int)((e2 >> 21) & 15);
+        const int v2 = (int)(int16_t)(e2 & 0xFFFF);
+        if (v2 != 0) cb[nat[pos2]] = (int16_t)v2;
+        kk = (e2 & kFastEob) ? 64 : pos2 + 1;
+      }
+    }
     if (kk >= 64 || bad) {                           // block done: blocks are stored in decode order
       cb += 64;
       kk = 0;
