@@ -228,6 +228,10 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
 // (the block buffer is pre-zeroed).  Block ends read the next block's
 // component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 128;
+#ifndef BBX_EXTRA_SYMBOLS
+#define BBX_EXTRA_SYMBOLS 2
+#endif
+constexpr int kExtraSymbols = BBX_EXTRA_SYMBOLS;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
 template <typename T>
@@ -410,17 +414,20 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     if (v != 0 && !bad) cb[nat[pos]] = (int16_t)v;
     kk = (e & kFastEob) ? 64 : pos + 1;
     // a second AC symbol in the same iteration when the block continues, the bit
-    // buffer certainly holds it (>= 27 bits) and its code + value resolve in the
+    // buffer holds the 11-bit peek (a full entry consumes at most that) and its code + value resolve in the
     // fast table; otherwise it is left for the next iteration
-    if (kk < 64 && !bad && nb >= 27) {
-      const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
-      if ((e2 & (kFastValid | kFastFull)) == (kFastValid | kFastFull)) {
-        acc <<= (e2 >> 25) & 31;
-        nb -= (int)((e2 >> 25) & 31);
-        const int pos2 = kk + (int)((e2 >> 21) & 15);
-        const int v2 = (int)(int16_t)(e2 & 0xFFFF);
-        if (v2 != 0) cb[nat[pos2]] = (int16_t)v2;
-        kk = (e2 & kFastEob) ? 64 : pos2 + 1;
+#pragma unroll
+    for (int extra = 0; extra < kExtraSymbols; ++extra) {
+      if (kk < 64 && !bad && nb >= kJpegFastBits) {   // a full entry never reads past the 11-bit peek
+        const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
+        if ((e2 & (kFastValid | kFastFull)) == (kFastValid | kFastFull)) {
+          acc <<= (e2 >> 25) & 31;
+          nb -= (int)((e2 >> 25) & 31);
+          const int pos2 = kk + (int)((e2 >> 21) & 15);
+          const int v2 = (int)(int16_t)(e2 & 0xFFFF);
+          if (v2 != 0) cb[nat[pos2]] = (int16_t)v2;
+          kk = (e2 & kFastEob) ? 64 : pos2 + 1;
+        }
       }
     }
     if (kk >= 64 || bad) {                           // block done: blocks are stored in decode order
