@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
 // component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 128;
 #ifndef BBX_EXTRA_SYMBOLS
-#define BBX_EXTRA_SYMBOLS 2
+#define BBX_EXTRA_SYMBOLS 4
 #endif
 constexpr int kExtraSymbols = BBX_EXTRA_SYMBOLS;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
