@@ -19,6 +19,7 @@ world_size * batch_size positions by rank; `device`.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import os
 import threading
 import time
@@ -141,6 +142,27 @@ def _dist_info(config: LoaderConfig) -> tuple[int, int]:
     return rank, world
 
 
+def agree_seed(config: LoaderConfig, device: int | None = None) -> int:
+    """distributed=True: the one collective of the path -- at construction, every
+    rank adopts rank 0's seed (one broadcast), so all ranks compute the same global
+    order and per-sample parameters.  No collective runs per batch."""
+    if not config.distributed:
+        return config.seed
+    try:
+        import torch
+        import torch.distributed as dist
+    except Exception:
+        return config.seed
+    if not (dist.is_available() and dist.is_initialized()):
+        return config.seed
+    dev = "cpu"
+    if dist.get_backend() == "nccl":
+        dev = f"cuda:{device if device is not None else torch.cuda.current_device()}"
+    t = torch.tensor([config.seed & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=0)
+    return int(t.item())
+
+
 def _fits_pinned(nbytes: int, fraction: float) -> bool:
     try:
         ram = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
@@ -192,6 +214,12 @@ class Loader:
             self.device = int(os.environ["LOCAL_RANK"])
         else:
             self.device = torch.cuda.current_device()
+        if config.distributed:   # one-time seed agreement (the only cross-rank traffic)
+            seed = agree_seed(config, self.device)
+            if seed != config.seed:
+                config = dataclasses.replace(config, seed=seed)
+                self.config = config
+                self.order = TraversalOrder(config.order, config.seed)
 
         schema = self.dataset.schema
         wanted = config.fields

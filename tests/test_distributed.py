@@ -63,3 +63,32 @@ def test_gloo_two_ranks_partition_each_global_batch():
             if g < len(parts[r]):
                 union += parts[r][g]
         assert union == batch
+
+
+def _seed_worker(rank, world, port, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2306_12517_b200.loader import LoaderConfig, agree_seed
+
+        cfg = LoaderConfig(batch_size=4, distributed=True, seed=100 + rank)   # ranks disagree locally
+        result_q.put((rank, agree_seed(cfg)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_one_time_seed_agreement():
+    """distributed=True: every rank adopts rank 0's seed with one broadcast at
+    Loader construction (north_star: the only collective of the path)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: 100, 1: 100}
