@@ -260,6 +260,50 @@ JPEG_LEGS = {
 }
 
 
+CIFAR_SPEC = "flip:0.5|normalize:127.5,64"           # the reference's C1 chain
+
+
+def cifar_workload(args, device, rank, world, barrier, reduce_max):
+    """configs[0]: CIFAR-10-shaped .bbox (50k x 32x32x3 RAW + label), RandomFlip(0.5) +
+    Normalize(127.5, 64) -> f32 NHWC, batch 512, random order (the reference-pinned chain)."""
+    import paper_2306_12517_b200 as bx
+
+    path = DATA_DIR / "cifar32_raw_50000.bbox"
+    if rank == 0 and not path.exists():
+        DATA_DIR.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(".tmp")
+        bx.write_dataset(bx.SyntheticImageSource(50000, 32, 32, 3, seed=1), tmp, bx.WriterConfig(seed=1))
+        os.replace(tmp, path)
+    barrier()
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=B, chain=CIFAR_SPEC)
+    ld.set_profiling(True)
+    secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
+    st = ld.stats()
+    ld.shutdown()
+    ds.close()
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=B, chain=CIFAR_SPEC)
+    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
+    st2 = ld2.stats()
+    ld2.shutdown()
+    ds2.close()
+    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
+    out = {"workload": "configs[0]: CIFAR-10-shaped synthetic .bbox (50k x 32x32x3 RAW + IntField label), "
+                       "RandomFlip(0.5) + Normalize(127.5, 64) -> f32 NHWC, random order",
+           "batch_per_gpu": B, "num_samples": 50000,
+           "value": world * args.steps * B / secs, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
+           "device_ms_per_batch": st["kernel_seconds"] / max(st["batches"], 1) * 1e3,
+           "e2e": {"value": world * args.steps * B / e2e_secs, "unit": "images/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_secs / args.steps * 1e3},
+           "gpu_launches": int(st["kernel_launches"])}
+    if world == 1 and rank == 0:
+        try:
+            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 3, B, "flip + normalize -> f32",
+                                               spec="decode|" + CIFAR_SPEC)
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    return out
+
+
 def jpeg_workload(args, device, rank, world, barrier, reduce_max, leg="jpeg"):
     """configs[2..4] on the synthetic JPEG .bbox, batch 1024 per GPU: `value` with the
     compressed heap resident in HBM, `e2e` staging every batch from host RAM."""
@@ -347,8 +391,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--workloads", default="raw,jpeg,val,ndarray",
-                    help="raw (configs[1], the headline), jpeg (configs[2]), val (configs[3]), ndarray (configs[4])")
+    ap.add_argument("--workloads", default="raw,cifar,jpeg,val,ndarray",
+                    help="raw (configs[1], the headline), cifar (configs[0]), jpeg (configs[2]), val (configs[3]), "
+                         "ndarray (configs[4])")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -464,7 +509,12 @@ def main():
               "path": "Loader(OsCache(zero_copy=True)): pinned host heap -> PCIe reads inside K1 (no CPU gather, "
                       "no staging copy)"}
 
-    jpeg = {JPEG_LEGS[w][0]: jpeg_workload(args, device, rank, world, barrier, reduce_max, w) for w in legs} or None
+    jpeg = {}
+    if "cifar" in args.workloads.split(","):
+        jpeg["configs[0]"] = cifar_workload(args, device, rank, world, barrier, reduce_max)
+    for w in legs:
+        jpeg[JPEG_LEGS[w][0]] = jpeg_workload(args, device, rank, world, barrier, reduce_max, w)
+    jpeg = jpeg or None
 
     if rank != 0:
         if dist is not None:
