@@ -546,10 +546,8 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
   int* slot_row = reinterpret_cast<int*>(smem + cw_meta_off(P));
-  int* s_shift = slot_row + nslot;
-  int* row_a = s_shift + nslot;                   // row_a[R], row_b[R], row_wy[R]
-  int* row_b = row_a + P.rows_per_tile;
-  int* row_wy = row_b + P.rows_per_tile;
+  int* s_base = slot_row + nslot;                 // slot j's first byte in srcbuf (j * span_pad + shift)
+  uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);   // per tile row: packed taps (below)
   uint8_t* srcbuf = smem + cw_src_off(P);
 
   const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
@@ -557,8 +555,21 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
   const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
   const uint32_t* M = T + 4 + tab_owp(P) + (size_t)tile * tab_tm(P);
   const int nvalid = (int)M[0];
-  if (tid < nslot) { slot_row[tid] = (int)M[1 + tid]; s_shift[tid] = 0; }
-  if (tid < 3 * P.rows_per_tile) row_a[tid] = (int)M[1 + nslot + tid];
+  if (tid < nslot) { slot_row[tid] = (int)M[1 + tid]; s_base[tid] = tid * span_pad; }
+  if (tid < R) {
+    // Taps a, b of a row are consecutive slots (b == a at the bottom clamp), so
+    // one is even and one odd: the walker keeps one register set per slot
+    // parity and a row never moves between them.  Packed: bits 0..11 weight of
+    // the even slot, 12..21 even slot, 22..31 odd slot.  When b == a the other
+    // parity gets slot a ^ 1 with weight 0 (its bytes never reach the result).
+    const uint32_t a = M[1 + nslot + tid], b = M[1 + nslot + P.rows_per_tile + tid];
+    const uint32_t wy = M[1 + nslot + 2 * P.rows_per_tile + tid];
+    uint32_t e, o, we;
+    if (a == b) { e = (a & 1) ? a ^ 1 : a; o = (a & 1) ? a : a ^ 1; we = (a & 1) ? 0u : 2048u; }
+    else if (a & 1) { e = b; o = a; we = wy; }
+    else { e = a; o = b; we = 2048u - wy; }
+    rowpk[tid] = we | e << 12 | o << 22;
+  }
   if constexpr (kVal == VAL_LUT) {
     const uint4* g = reinterpret_cast<const uint4*>(A.lut);
     uint4* l4 = reinterpret_cast<uint4*>(lut);
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
       uint8_t* dst = srcbuf + (size_t)j * span_pad;
       const uint8_t* s0 = reinterpret_cast<const uint8_t*>(a0);
       for (int c = lane; c < n16; c += 32) *reinterpret_cast<uint4*>(dst + 16 * c) = ld_nc_v4(s0 + 16 * c);
-      if (lane == 0) s_shift[j] = shift;
+      if (lane == 0) s_base[j] = j * span_pad + shift;
     }
   }
   __syncthreads();
@@ -586,6 +597,7 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
   constexpr int NP = 2;
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const int rg = (R + groups - 1) / groups;
+  const size_t ostep = (size_t)OW * C;
   for (int item = tid; item < npair * groups; item += kThreads) {
     const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
     const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
@@ -600,54 +612,37 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
       w1[q] = (e >> 16) & 0xFFFu;
       w0[q] = 2048u - w1[q];
     }
-    int k0 = -1, k1 = -1;                          // slots whose sums are cached in h0 / h1
-    uint32_t h0[NP * C], h1[NP * C];
+    int tag_e = -1, tag_o = -1;                    // slots whose sums are in he / ho
+    uint32_t he[NP * C], ho[NP * C];
 #pragma unroll
-    for (int k = 0; k < NP * C; ++k) { h0[k] = 0; h1[k] = 0; }
+    for (int k = 0; k < NP * C; ++k) { he[k] = 0; ho[k] = 0; }
     auto hsum = [&](int j, uint32_t* hv) {
-      const uint8_t* row = srcbuf + j * span_pad + s_shift[j];
+      const uint8_t* row = srcbuf + s_base[j];
 #pragma unroll
       for (int q = 0; q < NP; ++q)
 #pragma unroll
         for (int k = 0; k < C; ++k) hv[q * C + k] = w0[q] * row[off0[q] + k] + w1[q] * row[off1[q] + k];
     };
     const bool full = ox0 + NP <= OW;
-    for (int r = ra0; r < ra1; ++r) {
-      const int a = row_a[r], b = row_b[r];
-      const uint32_t wy1 = (uint32_t)row_wy[r], wy0 = 2048u - wy1;
-      uint32_t ta[NP * C], tb[NP * C];
-      // a and b only move forward: reuse the previous row's sums where they match
-      if (a == k0) {
-#pragma unroll
-        for (int k = 0; k < NP * C; ++k) ta[k] = h0[k];
-      } else if (a == k1) {
-#pragma unroll
-        for (int k = 0; k < NP * C; ++k) ta[k] = h1[k];
-      } else {
-        hsum(a, ta);
-      }
-      if (b == a) {
-#pragma unroll
-        for (int k = 0; k < NP * C; ++k) tb[k] = ta[k];
-      } else if (b == k1) {
-#pragma unroll
-        for (int k = 0; k < NP * C; ++k) tb[k] = h1[k];
-      } else {
-        hsum(b, tb);
-      }
-#pragma unroll
-      for (int k = 0; k < NP * C; ++k) { h0[k] = ta[k]; h1[k] = tb[k]; }
-      k0 = a; k1 = b;
+    OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
+    // 16-bit outputs: every row of this thread is 4-byte aligned when the first is and OW is even
+    const bool vec = sizeof(OutT) == 2 && full && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+    for (int r = ra0; r < ra1; ++r, o += ostep) {
+      const uint32_t pk = rowpk[r];
+      const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
+      const uint32_t we = pk & 0xFFFu, wo = 2048u - we;
+      // taps only move forward: a slot's sums are recomputed when it changes
+      if (je != tag_e) { hsum(je, he); tag_e = je; }
+      if (jo != tag_o) { hsum(jo, ho); tag_o = jo; }
       OutT v[NP * C];
 #pragma unroll
       for (int k = 0; k < NP * C; ++k) {
-        const uint32_t u = (wy0 * ta[k] + wy1 * tb[k] + (1u << 21)) >> 22;
+        const uint32_t u = (we * he[k] + wo * ho[k] + (1u << 21)) >> 22;
         if constexpr (kVal == VAL_LUT) v[k] = lut[(k % C) * 256 + u];
         else v[k] = value_generic<OutT, kVal>(P, u, k % C);
       }
-      OutT* o = out + ((size_t)r * OW + ox0) * C;
       if constexpr (sizeof(OutT) == 2) {
-        if (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0) {
+        if (vec || (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
           uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
           for (int k = 0; k < NP * C / 2; ++k) {
