@@ -440,19 +440,25 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     P.cw = 0;
     const char* cwe = std::getenv("BBX_CW");
     if (P.src_kind == SRC_RESAMPLE && C == 3 && !(cwe && std::atoi(cwe) == 0)) {
-      PlanDev Q = P;
-      Q.rows_per_tile = std::min(16, H);
-      if (const char* e = std::getenv("BBX_CW_ROWS")) Q.rows_per_tile = std::max(1, std::min(std::atoi(e), H));
-      Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
-      Q.lay = img_layout_host(Q);
-      Q.tab_stride = image_tab_stride(Q);
-      Q.cw_smem = cw_smem_host(Q);
-      Q.cw_npair = (W + 1) / 2;
-      Q.cw_groups = std::max(1, std::min(Q.rows_per_tile, kThreads / Q.cw_npair));
-      const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
-      Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
-                       ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
-      if (Q.cw_smem <= 100 * 1024) { P = Q; P.cw = 1; }
+      // rows per tile: 16, fewer when two pipeline stages of source rows would
+      // not leave room for 2 CTAs per SM (nslot = 2 x rows <= 64)
+      int rows_env = 0;
+      if (const char* e = std::getenv("BBX_CW_ROWS")) rows_env = std::max(1, std::min(std::atoi(e), 32));
+      for (int rows : {16, 8, 4, 2}) {
+        PlanDev Q = P;
+        Q.rows_per_tile = std::min(rows_env ? rows_env : rows, H);
+        Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
+        Q.lay = img_layout_host(Q);
+        Q.tab_stride = image_tab_stride(Q);
+        Q.cw_smem = cw_smem_host(Q);
+        Q.cw_npair = (W + 1) / 2;
+        Q.cw_groups = std::max(1, std::min(Q.rows_per_tile, kThreads / Q.cw_npair));
+        const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
+        Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
+                         ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
+        if (Q.cw_smem <= 110 * 1024) { P = Q; P.cw = 1; break; }
+        if (rows_env) break;
+      }
     }
     if ((W + 3 * H) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "output too large for the device plan");
   }

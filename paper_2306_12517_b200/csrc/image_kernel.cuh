@@ -19,6 +19,9 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "bbx_internal.h"
 
@@ -515,60 +518,140 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 }
 
 // ------------------------------------------------------- K1 (column walker)
-// Bilinear decoders, 3 channels.  grid = (tiles_per_sample, count); a tile is
-// rows_per_tile output rows.  After the tile's source rows are staged (as K1),
-// thread x owns output column x and walks the rows: the 2-tap horizontal sums
-// of a source row are computed in registers when a row first appears (and kept
-// for the next output row that reuses it), then the vertical blend, the value
-// table and the store.  Same integer arithmetic as image_kernel (bit-identical).
+// Bilinear decoders, 3 channels.  Persistent CTAs walk the batch's tiles
+// (tile = rows_per_tile output rows of one sample; CTA b takes tiles b, b + G,
+// ...) through a two-stage shared-memory pipeline: while a CTA computes tile i
+// out of one stage, the source-row segments and column table of tile i + 1 are
+// already landing in the other, moved by the copy engine (cp.async.bulk, one
+// 1-D bulk copy per source row, completion counted in bytes on the stage's
+// mbarrier).  Warp 0 issues a stage's copies; every thread waits on its
+// mbarrier phase.
+// Compute: thread x owns output columns 2x, 2x + 1 and walks a run of the
+// tile's rows: the 2-tap horizontal sums of a source row are computed in
+// registers when a row first appears (and kept for the next output row that
+// reuses it), then the vertical blend, the value table and the store.  Same
+// integer arithmetic as image_kernel (bit-identical).
 __host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }
 __host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
 __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
   return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
 }
-__host__ __device__ inline int cw_meta_off(const PlanDev& P) { return cw_lut_bytes(P); }
-__host__ __device__ inline int cw_src_off(const PlanDev& P) {
-  return cw_meta_off(P) + align_up((2 * cw_nslot(P) + 3 * P.rows_per_tile) * 4, 16);
+__host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
+__host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16; }
+// stage: column table xt[owp] | s_base[nslot] | rowpk[rows_per_tile] | source rows (nslot x span_pad)
+__host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
+  return align_up((tab_owp(P) + cw_nslot(P) + P.rows_per_tile) * 4, 16);
 }
-__host__ __device__ inline int cw_smem_bytes(const PlanDev& P) { return cw_src_off(P) + cw_nslot(P) * cw_span_pad(P); }
+__host__ __device__ inline int cw_stage_bytes(const PlanDev& P) { return cw_stage_meta(P) + cw_nslot(P) * cw_span_pad(P); }
+__host__ __device__ inline int cw_smem_bytes(const PlanDev& P) { return cw_stage_off(P) + 2 * cw_stage_bytes(P); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* m, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned ends, size a multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
 
 template <typename OutT, int kVal>
 __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
-  constexpr int C = 3;
-  const int s = blockIdx.y;
-  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-  if (d->skip) return;
-  const int tile = blockIdx.x, r0 = tile * P.rows_per_tile;
-  const int R = min(P.rows_per_tile, P.out_h - r0);
-  if (R <= 0) return;
-  const int OW = P.out_w, tid = threadIdx.x, nslot = cw_nslot(P), span_pad = cw_span_pad(P);
-  const SrcRows S = src_rows_of(P, A, d, s);
+  constexpr int C = 3, NP = 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
+  const int nslot = cw_nslot(P), span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_stage_bytes(P);
+  const int total = A.count * tps, G = gridDim.x;
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
-  int* slot_row = reinterpret_cast<int*>(smem + cw_meta_off(P));
-  int* s_base = slot_row + nslot;                 // slot j's first byte in srcbuf (j * span_pad + shift)
-  uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);   // per tile row: packed taps (below)
-  uint8_t* srcbuf = smem + cw_src_off(P);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));
+  uint8_t* stages = smem + cw_stage_off(P);
 
-  const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
-  const int col_lo = (int)T[0], col_hi = (int)T[1];
-  const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
-  const uint32_t* M = T + 4 + tab_owp(P) + (size_t)tile * tab_tm(P);
-  const int nvalid = (int)M[0];
-  if (tid < nslot) { slot_row[tid] = (int)M[1 + tid]; s_base[tid] = tid * span_pad; }
-  if (tid < R) {
-    // Taps a, b of a row are consecutive slots (b == a at the bottom clamp), so
-    // one is even and one odd: the walker keeps one register set per slot
-    // parity and a row never moves between them.  Packed: bits 0..11 weight of
-    // the even slot, 12..21 even slot, 22..31 odd slot.  When b == a the other
-    // parity gets slot a ^ 1 with weight 0 (its bytes never reach the result).
-    const uint32_t a = M[1 + nslot + tid], b = M[1 + nslot + P.rows_per_tile + tid];
-    const uint32_t wy = M[1 + nslot + 2 * P.rows_per_tile + tid];
-    uint32_t e, o, we;
-    if (a == b) { e = (a & 1) ? a ^ 1 : a; o = (a & 1) ? a : a ^ 1; we = (a & 1) ? 0u : 2048u; }
-    else if (a & 1) { e = b; o = a; we = wy; }
-    else { e = a; o = b; we = 2048u - wy; }
-    rowpk[tid] = we | e << 12 | o << 22;
+  // warp 0: tile t's tables and source rows -> stage b (nslot <= 64)
+  auto fill = [&](int t, int b) {
+    uint8_t* st = stages + (size_t)b * sbytes;
+    uint32_t* xt = reinterpret_cast<uint32_t*>(st);
+    int* s_base = reinterpret_cast<int*>(xt + owp);
+    uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
+    uint8_t* srcbuf = st + meta;
+    const int s = t / tps, tile = t - s * tps;
+    const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+    const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
+    uint32_t nb[2] = {0, 0}, tx = 0;
+    const uint8_t* src0[2] = {nullptr, nullptr};
+    const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
+    if (!d->skip && R > 0) {
+      const SrcRows S = src_rows_of(P, A, d, s);
+      const int col_lo = (int)T[0], col_hi = (int)T[1];
+      const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+      const uint32_t* M = T + 4 + owp + (size_t)tile * tab_tm(P);
+      const int nvalid = (int)M[0];
+      if (lane < R) {
+        // Taps a, b of a row are consecutive slots (b == a at the bottom clamp),
+        // so one is even and one odd: the walker keeps one register set per
+        // slot parity and a row never moves between them.  Packed: bits 0..11
+        // weight of the even slot, 12..21 even slot, 22..31 odd slot.  When
+        // b == a the other parity gets slot a ^ 1 with weight 0.
+        const uint32_t ra = M[1 + nslot + lane], rb = M[1 + nslot + Rt + lane], wy = M[1 + nslot + 2 * Rt + lane];
+        uint32_t e, o, we;
+        if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
+        else if (ra & 1) { e = rb; o = ra; we = wy; }
+        else { e = ra; o = rb; we = 2048u - wy; }
+        rowpk[lane] = we | e << 12 | o << 22;
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int j = k * 32 + lane;
+        if (j < nslot) {
+          int base = j * span_pad;
+          const int srow = j < nvalid ? (int)M[1 + j] : -1;
+          if (srow >= 0 && span_bytes > 0) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C);
+            const uintptr_t a0 = a & ~(uintptr_t)15;
+            const int shift = (int)(a - a0);
+            nb[k] = (uint32_t)((shift + span_bytes + 15) & ~15);
+            src0[k] = reinterpret_cast<const uint8_t*>(a0);
+            base += shift;
+          }
+          s_base[j] = base;
+        }
+      }
+      tx = nb[0] + nb[1];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+      tx += (uint32_t)owp * 4;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive_tx(&mbar[b], tx);
+      if (tx) bulk_g2s(xt, T + 4, (uint32_t)owp * 4, &mbar[b]);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (nb[k]) bulk_g2s(srcbuf + (size_t)(k * 32 + lane) * span_pad, src0[k], nb[k], &mbar[b]);
+  };
+
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if ((int)blockIdx.x < total) fill(blockIdx.x, 0);
+    if ((int)blockIdx.x + G < total) fill(blockIdx.x + G, 1);
   }
   if constexpr (kVal == VAL_LUT) {
     const uint4* g = reinterpret_cast<const uint4*>(A.lut);
@@ -576,91 +659,107 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
     for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += kThreads) l4[i] = g[i];
   }
   __syncthreads();
-  {   // stage source row segments (warp per slot, 16-byte vectors)
-    const int lane = tid & 31, warp = tid >> 5;
-    for (int j = warp; j < nvalid; j += kThreads / 32) {
-      const int srow = slot_row[j];
-      if (srow < 0 || span_bytes == 0) continue;
-      const uint8_t* src = S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C;
-      const uintptr_t a = reinterpret_cast<uintptr_t>(src), a0 = a & ~(uintptr_t)15;
-      const int shift = (int)(a - a0), n16 = (shift + span_bytes + 15) >> 4;
-      uint8_t* dst = srcbuf + (size_t)j * span_pad;
-      const uint8_t* s0 = reinterpret_cast<const uint8_t*>(a0);
-      for (int c = lane; c < n16; c += 32) *reinterpret_cast<uint4*>(dst + 16 * c) = ld_nc_v4(s0 + 16 * c);
-      if (lane == 0) s_base[j] = j * span_pad + shift;
-    }
-  }
-  __syncthreads();
-  OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * OW * C;
-  // a thread owns 2 adjacent output columns (3 packed 32-bit stores for 16-bit
-  // outputs) and a contiguous run of the tile's rows
-  constexpr int NP = 2;
+
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
-  const int rg = (R + groups - 1) / groups;
   const size_t ostep = (size_t)OW * C;
-  for (int item = tid; item < npair * groups; item += kThreads) {
-    const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
-    const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
-    const int ox0 = pr * NP;
-    int off0[NP], off1[NP];
-    uint32_t w0[NP], w1[NP];
+  int it = 0;
+  for (int t = blockIdx.x; t < total; t += G, ++it) {
+    const int b = it & 1;
+    const uint8_t* st = stages + (size_t)b * sbytes;
+    const uint32_t* xt = reinterpret_cast<const uint32_t*>(st);
+    const int* s_base = reinterpret_cast<const int*>(xt + owp);
+    const uint32_t* rowpk = reinterpret_cast<const uint32_t*>(s_base + nslot);
+    const uint8_t* srcbuf = st + meta;
+    const int s = t / tps, tile = t - s * tps;
+    const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+    const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
+    mbar_wait(&mbar[b], (it >> 1) & 1);
+    if (!d->skip && R > 0) {
+      OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep;
+      const int rg = (R + groups - 1) / groups;
+      for (int item = tid; item < npair * groups; item += kThreads) {
+        const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
+        const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
+        const int ox0 = pr * NP;
+        int off0[NP], off1[NP];
+        uint32_t w0[NP], w1[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) {
-      const uint32_t e = __ldg(T + 4 + min(ox0 + q, OW - 1));
-      off0[q] = (int)(e & 0xFFFFu);
-      off1[q] = (e >> 28) ? off0[q] : off0[q] + C;
-      w1[q] = (e >> 16) & 0xFFFu;
-      w0[q] = 2048u - w1[q];
-    }
-    int tag_e = -1, tag_o = -1;                    // slots whose sums are in he / ho
-    uint32_t he[NP * C], ho[NP * C];
+        for (int q = 0; q < NP; ++q) {
+          const uint32_t e = xt[min(ox0 + q, OW - 1)];
+          off0[q] = (int)(e & 0xFFFFu);
+          off1[q] = (e >> 28) ? off0[q] : off0[q] + C;
+          w1[q] = (e >> 16) & 0xFFFu;
+          w0[q] = 2048u - w1[q];
+        }
+        int tag_e = -1, tag_o = -1;                    // slots whose sums are in he / ho
+        uint32_t he[NP * C], ho[NP * C];
 #pragma unroll
-    for (int k = 0; k < NP * C; ++k) { he[k] = 0; ho[k] = 0; }
-    auto hsum = [&](int j, uint32_t* hv) {
-      const uint8_t* row = srcbuf + s_base[j];
+        for (int k = 0; k < NP * C; ++k) { he[k] = 0; ho[k] = 0; }
+        auto hsum = [&](int j, uint32_t* hv) {
+          const uint8_t* row = srcbuf + s_base[j];
 #pragma unroll
-      for (int q = 0; q < NP; ++q)
+          for (int q = 0; q < NP; ++q)
 #pragma unroll
-        for (int k = 0; k < C; ++k) hv[q * C + k] = w0[q] * row[off0[q] + k] + w1[q] * row[off1[q] + k];
-    };
-    const bool full = ox0 + NP <= OW;
-    OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
-    // 16-bit outputs: every row of this thread is 4-byte aligned when the first is and OW is even
-    const bool vec = sizeof(OutT) == 2 && full && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
-    for (int r = ra0; r < ra1; ++r, o += ostep) {
-      const uint32_t pk = rowpk[r];
-      const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
-      const uint32_t we = pk & 0xFFFu, wo = 2048u - we;
-      // taps only move forward: a slot's sums are recomputed when it changes
-      if (je != tag_e) { hsum(je, he); tag_e = je; }
-      if (jo != tag_o) { hsum(jo, ho); tag_o = jo; }
-      OutT v[NP * C];
+            for (int k = 0; k < C; ++k) hv[q * C + k] = w0[q] * row[off0[q] + k] + w1[q] * row[off1[q] + k];
+        };
+        const bool full = ox0 + NP <= OW;
+        OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
+        // 16-bit outputs: every row of this thread is 4-byte aligned when the first is and OW is even
+        const bool vec = sizeof(OutT) == 2 && full && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+        for (int r = ra0; r < ra1; ++r, o += ostep) {
+          const uint32_t pk = rowpk[r];
+          const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
+          const uint32_t we = pk & 0xFFFu, wo = 2048u - we;
+          // taps only move forward: a slot's sums are recomputed when it changes
+          if (je != tag_e) { hsum(je, he); tag_e = je; }
+          if (jo != tag_o) { hsum(jo, ho); tag_o = jo; }
+          OutT v[NP * C];
 #pragma unroll
-      for (int k = 0; k < NP * C; ++k) {
-        const uint32_t u = (we * he[k] + wo * ho[k] + (1u << 21)) >> 22;
-        if constexpr (kVal == VAL_LUT) v[k] = lut[(k % C) * 256 + u];
-        else v[k] = value_generic<OutT, kVal>(P, u, k % C);
-      }
-      if constexpr (sizeof(OutT) == 2) {
-        if (vec || (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
-          uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
-#pragma unroll
-          for (int k = 0; k < NP * C / 2; ++k) {
-            uint16_t lo, hi;
-            memcpy(&lo, &v[2 * k], 2);
-            memcpy(&hi, &v[2 * k + 1], 2);
-            o32[k] = (uint32_t)lo | (uint32_t)hi << 16;
+          for (int k = 0; k < NP * C; ++k) {
+            const uint32_t u = (we * he[k] + wo * ho[k] + (1u << 21)) >> 22;
+            if constexpr (kVal == VAL_LUT) v[k] = lut[(k % C) * 256 + u];
+            else v[k] = value_generic<OutT, kVal>(P, u, k % C);
           }
-          continue;
+          if constexpr (sizeof(OutT) == 2) {
+            if (vec || (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
+              uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+              for (int k = 0; k < NP * C / 2; ++k) {
+                uint16_t lo, hi;
+                memcpy(&lo, &v[2 * k], 2);
+                memcpy(&hi, &v[2 * k + 1], 2);
+                o32[k] = (uint32_t)lo | (uint32_t)hi << 16;
+              }
+              continue;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < NP * C; ++k) if (full || k < C) o[k] = v[k];
         }
       }
-#pragma unroll
-      for (int k = 0; k < NP * C; ++k) if (full || k < C) o[k] = v[k];
     }
+    __syncthreads();                                   // stage b free again
+    if (warp == 0 && t + 2 * G < total) fill(t + 2 * G, b);
   }
 }
 
 // ------------------------------------------------------------ K1 dispatch
+// CTAs of a persistent kernel: SMs x resident CTAs per SM at this smem size
+// (cached per kernel; the device is fixed for the process's loaders).
+inline int persistent_ctas(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find({fn, smem});
+  if (it != cache.end()) return it->second;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+  const int n = std::max(1, sms) * std::max(1, per);
+  cache[{fn, smem}] = n;
+  return n;
+}
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
   if constexpr (kRes && kC == 3) {
@@ -671,7 +770,9 @@ static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) 
       pk<<<A.count, kThreads, tsm, st>>>(P, A);
       auto k = image_cw_kernel<OutT, kVal == VAL_LUT ? VAL_LUT : kVal>;
       if (P.cw_smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.cw_smem);
-      k<<<dim3(P.tiles_per_sample, A.count), kThreads, P.cw_smem, st>>>(P, A);
+      const int total = P.tiles_per_sample * A.count;
+      const int grid = std::min(total, persistent_ctas(reinterpret_cast<const void*>(k), P.cw_smem));
+      if (grid > 0) k<<<grid, kThreads, P.cw_smem, st>>>(P, A);
       return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
   }
