@@ -70,6 +70,7 @@ struct PlanDev {
   // tile's rows; no horizontal-pass buffer, so tiles are taller and CTAs smaller
   int32_t cw, cw_smem, cw_npair, cw_groups;
   uint32_t cw_magic;                       // ceil(2^32 / cw_npair) when exact for every item index
+  int32_t cw_warps;                        // compute warps per CTA (plus one copy-issuing warp)
   SmemLayout lay;
 };
 

@@ -452,7 +452,28 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
         Q.tab_stride = image_tab_stride(Q);
         Q.cw_smem = cw_smem_host(Q);
         Q.cw_npair = (W + 1) / 2;
-        Q.cw_groups = std::max(1, std::min(Q.rows_per_tile, kThreads / Q.cw_npair));
+        // items = column pairs x row groups; compute warps (<= 8) sized to the
+        // items so no warp idles at a tile: the fewest groups (longest row runs,
+        // most horizontal-sum reuse) that give >= 6 warps at >= 90 % lane use
+        {
+          int best_g = 1, best_w = 1;
+          double best_score = -1.0;
+          for (int g = 1; g <= Q.rows_per_tile; ++g) {
+            const int items = Q.cw_npair * g, w = std::min(8, (items + 31) / 32);
+            const int rounds = (items + 32 * w - 1) / (32 * w);
+            const double eff = (double)items / (rounds * 32.0 * w);
+            const bool ok = eff >= 0.9 && (w >= 6 || g == Q.rows_per_tile);
+            const double score = ok ? 2.0 : eff * std::min(1.0, w / 6.0);
+            if (score > best_score + 1e-9) { best_score = score; best_g = g; best_w = w; }
+            if (ok) break;
+          }
+          Q.cw_groups = best_g;
+          Q.cw_warps = best_w;
+          if (const char* e = std::getenv("BBX_CW_GROUPS")) {
+            Q.cw_groups = std::max(1, std::min(std::atoi(e), Q.rows_per_tile));
+            Q.cw_warps = std::min(8, (Q.cw_npair * Q.cw_groups + 31) / 32);
+          }
+        }
         const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
         Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
                          ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;

@@ -537,7 +537,7 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
   return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
-__host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16; }
+__host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 32; }
 // stage: column table xt[owp] | s_base[nslot] | rowpk[rows_per_tile] | source rows (nslot x span_pad)
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
   return align_up((tab_owp(P) + cw_nslot(P) + P.rows_per_tile) * 4, 16);
@@ -567,104 +567,111 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <typename OutT, int kVal>
-__global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
+__global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
   constexpr int C = 3, NP = 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncw = P.cw_warps, nct = ncw * 32;          // compute warps 0..ncw-1; warp ncw issues the copies
   const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
   const int nslot = cw_nslot(P), span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_stage_bytes(P);
   const int total = A.count * tps, G = gridDim.x;
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[2], empty[2]
+  uint64_t* empty = full + 2;
   uint8_t* stages = smem + cw_stage_off(P);
 
-  // warp 0: tile t's tables and source rows -> stage b (nslot <= 64)
-  auto fill = [&](int t, int b) {
-    uint8_t* st = stages + (size_t)b * sbytes;
-    uint32_t* xt = reinterpret_cast<uint32_t*>(st);
-    int* s_base = reinterpret_cast<int*>(xt + owp);
-    uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
-    uint8_t* srcbuf = st + meta;
-    const int s = t / tps, tile = t - s * tps;
-    const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-    const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-    uint32_t nb[2] = {0, 0}, tx = 0;
-    const uint8_t* src0[2] = {nullptr, nullptr};
-    const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
-    if (!d->skip && R > 0) {
-      const SrcRows S = src_rows_of(P, A, d, s);
-      const int col_lo = (int)T[0], col_hi = (int)T[1];
-      const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
-      const uint32_t* M = T + 4 + owp + (size_t)tile * tab_tm(P);
-      const int nvalid = (int)M[0];
-      if (lane < R) {
-        // Taps a, b of a row are consecutive slots (b == a at the bottom clamp),
-        // so one is even and one odd: the walker keeps one register set per
-        // slot parity and a row never moves between them.  Packed: bits 0..11
-        // weight of the even slot, 12..21 even slot, 22..31 odd slot.  When
-        // b == a the other parity gets slot a ^ 1 with weight 0.
-        const uint32_t ra = M[1 + nslot + lane], rb = M[1 + nslot + Rt + lane], wy = M[1 + nslot + 2 * Rt + lane];
-        uint32_t e, o, we;
-        if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
-        else if (ra & 1) { e = rb; o = ra; we = wy; }
-        else { e = ra; o = rb; we = 2048u - wy; }
-        rowpk[lane] = we | e << 12 | o << 22;
-      }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int j = k * 32 + lane;
-        if (j < nslot) {
-          int base = j * span_pad;
-          const int srow = j < nvalid ? (int)M[1 + j] : -1;
-          if (srow >= 0 && span_bytes > 0) {
-            const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C);
-            const uintptr_t a0 = a & ~(uintptr_t)15;
-            const int shift = (int)(a - a0);
-            nb[k] = (uint32_t)((shift + span_bytes + 15) & ~15);
-            src0[k] = reinterpret_cast<const uint8_t*>(a0);
-            base += shift;
-          }
-          s_base[j] = base;
-        }
-      }
-      tx = nb[0] + nb[1];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
-      tx += (uint32_t)owp * 4;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive_tx(&mbar[b], tx);
-      if (tx) bulk_g2s(xt, T + 4, (uint32_t)owp * 4, &mbar[b]);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      if (nb[k]) bulk_g2s(srcbuf + (size_t)(k * 32 + lane) * span_pad, src0[k], nb[k], &mbar[b]);
-  };
-
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], ncw);
+    mbar_init(&empty[1], ncw);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 0) {
-    if ((int)blockIdx.x < total) fill(blockIdx.x, 0);
-    if ((int)blockIdx.x + G < total) fill(blockIdx.x + G, 1);
   }
   if constexpr (kVal == VAL_LUT) {
     const uint4* g = reinterpret_cast<const uint4*>(A.lut);
     uint4* l4 = reinterpret_cast<uint4*>(lut);
-    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += kThreads) l4[i] = g[i];
+    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += blockDim.x) l4[i] = g[i];
   }
   __syncthreads();
 
+  if (warp == ncw) {
+    // ---- copy warp: tile t's tables and source rows -> stage b (nslot <= 64),
+    // once the compute warps have released the stage's previous tile
+    int k = 0;
+    for (int t = blockIdx.x; t < total; t += G, ++k) {
+      const int b = k & 1;
+      if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1);
+      uint8_t* st = stages + (size_t)b * sbytes;
+      uint32_t* xt = reinterpret_cast<uint32_t*>(st);
+      int* s_base = reinterpret_cast<int*>(xt + owp);
+      uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
+      uint8_t* srcbuf = st + meta;
+      const int s = t / tps, tile = t - s * tps;
+      const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+      const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
+      uint32_t nb[2] = {0, 0}, tx = 0;
+      const uint8_t* src0[2] = {nullptr, nullptr};
+      const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
+      if (!d->skip && R > 0) {
+        const SrcRows S = src_rows_of(P, A, d, s);
+        const int col_lo = (int)T[0], col_hi = (int)T[1];
+        const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+        const uint32_t* M = T + 4 + owp + (size_t)tile * tab_tm(P);
+        const int nvalid = (int)M[0];
+        if (lane < R) {
+          // Taps a, b of a row are consecutive slots (b == a at the bottom
+          // clamp), so one is even and one odd: the walker keeps one register
+          // set per slot parity and a row never moves between them.  Packed:
+          // bits 0..11 weight of the even slot, 12..21 even slot, 22..31 odd
+          // slot.  When b == a the other parity gets slot a ^ 1, weight 0.
+          const uint32_t ra = M[1 + nslot + lane], rb = M[1 + nslot + Rt + lane], wy = M[1 + nslot + 2 * Rt + lane];
+          uint32_t e, o, we;
+          if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
+          else if (ra & 1) { e = rb; o = ra; we = wy; }
+          else { e = ra; o = rb; we = 2048u - wy; }
+          rowpk[lane] = we | e << 12 | o << 22;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int j = q * 32 + lane;
+          if (j < nslot) {
+            int base = j * span_pad;
+            const int srow = j < nvalid ? (int)M[1 + j] : -1;
+            if (srow >= 0 && span_bytes > 0) {
+              const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C);
+              const uintptr_t a0 = a & ~(uintptr_t)15;
+              const int shift = (int)(a - a0);
+              nb[q] = (uint32_t)((shift + span_bytes + 15) & ~15);
+              src0[q] = reinterpret_cast<const uint8_t*>(a0);
+              base += shift;
+            }
+            s_base[j] = base;
+          }
+        }
+        tx = nb[0] + nb[1];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+        tx += (uint32_t)owp * 4;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&full[b], tx);
+        if (tx) bulk_g2s(xt, T + 4, (uint32_t)owp * 4, &full[b]);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (nb[q]) bulk_g2s(srcbuf + (size_t)(q * 32 + lane) * span_pad, src0[q], nb[q], &full[b]);
+    }
+    return;
+  }
+
+  // ---- compute warps
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
-  int it = 0;
-  for (int t = blockIdx.x; t < total; t += G, ++it) {
-    const int b = it & 1;
+  int k = 0;
+  for (int t = blockIdx.x; t < total; t += G, ++k) {
+    const int b = k & 1;
     const uint8_t* st = stages + (size_t)b * sbytes;
     const uint32_t* xt = reinterpret_cast<const uint32_t*>(st);
     const int* s_base = reinterpret_cast<const int*>(xt + owp);
@@ -673,11 +680,12 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
     const int s = t / tps, tile = t - s * tps;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-    mbar_wait(&mbar[b], (it >> 1) & 1);
-    if (!d->skip && R > 0) {
+    const bool live = !d->skip && R > 0;
+    mbar_wait(&full[b], (k >> 1) & 1);
+    if (live) {
       OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep;
       const int rg = (R + groups - 1) / groups;
-      for (int item = tid; item < npair * groups; item += kThreads) {
+      for (int item = tid; item < npair * groups; item += nct) {
         const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
         const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
         const int ox0 = pr * NP;
@@ -694,18 +702,18 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
         int tag_e = -1, tag_o = -1;                    // slots whose sums are in he / ho
         uint32_t he[NP * C], ho[NP * C];
 #pragma unroll
-        for (int k = 0; k < NP * C; ++k) { he[k] = 0; ho[k] = 0; }
+        for (int q = 0; q < NP * C; ++q) { he[q] = 0; ho[q] = 0; }
         auto hsum = [&](int j, uint32_t* hv) {
           const uint8_t* row = srcbuf + s_base[j];
 #pragma unroll
           for (int q = 0; q < NP; ++q)
 #pragma unroll
-            for (int k = 0; k < C; ++k) hv[q * C + k] = w0[q] * row[off0[q] + k] + w1[q] * row[off1[q] + k];
+            for (int c = 0; c < C; ++c) hv[q * C + c] = w0[q] * row[off0[q] + c] + w1[q] * row[off1[q] + c];
         };
-        const bool full = ox0 + NP <= OW;
+        const bool fullw = ox0 + NP <= OW;
         OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
         // 16-bit outputs: every row of this thread is 4-byte aligned when the first is and OW is even
-        const bool vec = sizeof(OutT) == 2 && full && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+        const bool vec = sizeof(OutT) == 2 && fullw && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
         for (int r = ra0; r < ra1; ++r, o += ostep) {
           const uint32_t pk = rowpk[r];
           const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
@@ -715,49 +723,50 @@ __global__ void __launch_bounds__(kThreads) image_cw_kernel(const PlanDev P, con
           if (jo != tag_o) { hsum(jo, ho); tag_o = jo; }
           OutT v[NP * C];
 #pragma unroll
-          for (int k = 0; k < NP * C; ++k) {
-            const uint32_t u = (we * he[k] + wo * ho[k] + (1u << 21)) >> 22;
-            if constexpr (kVal == VAL_LUT) v[k] = lut[(k % C) * 256 + u];
-            else v[k] = value_generic<OutT, kVal>(P, u, k % C);
+          for (int q = 0; q < NP * C; ++q) {
+            const uint32_t u = (we * he[q] + wo * ho[q] + (1u << 21)) >> 22;
+            if constexpr (kVal == VAL_LUT) v[q] = lut[(q % C) * 256 + u];
+            else v[q] = value_generic<OutT, kVal>(P, u, q % C);
           }
           if constexpr (sizeof(OutT) == 2) {
-            if (vec || (full && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
+            if (vec || (fullw && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
               uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
 #pragma unroll
-              for (int k = 0; k < NP * C / 2; ++k) {
+              for (int q = 0; q < NP * C / 2; ++q) {
                 uint16_t lo, hi;
-                memcpy(&lo, &v[2 * k], 2);
-                memcpy(&hi, &v[2 * k + 1], 2);
-                o32[k] = (uint32_t)lo | (uint32_t)hi << 16;
+                memcpy(&lo, &v[2 * q], 2);
+                memcpy(&hi, &v[2 * q + 1], 2);
+                o32[q] = (uint32_t)lo | (uint32_t)hi << 16;
               }
               continue;
             }
           }
 #pragma unroll
-          for (int k = 0; k < NP * C; ++k) if (full || k < C) o[k] = v[k];
+          for (int q = 0; q < NP * C; ++q) if (fullw || q < C) o[q] = v[q];
         }
       }
     }
-    __syncthreads();                                   // stage b free again
-    if (warp == 0 && t + 2 * G < total) fill(t + 2 * G, b);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
   }
 }
 
 // ------------------------------------------------------------ K1 dispatch
 // CTAs of a persistent kernel: SMs x resident CTAs per SM at this smem size
 // (cached per kernel; the device is fixed for the process's loaders).
-inline int persistent_ctas(const void* fn, int smem) {
+inline int persistent_ctas(const void* fn, int threads, int smem) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int> cache;
+  static std::map<std::pair<const void*, int64_t>, int> cache;
   std::lock_guard<std::mutex> g(mu);
-  auto it = cache.find({fn, smem});
+  const int64_t key = (int64_t)threads << 32 | smem;
+  auto it = cache.find({fn, key});
   if (it != cache.end()) return it->second;
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
   const int n = std::max(1, sms) * std::max(1, per);
-  cache[{fn, smem}] = n;
+  cache[{fn, key}] = n;
   return n;
 }
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
@@ -771,8 +780,9 @@ static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) 
       auto k = image_cw_kernel<OutT, kVal == VAL_LUT ? VAL_LUT : kVal>;
       if (P.cw_smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.cw_smem);
       const int total = P.tiles_per_sample * A.count;
-      const int grid = std::min(total, persistent_ctas(reinterpret_cast<const void*>(k), P.cw_smem));
-      if (grid > 0) k<<<grid, kThreads, P.cw_smem, st>>>(P, A);
+      const int threads = (P.cw_warps + 1) * 32;
+      const int grid = std::min(total, persistent_ctas(reinterpret_cast<const void*>(k), threads, P.cw_smem));
+      if (grid > 0) k<<<grid, threads, P.cw_smem, st>>>(P, A);
       return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
   }
