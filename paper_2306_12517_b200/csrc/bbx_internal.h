@@ -15,6 +15,7 @@ enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_LUT = 
 constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
 constexpr int kDescHeader = 32;     // bytes before the per-sample params
+constexpr int kCwCols = 2;          // column-walker K1: output columns per thread
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
@@ -71,6 +72,8 @@ struct PlanDev {
   int32_t cw, cw_smem, cw_npair, cw_groups;
   uint32_t cw_magic;                       // ceil(2^32 / cw_npair) when exact for every item index
   int32_t cw_warps;                        // compute warps per CTA (plus one copy-issuing warp)
+  int32_t cw_slots;                        // source rows one pipeline stage holds (even, <= 2 x rows_per_tile)
+  int32_t cw_rg;                           // rows per item of a full tile: ceil(rows_per_tile / cw_groups)
   SmemLayout lay;
 };
 

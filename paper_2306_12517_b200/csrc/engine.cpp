@@ -450,8 +450,21 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
         Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
         Q.lay = img_layout_host(Q);
         Q.tab_stride = image_tab_stride(Q);
+        {   // stage slots: source rows any tile can span.  Rows_per_tile output
+            // rows cover at most n canvas rows back through the y remaps, and n
+            // canvas rows at most ceil((n - 1) * crop / canvas) + 2 source rows
+            // (two taps) with crop <= the field's max height; the prologue then
+            // always takes its contiguous-range branch with <= that many slots.
+          int64_t n = Q.rows_per_tile;
+          for (int i = Q.n_remaps - 1; i >= 0; --i)
+            if (Q.remaps[i].kind == BBX_OP_RESIZE)
+              n = ((n - 1) * Q.remaps[i].in_h + Q.remaps[i].out_h - 1) / Q.remaps[i].out_h + 1;
+          const int64_t src = ((n - 1) * f.info.max_height + Q.canvas_h - 1) / Q.canvas_h + 2;
+          if (src > 64) { if (rows_env) break; continue; }
+          Q.cw_slots = (int)((src + 1) & ~1LL);
+        }
         Q.cw_smem = cw_smem_host(Q);
-        Q.cw_npair = (W + 1) / 2;
+        Q.cw_npair = (W + kCwCols - 1) / kCwCols;   // column groups
         // items = column pairs x row groups; compute warps (<= 8) sized to the
         // items so no warp idles at a tile: the fewest groups (longest row runs,
         // most horizontal-sum reuse) that give >= 6 warps at >= 90 % lane use
@@ -474,6 +487,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
             Q.cw_warps = std::min(8, (Q.cw_npair * Q.cw_groups + 31) / 32);
           }
         }
+        Q.cw_rg = (Q.rows_per_tile + Q.cw_groups - 1) / Q.cw_groups;
         const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
         Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
                          ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
@@ -1146,7 +1160,7 @@ static int process_slot(bbx_loader* L, int s) {
       }
     }
     if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    launches += pl.dev.src_kind == SRC_ARRAY ? 1 : 2;   // K1 = prologue + tiles
+    launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.cw) ? 1 : 2;   // K1 = prologue + tiles (column walker: one kernel)
   }
   if (prof) CK(cudaEventRecord(S.k1, L->comp_st));
   S.timed = prof;

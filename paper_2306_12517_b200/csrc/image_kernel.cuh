@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <map>
+#include <type_traits>
 #include <mutex>
 
 #include "bbx_internal.h"
@@ -520,30 +521,35 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 // ------------------------------------------------------- K1 (column walker)
 // Bilinear decoders, 3 channels.  Persistent CTAs walk the batch's tiles
 // (tile = rows_per_tile output rows of one sample; CTA b takes tiles b, b + G,
-// ...) through a two-stage shared-memory pipeline: while a CTA computes tile i
-// out of one stage, the source-row segments and column table of tile i + 1 are
+// ...) through a two-stage shared-memory pipeline: while the compute warps
+// work on tile i out of one stage, the source-row segments of tile i + 1 are
 // already landing in the other, moved by the copy engine (cp.async.bulk, one
 // 1-D bulk copy per source row, completion counted in bytes on the stage's
-// mbarrier).  Warp 0 issues a stage's copies; every thread waits on its
-// mbarrier phase.
+// "full" mbarrier).  A dedicated copy warp computes each tile's geometry
+// (column table, source-row range, row taps) into the stage, issues its
+// copies once the compute warps have released the stage ("empty" mbarrier),
+// and runs ahead by one tile.
 // Compute: thread x owns output columns 2x, 2x + 1 and walks a run of the
 // tile's rows: the 2-tap horizontal sums of a source row are computed in
 // registers when a row first appears (and kept for the next output row that
 // reuses it), then the vertical blend, the value table and the store.  Same
 // integer arithmetic as image_kernel (bit-identical).
-__host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }
+__host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }   // table slots
 __host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
 __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
   return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 32; }
-// stage: column table xt[owp] | s_base[nslot] | rowpk[rows_per_tile] | source rows (nslot x span_pad)
+// geometry ring (3 entries): column table xt[owp] | s_base[cw_slots] | rowpk[rows_per_tile];
+// source-row stages (2): cw_slots x span_pad
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
-  return align_up((tab_owp(P) + cw_nslot(P) + P.rows_per_tile) * 4, 16);
+  return align_up((tab_owp(P) + P.cw_slots + P.rows_per_tile) * 4, 16);
 }
-__host__ __device__ inline int cw_stage_bytes(const PlanDev& P) { return cw_stage_meta(P) + cw_nslot(P) * cw_span_pad(P); }
-__host__ __device__ inline int cw_smem_bytes(const PlanDev& P) { return cw_stage_off(P) + 2 * cw_stage_bytes(P); }
+__host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
+__host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
+  return cw_stage_off(P) + 3 * cw_stage_meta(P) + 2 * cw_src_stage(P);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
@@ -568,17 +574,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <typename OutT, int kVal>
 __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
-  constexpr int C = 3, NP = 2;
+  constexpr int C = 3, NP = kCwCols;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = P.cw_warps, nct = ncw * 32;          // compute warps 0..ncw-1; warp ncw issues the copies
   const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
-  const int nslot = cw_nslot(P), span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_stage_bytes(P);
+  // nslot: source-row slots a stage holds (the host proves every tile's
+  // contiguous row range fits)
+  const int nslot = P.cw_slots, span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
   const int total = A.count * tps, G = gridDim.x;
+  const int gs = G / tps, gt = G - gs * tps;           // grid stride in (sample, tile)
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[2], empty[2]
   uint64_t* empty = full + 2;
-  uint8_t* stages = smem + cw_stage_off(P);
+  uint8_t* metas = smem + cw_stage_off(P);              // geometry ring: tile k uses entry k % 3
+  uint8_t* stages = metas + 3 * meta;                   // source rows: tile k uses stage k & 1
 
   if (tid == 0) {
     mbar_init(&full[0], 1);
@@ -595,40 +605,59 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   __syncthreads();
 
   if (warp == ncw) {
-    // ---- copy warp: tile t's tables and source rows -> stage b (nslot <= 64),
-    // once the compute warps have released the stage's previous tile
-    int k = 0;
-    for (int t = blockIdx.x; t < total; t += G, ++k) {
+    // ---- copy warp: tile k's geometry -> ring entry k % 3 (free: iteration
+    // k - 1 waited for tile k - 3), then, once the compute warps have
+    // released tile k - 2's stage, its source rows -> stage k & 1 (nslot <= 64)
+    int k = 0, m = 0, s = blockIdx.x / tps, tile = blockIdx.x - s * tps;
+    for (int t = blockIdx.x; t < total; t += G, ++k, s += gs, tile += gt, m = m == 2 ? 0 : m + 1) {
+      if (tile >= tps) { tile -= tps; ++s; }
       const int b = k & 1;
-      if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1);
-      uint8_t* st = stages + (size_t)b * sbytes;
-      uint32_t* xt = reinterpret_cast<uint32_t*>(st);
-      int* s_base = reinterpret_cast<int*>(xt + owp);
-      uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
-      uint8_t* srcbuf = st + meta;
-      const int s = t / tps, tile = t - s * tps;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
       uint32_t nb[2] = {0, 0}, tx = 0;
       const uint8_t* src0[2] = {nullptr, nullptr};
-      const uint32_t* T = A.tables + (size_t)s * P.tab_stride;
       if (!d->skip && R > 0) {
+        // what sample_tables_kernel computes for the other K1 variants
+        uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta);
+        int* s_base = reinterpret_cast<int*>(xt + owp);
+        uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
+        const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
-        const int col_lo = (int)T[0], col_hi = (int)T[1];
+        const int top = prm[0], left = prm[1], ch = prm[2], cwd = prm[3], sh = S.sh;
+        const int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
+        int a0, a1, aw, b0, b1, bw;   // the composed maps are monotone: the end columns span the range
+        lin_axis(min(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, a0, a1, aw);
+        lin_axis(max(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, b0, b1, bw);
+        const int col_lo = (left + a0) >> sh, col_hi = (left + b1) >> sh;
         const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
-        const uint32_t* M = T + 4 + owp + (size_t)tile * tab_tm(P);
-        const int nvalid = (int)M[0];
+        for (int ox = lane; ox < OW; ox += 32) {
+          int x0, x1, wx;
+          lin_axis(back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
+          const int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
+          xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+        }
+        int ya = 0, yb = 0, wy = 0;
+        if (lane < R) {
+          int y0, y1;
+          lin_axis(back_y(P, prm, r0 + lane), P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
+          ya = (top + y0) >> sh;
+          yb = (top + y1) >> sh;
+        }
+        // rows [lo, hi] are contiguous and at most nslot of them (host bound,
+        // engine.cpp plan_compile: cw_slots)
+        const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
+        const int nvalid = min(hi - lo + 1, nslot);
         if (lane < R) {
           // Taps a, b of a row are consecutive slots (b == a at the bottom
           // clamp), so one is even and one odd: the walker keeps one register
           // set per slot parity and a row never moves between them.  Packed:
           // bits 0..11 weight of the even slot, 12..21 even slot, 22..31 odd
           // slot.  When b == a the other parity gets slot a ^ 1, weight 0.
-          const uint32_t ra = M[1 + nslot + lane], rb = M[1 + nslot + Rt + lane], wy = M[1 + nslot + 2 * Rt + lane];
+          const uint32_t ra = (uint32_t)(ya - lo), rb = (uint32_t)(yb - lo);
           uint32_t e, o, we;
           if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
-          else if (ra & 1) { e = rb; o = ra; we = wy; }
-          else { e = ra; o = rb; we = 2048u - wy; }
+          else if (ra & 1) { e = rb; o = ra; we = (uint32_t)wy; }
+          else { e = ra; o = rb; we = 2048u - (uint32_t)wy; }
           rowpk[lane] = we | e << 12 | o << 22;
         }
 #pragma unroll
@@ -636,13 +665,13 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
           const int j = q * 32 + lane;
           if (j < nslot) {
             int base = j * span_pad;
-            const int srow = j < nvalid ? (int)M[1 + j] : -1;
+            const int srow = (j < nvalid && lo + j < S.rows) ? lo + j : -1;
             if (srow >= 0 && span_bytes > 0) {
               const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C);
-              const uintptr_t a0 = a & ~(uintptr_t)15;
-              const int shift = (int)(a - a0);
+              const uintptr_t al = a & ~(uintptr_t)15;
+              const int shift = (int)(a - al);
               nb[q] = (uint32_t)((shift + span_bytes + 15) & ~15);
-              src0[q] = reinterpret_cast<const uint8_t*>(a0);
+              src0[q] = reinterpret_cast<const uint8_t*>(al);
               base += shift;
             }
             s_base[j] = base;
@@ -651,13 +680,13 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         tx = nb[0] + nb[1];
 #pragma unroll
         for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
-        tx += (uint32_t)owp * 4;
       }
+      if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1);
+      uint8_t* srcbuf = stages + (size_t)b * sbytes;
       __syncwarp();
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(&full[b], tx);
-        if (tx) bulk_g2s(xt, T + 4, (uint32_t)owp * 4, &full[b]);
       }
 #pragma unroll
       for (int q = 0; q < 2; ++q)
@@ -669,22 +698,21 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   // ---- compute warps
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
-  int k = 0;
-  for (int t = blockIdx.x; t < total; t += G, ++k) {
+  int k = 0, m = 0, s = blockIdx.x / tps, tile = blockIdx.x - s * tps;
+  for (int t = blockIdx.x; t < total; t += G, ++k, s += gs, tile += gt, m = m == 2 ? 0 : m + 1) {
+    if (tile >= tps) { tile -= tps; ++s; }
     const int b = k & 1;
-    const uint8_t* st = stages + (size_t)b * sbytes;
-    const uint32_t* xt = reinterpret_cast<const uint32_t*>(st);
+    const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
     const int* s_base = reinterpret_cast<const int*>(xt + owp);
     const uint32_t* rowpk = reinterpret_cast<const uint32_t*>(s_base + nslot);
-    const uint8_t* srcbuf = st + meta;
-    const int s = t / tps, tile = t - s * tps;
+    const uint8_t* srcbuf = stages + (size_t)b * sbytes;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
     const bool live = !d->skip && R > 0;
     mbar_wait(&full[b], (k >> 1) & 1);
     if (live) {
       OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep;
-      const int rg = (R + groups - 1) / groups;
+      const int rg = R == Rt ? P.cw_rg : (R + groups - 1) / groups;
       for (int item = tid; item < npair * groups; item += nct) {
         const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
         const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
@@ -712,8 +740,11 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         };
         const bool fullw = ox0 + NP <= OW;
         OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
-        // 16-bit outputs: every row of this thread is 4-byte aligned when the first is and OW is even
-        const bool vec = sizeof(OutT) == 2 && fullw && (OW & 1) == 0 && (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+        // NP pixels = 3 x NP values: three aligned stores of NP values each when
+        // every row of this thread starts on an NP-pixel boundary (OW % NP == 0)
+        constexpr int kVB = NP * (int)sizeof(OutT);
+        const bool vec = fullw && OW % NP == 0 && (reinterpret_cast<uintptr_t>(o) & (kVB - 1)) == 0;
+        const int nval = fullw ? NP * C : (OW - ox0) * C;
         for (int r = ra0; r < ra1; ++r, o += ostep) {
           const uint32_t pk = rowpk[r];
           const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
@@ -728,21 +759,18 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
             if constexpr (kVal == VAL_LUT) v[q] = lut[(q % C) * 256 + u];
             else v[q] = value_generic<OutT, kVal>(P, u, q % C);
           }
-          if constexpr (sizeof(OutT) == 2) {
-            if (vec || (fullw && (reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
-              uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+          if (vec) {
+            using VT = typename std::conditional<kVB == 2, uint16_t, typename std::conditional<kVB == 4, uint32_t,
+                       typename std::conditional<kVB == 8, uint2, uint4>::type>::type>::type;
+            VT wv[3];
+            memcpy(wv, v, sizeof v);
+            VT* p = reinterpret_cast<VT*>(o);
 #pragma unroll
-              for (int q = 0; q < NP * C / 2; ++q) {
-                uint16_t lo, hi;
-                memcpy(&lo, &v[2 * q], 2);
-                memcpy(&hi, &v[2 * q + 1], 2);
-                o32[q] = (uint32_t)lo | (uint32_t)hi << 16;
-              }
-              continue;
-            }
+            for (int q = 0; q < 3; ++q) p[q] = wv[q];
+            continue;
           }
 #pragma unroll
-          for (int q = 0; q < NP * C; ++q) if (fullw || q < C) o[q] = v[q];
+          for (int q = 0; q < NP * C; ++q) if (q < nval) o[q] = v[q];
         }
       }
     }
@@ -772,11 +800,7 @@ inline int persistent_ctas(const void* fn, int threads, int smem) {
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
   if constexpr (kRes && kC == 3) {
-    if (P.cw) {
-      auto pk = sample_tables_kernel<kRes>;
-      int tsm = (P.out_w + 3 * P.out_h) * 4;
-      if (tsm > 48 * 1024) cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm);
-      pk<<<A.count, kThreads, tsm, st>>>(P, A);
+    if (P.cw) {   // the copy warp computes the geometry: no prologue launch
       auto k = image_cw_kernel<OutT, kVal == VAL_LUT ? VAL_LUT : kVal>;
       if (P.cw_smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.cw_smem);
       const int total = P.tiles_per_sample * A.count;
