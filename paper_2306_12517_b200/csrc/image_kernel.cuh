@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 
 // ------------------------------------------------------- K1 (column walker)
 // Bilinear decoders, 3 channels.  Persistent CTAs walk the batch's tiles
-// (tile = rows_per_tile output rows of one sample; CTA b takes tiles b, b + G,
-// ...) through a two-stage shared-memory pipeline: while the compute warps
+// (tile = rows_per_tile output rows of one sample; CTA b takes a run of
+// consecutive tiles) through a two-stage shared-memory pipeline: while the compute warps
 // work on tile i out of one stage, the source-row segments of tile i + 1 are
 // already landing in the other, moved by the copy engine (cp.async.bulk, one
 // 1-D bulk copy per source row, completion counted in bytes on the stage's
@@ -582,7 +582,8 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   // contiguous row range fits)
   const int nslot = P.cw_slots, span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
   const int total = A.count * tps, G = gridDim.x;
-  const int gs = G / tps, gt = G - gs * tps;           // grid stride in (sample, tile)
+  // CTA b takes the consecutive tiles [t_begin, t_end) (balanced to one tile)
+  const int t_begin = (int)((int64_t)blockIdx.x * total / G), t_end = (int)((int64_t)(blockIdx.x + 1) * total / G);
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[2], empty[2]
@@ -608,9 +609,10 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
     // ---- copy warp: tile k's geometry -> ring entry k % 3 (free: iteration
     // k - 1 waited for tile k - 3), then, once the compute warps have
     // released tile k - 2's stage, its source rows -> stage k & 1 (nslot <= 64)
-    int k = 0, m = 0, s = blockIdx.x / tps, tile = blockIdx.x - s * tps;
-    for (int t = blockIdx.x; t < total; t += G, ++k, s += gs, tile += gt, m = m == 2 ? 0 : m + 1) {
-      if (tile >= tps) { tile -= tps; ++s; }
+    int k = 0, m = 0, s = t_begin / tps, tile = t_begin - s * tps;
+    int cur_s = -1, prev_m = 0, col_lo = 0, span_bytes = 0;   // the column table of sample cur_s sits in entry prev_m
+    for (int t = t_begin; t < t_end; ++t, ++k, m = m == 2 ? 0 : m + 1) {
+      if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
       const int b = k & 1;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
@@ -623,19 +625,28 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
         const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
-        const int top = prm[0], left = prm[1], ch = prm[2], cwd = prm[3], sh = S.sh;
-        const int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
-        int a0, a1, aw, b0, b1, bw;   // the composed maps are monotone: the end columns span the range
-        lin_axis(min(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, a0, a1, aw);
-        lin_axis(max(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, b0, b1, bw);
-        const int col_lo = (left + a0) >> sh, col_hi = (left + b1) >> sh;
-        const int span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
-        for (int ox = lane; ox < OW; ox += 32) {
-          int x0, x1, wx;
-          lin_axis(back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
-          const int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
-          xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+        const int top = prm[0], ch = prm[2], sh = S.sh;
+        if (s != cur_s) {   // a CTA's tiles are consecutive: the column table is built once per sample
+          const int left = prm[1], cwd = prm[3];
+          const int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
+          int a0, a1, aw, b0, b1, bw;   // the composed maps are monotone: the end columns span the range
+          lin_axis(min(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, a0, a1, aw);
+          lin_axis(max(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, b0, b1, bw);
+          col_lo = (left + a0) >> sh;
+          const int col_hi = (left + b1) >> sh;
+          span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+          for (int ox = lane; ox < OW; ox += 32) {
+            int x0, x1, wx;
+            lin_axis(back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
+            const int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
+            xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+          }
+          cur_s = s;
+        } else if (m != prev_m) {
+          const uint32_t* xp = reinterpret_cast<const uint32_t*>(metas + prev_m * meta);
+          for (int ox = lane; ox < OW; ox += 32) xt[ox] = xp[ox];
         }
+        prev_m = m;
         int ya = 0, yb = 0, wy = 0;
         if (lane < R) {
           int y0, y1;
@@ -698,9 +709,9 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   // ---- compute warps
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
-  int k = 0, m = 0, s = blockIdx.x / tps, tile = blockIdx.x - s * tps;
-  for (int t = blockIdx.x; t < total; t += G, ++k, s += gs, tile += gt, m = m == 2 ? 0 : m + 1) {
-    if (tile >= tps) { tile -= tps; ++s; }
+  int k = 0, m = 0, s = t_begin / tps, tile = t_begin - s * tps;
+  for (int t = t_begin; t < t_end; ++t, ++k, m = m == 2 ? 0 : m + 1) {
+    if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
     const int b = k & 1;
     const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
     const int* s_base = reinterpret_cast<const int*>(xt + owp);
