@@ -541,10 +541,10 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 32; }
-// geometry ring (3 entries): column table xt[owp] | s_base[cw_slots] | rowpk[rows_per_tile];
+// geometry ring (3 entries): column table xt[owp] | s_base[cw_slots] | rowtap[rows_per_tile] (uint2);
 // source-row stages (2): cw_slots x span_pad
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
-  return align_up((tab_owp(P) + P.cw_slots + P.rows_per_tile) * 4, 16);
+  return align_up((tab_owp(P) + P.cw_slots + 2 * P.rows_per_tile) * 4, 16);
 }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         // what sample_tables_kernel computes for the other K1 variants
         uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta);
         int* s_base = reinterpret_cast<int*>(xt + owp);
-        uint32_t* rowpk = reinterpret_cast<uint32_t*>(s_base + nslot);
+        uint2* rowtap = reinterpret_cast<uint2*>(s_base + nslot);
         const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
         const int top = prm[0], ch = prm[2], sh = S.sh;
@@ -658,19 +658,6 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         // engine.cpp plan_compile: cw_slots)
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
         const int nvalid = min(hi - lo + 1, nslot);
-        if (lane < R) {
-          // Taps a, b of a row are consecutive slots (b == a at the bottom
-          // clamp), so one is even and one odd: the walker keeps one register
-          // set per slot parity and a row never moves between them.  Packed:
-          // bits 0..11 weight of the even slot, 12..21 even slot, 22..31 odd
-          // slot.  When b == a the other parity gets slot a ^ 1, weight 0.
-          const uint32_t ra = (uint32_t)(ya - lo), rb = (uint32_t)(yb - lo);
-          uint32_t e, o, we;
-          if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
-          else if (ra & 1) { e = rb; o = ra; we = (uint32_t)wy; }
-          else { e = ra; o = rb; we = 2048u - (uint32_t)wy; }
-          rowpk[lane] = we | e << 12 | o << 22;
-        }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int j = q * 32 + lane;
@@ -687,6 +674,21 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
             }
             s_base[j] = base;
           }
+        }
+        __syncwarp();
+        if (lane < R) {
+          // Taps a, b of a row are consecutive slots (b == a at the bottom
+          // clamp), so one is even and one odd: the walker keeps one register
+          // set per slot parity and a row never moves between them.  When
+          // b == a the other parity gets slot a ^ 1 with weight 0.  Stored:
+          // x = byte base of the even slot's row | its weight << 20, y = byte
+          // base of the odd slot's row (bases identify slots: the walker's tags).
+          const uint32_t ra = (uint32_t)(ya - lo), rb = (uint32_t)(yb - lo);
+          uint32_t e, o, we;
+          if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
+          else if (ra & 1) { e = rb; o = ra; we = (uint32_t)wy; }
+          else { e = ra; o = rb; we = 2048u - (uint32_t)wy; }
+          rowtap[lane] = make_uint2((uint32_t)s_base[e] | we << 20, (uint32_t)s_base[o]);
         }
         tx = nb[0] + nb[1];
 #pragma unroll
@@ -714,8 +716,7 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
     if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
     const int b = k & 1;
     const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
-    const int* s_base = reinterpret_cast<const int*>(xt + owp);
-    const uint32_t* rowpk = reinterpret_cast<const uint32_t*>(s_base + nslot);
+    const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp + nslot);
     const uint8_t* srcbuf = stages + (size_t)b * sbytes;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
@@ -738,12 +739,12 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
           w1[q] = (e >> 16) & 0xFFFu;
           w0[q] = 2048u - w1[q];
         }
-        int tag_e = -1, tag_o = -1;                    // slots whose sums are in he / ho
+        uint32_t tag_e = ~0u, tag_o = ~0u;             // rows (byte bases) whose sums are in he / ho
         uint32_t he[NP * C], ho[NP * C];
 #pragma unroll
         for (int q = 0; q < NP * C; ++q) { he[q] = 0; ho[q] = 0; }
-        auto hsum = [&](int j, uint32_t* hv) {
-          const uint8_t* row = srcbuf + s_base[j];
+        auto hsum = [&](uint32_t base, uint32_t* hv) {
+          const uint8_t* row = srcbuf + base;
 #pragma unroll
           for (int q = 0; q < NP; ++q)
 #pragma unroll
@@ -756,13 +757,14 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         constexpr int kVB = NP * (int)sizeof(OutT);
         const bool vec = fullw && OW % NP == 0 && (reinterpret_cast<uintptr_t>(o) & (kVB - 1)) == 0;
         const int nval = fullw ? NP * C : (OW - ox0) * C;
+        uint2 tn = rowtap[ra0];
         for (int r = ra0; r < ra1; ++r, o += ostep) {
-          const uint32_t pk = rowpk[r];
-          const int je = (int)((pk >> 12) & 0x3FFu), jo = (int)(pk >> 22);
-          const uint32_t we = pk & 0xFFFu, wo = 2048u - we;
-          // taps only move forward: a slot's sums are recomputed when it changes
-          if (je != tag_e) { hsum(je, he); tag_e = je; }
-          if (jo != tag_o) { hsum(jo, ho); tag_o = jo; }
+          const uint2 tp = tn;
+          if (r + 1 < ra1) tn = rowtap[r + 1];         // next row's taps, one row ahead
+          const uint32_t be = tp.x & 0xFFFFFu, bo = tp.y, we = tp.x >> 20, wo = 2048u - we;
+          // taps only move forward: a parity's sums are recomputed when its row changes
+          if (be != tag_e) { hsum(be, he); tag_e = be; }
+          if (bo != tag_o) { hsum(bo, ho); tag_o = bo; }
           OutT v[NP * C];
 #pragma unroll
           for (int q = 0; q < NP * C; ++q) {
@@ -775,9 +777,14 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
                        typename std::conditional<kVB == 8, uint2, uint4>::type>::type>::type;
             VT wv[3];
             memcpy(wv, v, sizeof v);
-            VT* p = reinterpret_cast<VT*>(o);
+            if constexpr (kVB == 4) {   // one asm block: three live source registers, no reuse hazard between the stores
+              asm volatile("st.global.b32 [%0], %1;\n\tst.global.b32 [%0+4], %2;\n\tst.global.b32 [%0+8], %3;"
+                           ::"l"(o), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]));
+            } else {
+              VT* p = reinterpret_cast<VT*>(o);
 #pragma unroll
-            for (int q = 0; q < 3; ++q) p[q] = wv[q];
+              for (int q = 0; q < 3; ++q) p[q] = wv[q];
+            }
             continue;
           }
 #pragma unroll
