@@ -64,6 +64,10 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
+    lib_path = Path(os.environ.get("BBX_LIB", LIB_PATH))   # BBX_LIB: load another build (kernel experiments)
+    if lib_path != LIB_PATH:
+        L = ctypes.CDLL(str(lib_path))
+        return _bind(L)
     if os.environ.get("BBX_NO_BUILD") != "1":
         from . import _build
         try:
@@ -73,7 +77,11 @@ def lib():
                 raise E.DeviceError(f"libbbx.so is missing and could not be built: {e}") from e
     if not LIB_PATH.exists():
         raise E.DeviceError(f"libbbx.so not found at {LIB_PATH}; run __graft_entry__.build()")
-    L = ctypes.CDLL(str(LIB_PATH))
+    return _bind(ctypes.CDLL(str(LIB_PATH)))
+
+
+def _bind(L):
+    global _lib
     P = ctypes.POINTER
     sig = {
         "bbx_last_error": (ctypes.c_char_p, []),
