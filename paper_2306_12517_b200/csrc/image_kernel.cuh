@@ -541,10 +541,10 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 32; }
-// geometry ring (3 entries): column table xt[owp] | s_base[cw_slots] | rowtap[rows_per_tile] (uint2);
-// source-row stages (2): cw_slots x span_pad
+// geometry ring (3 entries): column table xt[owp] | rowtap[rows_per_tile] (uint2);
+// source-row stages (2): cw_slots x span_pad (whole rows at the image's row stride)
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
-  return align_up((tab_owp(P) + P.cw_slots + 2 * P.rows_per_tile) * 4, 16);
+  return align_up((tab_owp(P) + 2 * P.rows_per_tile) * 4, 16);
 }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
   // nslot: source-row slots a stage holds (the host proves every tile's
   // contiguous row range fits)
-  const int nslot = P.cw_slots, span_pad = cw_span_pad(P), meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
+  const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
   const int total = A.count * tps, G = gridDim.x;
   // CTA b takes the consecutive tiles [t_begin, t_end) (balanced to one tile)
   const int t_begin = (int)((int64_t)blockIdx.x * total / G), t_end = (int)((int64_t)(blockIdx.x + 1) * total / G);
@@ -621,13 +621,12 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
       const int b = k & 1;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-      uint32_t nb[2] = {0, 0}, tx = 0;
-      const uint8_t* src0[2] = {nullptr, nullptr};
+      uint32_t tx = 0;
+      const uint8_t* src = nullptr;
       if (!d->skip && R > 0) {
         // what sample_tables_kernel computes for the other K1 variants
         uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta);
-        int* s_base = reinterpret_cast<int*>(xt + owp);
-        uint2* rowtap = reinterpret_cast<uint2*>(s_base + nslot);
+        uint2* rowtap = reinterpret_cast<uint2*>(xt + owp);
         const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
         const int top = prm[0], ch = prm[2], sh = S.sh;
@@ -663,24 +662,17 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         // engine.cpp plan_compile: cw_slots)
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
         const int nvalid = min(hi - lo + 1, nslot);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int j = q * 32 + lane;
-          if (j < nslot) {
-            int base = j * span_pad;
-            const int srow = (j < nvalid && lo + j < S.rows) ? lo + j : -1;
-            if (srow >= 0 && span_bytes > 0) {
-              const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)srow * S.rstride + (int64_t)col_lo * C);
-              const uintptr_t al = a & ~(uintptr_t)15;
-              const int shift = (int)(a - al);
-              nb[q] = (uint32_t)((shift + span_bytes + 15) & ~15);
-              src0[q] = reinterpret_cast<const uint8_t*>(al);
-              base += shift;
-            }
-            s_base[j] = base;
-          }
+        // the tile's source rows [lo, lo + ncopy) are consecutive rows of one
+        // row-strided image: ONE bulk copy of whole rows (16-byte aligned
+        // ends), row j at byte j * rstride + shift of the stage
+        const int ncopy = max(0, min(nvalid, S.rows - lo));
+        const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)lo * S.rstride);
+        const uintptr_t al = a & ~(uintptr_t)15;
+        const uint32_t rstr = (uint32_t)S.rstride, base0 = (uint32_t)(a - al) + (uint32_t)(col_lo * C);
+        if (span_bytes > 0 && ncopy > 0) {
+          tx = (uint32_t)(((a - al) + (uint64_t)ncopy * rstr + 15) & ~(uint64_t)15);
+          src = reinterpret_cast<const uint8_t*>(al);
         }
-        __syncwarp();
         if (lane < R) {
           // Taps a, b of a row are consecutive slots (b == a at the bottom
           // clamp), so one is even and one odd: the walker keeps one register
@@ -693,11 +685,8 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
           if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
           else if (ra & 1) { e = rb; o = ra; we = (uint32_t)wy; }
           else { e = ra; o = rb; we = 2048u - (uint32_t)wy; }
-          rowtap[lane] = make_uint2((uint32_t)s_base[e] | we << 20, (uint32_t)s_base[o]);
+          rowtap[lane] = make_uint2((base0 + e * rstr) | we << 20, base0 + o * rstr);
         }
-        tx = nb[0] + nb[1];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
       }
       if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1);
       uint8_t* srcbuf = stages + (size_t)b * sbytes;
@@ -705,10 +694,8 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(&full[b], tx);
+        if (tx) bulk_g2s(srcbuf, src, tx, &full[b]);
       }
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (nb[q]) bulk_g2s(srcbuf + (size_t)(q * 32 + lane) * span_pad, src0[q], nb[q], &full[b]);
     }
     return;
   }
@@ -721,13 +708,18 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
     if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
     const int b = k & 1;
     const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
-    const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp + nslot);
+    const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp);
     const uint8_t* srcbuf = stages + (size_t)b * sbytes;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
     const bool live = !d->skip && R > 0;
     mbar_wait(&full[b], (k >> 1) & 1);
+#ifdef BBX_EXP_NOCOMPUTE
+    if (live && srcbuf[tid] == 0x7f && xt[0] == 0x12345u) static_cast<uint8_t*>(A.out)[0] = 1;   // keep the copies observable
+    if (false) {
+#else
     if (live) {
+#endif
       OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep;
       const int rg = R == Rt ? P.cw_rg : (R + groups - 1) / groups;
       for (int item = tid; item < npair * groups; item += nct) {
