@@ -663,14 +663,15 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
         const int nvalid = min(hi - lo + 1, nslot);
         // the tile's source rows [lo, lo + ncopy) are consecutive rows of one
-        // row-strided image: ONE bulk copy of whole rows (16-byte aligned
-        // ends), row j at byte j * rstride + shift of the stage
+        // row-strided image: ONE bulk copy (16-byte aligned ends) from column
+        // col_lo of row lo to column col_hi of the last row; row j's column
+        // col_lo lands at byte j * rstride + shift of the stage
         const int ncopy = max(0, min(nvalid, S.rows - lo));
-        const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)lo * S.rstride);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)lo * S.rstride + (int64_t)col_lo * C);
         const uintptr_t al = a & ~(uintptr_t)15;
-        const uint32_t rstr = (uint32_t)S.rstride, base0 = (uint32_t)(a - al) + (uint32_t)(col_lo * C);
+        const uint32_t rstr = (uint32_t)S.rstride, base0 = (uint32_t)(a - al);
         if (span_bytes > 0 && ncopy > 0) {
-          tx = (uint32_t)(((a - al) + (uint64_t)ncopy * rstr + 15) & ~(uint64_t)15);
+          tx = (uint32_t)((base0 + (uint64_t)(ncopy - 1) * rstr + span_bytes + 15) & ~(uint64_t)15);
           src = reinterpret_cast<const uint8_t*>(al);
         }
         if (lane < R) {
