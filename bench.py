@@ -535,7 +535,7 @@ def main():
         "e2e_zero_copy": e2e_zc,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": load_traffic(),
-                     "kernel": "image_kernel<half, resample> (K1)", "kernel_us": kern_s * 1e6,
+                     "kernel": "image_cw_kernel<half, 3> (K1: persistent column walker, bulk-copy pipeline)", "kernel_us": kern_s * 1e6,
                      "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src},
         "gpu_launches": int(st["kernel_launches"]),
         "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
