@@ -45,6 +45,7 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
 //   pass 2: an exclusive scan over the warps gives each warp its start cursor,
 //   pass 3: every warp replays its chunks and writes bytes / interval bounds.
 constexpr int kUnstuffWarps = 8;
+constexpr int kUnstuffBuf = 1024;                  // per-warp output window of pass 3 (bytes)
 constexpr uint32_t kAlignMask = kJpegIntAlign - 1;
 
 __device__ __forceinline__ uint32_t align_int(uint32_t x) { return (x + kAlignMask) & ~kAlignMask; }
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
   __shared__ CursorFn s_fn[kUnstuffWarps];
   __shared__ uint32_t s_nr[kUnstuffWarps], s_x[kUnstuffWarps], s_k[kUnstuffWarps];
   __shared__ int s_bad;
+  __shared__ __align__(16) uint8_t s_ob[kUnstuffWarps][kUnstuffBuf];
   const uint8_t* base = A.payload + sdesc(A, s)->src;
   uint8_t* out = A.bits + J.bs_base;
   uint32_t* st = A.istart + J.int_base;
@@ -181,9 +183,14 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
   }
   __syncthreads();
   if (A.status[s].kind != 0) return;
-  // pass 3: replay, writing bytes and interval bounds
+  // pass 3: replay, writing bytes and interval bounds.  A round's output (the
+  // warp's 512 input bytes minus stuffing, plus restart padding) is assembled
+  // in a zeroed shared-memory window aligned like the output, then written
+  // with 16-byte stores (byte stores only at the two partial edge chunks);
+  // a round too large for the window writes straight to global.
   uint32_t xw = s_x[warp], kw = s_k[warp];
   bool seq_bad = false;
+  uint8_t* ob = s_ob[warp];
   for (uint32_t r = 0; r < rounds; ++r) {
     const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
     const uint32_t nr = __popc(M.rst);
@@ -193,7 +200,16 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
     CursorFn exc{__shfl_up_sync(0xffffffffu, inc.aligned, 1), __shfl_up_sync(0xffffffffu, inc.a, 1),
                  __shfl_up_sync(0xffffffffu, inc.c, 1)};
     if (lane == 0) exc = CursorFn{0u, 0u, 0u};
+    const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
+                       __shfl_sync(0xffffffffu, inc.c, 31)};
+    const uint32_t xe = apply(all, xw), wb = xw & ~kAlignMask;   // round output [xw, xe); window base
     uint32_t x = apply(exc, xw), k = kw + nr_incl - nr;
+    const bool staged = xe - wb <= (uint32_t)kUnstuffBuf;
+    if (staged) {
+      for (uint32_t c = lane; c < (xe - wb + 15) / 16; c += 32) reinterpret_cast<uint4*>(ob)[c] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    uint8_t* dst = staged ? ob - wb : out;           // byte x of the output goes to dst[x]
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (M.rst >> j & 1) {                          // interval k ends: zero tail, next one starts aligned
@@ -202,15 +218,24 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
         const uint32_t nx = align_int(x) + kJpegIntPad;
         en[k] = x;
         st[k + 1] = nx;
-        for (uint32_t z = x; z < nx; ++z) out[z] = 0;
+        if (!staged) for (uint32_t z = x; z < nx; ++z) out[z] = 0;
         x = nx;
         ++k;
       }
-      if (M.keep >> j & 1) out[x++] = (uint8_t)(M.w[j >> 2] >> ((j & 3) * 8));
+      if (M.keep >> j & 1) dst[x++] = (uint8_t)(M.w[j >> 2] >> ((j & 3) * 8));
     }
-    const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
-                       __shfl_sync(0xffffffffu, inc.c, 31)};
-    xw = apply(all, xw);
+    if (staged) {
+      __syncwarp();
+      const uint32_t h1 = min(align_int(xw), xe), t0 = max(xe & ~kAlignMask, h1);
+      for (uint32_t c = align_int(xw) / 16 + lane; c < t0 / 16; c += 32)   // whole chunks
+        reinterpret_cast<uint4*>(out)[c] = reinterpret_cast<const uint4*>(ob)[c - wb / 16];
+      if (lane < 16) {                               // partial edge chunks
+        if (xw + lane < h1) out[xw + lane] = ob[xw + lane - wb];
+        if (t0 + lane < xe) out[t0 + lane] = ob[t0 + lane - wb];
+      }
+      __syncwarp();
+    }
+    xw = xe;
     kw += __shfl_sync(0xffffffffu, nr_incl, 31);
   }
   if (__any_sync(0xffffffffu, seq_bad) && lane == 0) A.status[s].kind = JST_MARKER_SEQ;
