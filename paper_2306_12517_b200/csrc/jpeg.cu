@@ -511,7 +511,7 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
   int w[64];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
-    const uint4 cv = ld_nc_v4(src + r), qv = __ldg(q4 + r);
+    const uint4 cv = __ldg(src + r), qv = __ldg(q4 + r);   // L1-allocating: the 8 loads share 4 lines
     const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
