@@ -1361,6 +1361,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (const char* e = std::getenv("BBX_JPEG_ROI")) L->jpeg_roi = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (const char* e = std::getenv("BBX_STAGING_THREADS")) if (staging_threads <= 0) nt = std::max(1, std::atoi(e));
   L->pool = std::make_unique<Pool>(nt);
   if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&L->comp_st, cudaStreamNonBlocking)) != cudaSuccess)
