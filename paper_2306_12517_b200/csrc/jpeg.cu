@@ -672,31 +672,62 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
     const uint8_t* cbp = sP[1].p;
     const uint8_t* crp = sP[2].p;
     const int ypw = sP[0].pw, cpw = sP[1].pw, dw = sP[1].dw, dh = sP[1].dh;
-    for (int t = threadIdx.x; t < n; t += kColorThreads) {
-      const int yy = t / no, q = t - yy * no + q_lo, y = y_lo + yy, x0 = 8 * q;
-      const uint2 y8 = __ldg(reinterpret_cast<const uint2*>(yp + (size_t)y * ypw + x0));
+    const int lane = threadIdx.x & 31;
+    // item t = (row yy, octet q): consecutive threads take consecutive octets of a
+    // row, so a chroma word's edge neighbours come from the adjacent lanes
+    int yy = threadIdx.x / no, qq = threadIdx.x - yy * no;
+    const int dyy = kColorThreads / no, dqq = kColorThreads - dyy * no;
+    for (int t = threadIdx.x; __any_sync(0xffffffffu, t < n); t += kColorThreads) {
+      const bool act = t < n;
+      const int q = qq + q_lo, y = y_lo + yy, x0 = 8 * q;
       const int i = y >> 1, i1 = (y & 1) ? min(i + 1, dh - 1) : max(i - 1, 0), j0 = 4 * q;
       const int ja = max(j0 - 1, 0), je = min(j0 + 4, dw - 1);
+      const bool whole = j0 + 4 <= dw;
+      uint2 y8 = make_uint2(0, 0);
+      uint32_t w4[4] = {0, 0, 0, 0};                 // Cb row i, Cb row i1, Cr row i, Cr row i1 (bytes j0 .. j0+3)
+      if (act) {
+        y8 = __ldg(reinterpret_cast<const uint2*>(yp + (size_t)y * ypw + x0));
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const uint8_t* ra = (c ? crp : cbp) + (size_t)i * cpw;
+          const uint8_t* rb = (c ? crp : cbp) + (size_t)i1 * cpw;
+          if (whole) {
+            w4[2 * c] = __ldg(reinterpret_cast<const uint32_t*>(ra + j0));
+            w4[2 * c + 1] = __ldg(reinterpret_cast<const uint32_t*>(rb + j0));
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int jj = min(j0 + k, dw - 1);
+              w4[2 * c] |= (uint32_t)__ldg(ra + jj) << (8 * k);
+              w4[2 * c + 1] |= (uint32_t)__ldg(rb + jj) << (8 * k);
+            }
+          }
+        }
+      }
+      // neighbours' words: lane - 1 holds octet q - 1 of the same row when tl == t - 1 etc.
+      const int tl = __shfl_up_sync(0xffffffffu, t, 1), tr = __shfl_down_sync(0xffffffffu, t, 1);
+      uint32_t wl[4], wr[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        wl[k] = __shfl_up_sync(0xffffffffu, w4[k], 1);
+        wr[k] = __shfl_down_sync(0xffffffffu, w4[k], 1);
+      }
+      if (!act) { yy += dyy; qq += dqq; if (qq >= no) { qq -= no; ++yy; } continue; }
+      const bool left_ok = lane > 0 && tl == t - 1 && qq > 0, right_ok = lane < 31 && tr == t + 1 && qq + 1 < no && whole;
       int u[2][8];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {                  // chroma columns j0-1 .. j0+4 (edge-clamped)
         const uint8_t* ra = (c ? crp : cbp) + (size_t)i * cpw;
         const uint8_t* rb = (c ? crp : cbp) + (size_t)i1 * cpw;
+        const uint32_t a4 = w4[2 * c], b4 = w4[2 * c + 1];
         int cs[6];
-        cs[0] = 3 * __ldg(ra + ja) + __ldg(rb + ja);
-        cs[5] = 3 * __ldg(ra + je) + __ldg(rb + je);
-        if (j0 + 4 <= dw) {
-          const uint32_t a4 = __ldg(reinterpret_cast<const uint32_t*>(ra + j0));
-          const uint32_t b4 = __ldg(reinterpret_cast<const uint32_t*>(rb + j0));
+        if (j0 == 0) cs[0] = 3 * (int)(a4 & 0xFF) + (int)(b4 & 0xFF);
+        else if (left_ok) cs[0] = 3 * (int)(wl[2 * c] >> 24) + (int)(wl[2 * c + 1] >> 24);
+        else cs[0] = 3 * __ldg(ra + ja) + __ldg(rb + ja);
+        if (right_ok && j0 + 4 < dw) cs[5] = 3 * (int)(wr[2 * c] & 0xFF) + (int)(wr[2 * c + 1] & 0xFF);
+        else cs[5] = 3 * __ldg(ra + je) + __ldg(rb + je);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) cs[1 + k] = 3 * (int)((a4 >> (8 * k)) & 0xFF) + (int)((b4 >> (8 * k)) & 0xFF);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int jj = min(j0 + k, dw - 1);
-            cs[1 + k] = 3 * __ldg(ra + jj) + __ldg(rb + jj);
-          }
-        }
+        for (int k = 0; k < 4; ++k) cs[1 + k] = 3 * (int)((a4 >> (8 * k)) & 0xFF) + (int)((b4 >> (8 * k)) & 0xFF);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           u[c][2 * k] = ((3 * cs[1 + k] + cs[k] + 8) >> 4) - 128;
@@ -710,6 +741,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
         px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
       }
       store_px(out + ((size_t)y * w + x0) * 3, px, 3 * min(8, w - x0));
+      yy += dyy; qq += dqq; if (qq >= no) { qq -= no; ++yy; }
     }
     return;
   }
