@@ -162,6 +162,8 @@ struct Slot {
   SampleStatus* d_status = nullptr;
   SampleStatus* h_status = nullptr;
   cudaEvent_t h2d_done{}, done{}, release{};
+  cudaEvent_t h2d_t{};             // profiling: timed copy of h2d_done
+  bool h2d_timed = false;
   cudaEvent_t k0{}, k1{};          // profiling: around the transform kernels
   bool timed = false;
   int64_t timed_launches = 0, timed_bytes = 0;
@@ -215,6 +217,7 @@ struct bbx_loader {
   JpegTables jt;
   bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
   bool jpeg_roi = true;               // decode only the MCUs a sample's chain reads (BBX_JPEG_ROI=0: whole image)
+  bool jpeg_prefetch = true;          // parse every sample's header at finalize (file fits in RAM; BBX_JPEG_PREFETCH=0: lazily)
   bool zero_copy = false;             // requested: kernels read payloads from the pinned host heap
   const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
   bool zc = false;                    // payload_dev is host memory (zero-copy)
@@ -230,6 +233,8 @@ struct bbx_loader {
   bool stop = false;
   bbx_loader_stats stats{};
   bool profiling = false;
+  cudaEvent_t t_ref{};               // profiling: reference for absolute batch times (idle gaps)
+  float last_k1_ms = -1.f;
   std::mutex stats_mu;
 };
 
@@ -663,27 +668,30 @@ static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h = 14695981039346656
   for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 1099511628211ull;
   return h;
 }
-static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, bool is_ac, int* id) {
-  uint8_t key[1 + 16 + 256];
-  key[0] = is_ac ? 'A' : 'D';
-  std::memcpy(key + 1, h.counts, 16);
-  std::memcpy(key + 17, h.vals, h.nvals);
-  const size_t n = 17 + h.nvals;
-  const uint64_t hv = fnv1a(key, n);
-  for (auto [it, end] = T.hmap.equal_range(hv); it != end; ++it) {
-    const auto& k = T.hkey[it->second];
-    if (k.size() == n && !std::memcmp(k.data(), key, n)) { *id = it->second; return 0; }
+// Table keys and hashes are built outside the registry lock; the lock covers
+// only the lookup (and, for a table never seen before, its registration).
+struct HuffKey { uint8_t key[1 + 16 + 256]; size_t n; uint64_t hv; };
+static void huff_key(const JpegHeader::Huff& h, bool is_ac, HuffKey* k) {
+  k->key[0] = is_ac ? 'A' : 'D';
+  std::memcpy(k->key + 1, h.counts, 16);
+  std::memcpy(k->key + 17, h.vals, h.nvals);
+  k->n = 17 + h.nvals;
+  k->hv = fnv1a(k->key, k->n);
+}
+static int jpeg_table_id(JpegTables& T, const JpegHeader::Huff& h, bool is_ac, const HuffKey& k, int* id) {
+  for (auto [it, end] = T.hmap.equal_range(k.hv); it != end; ++it) {
+    const auto& e = T.hkey[it->second];
+    if (e.size() == k.n && !std::memcmp(e.data(), k.key, k.n)) { *id = it->second; return 0; }
   }
   if (T.n_huff >= kJpegMaxHuff) return 2;
   if (!jpeg_build_huff(h, is_ac, &T.h_huff[T.n_huff])) return 1;
-  T.hkey.emplace_back(key, key + n);
-  T.hmap.emplace(hv, T.n_huff);
+  T.hkey.emplace_back(k.key, k.key + k.n);
+  T.hmap.emplace(k.hv, T.n_huff);
   *id = T.n_huff++;
   return 0;
 }
-static int jpeg_quant_id(JpegTables& T, const JpegHeader::Quant& q, int* id) {
+static int jpeg_quant_id(JpegTables& T, const JpegHeader::Quant& q, uint64_t hv, int* id) {
   const uint8_t* key = reinterpret_cast<const uint8_t*>(q.q);
-  const uint64_t hv = fnv1a(key, sizeof q.q);
   for (auto [it, end] = T.qmap.equal_range(hv); it != end; ++it)
     if (!std::memcmp(T.qkey[it->second].data(), key, sizeof q.q)) { *id = it->second; return 0; }
   if (T.n_quant >= kJpegMaxQuant) return 2;
@@ -721,16 +729,29 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
   uint32_t blocks = 0;
   int mcu_off = 0;
   JpegTables& T = L->jt;
+  HuffKey kd[3], ka[3];
+  uint64_t kq[3];
+  for (int i = 0; i < H.ncomp; ++i) {
+    const auto& c = H.comp[i];
+    huff_key(H.dc[c.td], false, &kd[i]);
+    huff_key(H.ac[c.ta], true, &ka[i]);
+    kq[i] = fnv1a(reinterpret_cast<const uint8_t*>(H.qt[c.tq].q), sizeof H.qt[c.tq].q);
+  }
+  int ids[3][3];
+  {
+    std::lock_guard<std::mutex> g(T.mu);
+    for (int i = 0; i < H.ncomp; ++i) {
+      const auto& c = H.comp[i];
+      int r;
+      if ((r = jpeg_table_id(T, H.dc[c.td], false, kd[i], &ids[i][0])) ||
+          (r = jpeg_table_id(T, H.ac[c.ta], true, ka[i], &ids[i][1])) || (r = jpeg_quant_id(T, H.qt[c.tq], kq[i], &ids[i][2])))
+        return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
+    }
+  }
   for (int i = 0; i < H.ncomp; ++i) {
     const auto& c = H.comp[i];
     JComp& o = J->comp[i];
-    int dc, ac, q, r;
-    {
-      std::lock_guard<std::mutex> g(T.mu);
-      if ((r = jpeg_table_id(T, H.dc[c.td], false, &dc)) || (r = jpeg_table_id(T, H.ac[c.ta], true, &ac)) ||
-          (r = jpeg_quant_id(T, H.qt[c.tq], &q)))
-        return bad(r == 2 ? "jpeg: too many distinct tables for the device table pool" : "jpeg: bad Huffman table");
-    }
+    const int dc = ids[i][0], ac = ids[i][1], q = ids[i][2];
     o.dc = (uint16_t)dc; o.ac = (uint16_t)ac; o.q = (uint16_t)q;
     o.h = (uint8_t)c.h; o.v = (uint8_t)c.v;
     o.bw = (uint16_t)(H.ncomp == 1 ? mx : mx * c.h);
@@ -849,6 +870,32 @@ static int finalize(bbx_loader* L) {
     CK(cudaHostAlloc(&T.h_quant, sizeof(JQuant) * kJpegMaxQuant, cudaHostAllocDefault));
     CK(cudaMalloc(&T.d_huff, sizeof(JHuff) * kJpegMaxHuff));
     CK(cudaMalloc(&T.d_quant, sizeof(JQuant) * kJpegMaxQuant));
+  }
+  // Every sample's JPEG header, parsed once up front on the pool when the file
+  // sits comfortably in RAM (reading the headers touches every sample): the
+  // first epoch's batches then cost what later ones do.  Samples whose header
+  // does not parse stay uncached and report their error in their batch.
+  if (any_jpeg && L->jpeg_cache && L->jpeg_prefetch) {
+    const bbx_dataset* ds = L->ds;
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    if ((double)ds->map_len < 0.25 * (double)pages * (double)psz) {
+      for (auto& pl : L->plans) {
+        if (pl.scalar || !pl.field_has_jpeg) continue;
+        const Field& f = ds->fields[pl.field_index];
+        L->pool->parallel_for(ds->num_samples, [&](int64_t i) {
+          const ImageCell c = image_cell(ds, i, f);
+          if (c.codec != CODEC_JPEG || c.length > 0xFFFFFFFFull || c.offset + c.length > ds->map_len) return;
+          SampleDesc d{};
+          d.h = (uint16_t)c.h; d.w = (uint16_t)c.w; d.c = (uint8_t)c.c;
+          JpegDesc J;
+          HostErr e;
+          if (jpeg_prepare(L, pl, ds->map + c.offset, (uint32_t)c.length, &d, &J, e, 0, 0)) {
+            pl.jcache[i] = J;
+            pl.jcached[i] = 1;
+          }
+        });
+      }
+    }
   }
   // Page-lock the mmap'd file once per dataset so the copy engine reads
   // payloads straight out of the page cache (no CPU gather).  Only when the
@@ -1087,6 +1134,12 @@ static int process_slot(bbx_loader* L, int s) {
     CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
   }
   CK(cudaEventRecord(S.h2d_done, L->copy_st));
+  S.h2d_timed = false;
+  if (L->profiling) {
+    if (!S.h2d_t) CK(cudaEventCreate(&S.h2d_t));
+    CK(cudaEventRecord(S.h2d_t, L->copy_st));
+    S.h2d_timed = true;
+  }
   CK(cudaStreamWaitEvent(L->comp_st, S.h2d_done, 0));
   bool wait_release;
   {
@@ -1098,6 +1151,10 @@ static int process_slot(bbx_loader* L, int s) {
   int launches = 0;
   const bool prof = L->profiling;
   int64_t kbytes = 0, klaunch = 0;
+  if (prof && !L->t_ref) {
+    CK(cudaEventCreate(&L->t_ref));
+    CK(cudaEventRecord(L->t_ref, L->comp_st));
+  }
   if (prof) CK(cudaEventRecord(S.k0, L->comp_st));
   int64_t d2h = 0;
   bool any_rle = false, any_jpeg = false;
@@ -1359,6 +1416,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (const char* e = std::getenv("BBX_DMA")) L->dma_allowed = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_JPEG_CACHE")) L->jpeg_cache = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_JPEG_ROI")) L->jpeg_roi = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BBX_JPEG_PREFETCH")) L->jpeg_prefetch = std::atoi(e) != 0;
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   if (const char* e = std::getenv("BBX_STAGING_THREADS")) if (staging_threads <= 0) nt = std::max(1, std::atoi(e));
@@ -1461,6 +1519,17 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
     if (e == cudaSuccess && S.timed) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, S.k0, S.k1) == cudaSuccess) {
+        float a0 = 0.f, a1 = 0.f;   // absolute k0 / k1 against the loader's reference event
+        if (L->t_ref && cudaEventElapsedTime(&a0, L->t_ref, S.k0) == cudaSuccess &&
+            cudaEventElapsedTime(&a1, L->t_ref, S.k1) == cudaSuccess) {
+          if (L->last_k1_ms >= 0.f && a0 > L->last_k1_ms) {
+            L->stats.gap_seconds += (a0 - L->last_k1_ms) * 1e-3;
+            float ah = 0.f;   // of that gap: the part spent waiting for this batch's H2D (host-late staging)
+            if (S.h2d_timed && cudaEventElapsedTime(&ah, L->t_ref, S.h2d_t) == cudaSuccess && ah > L->last_k1_ms)
+              L->stats.h2d_late_seconds += (std::min(ah, a0) - L->last_k1_ms) * 1e-3;
+          }
+          L->last_k1_ms = a1;
+        }
         L->stats.kernel_seconds += ms * 1e-3;
         L->stats.kernel_timed += S.timed_launches;
         L->stats.kernel_bytes += S.timed_bytes;
@@ -1555,7 +1624,9 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (S.d_stage) cudaFree(S.d_stage);
     if (S.d_status) cudaFree(S.d_status);
     if (S.h_status) cudaFreeHost(S.h_status);
+    if (&S == &L->slots[0] && L->t_ref) { cudaEventDestroy(L->t_ref); L->t_ref = nullptr; }
     if (S.h2d_done) cudaEventDestroy(S.h2d_done);
+    if (S.h2d_t) cudaEventDestroy(S.h2d_t);
     if (S.done) cudaEventDestroy(S.done);
     if (S.release) cudaEventDestroy(S.release);
     if (S.k0) cudaEventDestroy(S.k0);
@@ -1598,6 +1669,7 @@ bbx_status bbx_loader_reset_stats(bbx_loader* L) {
   if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
   std::lock_guard<std::mutex> g(L->stats_mu);
   L->stats = bbx_loader_stats{};
+  L->last_k1_ms = -1.f;
   return BBX_OK;
 }
 bbx_status bbx_loader_set_profiling(bbx_loader* L, int enabled) {
