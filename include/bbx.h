@@ -176,6 +176,7 @@ typedef struct {
   int64_t zero_copy_bytes;    /* payload bytes kernels read straight from pinned host memory over PCIe */
   double  gap_seconds;        /* profiling: compute-stream idle between consecutive timed batches */
   double  h2d_late_seconds;   /* profiling: part of that idle time spent waiting for the batch's H2D */
+  int64_t timed_batches;      /* profiling: batches whose kernel window (kernel_seconds) was timed */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
  * RLE / JPEG fields, kernels read each sample's payload window straight from

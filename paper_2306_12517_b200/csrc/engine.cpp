@@ -1531,6 +1531,7 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
           L->last_k1_ms = a1;
         }
         L->stats.kernel_seconds += ms * 1e-3;
+        L->stats.timed_batches += 1;
         L->stats.kernel_timed += S.timed_launches;
         L->stats.kernel_bytes += S.timed_bytes;
       }
