@@ -540,7 +540,7 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
   return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
-__host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 32; }
+__host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16 * kCwStages; }
 // geometry ring (3 entries): column table xt[owp] | rowtap[rows_per_tile] (uint2);
 // source-row stages (2): cw_slots x span_pad (whole rows at the image's row stride)
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
@@ -548,7 +548,7 @@ __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
 }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
-  return cw_stage_off(P) + 3 * cw_stage_meta(P) + 2 * cw_src_stage(P);
+  return cw_stage_off(P) + (kCwStages + 1) * cw_stage_meta(P) + kCwStages * cw_src_stage(P);
 }
 
 __device__ __forceinline__ uint32_t u32_sink(const void* p, size_t n) {   // experiments: keep values live
@@ -591,16 +591,15 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   const int t_begin = (int)((int64_t)blockIdx.x * total / G), t_end = (int)((int64_t)(blockIdx.x + 1) * total / G);
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[2], empty[2]
-  uint64_t* empty = full + 2;
-  uint8_t* metas = smem + cw_stage_off(P);              // geometry ring: tile k uses entry k % 3
-  uint8_t* stages = metas + 3 * meta;                   // source rows: tile k uses stage k & 1
+  constexpr int NS = kCwStages, NR = kCwStages + 1;   // source stages; geometry ring entries
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[NS], empty[NS]
+  uint64_t* empty = full + NS;
+  uint8_t* metas = smem + cw_stage_off(P);              // geometry ring: tile k uses entry k % NR
+  uint8_t* stages = metas + NR * meta;                  // source rows: tile k uses stage k % NS
 
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(&empty[0], ncw);
-    mbar_init(&empty[1], ncw);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], ncw); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if constexpr (kVal == VAL_LUT) {
@@ -611,14 +610,16 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   __syncthreads();
 
   if (warp == ncw) {
-    // ---- copy warp: tile k's geometry -> ring entry k % 3 (free: iteration
-    // k - 1 waited for tile k - 3), then, once the compute warps have
-    // released tile k - 2's stage, its source rows -> stage k & 1 (nslot <= 64)
-    int k = 0, m = 0, s = t_begin / tps, tile = t_begin - s * tps;
+    // ---- copy warp: tile k's geometry -> ring entry k % NR (free: iteration
+    // k - 1 waited for tile k - 1 - NS), then, once the compute warps have
+    // released tile k - NS's stage, its source rows -> stage k % NS (nslot <= 64)
+    int k = 0, m = 0, b = 0, ph = 0, s = t_begin / tps, tile = t_begin - s * tps;
     int cur_s = -1, prev_m = 0, col_lo = 0, span_bytes = 0;   // the column table of sample cur_s sits in entry prev_m
-    for (int t = t_begin; t < t_end; ++t, ++k, m = m == 2 ? 0 : m + 1) {
-      if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
-      const int b = k & 1;
+    for (int t = t_begin; t < t_end; ++t, ++k, m = m == NR - 1 ? 0 : m + 1) {
+      if (t > t_begin) {
+        if (++tile == tps) { tile = 0; ++s; }
+        if (++b == NS) { b = 0; ph ^= 1; }              // ph: parity of this stage's use count
+      }
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
       uint32_t tx = 0;
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
           rowtap[lane] = make_uint2((base0 + e * rstr) | we << 20, base0 + o * rstr);
         }
       }
-      if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1);
+      if (k >= NS) mbar_wait(&empty[b], ph ^ 1);      // the previous use's release
       uint8_t* srcbuf = stages + (size_t)b * sbytes;
       __syncwarp();
       if (lane == 0) {
@@ -704,17 +705,19 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
   // ---- compute warps
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
-  int k = 0, m = 0, s = t_begin / tps, tile = t_begin - s * tps;
-  for (int t = t_begin; t < t_end; ++t, ++k, m = m == 2 ? 0 : m + 1) {
-    if (t > t_begin && ++tile == tps) { tile = 0; ++s; }
-    const int b = k & 1;
+  int m = 0, b = 0, ph = 0, s = t_begin / tps, tile = t_begin - s * tps;
+  for (int t = t_begin; t < t_end; ++t, m = m == NR - 1 ? 0 : m + 1) {
+    if (t > t_begin) {
+      if (++tile == tps) { tile = 0; ++s; }
+      if (++b == NS) { b = 0; ph ^= 1; }
+    }
     const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
     const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp);
     const uint8_t* srcbuf = stages + (size_t)b * sbytes;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
     const bool live = !d->skip && R > 0;
-    mbar_wait(&full[b], (k >> 1) & 1);
+    mbar_wait(&full[b], ph);
 #ifdef BBX_EXP_NOCOMPUTE
     if (live && srcbuf[tid] == 0x7f && xt[0] == 0x12345u) static_cast<uint8_t*>(A.out)[0] = 1;   // keep the copies observable
     if (false) {
