@@ -21,6 +21,9 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <unordered_map>
 
 #include "engine.h"
@@ -924,6 +927,28 @@ static int finalize(bbx_loader* L) {
 }
 
 // The per-batch pipeline body (runs on the loader thread).
+// Window rows into the pinned slot: 16-byte-aligned destination rows written
+// with non-temporal stores (no read-for-ownership of the slot: the gather is
+// host-memory bound, and the slot is next read by the H2D DMA, not the CPU).
+// A row's last chunk may read up to 15 bytes past it (never past the mapping).
+static void gather_rows(uint8_t* dst, uint32_t dst_stride, const uint8_t* src, uint32_t src_stride, uint32_t row_bytes,
+                        uint32_t rows, const uint8_t* src_end) {
+#if defined(__SSE2__)
+  const uint32_t n16 = (row_bytes + 15) / 16;
+  for (uint32_t r = 0; r < rows; ++r) {
+    const uint8_t* s = src + (size_t)r * src_stride;
+    uint8_t* d = dst + (size_t)r * dst_stride;
+    if (s + (size_t)n16 * 16 > src_end || (reinterpret_cast<uintptr_t>(d) & 15)) { std::memcpy(d, s, row_bytes); continue; }
+    for (uint32_t i = 0; i < n16; ++i)
+      _mm_stream_si128(reinterpret_cast<__m128i*>(d + 16 * i), _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + 16 * i)));
+  }
+  _mm_sfence();   // the streaming stores are visible before the pool reports the batch gathered
+#else
+  for (uint32_t r = 0; r < rows; ++r) std::memcpy(dst + (size_t)r * dst_stride, src + (size_t)r * src_stride, row_bytes);
+  (void)src_end;
+#endif
+}
+
 static int process_slot(bbx_loader* L, int s) {
   Slot& S = L->slots[s];
   const bbx_dataset* ds = L->ds;
@@ -954,7 +979,7 @@ static int process_slot(bbx_loader* L, int s) {
     }
   }
   // descriptors + payload plan (serial: ~100 ns per sample per field)
-  struct Copy { const uint8_t* src; uint8_t* dst; uint32_t row_bytes, rows, src_stride; };
+  struct Copy { const uint8_t* src; uint8_t* dst; uint32_t row_bytes, rows, src_stride, dst_stride; };
   std::vector<Copy> copies;
   struct JParse { int plan; int pos; int64_t idx; uint64_t off; uint32_t len; };
   std::vector<JParse> jparse;
@@ -1007,17 +1032,20 @@ static int process_slot(bbx_loader* L, int s) {
         int y0, y1, x0, x1;
         read_window(pl.dev, d, reinterpret_cast<const int32_t*>(desc + kDescHeader), &y0, &y1, &x0, &x1);
         const uint32_t wb = (uint32_t)(x1 - x0) * d->c, wr = (uint32_t)(y1 - y0);
-        if ((uint64_t)wb * wr * 10 < (uint64_t)len * 9) {   // worth it: < 90% of the payload
+        // staged rows start 16-byte aligned (the gather streams whole 16-B chunks);
+        // worth it below 90 % of the payload, and never above the sample's staging share
+        const uint32_t ws = (wb + 15) & ~15u;
+        if ((uint64_t)wb * wr * 10 < (uint64_t)len * 9 && (uint64_t)ws * wr <= ((uint64_t)len + 15) / 16 * 16) {
           d->flags |= kDescWindowed;
-          d->wstride = wb; d->wy0 = (uint16_t)y0; d->wx0 = (uint16_t)x0;
+          d->wstride = ws; d->wy0 = (uint16_t)y0; d->wx0 = (uint16_t)x0;
           if (wb && wr)
             copies.push_back({ds->map + off + ((uint64_t)y0 * d->w + x0) * d->c, H + cursor, wb, wr,
-                              (uint32_t)d->w * d->c});
-          cursor += ((size_t)wb * wr + 15) / 16 * 16;
+                              (uint32_t)d->w * d->c, ws});
+          cursor += (size_t)ws * wr;
           continue;
         }
       }
-      if (len) copies.push_back({ds->map + off, H + cursor, len, 1, len});
+      if (len) copies.push_back({ds->map + off, H + cursor, len, 1, len, len});
       cursor += ((size_t)len + 15) / 16 * 16;
     }
   }
@@ -1119,11 +1147,11 @@ static int process_slot(bbx_loader* L, int s) {
   }
   // gather mode: mmap page cache -> pinned slot (row segments for windows)
   if (!dma_done && !copies.empty()) {
+    const uint8_t* map_end = ds->map + ds->map_len;
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
       if (c.rows == 1) { std::memcpy(c.dst, c.src, c.row_bytes); return; }
-      for (uint32_t r = 0; r < c.rows; ++r)
-        std::memcpy(c.dst + (size_t)r * c.row_bytes, c.src + (size_t)r * c.src_stride, c.row_bytes);
+      gather_rows(c.dst, c.dst_stride, c.src, c.src_stride, c.row_bytes, c.rows, map_end);
     });
   }
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
