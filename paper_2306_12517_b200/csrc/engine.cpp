@@ -1150,7 +1150,6 @@ static int process_slot(bbx_loader* L, int s) {
     const uint8_t* map_end = ds->map + ds->map_len;
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
-      if (c.rows == 1) { std::memcpy(c.dst, c.src, c.row_bytes); return; }
       gather_rows(c.dst, c.dst_stride, c.src, c.src_stride, c.row_bytes, c.rows, map_end);
     });
   }
