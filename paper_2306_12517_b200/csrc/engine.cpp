@@ -147,6 +147,7 @@ struct Plan {
   int64_t jpeg_bits_cap = 0;     // per sample
   uint32_t* d_istart = nullptr;
   uint32_t* d_iend = nullptr;
+  uint32_t* d_isample = nullptr;
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
@@ -184,6 +185,7 @@ struct Slot {
   std::vector<uint32_t> jpeg_total_int;
   std::vector<uint64_t> jpeg_total_blk;
   std::vector<int32_t> jpeg_max_quads;
+  std::vector<uint32_t> jpeg_max_blocks;
 };
 
 // Device pools of the Huffman / quant tables the JPEG samples reference,
@@ -866,6 +868,7 @@ static int finalize(bbx_loader* L) {
     CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
     CK(cudaMalloc(&pl.d_istart, ints * 4 + 64));
     CK(cudaMalloc(&pl.d_iend, ints * 4 + 64));
+    CK(cudaMalloc(&pl.d_isample, ints * 4 + 64));
   }
   if (any_jpeg && !L->jt.d_huff) {
     JpegTables& T = L->jt;
@@ -964,6 +967,7 @@ static int process_slot(bbx_loader* L, int s) {
   S.jpeg_total_int.assign(L->plans.size(), 0);
   S.jpeg_total_blk.assign(L->plans.size(), 0);
   S.jpeg_max_quads.assign(L->plans.size(), 0);
+  S.jpeg_max_blocks.assign(L->plans.size(), 0);
   uint8_t* H = S.h_stage;
   std::memcpy(H + L->idx_off, S.idx.data(), (size_t)count * 8);
   for (int64_t pos = 0; pos < count; ++pos) {
@@ -1077,6 +1081,7 @@ static int process_slot(bbx_loader* L, int s) {
     uint32_t ti = 0;
     uint64_t tb = 0, bs = 0;
     int32_t mq = 0;
+    uint32_t mb = 0;
     for (int pos = 0; pos < count; ++pos) {
       JpegDesc& J = jds[pos];
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
@@ -1095,10 +1100,11 @@ static int process_slot(bbx_loader* L, int s) {
       if (J.n_int) {
         bs += (uint64_t)pl.jpeg_bits_cap;
         mq = std::max(mq, (int32_t)d->h);
+        mb = std::max(mb, J.n_blocks);
       }
     }
     ipre[count] = ti; bpre[count] = tb;
-    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_quads[p] = mq;
+    S.jpeg_total_int[p] = ti; S.jpeg_total_blk[p] = tb; S.jpeg_max_quads[p] = mq; S.jpeg_max_blocks[p] = mb;
     if (ti == 0) S.plan_has_jpeg[p] = 0;
   }
   {   // new JPEG tables: append-only upload ahead of this slot's H2D (same copy stream)
@@ -1218,11 +1224,12 @@ static int process_slot(bbx_loader* L, int s) {
       J.jd = reinterpret_cast<const JpegDesc*>(jb);
       J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
       J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
-      J.istart = pl.d_istart; J.iend = pl.d_iend; J.bits = pl.d_bits; J.coef = pl.d_coef; J.planes = pl.d_planes;
+      J.istart = pl.d_istart; J.iend = pl.d_iend; J.isample = pl.d_isample; J.bits = pl.d_bits; J.coef = pl.d_coef; J.planes = pl.d_planes;
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
       J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
       J.coef_zeroed = 1;
       J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
+      J.max_blocks = S.jpeg_max_blocks[p];
       // J2 stores only nonzero coefficients
       CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
       if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1305,7 +1312,8 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   const size_t o_q = o_hf + sizeof(JHuff) * L.jt.n_huff;
   const size_t o_is = (o_q + sizeof(JQuant) * L.jt.n_quant + 255) / 256 * 256;
   const size_t o_ie = o_is + 4 * (size_t)J.n_int + 16;
-  const size_t o_bs = (o_ie + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
+  const size_t o_isa = o_ie + 4 * (size_t)J.n_int + 16;
+  const size_t o_bs = (o_isa + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
   const size_t o_cf = (o_bs + (size_t)pl.jpeg_bits_cap + 255) / 256 * 256;
   const size_t o_pl = (o_cf + 128 * (size_t)J.n_blocks + 255) / 256 * 256;
   const size_t o_st = (o_pl + 64 * (size_t)J.n_blocks + 255) / 256 * 256;
@@ -1331,13 +1339,14 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   A.int_prefix = reinterpret_cast<const uint32_t*>(dev + o_ip);
   A.blk_prefix = reinterpret_cast<const uint64_t*>(dev + o_bp);
   A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
+  A.isample = reinterpret_cast<uint32_t*>(dev + o_isa);
   A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
   A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
   A.n_huff = L.jt.n_huff;
   A.coef_zeroed = 1;
   A.status = reinterpret_cast<SampleStatus*>(dev + o_st);
-  A.count = 1; A.total_int = J.n_int; A.total_blocks = J.n_blocks; A.max_quads = h;
+  A.count = 1; A.total_int = J.n_int; A.total_blocks = J.n_blocks; A.max_quads = h; A.max_blocks = J.n_blocks;
   int rc = e == cudaSuccess ? launch_jpeg(A, nullptr) : 1;
   SampleStatus st{};
   if (e == cudaSuccess) e = cudaMemcpy(&st, dev + o_st, sizeof st, cudaMemcpyDeviceToHost);
@@ -1670,6 +1679,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (pl.d_planes) cudaFree(pl.d_planes);
     if (pl.d_istart) cudaFree(pl.d_istart);
     if (pl.d_iend) cudaFree(pl.d_iend);
+    if (pl.d_isample) cudaFree(pl.d_isample);
   }
   if (L->jt.h_huff) cudaFreeHost(L->jt.h_huff);
   if (L->jt.h_quant) cudaFreeHost(L->jt.h_quant);

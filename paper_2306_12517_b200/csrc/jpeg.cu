@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
   const uint32_t rounds = (nch + 32 * kUnstuffWarps - 1) / (32 * kUnstuffWarps);
   const uint32_t ch0 = warp * rounds * 32;
   if (threadIdx.x == 0) s_bad = 0;
+  for (uint32_t k = threadIdx.x; k < nint; k += 32 * kUnstuffWarps) A.isample[J.int_base + k] = (uint32_t)s;
   // pass 1: this warp's cursor function and marker count
   CursorFn F{0u, 0u, 0u};
   uint32_t NR = 0;
@@ -259,15 +260,6 @@ constexpr int kHuffThreads = 128;
 constexpr int kExtraSymbols = BBX_EXTRA_SYMBOLS;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
-template <typename T>
-__device__ __forceinline__ int find_sample(const T* prefix, int count, T t) {   // largest s: prefix[s] <= t
-  int lo = 0, hi = count;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(&prefix[mid]) <= t) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
 template <typename T>
 __device__ __forceinline__ T sel3(int i, T a, T b, T c) { return i == 0 ? a : (i == 1 ? b : c); }
@@ -326,7 +318,7 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
   };
   // set up interval t; false when it has nothing to decode
   auto start = [&](uint32_t t) -> bool {
-    s = find_sample(A.int_prefix, A.count, t);
+    s = (int)__ldg(&A.isample[t]);                  // written by J1 (no search over the prefix)
     if (A.status[s].kind != 0) return false;         // J1 rejected the marker layout
     const JpegDesc& J = A.jd[s];
     k = t - J.int_base;
@@ -552,12 +544,13 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
 constexpr int kIdctThreads = 128;
 
 __global__ void __launch_bounds__(kIdctThreads) jpeg_idct_kernel(const JpegArgs A) {
-  const uint64_t g = (uint64_t)blockIdx.x * kIdctThreads + threadIdx.x;
-  if (g >= A.total_blocks) return;
-  const int s = find_sample(A.blk_prefix, A.count, g);
+  // grid (block chunks of the largest sample, samples): no search for the sample
+  const int s = blockIdx.y;
   const JpegDesc& J = A.jd[s];
-  if (A.status[s].kind != 0) return;
-  const uint32_t rel = (uint32_t)(g - J.blk_base), bpm = J.bpm;
+  const uint32_t rel = blockIdx.x * kIdctThreads + threadIdx.x;
+  if (rel >= J.n_blocks || J.n_int == 0 || A.status[s].kind != 0) return;
+  const uint64_t g = J.blk_base + rel;
+  const uint32_t bpm = J.bpm;
   const uint32_t m = rel / bpm, b = rel - m * bpm;
   const uint32_t e = (uint32_t)(J.sched >> (4 * b)) & 15u, c = e & 3;
   const JComp& C = J.comp[c];
@@ -778,7 +771,7 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
     cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
     jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
   }
-  jpeg_idct_kernel<<<(unsigned)((A.total_blocks + kIdctThreads - 1) / kIdctThreads), kIdctThreads, 0, st>>>(A);
+  jpeg_idct_kernel<<<dim3((A.max_blocks + kIdctThreads - 1) / kIdctThreads, A.count), kIdctThreads, 0, st>>>(A);
   jpeg_color_kernel<<<dim3((A.max_quads + kColorRows - 1) / kColorRows, A.count), kColorThreads, 0, st>>>(A);
   return cudaGetLastError() != cudaSuccess;
 }

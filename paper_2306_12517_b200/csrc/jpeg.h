@@ -139,6 +139,7 @@ struct JpegArgs {
   uint8_t* planes;                        // total blocks x 64: component planes (J3 -> J4)
   uint32_t* istart;                       // per interval: bitstream start / end (sample-relative)
   uint32_t* iend;
+  uint32_t* isample;                      // per interval: its sample (written by J1; J2 needs no search)
   uint8_t* bits;                          // unstuffed bitstreams
   int16_t* coef;                          // total blocks x 64
   uint8_t* scratch;                       // count x scratch_bytes: decoded HWC u8
@@ -152,6 +153,7 @@ struct JpegArgs {
   uint32_t total_int;
   uint64_t total_blocks;
   int32_t max_quads;                      // largest image height in the batch (J4 grid: bands of rows)
+  uint32_t max_blocks;                    // most blocks of one sample in the batch (J3 grid)
 };
 
 // jpeg.cu
