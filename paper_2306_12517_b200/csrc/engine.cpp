@@ -222,6 +222,7 @@ struct bbx_loader {
   JpegTables jt;
   bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
   bool jpeg_roi = true;               // decode only the MCUs a sample's chain reads (BBX_JPEG_ROI=0: whole image)
+  int j2_per_lane = 0;                // > 0: intervals per J2 lane (experiments)
   bool jpeg_prefetch = true;          // parse every sample's header at finalize (file fits in RAM; BBX_JPEG_PREFETCH=0: lazily)
   bool zero_copy = false;             // requested: kernels read payloads from the pinned host heap
   const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
@@ -1230,6 +1231,7 @@ static int process_slot(bbx_loader* L, int s) {
       J.coef_zeroed = 1;
       J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
       J.max_blocks = S.jpeg_max_blocks[p];
+      J.j2_per_lane = L->j2_per_lane;
       // J2 stores only nonzero coefficients
       CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
       if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1453,6 +1455,7 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (const char* e = std::getenv("BBX_JPEG_CACHE")) L->jpeg_cache = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_JPEG_ROI")) L->jpeg_roi = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_JPEG_PREFETCH")) L->jpeg_prefetch = std::atoi(e) != 0;
+  if (const char* e = std::getenv("BBX_J2_PER_LANE")) L->j2_per_lane = std::atoi(e);
   int nt = staging_threads;
   if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   if (const char* e = std::getenv("BBX_STAGING_THREADS")) if (staging_threads <= 0) nt = std::max(1, std::atoi(e));

@@ -761,7 +761,8 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   // lanes pull intervals from a per-CTA queue: a few intervals per lane balance their
   // unequal lengths once there are enough intervals to keep every SM busy
   const uint32_t lanes = 148u * 4u * kHuffThreads;
-  const uint32_t per_lane = min(8u, max(1u, A.total_int / lanes));
+  uint32_t per_lane = min(8u, max(1u, A.total_int / lanes));
+  if (A.j2_per_lane > 0) per_lane = (uint32_t)A.j2_per_lane;
   const uint32_t chunk = per_lane * kHuffThreads;
   const unsigned hgrid = (A.total_int + chunk - 1) / chunk;
   if (smem) {
