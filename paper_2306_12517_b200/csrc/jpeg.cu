@@ -632,18 +632,22 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
   const int w = d->w, nc = J.ncomp;
   const int y_lo = max((int)blockIdx.x * kColorRows, (int)J.win[0]);
   const int y_hi = min((int)(blockIdx.x + 1) * kColorRows, (int)J.win[1]);
-  if (threadIdx.x == 0) {
-    s_ok = J.n_int != 0 && A.status[s].kind == 0 && y_lo < y_hi && J.win[2] < J.win[3];
-    const uint8_t* planes = A.planes + J.blk_base * 64;
-    for (int c = 0; c < nc; ++c) {
+  if (threadIdx.x < 3) {                            // one lane per component (independent loads)
+    const int c = threadIdx.x;
+    if (c < nc) {
       const JComp& C = J.comp[c];
-      sP[c].p = planes + (size_t)J.plane_blk[c] * 64;
-      sP[c].pw = C.bw * 8; sP[c].dw = C.dw; sP[c].dh = C.dh; sP[c].rh = J.hmax / C.h; sP[c].rv = J.vmax / C.v;
+      Plane q;
+      q.p = A.planes + (J.blk_base + J.plane_blk[c]) * 64;
+      q.pw = C.bw * 8; q.dw = C.dw; q.dh = C.dh; q.rh = J.hmax / C.h; q.rv = J.vmax / C.v;
+      sP[c] = q;
     }
+    if (c == 0) s_ok = J.n_int != 0 && A.status[s].kind == 0 && y_lo < y_hi && J.win[2] < J.win[3];
+  }
+  __syncwarp();
+  if (threadIdx.x == 0)
     s_fast = nc == 3 && sP[0].rh == 1 && sP[0].rv == 1 && sP[1].rh == 2 && sP[1].rv == 2 && sP[2].rh == 2 &&
              sP[2].rv == 2 && sP[1].dw > 2 && sP[2].dw > 2 && sP[1].dw == sP[2].dw && sP[1].dh == sP[2].dh &&
              sP[1].pw == sP[2].pw;
-  }
   __syncthreads();
   if (!s_ok) return;
   // octets covering the window's columns (their extra pixels lie inside the decoded MCUs)
