@@ -602,12 +602,7 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], ncw); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if constexpr (kVal == VAL_LUT) {
-    const uint4* g = reinterpret_cast<const uint4*>(A.lut);
-    uint4* l4 = reinterpret_cast<uint4*>(lut);
-    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += blockDim.x) l4[i] = g[i];
-  }
-  __syncthreads();
+  __syncthreads();                                   // barriers initialised
 
   if (warp == ncw) {
     // ---- copy warp: tile k's geometry -> ring entry k % NR (free: iteration
@@ -702,7 +697,13 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
     return;
   }
 
-  // ---- compute warps
+  // ---- compute warps: the value table (while the copy warp stages the first tiles)
+  if constexpr (kVal == VAL_LUT) {
+    const uint4* g = reinterpret_cast<const uint4*>(A.lut);
+    uint4* l4 = reinterpret_cast<uint4*>(lut);
+    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += nct) l4[i] = g[i];
+    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");   // compute warps only
+  }
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
   int m = 0, b = 0, ph = 0, s = t_begin / tps, tile = t_begin - s * tps;
