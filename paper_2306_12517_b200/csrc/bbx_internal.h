@@ -101,6 +101,14 @@ struct SampleStatus {
   int64_t value;
 };
 
+struct ScalarArgs {
+  const int64_t* idx;        // count indices (device)
+  int32_t count;
+  int32_t n_fields;
+  const uint64_t* cols[16];  // device columns, num_samples entries each
+  uint64_t* outs[16];
+};
+
 struct LaunchArgs {
   const uint8_t* desc;       // count * desc_stride bytes (device)
   const uint8_t* payload;    // payload base (device): staged region or file image in HBM
@@ -110,14 +118,7 @@ struct LaunchArgs {
   uint32_t* tables;          // K1 prologue tables: count x tab_stride u32
   SampleStatus* status;      // count entries
   int32_t count;
-};
-
-struct ScalarArgs {
-  const int64_t* idx;        // count indices (device)
-  int32_t count;
-  int32_t n_fields;
-  const uint64_t* cols[16];  // device columns, num_samples entries each
-  uint64_t* outs[16];
+  ScalarArgs sc;             // column-walker K1: scalar fields gathered by the copy warp (n_fields 0: none)
 };
 
 // kernels.cu

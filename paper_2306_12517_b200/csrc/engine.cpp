@@ -1195,9 +1195,24 @@ static int process_slot(bbx_loader* L, int s) {
   ScalarArgs SA{};
   SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
   SA.count = count;
+  // up to 16 scalar fields ride along with the first column-walker K1 launch (its
+  // copy warp gathers them); otherwise, or beyond that, scalar_gather_kernel
+  int n_scalar = 0, fused_plan = -1;
+  for (const Plan& pl : L->plans) n_scalar += pl.scalar ? 1 : 0;
+  if (n_scalar > 0 && n_scalar <= 16 && count > 0)
+    for (size_t p = 0; p < L->plans.size(); ++p)
+      if (!L->plans[p].scalar && L->plans[p].dev.cw) { fused_plan = (int)p; break; }
+  if (fused_plan >= 0)
+    for (const Plan& pl : L->plans)
+      if (pl.scalar) {
+        SA.cols[SA.n_fields] = pl.d_col;
+        SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
+        ++SA.n_fields;
+      }
   for (size_t p = 0; p < L->plans.size(); ++p) {
     Plan& pl = L->plans[p];
     if (pl.scalar) {
+      if (fused_plan >= 0) continue;
       SA.cols[SA.n_fields] = pl.d_col;
       SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
       ++SA.n_fields;
@@ -1213,6 +1228,7 @@ static int process_slot(bbx_loader* L, int s) {
     A.out = pl.outs[s];
     A.status = S.d_status + (size_t)p * L->batch;
     A.count = count;
+    if ((int)p == fused_plan) A.sc = SA;
     if (count == 0) continue;
     if (S.plan_has_rle[p]) {
       if (launch_rle_expand(pl.dev, A, L->comp_st)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1259,7 +1275,7 @@ static int process_slot(bbx_loader* L, int s) {
   S.timed = prof;
   S.timed_launches = klaunch;
   S.timed_bytes = kbytes;
-  if (SA.n_fields && count) {
+  if (SA.n_fields && count && fused_plan < 0) {
     if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
     ++launches;
   }

@@ -619,6 +619,10 @@ __global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
       uint32_t tx = 0;
       const uint8_t* src = nullptr;
+      if (tile == 0 && lane < A.sc.n_fields) {         // the batch's scalar fields, once per sample
+        const int64_t i = A.sc.idx[s];
+        A.sc.outs[lane][s] = A.sc.cols[lane][i];
+      }
       if (!d->skip && R > 0) {
         // what sample_tables_kernel computes for the other K1 variants
         uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta);
