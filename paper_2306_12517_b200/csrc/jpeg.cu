@@ -46,6 +46,7 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
 //   pass 3: every warp replays its chunks and writes bytes / interval bounds.
 constexpr int kUnstuffWarps = 8;
 constexpr int kUnstuffBuf = 1024;                  // per-warp output window of pass 3 (bytes)
+constexpr int kScanCache = 8;                      // rounds whose pass-1 scans pass 3 reuses (later rounds rescan)
 constexpr uint32_t kAlignMask = kJpegIntAlign - 1;
 
 __device__ __forceinline__ uint32_t align_int(uint32_t x) { return (x + kAlignMask) & ~kAlignMask; }
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
   __shared__ uint32_t s_nr[kUnstuffWarps], s_x[kUnstuffWarps], s_k[kUnstuffWarps];
   __shared__ int s_bad;
   __shared__ __align__(16) uint8_t s_ob[kUnstuffWarps][kUnstuffBuf];
+  __shared__ uint2 s_scan[kUnstuffWarps][kScanCache][32];   // pass 1's per-lane inclusive scans (packed)
   const uint8_t* base = A.payload + sdesc(A, s)->src;
   uint8_t* out = A.bits + J.bs_base;
   uint32_t* st = A.istart + J.int_base;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
     term |= M.term != 0;
     uint32_t nr = __popc(M.rst);
     const CursorFn inc = warp_scan(lane_fn(M), nr, lane);
+    if (r < kScanCache) s_scan[warp][r][lane] = make_uint2(inc.a | inc.aligned << 31, inc.c | nr << 16);
     const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
                        __shfl_sync(0xffffffffu, inc.c, 31)};
     F = compose(F, all);
@@ -195,14 +198,25 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
   for (uint32_t r = 0; r < rounds; ++r) {
     const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
     const uint32_t nr = __popc(M.rst);
-    uint32_t nr_incl = nr;
-    const CursorFn f = lane_fn(M);
-    const CursorFn inc = warp_scan(f, nr_incl, lane);
-    CursorFn exc{__shfl_up_sync(0xffffffffu, inc.aligned, 1), __shfl_up_sync(0xffffffffu, inc.a, 1),
-                 __shfl_up_sync(0xffffffffu, inc.c, 1)};
-    if (lane == 0) exc = CursorFn{0u, 0u, 0u};
-    const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
-                       __shfl_sync(0xffffffffu, inc.c, 31)};
+    uint32_t nr_incl = nr, nr_all;
+    CursorFn exc, all;
+    if (r < kScanCache) {                            // pass 1's scan of this round, from shared memory
+      auto unpack = [](uint2 v) { return CursorFn{v.x >> 31, v.x & 0x7FFFFFFFu, v.y & 0xFFFFu}; };
+      const uint2 me = s_scan[warp][r][lane], lv = s_scan[warp][r][31];
+      const uint2 pv = lane ? s_scan[warp][r][lane - 1] : make_uint2(0u, 0u);
+      exc = unpack(pv);
+      all = unpack(lv);
+      nr_incl = me.y >> 16;
+      nr_all = lv.y >> 16;
+    } else {
+      const CursorFn inc = warp_scan(lane_fn(M), nr_incl, lane);
+      exc = CursorFn{__shfl_up_sync(0xffffffffu, inc.aligned, 1), __shfl_up_sync(0xffffffffu, inc.a, 1),
+                     __shfl_up_sync(0xffffffffu, inc.c, 1)};
+      if (lane == 0) exc = CursorFn{0u, 0u, 0u};
+      all = CursorFn{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
+                     __shfl_sync(0xffffffffu, inc.c, 31)};
+      nr_all = __shfl_sync(0xffffffffu, nr_incl, 31);
+    }
     const uint32_t xe = apply(all, xw), wb = xw & ~kAlignMask;   // round output [xw, xe); window base
     uint32_t x = apply(exc, xw), k = kw + nr_incl - nr;
     const bool staged = xe - wb <= (uint32_t)kUnstuffBuf;
@@ -237,7 +251,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
       __syncwarp();
     }
     xw = xe;
-    kw += __shfl_sync(0xffffffffu, nr_incl, 31);
+    kw += nr_all;
   }
   if (__any_sync(0xffffffffu, seq_bad) && lane == 0) A.status[s].kind = JST_MARKER_SEQ;
 }
