@@ -578,7 +578,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <typename OutT, int kVal>
-__global__ void __launch_bounds__(kThreads + 32) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
+__global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
   constexpr int C = 3, NP = kCwCols;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = P.cw_warps, nct = ncw * 32;          // compute warps 0..ncw-1; warp ncw issues the copies
