@@ -20,6 +20,7 @@ constexpr int kCwCols = 2;          // column-walker K1: output columns per thre
 #define BBX_CW_STAGES 2
 #endif
 constexpr int kCwStages = BBX_CW_STAGES;   // column-walker K1: source-row pipeline stages
+constexpr int kCwRun = 4;            // column-walker K1: consecutive tiles a CTA takes per ticket
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
@@ -119,6 +120,7 @@ struct LaunchArgs {
   SampleStatus* status;      // count entries
   int32_t count;
   ScalarArgs sc;             // column-walker K1: scalar fields gathered by the copy warp (n_fields 0: none)
+  unsigned long long* ticket;  // column-walker K1: [0] next tile run, [1] CTAs done (self-resetting, zero between launches)
 };
 
 // kernels.cu

@@ -148,6 +148,7 @@ struct Plan {
   uint32_t* d_istart = nullptr;
   uint32_t* d_iend = nullptr;
   uint32_t* d_isample = nullptr;
+  unsigned long long* d_ticket = nullptr;   // column-walker K1 tile ticket (2 x u64, zero between launches)
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
@@ -851,6 +852,11 @@ static int finalize(bbx_loader* L) {
     CK(cudaEventCreate(&S.k1));
   }
   for (auto& pl : L->plans) {
+    if (pl.scalar || !pl.dev.cw) continue;
+    CK(cudaMalloc(&pl.d_ticket, 16));
+    CK(cudaMemset(pl.d_ticket, 0, 16));
+  }
+  for (auto& pl : L->plans) {
     if (pl.scalar || pl.dev.src_kind == SRC_ARRAY) continue;
     pl.d_tables.assign(L->nslots, nullptr);
     for (int s = 0; s < L->nslots; ++s) CK(cudaMalloc(&pl.d_tables[s], (size_t)L->batch * pl.dev.tab_stride * 4 + 64));
@@ -1229,6 +1235,7 @@ static int process_slot(bbx_loader* L, int s) {
     A.status = S.d_status + (size_t)p * L->batch;
     A.count = count;
     if ((int)p == fused_plan) A.sc = SA;
+    A.ticket = pl.d_ticket;
     if (count == 0) continue;
     if (S.plan_has_rle[p]) {
       if (launch_rle_expand(pl.dev, A, L->comp_st)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1699,6 +1706,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (pl.d_istart) cudaFree(pl.d_istart);
     if (pl.d_iend) cudaFree(pl.d_iend);
     if (pl.d_isample) cudaFree(pl.d_isample);
+    if (pl.d_ticket) cudaFree(pl.d_ticket);
   }
   if (L->jt.h_huff) cudaFreeHost(L->jt.h_huff);
   if (L->jt.h_quant) cudaFreeHost(L->jt.h_quant);

@@ -541,10 +541,10 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16 * kCwStages; }
-// geometry ring (3 entries): column table xt[owp] | rowtap[rows_per_tile] (uint2);
+// geometry ring (stages + 1 entries): tile id (16 B) | column table xt[owp] | rowtap[rows_per_tile] (uint2);
 // source-row stages (2): cw_slots x span_pad (whole rows at the image's row stride)
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
-  return align_up((tab_owp(P) + 2 * P.rows_per_tile) * 4, 16);
+  return 16 + align_up((tab_owp(P) + 2 * P.rows_per_tile) * 4, 16);   // [tile id, pad x3] | xt | rowtap
 }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
@@ -587,8 +587,9 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
   // contiguous row range fits)
   const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
   const int total = A.count * tps, G = gridDim.x;
-  // CTA b takes the consecutive tiles [t_begin, t_end) (balanced to one tile)
-  const int t_begin = (int)((int64_t)blockIdx.x * total / G), t_end = (int)((int64_t)(blockIdx.x + 1) * total / G);
+  // tiles are handed out in runs of kCwRun consecutive tiles (sample-major order)
+  // from a global ticket, so CTAs whose samples resample cheaply take more
+  const int nruns = (total + kCwRun - 1) / kCwRun;
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
   constexpr int NS = kCwStages, NR = kCwStages + 1;   // source stages; geometry ring entries
@@ -608,13 +609,42 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
     // ---- copy warp: tile k's geometry -> ring entry k % NR (free: iteration
     // k - 1 waited for tile k - 1 - NS), then, once the compute warps have
     // released tile k - NS's stage, its source rows -> stage k % NS (nslot <= 64)
-    int k = 0, m = 0, b = 0, ph = 0, s = t_begin / tps, tile = t_begin - s * tps;
+    int k = 0, m = 0, b = 0, ph = 0;                   // ph: parity of stage b's use count
+    int t = 0, left = 0;                               // next tile, tiles left in the current run
     int cur_s = -1, prev_m = 0, col_lo = 0, span_bytes = 0;   // the column table of sample cur_s sits in entry prev_m
-    for (int t = t_begin; t < t_end; ++t, ++k, m = m == NR - 1 ? 0 : m + 1) {
-      if (t > t_begin) {
-        if (++tile == tps) { tile = 0; ++s; }
-        if (++b == NS) { b = 0; ph ^= 1; }              // ph: parity of this stage's use count
+    for (;; ++k, m = m == NR - 1 ? 0 : m + 1) {
+      if (k > 0 && ++b == NS) { b = 0; ph ^= 1; }
+      if (left == 0) {
+        unsigned long long u = 0;
+        if (lane == 0) u = atomicAdd(&A.ticket[0], 1ull);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= (unsigned long long)nruns) {
+          t = -1;
+        } else {
+          t = (int)u * kCwRun;
+          left = min(kCwRun, total - t);
+        }
       }
+      int32_t* hdr = reinterpret_cast<int32_t*>(metas + m * meta);
+      if (t < 0) {                                     // no tiles left: a stop entry for the compute warps
+        if (k >= NS) mbar_wait(&empty[b], ph ^ 1);
+        if (lane == 0) {
+          hdr[0] = -1;
+          mbar_arrive_tx(&full[b], 0);
+          // the last CTA to finish re-zeroes the ticket for the next launch
+          __threadfence();
+          if (atomicAdd(&A.ticket[1], 1ull) == (unsigned long long)gridDim.x - 1) {
+            A.ticket[0] = 0;
+            A.ticket[1] = 0;
+            __threadfence();
+          }
+        }
+        break;
+      }
+      const int s = t / tps, tile = t - s * tps;
+      ++t;
+      --left;
+      if (lane == 0) hdr[0] = t - 1;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
       uint32_t tx = 0;
@@ -625,7 +655,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
       }
       if (!d->skip && R > 0) {
         // what sample_tables_kernel computes for the other K1 variants
-        uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta);
+        uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
         uint2* rowtap = reinterpret_cast<uint2*>(xt + owp);
         const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
@@ -647,7 +677,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
           }
           cur_s = s;
         } else if (m != prev_m) {
-          const uint32_t* xp = reinterpret_cast<const uint32_t*>(metas + prev_m * meta);
+          const uint32_t* xp = reinterpret_cast<const uint32_t*>(metas + prev_m * meta + 16);
           for (int ox = lane; ox < OW; ox += 32) xt[ox] = xp[ox];
         }
         prev_m = m;
@@ -710,19 +740,17 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
   }
   const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
   const size_t ostep = (size_t)OW * C;
-  int m = 0, b = 0, ph = 0, s = t_begin / tps, tile = t_begin - s * tps;
-  for (int t = t_begin; t < t_end; ++t, m = m == NR - 1 ? 0 : m + 1) {
-    if (t > t_begin) {
-      if (++tile == tps) { tile = 0; ++s; }
-      if (++b == NS) { b = 0; ph ^= 1; }
-    }
-    const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta);
+  for (int m = 0, b = 0, ph = 0;; m = m == NR - 1 ? 0 : m + 1) {
+    mbar_wait(&full[b], ph);
+    const int t = *reinterpret_cast<const volatile int32_t*>(metas + m * meta);
+    if (t < 0) break;                                  // the copy warp's stop entry
+    const int s = t / tps, tile = t - s * tps;
+    const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta + 16);
     const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp);
     const uint8_t* srcbuf = stages + (size_t)b * sbytes;
     const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
     const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
     const bool live = !d->skip && R > 0;
-    mbar_wait(&full[b], ph);
 #ifdef BBX_EXP_NOCOMPUTE
     if (live && srcbuf[tid] == 0x7f && xt[0] == 0x12345u) static_cast<uint8_t*>(A.out)[0] = 1;   // keep the copies observable
     if (false) {
@@ -816,6 +844,7 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
+    if (++b == NS) { b = 0; ph ^= 1; }
   }
 }
 
