@@ -20,7 +20,6 @@ constexpr int kCwCols = 2;          // column-walker K1: output columns per thre
 #define BBX_CW_STAGES 2
 #endif
 constexpr int kCwStages = BBX_CW_STAGES;   // column-walker K1: source-row pipeline stages
-constexpr int kCwRun = 4;            // column-walker K1: consecutive tiles a CTA takes per ticket
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
@@ -79,6 +78,7 @@ struct PlanDev {
   int32_t cw_warps;                        // compute warps per CTA (plus one copy-issuing warp)
   int32_t cw_slots;                        // source rows one pipeline stage holds (even, <= 2 x rows_per_tile)
   int32_t cw_rg;                           // rows per item of a full tile: ceil(rows_per_tile / cw_groups)
+  int32_t cw_run;                          // consecutive tiles a CTA takes per ticket (BBX_CW_RUN, default 3)
   SmemLayout lay;
 };
 

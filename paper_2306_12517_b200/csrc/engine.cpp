@@ -500,6 +500,8 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
           }
         }
         Q.cw_rg = (Q.rows_per_tile + Q.cw_groups - 1) / Q.cw_groups;
+        Q.cw_run = 3;
+        if (const char* e = std::getenv("BBX_CW_RUN")) Q.cw_run = std::max(1, std::atoi(e));
         const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
         Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
                          ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;

@@ -587,9 +587,9 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
   // contiguous row range fits)
   const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
   const int total = A.count * tps, G = gridDim.x;
-  // tiles are handed out in runs of kCwRun consecutive tiles (sample-major order)
+  // tiles are handed out in runs of cw_run consecutive tiles (sample-major order)
   // from a global ticket, so CTAs whose samples resample cheaply take more
-  const int nruns = (total + kCwRun - 1) / kCwRun;
+  const int run = P.cw_run, nruns = (total + run - 1) / run;
   extern __shared__ __align__(16) uint8_t smem[];
   OutT* lut = reinterpret_cast<OutT*>(smem);
   constexpr int NS = kCwStages, NR = kCwStages + 1;   // source stages; geometry ring entries
@@ -621,8 +621,8 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
         if (u >= (unsigned long long)nruns) {
           t = -1;
         } else {
-          t = (int)u * kCwRun;
-          left = min(kCwRun, total - t);
+          t = (int)u * run;
+          left = min(run, total - t);
         }
       }
       int32_t* hdr = reinterpret_cast<int32_t*>(metas + m * meta);
