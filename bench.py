@@ -179,11 +179,12 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
     returns (device seconds max over ranks, d2h bytes per step)."""
     import torch
 
-    it = loader.iterate_steps(warmup + steps)
+    warm = loader.iterate_steps(warmup)
     for _ in range(warmup):
-        b = next(it)
+        b = next(warm)
         if read_back:
             b["label"].cpu()
+    warm.close()   # drains the batches the warm-up prefetched: none of the timed steps is computed before the timer
     stream = torch.cuda.current_stream()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -191,6 +192,7 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
     loader.reset_stats()
     d2h = 0
     start.record(stream)
+    it = loader.iterate_steps(steps, start_epoch=1)   # submitted inside the timed region (pipeline fill included)
     for _ in range(steps):
         b = next(it)
         if read_back:   # the step's result back on the host (labels of the batch)
@@ -312,7 +314,7 @@ def jpeg_workload(args, device, rank, world, barrier, reduce_max, leg="jpeg"):
     name, desc, chain, order, nd = JPEG_LEGS[leg]
     path = ensure_jpeg_dataset(rank, barrier, nd)
     ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=JPEG_B, chain=chain,
-                         order=order, slot_count=int(os.environ.get("BBX_BENCH_SLOTS", "3")))
+                         order=order, slot_count=int(os.environ.get("BBX_BENCH_SLOTS", "6")))
     ld.set_profiling(True)
     with ClockSampler(device) as clk:
         secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
@@ -477,7 +479,8 @@ def main():
     path = ensure_dataset(rank, barrier)
 
     # ---- value: heap resident in HBM
-    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device))
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device),
+                         slot_count=int(os.environ.get("BBX_BENCH_SLOTS", "6")))
     ld.set_profiling(True)
     with ClockSampler(device) as clk:
         secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
@@ -542,6 +545,7 @@ def main():
                      "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src},
         "gpu_launches": int(st["kernel_launches"]),
         "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
+        "gpu_idle_ms_per_step": st["gap_seconds"] / max(st["timed_batches"], 1) * 1e3,
         "clocks": clk.summary(),
     }
     if world == 1:

@@ -177,7 +177,7 @@ def shard_batches(global_batches: list, rank: int, world_size: int, batch_size: 
     out = []
     for gb in global_batches:
         part = gb[rank * batch_size:(rank + 1) * batch_size]
-        if part:
+        if len(part):
             out.append(part)
     return out
 
@@ -323,10 +323,13 @@ class Loader:
 
     def epoch_batches(self, epoch: int) -> list:
         """This rank's index lists for `epoch` (the reference order, then sharded)."""
+        return [b.tolist() for b in self._epoch_batch_arrays(epoch)]
+
+    def _epoch_batch_arrays(self, epoch: int) -> list:
         cfg = self.config
         page_map = self.dataset.page_map() if OrderKind(cfg.order) == OrderKind.QUASI_RANDOM else None
         gbs = cfg.batch_size * self.world_size
-        batches = self.order.epoch_batches(epoch, self.dataset.num_samples, gbs, page_map, cfg.drop_last)
+        batches = self.order.epoch_batch_arrays(epoch, self.dataset.num_samples, gbs, page_map, cfg.drop_last)
         if self.world_size > 1:
             batches = shard_batches(batches, self.rank, self.world_size, cfg.batch_size)
         return batches
@@ -416,33 +419,43 @@ class _EpochRun:
         self.loader = loader
         self.epoch = epoch
         self.stats = EpochStats()
+        # batch index arrays, extended an epoch at a time as the stream needs them
+        # (iterate_steps: a continuous stream across epoch boundaries, no pipeline drain)
+        self.batch_lists, self.batch_epochs = [], []
+        self._steps = steps
+        self._next_epoch = epoch
+        self._exhausted = False
+        self._ensure(0)
         if steps is None:
-            self.batch_lists = loader.epoch_batches(epoch)
-            self.batch_epochs = [epoch] * len(self.batch_lists)
-        else:
-            # a continuous stream across epoch boundaries (no pipeline drain between epochs)
-            self.batch_lists, self.batch_epochs = [], []
-            e = epoch
-            while len(self.batch_lists) < steps:
-                bl = loader.epoch_batches(e)
-                if not bl:
-                    break
-                take = bl[:steps - len(self.batch_lists)]
-                self.batch_lists += take
-                self.batch_epochs += [e] * len(take)
-                e += 1
+            self._exhausted = True                      # exactly one epoch
         self._inflight: set = set()
         self._stopped = False
-        strategy = loader.dataset.strategy
-        if isinstance(strategy, ProcessCacheStrategy):
-            self._check_capacity(strategy.capacity_pages)
 
-    def _check_capacity(self, capacity: int) -> None:
+    def _ensure(self, g: int) -> bool:
+        """Batch g is known (extending the stream by whole epochs); False past the end."""
+        while len(self.batch_lists) <= g and not self._exhausted:
+            bl = self.loader._epoch_batch_arrays(self._next_epoch)
+            if not bl:
+                self._exhausted = True
+                break
+            if self._steps is not None:
+                bl = bl[:self._steps - len(self.batch_lists)]
+            strategy = self.loader.dataset.strategy
+            if isinstance(strategy, ProcessCacheStrategy):
+                self._check_capacity(bl, strategy.capacity_pages)
+            self.batch_lists += bl
+            self.batch_epochs += [self._next_epoch] * len(bl)
+            self._next_epoch += 1
+            if self._steps is not None and len(self.batch_lists) >= self._steps:
+                self._exhausted = True
+        return g < len(self.batch_lists)
+
+    def _check_capacity(self, batches, capacity: int) -> None:
         ds = self.loader.dataset
-        for batch in self.batch_lists:
+        for batch in batches:
             pages: set = set()
             for i in batch:
-                pages.update(ds.sample_pages(i))
+                pages.update(ds.sample_pages(int(i)))
             if len(pages) > capacity:
                 raise CapacityTooSmall(f"batch touches {len(pages)} pages, cache holds {capacity}")
 
@@ -461,17 +474,18 @@ class _EpochRun:
         ld = self.loader
         L = _lib.lib()
         S = ld.config.slot_count
-        nb = len(self.batch_lists)
-        if nb == 0:
+        if not self._ensure(0):
             return
         stream = torch.cuda.current_stream(ld.device)
         sp = ctypes.c_void_p(stream.cuda_stream)
-        for g in range(min(S - 1, nb)):
-            self._submit(g)
-        for g in range(nb):
+        for g in range(S - 1):
+            if self._ensure(g):
+                self._submit(g)
+        g = 0
+        while self._ensure(g):
             if self._stopped:
                 raise ShutdownError("epoch stopped")
-            if g + S - 1 < nb:
+            if self._ensure(g + S - 1):
                 if g >= 1:
                     L.bbx_loader_release(ld.handle, (g - 1) % S, sp)
                 self._submit(g + S - 1)
@@ -486,7 +500,7 @@ class _EpochRun:
                 exc = _lib.STATUS_EXC.get(rc, Exception)
                 msg = _lib.last_error()
                 if bad.value >= 0:
-                    raise exc(f"sample {indices[bad.value]} failed: {msg}")
+                    raise exc(f"sample {int(indices[bad.value])} failed: {msg}")
                 raise exc(msg)
             _lib.check(L.bbx_loader_stream_wait(ld.handle, slot, sp))
             count = len(indices)
@@ -498,7 +512,8 @@ class _EpochRun:
                 arrays[fd.name] = t
             self.stats.batches += 1
             self.stats.samples += count
-            yield Batch(arrays, indices, g)
+            yield Batch(arrays, indices.tolist(), g)
+            g += 1
 
     def stop(self) -> None:
         if self._stopped:

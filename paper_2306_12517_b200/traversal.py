@@ -76,8 +76,15 @@ class TraversalOrder:
                       drop_last: bool = False) -> list:
         if batch_size < 1:
             raise ValueError("batch_size must be >= 1")
+        return [b.tolist() for b in self.epoch_batch_arrays(epoch, num_samples, batch_size, page_map, drop_last)]
+
+    def epoch_batch_arrays(self, epoch: int, num_samples: int, batch_size: int, page_map=None,
+                           drop_last: bool = False) -> list:
+        """epoch_batches as int64 array views of one permutation (no per-index Python objects)."""
+        if batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
         perm = epoch_permutation(self.kind, self.seed, epoch, num_samples, page_map, batch_size)
-        out = [perm[i:i + batch_size].tolist() for i in range(0, num_samples, batch_size)]
+        out = [perm[i:i + batch_size] for i in range(0, num_samples, batch_size)]
         if drop_last and out and len(out[-1]) < batch_size:
             out.pop()
         return out
