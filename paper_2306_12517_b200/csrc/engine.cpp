@@ -1203,13 +1203,14 @@ static int process_slot(bbx_loader* L, int s) {
   ScalarArgs SA{};
   SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
   SA.count = count;
-  // up to 16 scalar fields ride along with the first column-walker K1 launch (its
-  // copy warp gathers them); otherwise, or beyond that, scalar_gather_kernel
+  // up to 16 scalar fields ride along with the first image plan's K1 launch (the
+  // column walker's copy warp, or tile 0 of the tile kernel, gathers them);
+  // otherwise, or beyond that, scalar_gather_kernel
   int n_scalar = 0, fused_plan = -1;
   for (const Plan& pl : L->plans) n_scalar += pl.scalar ? 1 : 0;
-  if (n_scalar > 0 && n_scalar <= 16 && count > 0)
+  if (n_scalar > 0 && n_scalar <= 16 && count > 0)   // an image plan's K1 (either variant) carries them
     for (size_t p = 0; p < L->plans.size(); ++p)
-      if (!L->plans[p].scalar && L->plans[p].dev.cw) { fused_plan = (int)p; break; }
+      if (!L->plans[p].scalar && L->plans[p].dev.src_kind != SRC_ARRAY) { fused_plan = (int)p; break; }
   if (fused_plan >= 0)
     for (const Plan& pl : L->plans)
       if (pl.scalar) {

@@ -418,6 +418,8 @@ template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, const LaunchArgs A) {
   constexpr int V = kVec ? (16 / (int)sizeof(OutT)) : 1;
   const int s = blockIdx.y;
+  if (blockIdx.x == 0 && (int)threadIdx.x < A.sc.n_fields)   // the batch's scalar fields, once per sample
+    A.sc.outs[threadIdx.x][s] = A.sc.cols[threadIdx.x][A.sc.idx[s]];
   const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
   if (d->skip) return;
   const int C = kC > 0 ? kC : P.channels;
