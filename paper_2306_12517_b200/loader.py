@@ -506,7 +506,9 @@ class _EpochRun:
             count = len(indices)
             arrays = {}
             for fd in ld._fields:
-                t = fd.outs[slot][:count]
+                t = fd.outs[slot]
+                if count != t.shape[0]:                  # full batches hand out the slot tensor itself
+                    t = t[:count]
                 if fd.nchw:
                     t = t.permute(0, 3, 1, 2)
                 arrays[fd.name] = t
