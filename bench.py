@@ -432,7 +432,9 @@ def main():
                           "(scale 0.08-1, ratio 3/4-4/3, bilinear) + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC",
               "batch_per_gpu": B, "global_batch": B * world, "num_samples": N_SAMPLES, "order": "random",
               "out_dtype": "f16", "l2_policy": "inputs larger than L2: each step reads ~100 MB of payload and "
-                                               "writes 113 MB of output; 3 output slots rotate"}
+                                               "writes 113 MB of output; 6 output slots rotate",
+              "timing": "timed steps come from a fresh iterator created inside the timed region (the warm-up "
+                        "iterator and its prefetched batches are drained first): pipeline fill included"}
 
     if args.impl == "reference":
         if rank != 0:
