@@ -496,7 +496,8 @@ def main():
     peak, peak_src = peaks()
 
     # ---- e2e: payloads staged from host (mmap -> pinned -> H2D) every step
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache())
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(),
+                           slot_count=int(os.environ.get("BBX_BENCH_E2E_SLOTS", "4")))
     e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
     st2 = ld2.stats()
     ld2.shutdown()
