@@ -184,7 +184,7 @@ typedef struct {
  * first submit; ignored when the plan cannot use it. */
 bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
 /* Turn per-launch CUDA-event timing of the transform kernels on/off. */
-bbx_status bbx_loader_set_profiling(bbx_loader* ld, int enabled);
+bbx_status bbx_loader_set_profiling(bbx_loader* ld, int enabled);   /* enabled > 1: every n-th batch */
 bbx_status bbx_loader_get_stats(const bbx_loader* ld, bbx_loader_stats* out);
 bbx_status bbx_loader_reset_stats(bbx_loader* ld);
 /* The CUDA stream the loader's kernels run on (cudaStream_t as void*). */

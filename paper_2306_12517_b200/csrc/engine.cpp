@@ -240,6 +240,8 @@ struct bbx_loader {
   bool stop = false;
   bbx_loader_stats stats{};
   bool profiling = false;
+  int prof_every = 1;                // profile every n-th batch (bbx_loader_set_profiling(n))
+  uint64_t prof_seq = 0;
   cudaEvent_t t_ref{};               // profiling: reference for absolute batch times (idle gaps)
   float last_k1_ms = -1.f;
   std::mutex stats_mu;
@@ -1177,7 +1179,7 @@ static int process_slot(bbx_loader* L, int s) {
   }
   CK(cudaEventRecord(S.h2d_done, L->copy_st));
   S.h2d_timed = false;
-  if (L->profiling) {
+  if (L->profiling && L->prof_every == 1) {   // idle-gap attribution needs every batch timed
     if (!S.h2d_t) CK(cudaEventCreate(&S.h2d_t));
     CK(cudaEventRecord(S.h2d_t, L->copy_st));
     S.h2d_timed = true;
@@ -1191,7 +1193,9 @@ static int process_slot(bbx_loader* L, int s) {
   }
   if (wait_release) CK(cudaStreamWaitEvent(L->comp_st, S.release, 0));
   int launches = 0;
-  const bool prof = L->profiling;
+  // profiling: every prof_every-th batch gets the CUDA-event window (sampling keeps
+  // the events' own cost off most batches)
+  const bool prof = L->profiling && (L->prof_seq++ % (uint64_t)L->prof_every) == 0;
   int64_t kbytes = 0, klaunch = 0;
   if (prof && !L->t_ref) {
     CK(cudaEventCreate(&L->t_ref));
@@ -1587,7 +1591,7 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
         float a0 = 0.f, a1 = 0.f;   // absolute k0 / k1 against the loader's reference event
         if (L->t_ref && cudaEventElapsedTime(&a0, L->t_ref, S.k0) == cudaSuccess &&
             cudaEventElapsedTime(&a1, L->t_ref, S.k1) == cudaSuccess) {
-          if (L->last_k1_ms >= 0.f && a0 > L->last_k1_ms) {
+          if (L->prof_every == 1 && L->last_k1_ms >= 0.f && a0 > L->last_k1_ms) {
             L->stats.gap_seconds += (a0 - L->last_k1_ms) * 1e-3;
             float ah = 0.f;   // of that gap: the part spent waiting for this batch's H2D (host-late staging)
             if (S.h2d_timed && cudaEventElapsedTime(&ah, L->t_ref, S.h2d_t) == cudaSuccess && ah > L->last_k1_ms)
@@ -1744,6 +1748,9 @@ bbx_status bbx_loader_set_profiling(bbx_loader* L, int enabled) {
   if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
   std::lock_guard<std::mutex> g(L->mu);
   L->profiling = enabled != 0;
+  L->prof_every = enabled > 1 ? enabled : 1;
+  L->prof_seq = 0;
+  L->last_k1_ms = -1.f;
   return BBX_OK;
 }
 void* bbx_loader_compute_stream(bbx_loader* L) { return L ? (void*)L->comp_st : nullptr; }

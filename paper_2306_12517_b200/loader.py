@@ -365,8 +365,9 @@ class Loader:
             with self._epoch_lock:
                 self._active = None
 
-    def set_profiling(self, enabled: bool = True) -> None:
-        """CUDA-event timing of the transform kernels (stats()['kernel_seconds'])."""
+    def set_profiling(self, enabled: bool | int = True) -> None:
+        """CUDA-event timing of the transform kernels (stats()['kernel_seconds']);
+        an int n > 1 times every n-th batch only (the events' cost stays off the rest)."""
         _lib.check(_lib.lib().bbx_loader_set_profiling(self._handle, int(enabled)))
 
     def reset_stats(self) -> None:
