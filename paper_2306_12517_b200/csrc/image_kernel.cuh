@@ -521,21 +521,24 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 }
 
 // ------------------------------------------------------- K1 (column walker)
-// Bilinear decoders, 3 channels.  Persistent CTAs walk the batch's tiles
-// (tile = rows_per_tile output rows of one sample; CTA b takes a run of
-// consecutive tiles) through a two-stage shared-memory pipeline: while the compute warps
-// work on tile i out of one stage, the source-row segments of tile i + 1 are
-// already landing in the other, moved by the copy engine (cp.async.bulk, one
-// 1-D bulk copy per source row, completion counted in bytes on the stage's
-// "full" mbarrier).  A dedicated copy warp computes each tile's geometry
-// (column table, source-row range, row taps) into the stage, issues its
-// copies once the compute warps have released the stage ("empty" mbarrier),
-// and runs ahead by one tile.
+// Bilinear decoders, 3 channels.  Persistent CTAs (SMs x resident CTAs) walk the
+// batch's tiles (tile = rows_per_tile output rows of one sample), taking runs of
+// cw_run consecutive tiles from a global ticket that the last CTA re-zeroes, so
+// SMs that drew cheap samples take more.  Per CTA a two-stage shared-memory
+// pipeline: while the compute warps work on tile i out of one stage, the
+// source rows of tile i + 1 are landing in the other, moved by the copy engine
+// (one cp.async.bulk per tile: the tile's rows are consecutive rows of a
+// row-strided image; completion counted in bytes on the stage's "full"
+// mbarrier).  A dedicated copy warp takes the tickets, computes each tile's
+// geometry (column table once per sample, row taps) into a ring entry, issues
+// the copy once the compute warps have released the stage ("empty" mbarrier),
+// gathers the batch's scalar fields with tile 0 of each sample, and finally
+// posts a stop entry.
 // Compute: thread x owns output columns 2x, 2x + 1 and walks a run of the
 // tile's rows: the 2-tap horizontal sums of a source row are computed in
-// registers when a row first appears (and kept for the next output row that
-// reuses it), then the vertical blend, the value table and the store.  Same
-// integer arithmetic as image_kernel (bit-identical).
+// registers when a row first appears (one register set per slot parity, kept
+// for the next output row that reuses it), then the vertical blend, the value
+// table and the store.  Same integer arithmetic as image_kernel (bit-identical).
 __host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }   // table slots
 __host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
 __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
