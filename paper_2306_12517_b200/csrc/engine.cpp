@@ -1487,7 +1487,11 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (const char* e = std::getenv("BBX_JPEG_PREFETCH")) L->jpeg_prefetch = std::atoi(e) != 0;
   if (const char* e = std::getenv("BBX_J2_PER_LANE")) L->j2_per_lane = std::atoi(e);
   int nt = staging_threads;
-  if (nt <= 0) nt = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (nt <= 0) {   // automatic: the host's cores shared by the node's ranks (torchrun LOCAL_WORLD_SIZE)
+    unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) hc = std::max(1u, hc / (unsigned)std::max(1, std::atoi(e)));
+    nt = (int)std::min<unsigned>(16, hc);
+  }
   if (const char* e = std::getenv("BBX_STAGING_THREADS")) if (staging_threads <= 0) nt = std::max(1, std::atoi(e));
   L->pool = std::make_unique<Pool>(nt);
   if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
