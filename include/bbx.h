@@ -183,6 +183,20 @@ typedef struct {
  * host memory over PCIe -- no CPU gather, no staging copy.  Call before the
  * first submit; ignored when the plan cannot use it. */
 bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
+/* Loader tuning options (before the first submit; the defaults are the
+ * measured-best settings):
+ *   "window_staging"        1: stage only the rows x columns a RAW sample's chain reads
+ *   "dma"                   1: let the copy engine read a registered host heap directly
+ *   "jpeg_header_cache"     1: keep each JPEG sample's parsed header for later epochs
+ *   "jpeg_header_prefetch"  1: parse the headers of this loader's samples up front
+ *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
+ * Unknown names return BBX_INVALID_ARGUMENT. */
+bbx_status bbx_loader_set_option(bbx_loader* ld, const char* name, int64_t value);
+/* Samples whose JPEG headers the loader parses up front (before the first
+ * submit).  A distributed rank passes its shard of the first epoch so that
+ * ranks do not each parse every header; others are parsed on first sight
+ * and cached.  Without a call: every sample (single-process loaders). */
+bbx_status bbx_loader_prefetch_headers(bbx_loader* ld, const int64_t* idx, int64_t n);
 /* Turn per-launch CUDA-event timing of the transform kernels on/off. */
 bbx_status bbx_loader_set_profiling(bbx_loader* ld, int enabled);   /* enabled > 1: every n-th batch */
 bbx_status bbx_loader_get_stats(const bbx_loader* ld, bbx_loader_stats* out);

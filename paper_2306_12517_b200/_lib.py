@@ -65,10 +65,6 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    lib_path = Path(os.environ.get("BBX_LIB", LIB_PATH))   # BBX_LIB: load another build (kernel experiments)
-    if lib_path != LIB_PATH:
-        L = ctypes.CDLL(str(lib_path))
-        return _bind(L)
     if os.environ.get("BBX_NO_BUILD") != "1":
         from . import _build
         try:
@@ -111,6 +107,8 @@ def _bind(L):
         "bbx_loader_compute_stream": (c_vp, [c_vp]),
         "bbx_loader_set_profiling": (c_i32, [c_vp, ctypes.c_int]),
         "bbx_loader_set_zero_copy": (c_i32, [c_vp, ctypes.c_int]),
+        "bbx_loader_set_option": (c_i32, [c_vp, ctypes.c_char_p, c_i64]),
+        "bbx_loader_prefetch_headers": (c_i32, [c_vp, c_vp, c_i64]),
         "bbx_decode_image": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -128,7 +126,8 @@ EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_cl
             "bbx_loader_add_scalar", "bbx_loader_bind", "bbx_loader_submit", "bbx_loader_wait",
             "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",
             "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling",
-            "bbx_loader_set_zero_copy", "bbx_decode_image")
+            "bbx_loader_set_zero_copy", "bbx_loader_set_option", "bbx_loader_prefetch_headers",
+            "bbx_decode_image")
 
 
 def last_error() -> str:

@@ -16,10 +16,7 @@ constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
 constexpr int kDescHeader = 32;     // bytes before the per-sample params
 constexpr int kCwCols = 2;          // column-walker K1: output columns per thread
-#ifndef BBX_CW_STAGES
-#define BBX_CW_STAGES 2
-#endif
-constexpr int kCwStages = BBX_CW_STAGES;   // column-walker K1: source-row pipeline stages
+constexpr int kCwStages = 2;   // column-walker K1: source-row pipeline stages
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;

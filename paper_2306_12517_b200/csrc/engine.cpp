@@ -223,8 +223,8 @@ struct bbx_loader {
   JpegTables jt;
   bool jpeg_cache = true;             // keep each sample's prepared JpegDesc (headers parse once per loader)
   bool jpeg_roi = true;               // decode only the MCUs a sample's chain reads (BBX_JPEG_ROI=0: whole image)
-  int j2_per_lane = 0;                // > 0: intervals per J2 lane (experiments)
-  bool jpeg_prefetch = true;          // parse every sample's header at finalize (file fits in RAM; BBX_JPEG_PREFETCH=0: lazily)
+  bool jpeg_prefetch = true;          // parse headers at finalize (file fits in RAM; option "jpeg_header_prefetch" 0: lazily)
+  std::vector<int64_t> prefetch_set;  // samples whose headers finalize parses (empty: every sample)
   bool zero_copy = false;             // requested: kernels read payloads from the pinned host heap
   const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
   bool zc = false;                    // payload_dev is host memory (zero-copy)
@@ -410,21 +410,19 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       P.n_vops = 1;
     }
     // C <= 4: the whole value chain u8 -> output is a 256-entry table per
-    // channel, built on the host with the reference's exact arithmetic.
-    // value chain on a u8 input: a 256-entry table per channel (one smem load per
-    // element), or arithmetic (BBX_VALUE_ALU=1: the divide-free form when proven exact)
-    const bool alu = std::getenv("BBX_VALUE_ALU") && std::atoi(std::getenv("BBX_VALUE_ALU")) != 0;
+    // channel (one smem load per element), built on the host with the
+    // reference's exact arithmetic; wider images use the divide-free form
+    // when it is proven exact, else the IEEE divide.
     P.value_mode = !has_values ? VAL_COPY
-                 : (C <= 4 && !alu) ? VAL_LUT
+                 : C <= 4 ? VAL_LUT
                  : verify_fma_normalize(P, C) ? VAL_FMA : VAL_DIRECT;
     if (P.value_mode == VAL_COPY && out_dt != BBX_U8) return fail(BBX_SPEC_MISMATCH, "unexpected output dtype");
     // tile height: 16 rows, shrunk until the smem layout allows 4 CTAs per SM
     P.rows_per_tile = std::min(16, H);
-    if (const char* e = std::getenv("BBX_ROWS_PER_TILE")) P.rows_per_tile = std::max(1, std::min({std::atoi(e), H, 16}));
     for (;;) {
       P.lay = img_layout_host(P);
       P.smem_bytes = P.lay.total;
-      if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1 || std::getenv("BBX_ROWS_PER_TILE")) break;
+      if (P.smem_bytes <= kSmemTarget || P.rows_per_tile == 1) break;
       P.rows_per_tile = std::max(1, P.rows_per_tile / 2);
     }
     if (P.smem_bytes > kSmemBudget || (int64_t)P.src_row_w * C + 64 > 65535)
@@ -450,17 +448,14 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     P.lay = img_layout_host(P);
     P.h_tpc = std::max(1, kThreads / W);
     P.tab_stride = image_tab_stride(P);
-    // column-walker K1 for 3-channel bilinear decoders (BBX_CW=0 keeps the tile kernel)
+    // column-walker K1 for 3-channel bilinear decoders
     P.cw = 0;
-    const char* cwe = std::getenv("BBX_CW");
-    if (P.src_kind == SRC_RESAMPLE && C == 3 && !(cwe && std::atoi(cwe) == 0)) {
+    if (P.src_kind == SRC_RESAMPLE && C == 3) {
       // rows per tile: 16, fewer when two pipeline stages of source rows would
       // not leave room for 2 CTAs per SM (nslot = 2 x rows <= 64)
-      int rows_env = 0;
-      if (const char* e = std::getenv("BBX_CW_ROWS")) rows_env = std::max(1, std::min(std::atoi(e), 32));
       for (int rows : {16, 8, 4, 2}) {
         PlanDev Q = P;
-        Q.rows_per_tile = std::min(rows_env ? rows_env : rows, H);
+        Q.rows_per_tile = std::min(rows, H);
         Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
         Q.lay = img_layout_host(Q);
         Q.tab_stride = image_tab_stride(Q);
@@ -474,7 +469,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
             if (Q.remaps[i].kind == BBX_OP_RESIZE)
               n = ((n - 1) * Q.remaps[i].in_h + Q.remaps[i].out_h - 1) / Q.remaps[i].out_h + 1;
           const int64_t src = ((n - 1) * f.info.max_height + Q.canvas_h - 1) / Q.canvas_h + 2;
-          if (src > 64) { if (rows_env) break; continue; }
+          if (src > 64) continue;
           Q.cw_slots = (int)((src + 1) & ~1LL);
         }
         Q.cw_smem = cw_smem_host(Q);
@@ -496,19 +491,13 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
           }
           Q.cw_groups = best_g;
           Q.cw_warps = best_w;
-          if (const char* e = std::getenv("BBX_CW_GROUPS")) {
-            Q.cw_groups = std::max(1, std::min(std::atoi(e), Q.rows_per_tile));
-            Q.cw_warps = std::min(8, (Q.cw_npair * Q.cw_groups + 31) / 32);
-          }
         }
         Q.cw_rg = (Q.rows_per_tile + Q.cw_groups - 1) / Q.cw_groups;
         Q.cw_run = 3;
-        if (const char* e = std::getenv("BBX_CW_RUN")) Q.cw_run = std::max(1, std::atoi(e));
         const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
         Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
                          ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
         if (Q.cw_smem <= 110 * 1024) { P = Q; P.cw = 1; break; }
-        if (rows_env) break;
       }
     }
     if ((W + 3 * H) * 4 > kSmemBudget) return fail(BBX_SPEC_MISMATCH, "output too large for the device plan");
@@ -613,6 +602,12 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
     *src_off = c.offset; *len = (uint32_t)c.length;
     d->len = (uint32_t)c.length;
     if (c.length > 0xFFFFFFFFull) return bad(BBX_CORRUPT_PAYLOAD, "payload of %llu bytes is too large", (unsigned long long)c.length);
+    // the payload must lie inside the heap: staging reads the mmap and resident /
+    // paged plans read the HBM heap image, both of which span exactly the heap
+    if (c.length && ((int64_t)c.offset < ds->heap_offset || c.offset + c.length > (uint64_t)ds->alloc_table_offset))
+      return bad(BBX_CORRUPT_PAYLOAD, "payload [%llu, %llu) lies outside the heap [%lld, %lld)",
+                 (unsigned long long)c.offset, (unsigned long long)(c.offset + c.length), (long long)ds->heap_offset,
+                 (long long)ds->alloc_table_offset);
     int mh = f.info.max_height, mw = f.info.max_width, ch = f.info.channels;
     if (pl.dev.src_kind == SRC_DECODE) {        // decode_image(out[:h, :w, :]) shape check
       if (c.h > mh || c.w > mw || c.c != ch)
@@ -642,7 +637,10 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
     *src_off = u64_cell(ds, i, f);
     *len = (uint32_t)f.array_nbytes;
     d->len = (uint32_t)f.array_nbytes;
-    if (*src_off + f.array_nbytes > ds->map_len) return bad(BBX_INVALID_FILE, "array payload past end of file");
+    if ((int64_t)*src_off < ds->heap_offset || *src_off + f.array_nbytes > (uint64_t)ds->alloc_table_offset)
+      return bad(BBX_CORRUPT_PAYLOAD, "array payload [%llu, %llu) lies outside the heap [%lld, %lld)",
+                 (unsigned long long)*src_off, (unsigned long long)(*src_off + f.array_nbytes),
+                 (long long)ds->heap_offset, (long long)ds->alloc_table_offset);
   }
   // per-sample stream (loader.py:339): stream_seed(seed, TAG_SAMPLE, epoch, i, fidx)
   Rng r(fold(fold(fold(fold(seed, 2), epoch), (uint64_t)i), (uint64_t)pl.field_index));
@@ -892,16 +890,24 @@ static int finalize(bbx_loader* L) {
   // sits comfortably in RAM (reading the headers touches every sample): the
   // first epoch's batches then cost what later ones do.  Samples whose header
   // does not parse stay uncached and report their error in their batch.
+  // A distributed loader names the samples it will see first (its shard of the
+  // first epoch, bbx_loader_prefetch_headers), so ranks do not all parse every header.
   if (any_jpeg && L->jpeg_cache && L->jpeg_prefetch) {
     const bbx_dataset* ds = L->ds;
     const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
     if ((double)ds->map_len < 0.25 * (double)pages * (double)psz) {
+      const bool subset = !L->prefetch_set.empty();
+      const int64_t n = subset ? (int64_t)L->prefetch_set.size() : ds->num_samples;
       for (auto& pl : L->plans) {
         if (pl.scalar || !pl.field_has_jpeg) continue;
         const Field& f = ds->fields[pl.field_index];
-        L->pool->parallel_for(ds->num_samples, [&](int64_t i) {
+        L->pool->parallel_for(n, [&](int64_t k) {
+          const int64_t i = subset ? L->prefetch_set[k] : k;
+          if (i < 0 || i >= ds->num_samples || pl.jcached[i]) return;
           const ImageCell c = image_cell(ds, i, f);
-          if (c.codec != CODEC_JPEG || c.length > 0xFFFFFFFFull || c.offset + c.length > ds->map_len) return;
+          if (c.codec != CODEC_JPEG || c.length > 0xFFFFFFFFull || (int64_t)c.offset < ds->heap_offset ||
+              c.offset + c.length > (uint64_t)ds->alloc_table_offset)
+            return;
           SampleDesc d{};
           d.h = (uint16_t)c.h; d.w = (uint16_t)c.w; d.c = (uint8_t)c.c;
           JpegDesc J;
@@ -930,7 +936,6 @@ static int finalize(bbx_loader* L) {
         ds->host_registered = true;
       } else {
         cudaGetLastError();   // clear a refused registration; fall back to the gather pool
-        if (std::getenv("BBX_DEBUG")) std::fprintf(stderr, "bbx: cudaHostRegister(mmap) refused: %s\n", cudaGetErrorString(re));
       }
     }
     L->dma = ds->dma_base() != nullptr;
@@ -1158,7 +1163,6 @@ static int process_slot(bbx_loader* L, int s) {
       dma_done = true;
     } else {
       cudaGetLastError();
-      if (std::getenv("BBX_DEBUG")) std::fprintf(stderr, "bbx: cudaMemcpy3DBatchAsync failed (op %zu): %s\n", fail_idx, cudaGetErrorString(e));
       L->dma = false;   // unsupported here: gather on the host from now on
     }
   }
@@ -1261,7 +1265,6 @@ static int process_slot(bbx_loader* L, int s) {
       J.coef_zeroed = 1;
       J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
       J.max_blocks = S.jpeg_max_blocks[p];
-      J.j2_per_lane = L->j2_per_lane;
       // J2 stores only nonzero coefficients
       CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
       if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -1480,19 +1483,12 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   auto L = std::make_unique<bbx_loader>();
   L->ds = ds; L->device = device; L->batch = batch_size; L->nslots = slot_count;
   L->slots.resize(slot_count);
-  if (const char* e = std::getenv("BBX_WINDOW_STAGING")) L->window_staging = std::atoi(e) != 0;
-  if (const char* e = std::getenv("BBX_DMA")) L->dma_allowed = std::atoi(e) != 0;
-  if (const char* e = std::getenv("BBX_JPEG_CACHE")) L->jpeg_cache = std::atoi(e) != 0;
-  if (const char* e = std::getenv("BBX_JPEG_ROI")) L->jpeg_roi = std::atoi(e) != 0;
-  if (const char* e = std::getenv("BBX_JPEG_PREFETCH")) L->jpeg_prefetch = std::atoi(e) != 0;
-  if (const char* e = std::getenv("BBX_J2_PER_LANE")) L->j2_per_lane = std::atoi(e);
   int nt = staging_threads;
   if (nt <= 0) {   // automatic: the host's cores shared by the node's ranks (torchrun LOCAL_WORLD_SIZE)
     unsigned hc = std::max(1u, std::thread::hardware_concurrency());
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) hc = std::max(1u, hc / (unsigned)std::max(1, std::atoi(e)));
     nt = (int)std::min<unsigned>(16, hc);
   }
-  if (const char* e = std::getenv("BBX_STAGING_THREADS")) if (staging_threads <= 0) nt = std::max(1, std::atoi(e));
   L->pool = std::make_unique<Pool>(nt);
   if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&L->comp_st, cudaStreamNonBlocking)) != cudaSuccess)
@@ -1732,6 +1728,28 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* L, int enabled) {
   if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
   if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
   L->zero_copy = enabled != 0;
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_prefetch_headers(bbx_loader* L, const int64_t* idx, int64_t n) {
+  if (!L || (n > 0 && !idx)) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
+  L->prefetch_set.assign(idx, idx + std::max<int64_t>(n, 0));
+  std::sort(L->prefetch_set.begin(), L->prefetch_set.end());   // distinct: one pool task per sample
+  L->prefetch_set.erase(std::unique(L->prefetch_set.begin(), L->prefetch_set.end()), L->prefetch_set.end());
+  return BBX_OK;
+}
+
+bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value) {
+  if (!L || !name) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
+  const std::string n(name);
+  if (n == "window_staging") L->window_staging = value != 0;
+  else if (n == "dma") L->dma_allowed = value != 0;
+  else if (n == "jpeg_header_cache") L->jpeg_cache = value != 0;
+  else if (n == "jpeg_roi") L->jpeg_roi = value != 0;
+  else if (n == "jpeg_header_prefetch") L->jpeg_prefetch = value != 0;
+  else return (bbx_status)fail(BBX_INVALID_ARGUMENT, "unknown loader option '%s'", name);
   return BBX_OK;
 }
 

@@ -268,10 +268,7 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
 // (the block buffer is pre-zeroed).  Block ends read the next block's
 // component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 128;
-#ifndef BBX_EXTRA_SYMBOLS
-#define BBX_EXTRA_SYMBOLS 4
-#endif
-constexpr int kExtraSymbols = BBX_EXTRA_SYMBOLS;   // AC symbols decoded after the first in one iteration
+constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
 
@@ -780,7 +777,6 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   // unequal lengths once there are enough intervals to keep every SM busy
   const uint32_t lanes = 148u * 4u * kHuffThreads;
   uint32_t per_lane = min(8u, max(1u, A.total_int / lanes));
-  if (A.j2_per_lane > 0) per_lane = (uint32_t)A.j2_per_lane;
   const uint32_t chunk = per_lane * kHuffThreads;
   const unsigned hgrid = (A.total_int + chunk - 1) / chunk;
   if (smem) {

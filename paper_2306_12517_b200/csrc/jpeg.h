@@ -154,7 +154,6 @@ struct JpegArgs {
   uint64_t total_blocks;
   int32_t max_quads;                      // largest image height in the batch (J4 grid: bands of rows)
   uint32_t max_blocks;                    // most blocks of one sample in the batch (J3 grid)
-  int32_t j2_per_lane;                    // > 0: intervals per J2 lane (BBX_J2_PER_LANE; 0 = automatic)
 };
 
 // jpeg.cu

@@ -158,9 +158,10 @@ def agree_seed(config: LoaderConfig, device: int | None = None) -> int:
     dev = "cpu"
     if dist.get_backend() == "nccl":
         dev = f"cuda:{device if device is not None else torch.cuda.current_device()}"
-    t = torch.tensor([config.seed & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+    u = config.seed & 0xFFFFFFFFFFFFFFFF             # the full 64-bit seed, as two's-complement int64
+    t = torch.tensor([u - (1 << 64) if u >= (1 << 63) else u], dtype=torch.int64, device=dev)
     dist.broadcast(t, src=0)
-    return int(t.item())
+    return int(t.item()) & 0xFFFFFFFFFFFFFFFF
 
 
 def _fits_pinned(nbytes: int, fraction: float) -> bool:
@@ -173,20 +174,42 @@ def _fits_pinned(nbytes: int, fraction: float) -> bool:
 
 
 def shard_batches(global_batches: list, rank: int, world_size: int, batch_size: int) -> list:
-    """Rank r's slice [r*B, (r+1)*B) of every global batch."""
+    """Rank r's share of every global batch of world_size * B positions.
+
+    A full global batch gives rank r positions [r*B, (r+1)*B).  A short tail of
+    t positions is padded to t' = ceil(t / W) * W by wrapping around to the
+    epoch's first indices (as torch's DistributedSampler pads) and split evenly,
+    t' / W positions per rank, so every rank gets the same number of batches and
+    a DDP step never waits on a rank that has run out."""
     out = []
+    full = world_size * batch_size
     for gb in global_batches:
-        part = gb[rank * batch_size:(rank + 1) * batch_size]
-        if len(part):
-            out.append(part)
+        gb = np.asarray(gb, dtype=np.int64)
+        if len(gb) == full or world_size == 1:
+            out.append(gb[rank * batch_size:(rank + 1) * batch_size])
+            continue
+        t = len(gb)
+        per = -(-t // world_size)
+        pad = per * world_size - t
+        if pad:                                      # pad < W: the epoch's first indices (cycled)
+            head, have = [], 0
+            for b in global_batches:
+                head.append(np.asarray(b, dtype=np.int64))
+                have += len(head[-1])
+                if have >= pad:
+                    break
+            first = np.concatenate(head)
+            gb = np.concatenate([gb, first[np.arange(pad) % len(first)]])
+        out.append(gb[rank * per:(rank + 1) * per])
     return out
 
 
 class _Field:
-    __slots__ = ("name", "plan_id", "outs", "nchw", "scalar")
+    __slots__ = ("name", "plan_id", "outs", "nchw", "scalar", "contiguous")
 
-    def __init__(self, name, plan_id, outs, nchw, scalar):
+    def __init__(self, name, plan_id, outs, nchw, scalar, contiguous=False):
         self.name, self.plan_id, self.outs, self.nchw, self.scalar = name, plan_id, outs, nchw, scalar
+        self.contiguous = contiguous
 
 
 class Loader:
@@ -207,6 +230,7 @@ class Loader:
         self._epoch_lock = threading.Lock()
         self._active = None
         self._handle = None
+        self._headers_named = False
         self.rank, self.world_size = _dist_info(config)
         if config.device is not None:
             self.device = int(config.device)
@@ -216,7 +240,7 @@ class Loader:
             self.device = torch.cuda.current_device()
         if config.distributed:   # one-time seed agreement (the only cross-rank traffic)
             seed = agree_seed(config, self.device)
-            if seed != config.seed:
+            if seed != config.seed & 0xFFFFFFFFFFFFFFFF:
                 config = dataclasses.replace(config, seed=seed)
                 self.config = config
                 self.order = TraversalOrder(config.order, config.seed)
@@ -238,9 +262,11 @@ class Loader:
         strategy = self.dataset.strategy
         if isinstance(strategy, DeviceResident) or (
                 isinstance(strategy, ProcessCacheStrategy) and strategy.capacity_pages >= self.dataset.num_pages):
-            dev = strategy.device if isinstance(strategy, DeviceResident) and strategy.device is not None \
-                else self.device
-            self.dataset.make_resident(dev)
+            if isinstance(strategy, DeviceResident) and strategy.device is not None and \
+                    int(strategy.device) != self.device:
+                raise ValueError(f"DeviceResident(device={strategy.device}) but the loader runs on cuda:{self.device}: "
+                                 "the kernels read the heap from the loader's own device")
+            self.dataset.make_resident(self.device)
         elif isinstance(strategy, OsCache) and strategy.pinned and not self.dataset.pinned:
             if not _fits_pinned(self.dataset.header.heap_bytes, OsCache.PIN_HOST_RAM_FRACTION):
                 raise CapacityTooSmall("heap does not fit the pinned host budget")
@@ -288,7 +314,7 @@ class Loader:
                 if oshape != want_shape:
                     raise SpecMismatch(f"device plan shape {oshape} != spec {want_shape}")
                 outs = torch.empty((S, B, *oshape), dtype=_torch_dtype(odt.value), device=dev)
-                self._fields.append(_Field(f.name, pid.value, outs, comp.nchw_view, False))
+                self._fields.append(_Field(f.name, pid.value, outs, comp.nchw_view, False, comp.nchw_contiguous))
                 self.ledger.register(f"arena:{f.name}", outs.numel() * outs.element_size())
             if pipelines:
                 raise SchemaMismatch(f"pipelines for unknown fields: {sorted(pipelines)}")
@@ -313,13 +339,10 @@ class Loader:
         return self._handle
 
     def batches_per_epoch(self) -> int:
+        """The same on every rank (a short tail global batch is padded, shard_batches)."""
         n = self.dataset.num_samples
         gb = self.config.batch_size * self.world_size
-        full = n // gb if self.config.drop_last else -(-n // gb)
-        if self.world_size == 1 or self.config.drop_last:
-            return full
-        tail = n - (n // gb) * gb
-        return n // gb + (1 if tail > self.rank * self.config.batch_size else 0)
+        return n // gb if self.config.drop_last else -(-n // gb)
 
     def epoch_batches(self, epoch: int) -> list:
         """This rank's index lists for `epoch` (the reference order, then sharded)."""
@@ -479,6 +502,12 @@ class _EpochRun:
             return
         stream = torch.cuda.current_stream(ld.device)
         sp = ctypes.c_void_p(stream.cuda_stream)
+        if ld.world_size > 1 and not ld._headers_named:
+            # before the first submit: this rank's shard of the first epoch is what the
+            # loader parses up front (JPEG headers), not every sample of the dataset
+            ld._headers_named = True
+            mine = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int64) for b in self.batch_lists]))
+            _lib.check(L.bbx_loader_prefetch_headers(ld.handle, mine.ctypes.data, len(mine)))
         for g in range(S - 1):
             if self._ensure(g):
                 self._submit(g)
@@ -512,6 +541,8 @@ class _EpochRun:
                     t = t[:count]
                 if fd.nchw:
                     t = t.permute(0, 3, 1, 2)
+                    if fd.contiguous:                    # ToTorchImage(channels_last=False)
+                        t = t.contiguous()
                 arrays[fd.name] = t
             self.stats.batches += 1
             self.stats.samples += count

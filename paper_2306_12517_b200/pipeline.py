@@ -336,7 +336,9 @@ class NormalizeImage(Transform):
 
 
 class ToTorchImage(Transform):
-    """Batch view as (N, C, H, W) over the channels-last buffer (no copy)."""
+    """Batch as (N, C, H, W): channels_last=True is a view over the channels-last
+    buffer (no copy); channels_last=False is a contiguous NCHW copy (FFCV's
+    ToTorchImage fills a contiguous buffer in that case)."""
 
     name = "to-torch-image"
     view_only = True
@@ -453,6 +455,7 @@ class CompiledChain:
     ops: list                 # bbx_op records
     specs: list               # per-transform output specs (reference spec propagation)
     nchw_view: bool           # ToTorchImage at the end
+    nchw_contiguous: bool = False   # ToTorchImage(channels_last=False): contiguous NCHW copy
 
 
 def compile_chain(transforms, input_spec) -> CompiledChain:
@@ -465,7 +468,7 @@ def compile_chain(transforms, input_spec) -> CompiledChain:
         raise SpecMismatch("source transforms may only appear first")
     specs, ops = [], []
     spec = input_spec
-    nchw = False
+    nchw = contiguous = False
     for t in transforms:
         out = t.output_spec(spec)
         t.prepare(spec, out)
@@ -474,9 +477,10 @@ def compile_chain(transforms, input_spec) -> CompiledChain:
                                "(no CPU fallback); express it with device transforms")
         if isinstance(t, ToTorchImage):
             nchw = t.channels_last is not None
+            contiguous = t.channels_last is False
         elif nchw and not getattr(t, "view_only", False):
             raise SpecMismatch("to-torch-image must be the last transform")
         ops.extend(t.to_ops(spec))
         specs.append(out)
         spec = out
-    return CompiledChain(ops, specs, nchw)
+    return CompiledChain(ops, specs, nchw, contiguous)
