@@ -79,6 +79,13 @@ struct PlanDev {
   SmemLayout lay;
 };
 
+// Row pitch of a JPEG sample's decoded (HWC u8) scratch image: 16-byte aligned
+// rows, so J4 stores whole 8-byte words and K1 bulk-copies from aligned rows.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int64_t jpeg_scratch_pitch(int w, int c) { return ((int64_t)w * c + 15) / 16 * 16; }
+
 // Per-sample descriptor header (kDescHeader bytes), followed by n_params int32.
 struct SampleDesc {
   uint64_t src;    // payload byte offset from the launch's payload base

@@ -428,7 +428,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     if (P.smem_bytes > kSmemBudget || (int64_t)P.src_row_w * C + 64 > 65535)
       return fail(BBX_SPEC_MISMATCH, "image rows too wide for the device plan (%d x %d channels)", P.src_row_w, C);
     P.tiles_per_sample = (H + P.rows_per_tile - 1) / P.rows_per_tile;
-    P.scratch_bytes = ((int64_t)f.info.max_height * f.info.max_width * C + 15) / 16 * 16;
+    P.scratch_bytes = (int64_t)f.info.max_height * jpeg_scratch_pitch(f.info.max_width, C);   // RLE: h*w*C <= this
     // fast-division constants (exact when n * d < 2^32)
     const uint64_t two32 = 1ull << 32;
     const int nslot = P.rows_per_tile * (P.src_kind == SRC_RESAMPLE ? 2 : 1);
@@ -1376,7 +1376,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
   A.isample = reinterpret_cast<uint32_t*>(dev + o_isa);
   A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
-  A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c;
+  A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c; A.exact_pitch = 1;   // (h, w, c) output, no row padding
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
   A.n_huff = L.jt.n_huff;
   A.coef_zeroed = 1;

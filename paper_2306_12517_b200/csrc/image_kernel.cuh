@@ -180,7 +180,8 @@ __device__ __forceinline__ SrcRows src_rows_of(const PlanDev& P, const LaunchArg
   SrcRows S;
   const int C = P.channels, w = d->w, h = d->h;
   if (d->codec == CODEC_RLE || d->codec == CODEC_JPEG) {   // decoded into scratch by K2 / J1-J4
-    S.base = A.scratch + (size_t)s * P.scratch_bytes; S.sh = 0; S.rstride = (int64_t)w * C;
+    S.base = A.scratch + (size_t)s * P.scratch_bytes; S.sh = 0;
+    S.rstride = d->codec == CODEC_JPEG ? jpeg_scratch_pitch(w, C) : (int64_t)w * C;
   } else if (d->flags & kDescWindowed) {
     // only the rows/columns the chain reads were staged: a virtual origin makes
     // every in-window image coordinate address its staged byte

@@ -14,12 +14,6 @@
 
 namespace bbx {
 
-__constant__ uint8_t c_natural[80] = {   // zig-zag -> natural, + overrun guard (T.81 Fig. A.6)
-    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,  12, 19, 26, 33,
-    40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28, 35, 42, 49, 56, 57, 50, 43, 36,
-    29, 22, 15, 23, 30, 37, 44, 51, 58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54,
-    47, 55, 62, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63, 63};
-
 __device__ __forceinline__ const SampleDesc* sdesc(const JpegArgs& A, int s) {
   return reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * A.desc_stride);
 }
@@ -267,7 +261,8 @@ __global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const 
 // a branch-free EXTEND, and a store of the coefficient when it is nonzero
 // (the block buffer is pre-zeroed).  Block ends read the next block's
 // component / offset / tables from a per-thread slot table in shared memory.
-constexpr int kHuffThreads = 128;
+constexpr int kHuffThreads = 256;           // 8 warps share one copy of the smem tables
+constexpr int kHuffCtasPerSm = 4;           // 32 warps per SM: <= 64 registers per thread
 constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
@@ -276,10 +271,8 @@ template <typename T>
 __device__ __forceinline__ T sel3(int i, T a, T b, T c) { return i == 0 ? a : (i == 1 ? b : c); }
 
 template <bool kSmem>
-__global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegArgs A, uint32_t chunk) {
+__global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_kernel(const JpegArgs A) {
   extern __shared__ __align__(16) uint8_t hsm[];
-  __shared__ uint8_t nat[80];
-  __shared__ uint32_t s_next;
   constexpr int TW = 1 << kJpegFastBits;
   constexpr uint32_t TSTRIDE = kSmem ? TW : (uint32_t)(sizeof(JHuff) / 4);
   const int tabs_bytes = kSmem ? A.n_huff * TW * 4 : 0;
@@ -301,17 +294,45 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
       slow[i] = v;
     }
   }
-  for (int i = threadIdx.x; i < 80; i += kHuffThreads) nat[i] = c_natural[i];
-  // this CTA's intervals [c0, c1): lanes start on the first kHuffThreads, then pull from s_next
-  const uint32_t c0 = blockIdx.x * chunk, c1 = min(c0 + chunk, A.total_int);
-  if (threadIdx.x == 0) s_next = c0 + kHuffThreads;
+  // This CTA's intervals [c0, c0 + kHuffThreads), ordered longest first so
+  // that each warp decodes intervals of similar length (a warp runs until its
+  // longest lane finishes; interval lengths vary ~4x within an image).  Key:
+  // unstuffed bytes + 1 (0: outside the region of interest or a rejected
+  // sample: never decoded) | position.
+  __shared__ uint32_t skey[kHuffThreads];
+  const uint32_t c0 = blockIdx.x * kHuffThreads;
+  {
+    const uint32_t t = c0 + threadIdx.x;
+    uint32_t key = 0;
+    if (t < A.total_int) {
+      const uint32_t si = __ldg(&A.isample[t]);
+      if (A.status[si].kind == 0) {
+        const JpegDesc& J = A.jd[si];
+        if (jpeg_interval_live(J, jpeg_mcu_rect(J), t - J.int_base))
+          key = min(A.iend[t] - A.istart[t] + 1u, 0xFFFFFFu) << 8;
+      }
+    }
+    skey[threadIdx.x] = key | threadIdx.x;
+  }
   __syncthreads();
+#pragma unroll 1
+  for (int kb = 2; kb <= kHuffThreads; kb <<= 1)      // bitonic sort, descending
+#pragma unroll 1
+    for (int j = kb >> 1; j > 0; j >>= 1) {
+      const int ixj = threadIdx.x ^ j;
+      if (ixj > (int)threadIdx.x) {
+        const uint32_t a = skey[threadIdx.x], b = skey[ixj];
+        if (((threadIdx.x & kb) == 0) ? a < b : a > b) { skey[threadIdx.x] = b; skey[ixj] = a; }
+      }
+      __syncthreads();
+    }
+  const uint32_t mine = skey[threadIdx.x];
 
   // per-lane decoder state of the current restart interval
   const uint4* p16 = nullptr;
   const uint4* plast = nullptr;
-  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;          // next stream words; nxt = the chunk after them
-  uint4 nxt = make_uint4(0, 0, 0, 0);
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;          // next stream words; nxt, nxt2 = the two chunks after them
+  uint4 nxt = make_uint4(0, 0, 0, 0), nxt2 = make_uint4(0, 0, 0, 0);   // (two loads in flight hide L2 latency)
   uint64_t acc = 0;
   int nb = 0, wi = 0;
   uint32_t m = 0, m1 = 0;                            // MCU counter / end
@@ -337,12 +358,6 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     m = k * J.restart;
     m1 = min(m + J.restart, total);
     if (m >= m1) return false;
-    {                                                // region of interest (conservative across row wraps)
-      const McuRect R = jpeg_mcu_rect(J);
-      const uint32_t mx = J.mcus_x, ra = m / mx, rb = (m1 - 1) / mx;
-      if ((int)rb < R.y0 || (int)ra >= R.y1) return false;
-      if (ra == rb && ((int)((m1 - 1) % mx) < R.x0 || (int)(m % mx) >= R.x1)) return false;
-    }
     bpm = J.bpm;
     sched = 0;
     for (int q = 0; q < bpm; ++q) sched |= ((uint32_t)(J.sched >> (4 * q)) & 3u) << (2 * q);
@@ -356,20 +371,15 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
     q0 = c.x; q1 = c.y; q2 = c.z; q3 = c.w;
     p16 += p16 < plast ? 1 : 0;
     nxt = ld_nc_v4(p16);
+    p16 += p16 < plast ? 1 : 0;
+    nxt2 = ld_nc_v4(p16);
     wi = 0; acc = 0; nb = 0;
     b = 0; kk = 0;
     pred0 = pred1 = pred2 = 0;
     comp_tables();
     return true;
   };
-  auto acquire = [&](uint32_t t) -> bool {
-    for (;;) {
-      if (t >= c1) return false;
-      if (start(t)) return true;
-      t = atomicAdd(&s_next, 1u);
-    }
-  };
-  bool active = acquire(c0 + threadIdx.x);
+  bool active = (mine >> 8) != 0 && start(c0 + (mine & 0xFFu));
   while (__any_sync(0xffffffffu, active)) {
     if (!active) continue;
     {                                                // predicated 32-bit refill
@@ -382,8 +392,9 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
       if (wi == 4) {
         wi = 0;
         q0 = nxt.x; q1 = nxt.y; q2 = nxt.z; q3 = nxt.w;
+        nxt = nxt2;
         p16 += p16 < plast ? 1 : 0;
-        nxt = ld_nc_v4(p16);
+        nxt2 = ld_nc_v4(p16);
       }
     }
     uint32_t e = tab[(kk ? tac : tdc) + (uint32_t)(acc >> (64 - kJpegFastBits))];
@@ -439,7 +450,7 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
       pred2 = ci == 2 ? v : pred2;
     }
     const int pos = kk + run;
-    if (v != 0 && !bad) cb[nat[pos]] = (int16_t)v;
+    if (v != 0 && !bad) cb[min(pos, 63)] = (int16_t)v;   // zig-zag order (J3 de-zigzags at compile time)
     kk = (e & kFastEob) ? 64 : pos + 1;
     // a second AC symbol in the same iteration when the block continues, the bit
     // buffer holds the 11-bit peek (a full entry consumes at most that) and its code + value resolve in the
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
           nb -= (int)((e2 >> 25) & 31);
           const int pos2 = kk + (int)((e2 >> 21) & 15);
           const int v2 = (int)(int16_t)(e2 & 0xFFFF);
-          if (v2 != 0) cb[nat[pos2]] = (int16_t)v2;
+          if (v2 != 0) cb[min(pos2, 63)] = (int16_t)v2;
           kk = (e2 & kFastEob) ? 64 : pos2 + 1;
         }
       }
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(kHuffThreads) jpeg_huffman_kernel(const JpegAr
       if (++b == bpm) { b = 0; ++m; }
       if (bad || m >= m1) {
         if (bad) { A.status[s].value = k; A.status[s].kind = JST_BAD_CODE; }
-        active = acquire(atomicAdd(&s_next, 1u));
+        active = false;
       } else {
         comp_tables();
       }
@@ -507,20 +518,30 @@ __device__ __forceinline__ void idct_1d(int& x0, int& x1, int& x2, int& x3, int&
   x3 = (int)(t13 + t0 + RND) >> SH; x4 = (int)(t13 - t0 + RND) >> SH;
 }
 
-// One block: coefficients (global, natural order) -> 8 rows of 8 bytes at dst (stride bytes).
+// One block: coefficients (global, zig-zag order as J2 stores them) -> 8 rows
+// of 8 bytes at dst (stride bytes).  The de-zigzag is a compile-time register
+// permutation; the quant table is in natural order.
 __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* q, uint8_t* dst, int stride) {
+  constexpr uint8_t kNat[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+                                12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+                                35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+                                58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
   const uint4* src = reinterpret_cast<const uint4*>(coef);
   const uint4* q4 = reinterpret_cast<const uint4*>(q);
-  int w[64];
+  uint32_t cw[32], qw[32];
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const uint4 cv = __ldg(src + r), qv = __ldg(q4 + r);   // L1-allocating: the 8 loads share 4 lines
-    const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
+    cw[4 * r] = cv.x; cw[4 * r + 1] = cv.y; cw[4 * r + 2] = cv.z; cw[4 * r + 3] = cv.w;
+    qw[4 * r] = qv.x; qw[4 * r + 1] = qv.y; qw[4 * r + 2] = qv.z; qw[4 * r + 3] = qv.w;
+  }
+  int w[64];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      w[r * 8 + 2 * j] = (int)((uint32_t)(int)(int16_t)(cw[j] & 0xFFFF) * (qw[j] & 0xFFFF));
-      w[r * 8 + 2 * j + 1] = (int)((uint32_t)(int)(int16_t)(cw[j] >> 16) * (qw[j] >> 16));
-    }
+  for (int k = 0; k < 64; ++k) {
+    const int n = kNat[k];
+    const int c = (int)(int16_t)((k & 1) ? cw[k >> 1] >> 16 : cw[k >> 1] & 0xFFFF);
+    const uint32_t qq = (n & 1) ? qw[n >> 1] >> 16 : qw[n >> 1] & 0xFFFF;
+    w[n] = (int)((uint32_t)c * qq);
   }
 #pragma unroll
   for (int col = 0; col < 8; ++col) {
@@ -664,6 +685,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
   // octets covering the window's columns (their extra pixels lie inside the decoded MCUs)
   const int q_lo = J.win[2] >> 3, no = ((J.win[3] + 7) >> 3) - q_lo, n = (y_hi - y_lo) * no;
   uint8_t* const out = A.scratch + (size_t)s * A.scratch_bytes;
+  const size_t pitch = A.exact_pitch ? (size_t)w * nc : (size_t)jpeg_scratch_pitch(w, nc);
   if (nc == 1) {
     const Plane P0 = sP[0];
     for (int t = threadIdx.x; t < n; t += kColorThreads) {
@@ -671,7 +693,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
       uint32_t px[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) px[k] = (uint32_t)plane_sample(P0, y, min(x0 + k, w - 1));
-      store_px(out + (size_t)y * w + x0, px, min(8, w - x0));
+      store_px(out + (size_t)y * pitch + x0, px, min(8, w - x0));
     }
     return;
   }
@@ -748,7 +770,7 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
         const int Y = (int)(((k < 4 ? y8.x : y8.y) >> (8 * (k & 3))) & 0xFF), cb = u[0][k], cr = u[1][k];
         px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
       }
-      store_px(out + ((size_t)y * w + x0) * 3, px, 3 * min(8, w - x0));
+      store_px(out + (size_t)y * pitch + (size_t)x0 * 3, px, 3 * min(8, w - x0));
       yy += dyy; qq += dqq; if (qq >= no) { qq -= no; ++yy; }
     }
     return;
@@ -763,8 +785,17 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
       const int Y = plane_sample(P0, y, x), cb = plane_sample(P1, y, x) - 128, cr = plane_sample(P2, y, x) - 128;
       px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
     }
-    store_px(out + ((size_t)y * w + x0) * 3, px, 3 * min(8, w - x0));
+    store_px(out + (size_t)y * pitch + (size_t)x0 * 3, px, 3 * min(8, w - x0));
   }
+}
+
+static int sm_count() {                     // of the current device (cached per device)
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] > 0 ? cache[dev] : 148;
 }
 
 int launch_jpeg(const JpegArgs& A, void* stream) {
@@ -773,18 +804,14 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   jpeg_unstuff_kernel<<<A.count, 32 * kUnstuffWarps, 0, st>>>(A);
   const bool smem = A.n_huff <= kJpegSmemTables;
   const int hsmem = smem ? A.n_huff * (int)sizeof(JHuff::fast) + (A.n_huff * (10 * 4 + 256) + 15) / 16 * 16 : 0;
-  // lanes pull intervals from a per-CTA queue: a few intervals per lane balance their
-  // unequal lengths once there are enough intervals to keep every SM busy
-  const uint32_t lanes = 148u * 4u * kHuffThreads;
-  uint32_t per_lane = min(8u, max(1u, A.total_int / lanes));
-  const uint32_t chunk = per_lane * kHuffThreads;
-  const unsigned hgrid = (A.total_int + chunk - 1) / chunk;
+  // a thread per restart interval, CTAs of kHuffThreads consecutive intervals
+  const unsigned hgrid = (unsigned)(((uint64_t)A.total_int + kHuffThreads - 1) / kHuffThreads);
   if (smem) {
     cudaFuncSetAttribute(jpeg_huffman_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
-    jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
+    jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A);
   } else {
     cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
-    jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A, chunk);
+    jpeg_huffman_kernel<false><<<hgrid, kHuffThreads, hsmem, st>>>(A);
   }
   jpeg_idct_kernel<<<dim3((A.max_blocks + kIdctThreads - 1) / kIdctThreads, A.count), kIdctThreads, 0, st>>>(A);
   jpeg_color_kernel<<<dim3((A.max_quads + kColorRows - 1) / kColorRows, A.count), kColorThreads, 0, st>>>(A);

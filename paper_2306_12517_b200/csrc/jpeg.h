@@ -125,6 +125,19 @@ BBX_HD inline McuRect jpeg_mcu_rect(const JpegDesc& J) {
   return r;
 }
 
+// Restart interval k of a sample holds MCUs of the region of interest?  (DC
+// predictors restart per interval, so intervals outside it are never decoded;
+// conservative across MCU-row wraps.)
+BBX_HD inline bool jpeg_interval_live(const JpegDesc& J, const McuRect& R, uint32_t k) {
+  const uint32_t total = (uint32_t)J.mcus_x * J.mcus_y, m = k * J.restart;
+  const uint32_t m1 = m + J.restart < total ? m + J.restart : total;
+  if (m >= m1) return false;
+  const uint32_t mx = J.mcus_x, ra = m / mx, rb = (m1 - 1) / mx;
+  if ((int)rb < R.y0 || (int)ra >= R.y1) return false;
+  if (ra == rb && ((int)((m1 - 1) % mx) < R.x0 || (int)(m % mx) >= R.x1)) return false;
+  return true;
+}
+
 // Per-sample status kinds written by J1/J2 (SampleStatus::kind).
 enum : int32_t { JST_BAD_CODE = 3, JST_MARKER_COUNT = 4, JST_MARKER_SEQ = 5 };
 
@@ -144,6 +157,7 @@ struct JpegArgs {
   int16_t* coef;                          // total blocks x 64
   uint8_t* scratch;                       // count x scratch_bytes: decoded HWC u8
   int64_t scratch_bytes;
+  int32_t exact_pitch;                    // 1: rows w*c bytes apart; 0: jpeg_scratch_pitch (16-B aligned rows)
   const JHuff* huff;                      // table pools
   const JQuant* quant;
   int32_t n_huff;                         // pool entries in use
