@@ -142,18 +142,14 @@ struct Plan {
   int64_t jpeg_blocks_cap = 0;   // per sample: coefficient blocks (any sampling with factors <= 2)
   int64_t jpeg_int_cap = 0;      // per sample: restart intervals (<= MCUs)
   int16_t* d_coef = nullptr;     // JPEG scratch shared by the slots (one compute stream orders them)
-  uint8_t* d_bits = nullptr;     // unstuffed restart-interval bitstreams
   uint8_t* d_planes = nullptr;   // IDCT output: component planes
-  int64_t jpeg_bits_cap = 0;     // per sample
-  uint32_t* d_istart = nullptr;
-  uint32_t* d_iend = nullptr;
-  uint32_t* d_isample = nullptr;
   unsigned long long* d_ticket = nullptr;   // column-walker K1 tile ticket (2 x u64, zero between launches)
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
   std::vector<uint32_t*> d_tables;   // per slot: K1 prologue tables
   std::vector<JpegDesc> jcache;      // per sample, valid where jcached[i] (JPEG fields)
+  std::vector<std::vector<uint32_t>> jstarts;   // per sample: first byte of each restart interval
   std::vector<uint8_t> jcached;
   uint64_t* d_col = nullptr;     // scalar column (num_samples x 8 B)
 };
@@ -539,7 +535,6 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     const int64_t mh = f.info.max_height, mw = f.info.max_width;
     pl.jpeg_blocks_cap = (int64_t)f.info.channels * (2 * ((mh + 15) / 16)) * (2 * ((mw + 15) / 16));
     pl.jpeg_int_cap = ((mh + 7) / 8) * ((mw + 7) / 8);
-    pl.jpeg_bits_cap = (mx + (kJpegIntAlign + kJpegIntPad) * pl.jpeg_int_cap + 64 + 15) / 16 * 16;
   }
   return BBX_OK;
 }
@@ -714,7 +709,7 @@ static int jpeg_quant_id(JpegTables& T, const JpegHeader::Quant& q, uint64_t hv,
 // Host half of the JPEG decode of one sample: parse the header, check it
 // against the cell, resolve table ids and size the device work.
 static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint32_t len, SampleDesc* d, JpegDesc* J,
-                         HostErr& err, int64_t pos, int plan_idx) {
+                         std::vector<uint32_t>* starts, HostErr& err, int64_t pos, int plan_idx) {
   auto bad = [&](const char* m) {
     d->skip = 1;
     if (err.pos < 0 || pos < err.pos || (pos == err.pos && plan_idx < err.plan)) {
@@ -791,9 +786,40 @@ static bool jpeg_prepare(bbx_loader* L, const Plan& pl, const uint8_t* pay, uint
       for (int h = 0; h < J->comp[i].h; ++h, ++bpm)
         J->sched |= (uint64_t)(i | v << 2 | h << 3) << (4 * bpm);
   J->bpm = (uint8_t)bpm;
-  if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap ||
-      (int64_t)len + (kJpegIntAlign + kJpegIntPad) * (int64_t)J->n_int + 64 > pl.jpeg_bits_cap)
+  if ((int64_t)blocks > pl.jpeg_blocks_cap || (int64_t)J->n_int > pl.jpeg_int_cap)
     return bad("jpeg: geometry exceeds the field's device capacity");
+  // Restart intervals (T.81 B.2.5): the entropy-coded bytes between RSTn
+  // markers.  A marker is 0xFF followed by neither 0x00 (stuffing) nor 0xFF
+  // (fill); every one inside the scan must be the next RSTn in sequence, and
+  // there must be exactly n_int - 1 of them.  starts[k] = interval k's first byte.
+  starts->clear();
+  starts->reserve(J->n_int);
+  starts->push_back(H.scan_off);
+  char m2[96];
+  for (uint32_t q = H.scan_off; q + 1 < end;) {
+    const void* f = std::memchr(pay + q, 0xFF, end - 1 - q);
+    if (!f) break;
+    q = (uint32_t)(static_cast<const uint8_t*>(f) - pay);
+    const uint8_t c = pay[q + 1];
+    if (c == 0x00) { q += 2; continue; }
+    if (c == 0xFF) { q += 1; continue; }
+    if ((c & 0xF8) != 0xD0) {
+      std::snprintf(m2, sizeof m2, "jpeg: restart marker count %d does not match the header", -1);
+      return bad(m2);
+    }
+    const uint32_t n = (uint32_t)starts->size();   // this is RST number n - 1 of the scan
+    if (n >= J->n_int) {
+      std::snprintf(m2, sizeof m2, "jpeg: restart marker count %u does not match the header", n);
+      return bad(m2);
+    }
+    if ((uint32_t)(c & 7) != ((n - 1) & 7u)) return bad("jpeg: restart markers out of sequence");
+    starts->push_back(q + 2);
+    q += 2;
+  }
+  if (starts->size() != J->n_int) {
+    std::snprintf(m2, sizeof m2, "jpeg: restart marker count %u does not match the header", (uint32_t)starts->size() - 1);
+    return bad(m2);
+  }
   return true;
 }
 
@@ -825,7 +851,7 @@ static int finalize(bbx_loader* L) {
     if (L->plans[p].scalar || !L->plans[p].field_has_jpeg) continue;
     any_jpeg = true;
     L->jpeg_off[p] = off;
-    off += jpeg_block_bytes(L->batch);
+    off += jpeg_block_bytes(L->batch) + (size_t)L->batch * L->plans[p].jpeg_int_cap * 4;   // + interval starts
     off = (off + 255) / 256 * 256;
   }
   L->desc_bytes = off;
@@ -870,14 +896,14 @@ static int finalize(bbx_loader* L) {
   }
   for (auto& pl : L->plans) {
     if (pl.scalar || !pl.field_has_jpeg) continue;
-    if (L->jpeg_cache) { pl.jcache.resize(L->ds->num_samples); pl.jcached.assign(L->ds->num_samples, 0); }
+    if (L->jpeg_cache) {
+      pl.jcache.resize(L->ds->num_samples);
+      pl.jstarts.assign(L->ds->num_samples, {});
+      pl.jcached.assign(L->ds->num_samples, 0);
+    }
     const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
     CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
-    CK(cudaMalloc(&pl.d_bits, (size_t)L->batch * pl.jpeg_bits_cap + 256));
     CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
-    CK(cudaMalloc(&pl.d_istart, ints * 4 + 64));
-    CK(cudaMalloc(&pl.d_iend, ints * 4 + 64));
-    CK(cudaMalloc(&pl.d_isample, ints * 4 + 64));
   }
   if (any_jpeg && !L->jt.d_huff) {
     JpegTables& T = L->jt;
@@ -912,7 +938,7 @@ static int finalize(bbx_loader* L) {
           d.h = (uint16_t)c.h; d.w = (uint16_t)c.w; d.c = (uint8_t)c.c;
           JpegDesc J;
           HostErr e;
-          if (jpeg_prepare(L, pl, ds->map + c.offset, (uint32_t)c.length, &d, &J, e, 0, 0)) {
+          if (jpeg_prepare(L, pl, ds->map + c.offset, (uint32_t)c.length, &d, &J, &pl.jstarts[i], e, 0, 0)) {
             pl.jcache[i] = J;
             pl.jcached[i] = 1;
           }
@@ -1003,6 +1029,10 @@ static int process_slot(bbx_loader* L, int s) {
   std::vector<Copy> copies;
   struct JParse { int plan; int pos; int64_t idx; uint64_t off; uint32_t len; };
   std::vector<JParse> jparse;
+  // interval starts of this batch's JPEG samples, per plan and position: the
+  // loader cache's entry, or (no cache / duplicate index) a slot-local vector
+  std::vector<std::vector<const std::vector<uint32_t>*>> jst(L->plans.size());
+  std::vector<std::vector<uint32_t>> jlocal;
   if (!resident) copies.reserve((size_t)count * L->plans.size());
   double t0 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // one compact payload region for every plan: [pay_base, cursor)
@@ -1014,7 +1044,7 @@ static int process_slot(bbx_loader* L, int s) {
     uint8_t* dblk = H + L->desc_off[p];
     const bool image = ds->fields[pl.field_index].info.kind == 4;
     JpegDesc* jds = pl.field_has_jpeg ? reinterpret_cast<JpegDesc*>(H + L->jpeg_off[p]) : nullptr;
-    if (jds) std::memset(jds, 0, sizeof(JpegDesc) * count);
+    if (jds) { std::memset(jds, 0, sizeof(JpegDesc) * count); jst[p].assign(count, nullptr); }
     for (int pos = 0; pos < count; ++pos) {
       int64_t i = S.idx[pos];
       uint8_t* desc = dblk + (size_t)pos * pl.dev.desc_stride;
@@ -1030,7 +1060,7 @@ static int process_slot(bbx_loader* L, int s) {
       if (!ok) continue;
       if (d->codec == CODEC_RLE && ds->fields[pl.field_index].info.kind == 4) S.plan_has_rle[p] = 1;
       if (image && d->codec == CODEC_JPEG) {   // header: from the cache, else parsed on the pool below
-        if (L->jpeg_cache && pl.jcached[i]) jds[pos] = pl.jcache[i];
+        if (L->jpeg_cache && pl.jcached[i]) { jds[pos] = pl.jcache[i]; jst[p][pos] = &pl.jstarts[i]; }
         else jparse.push_back({(int)p, pos, i, off, len});
         S.plan_has_jpeg[p] = 1;
       }
@@ -1072,15 +1102,26 @@ static int process_slot(bbx_loader* L, int s) {
   // JPEG headers not seen before: parse on the pool (tables registered under a mutex)
   if (!jparse.empty()) {
     std::vector<HostErr> jerr(jparse.size());
+    jlocal.assign(jparse.size(), {});
+    // the cache entry of a sample is written by its first occurrence in the batch
+    // only (a padded distributed tail can repeat an index)
+    std::vector<char> first(jparse.size(), 1);
+    if (L->jpeg_cache) {
+      std::unordered_map<int64_t, size_t> seen;
+      for (size_t q = 0; q < jparse.size(); ++q)
+        if (!seen.emplace(jparse[q].idx * 64 + jparse[q].plan, q).second) first[q] = 0;
+    }
     L->pool->parallel_for((int64_t)jparse.size(), [&](int64_t q) {
       const JParse& j = jparse[q];
       Plan& pl = L->plans[j.plan];
       uint8_t* desc = H + L->desc_off[j.plan] + (size_t)j.pos * pl.dev.desc_stride;
       JpegDesc* jd = reinterpret_cast<JpegDesc*>(H + L->jpeg_off[j.plan]) + j.pos;
-      if (jpeg_prepare(L, pl, ds->map + j.off, j.len, reinterpret_cast<SampleDesc*>(desc), jd, jerr[q], j.pos, j.plan)) {
-        if (L->jpeg_cache) { pl.jcache[j.idx] = *jd; pl.jcached[j.idx] = 1; }   // distinct samples: no race
+      if (jpeg_prepare(L, pl, ds->map + j.off, j.len, reinterpret_cast<SampleDesc*>(desc), jd, &jlocal[q], jerr[q],
+                       j.pos, j.plan)) {
+        if (L->jpeg_cache && first[q]) { pl.jcache[j.idx] = *jd; pl.jstarts[j.idx] = jlocal[q]; pl.jcached[j.idx] = 1; }
       }
     });
+    for (size_t q = 0; q < jparse.size(); ++q) jst[jparse[q].plan][jparse[q].pos] = &jlocal[q];
     for (const HostErr& e : jerr)
       if (e.pos >= 0 && (S.herr.pos < 0 || e.pos < S.herr.pos || (e.pos == S.herr.pos && e.plan < S.herr.plan)))
         S.herr = e;
@@ -1093,9 +1134,10 @@ static int process_slot(bbx_loader* L, int s) {
     JpegDesc* jds = reinterpret_cast<JpegDesc*>(jb);
     uint32_t* ipre = reinterpret_cast<uint32_t*>(jb + jpeg_iprefix_off(L->batch));
     uint64_t* bpre = reinterpret_cast<uint64_t*>(jb + jpeg_bprefix_off(L->batch));
+    uint32_t* starts = reinterpret_cast<uint32_t*>(jb + jpeg_block_bytes(L->batch));
     const uint8_t* dblk = H + L->desc_off[p];
     uint32_t ti = 0;
-    uint64_t tb = 0, bs = 0;
+    uint64_t tb = 0;
     int32_t mq = 0;
     uint32_t mb = 0;
     for (int pos = 0; pos < count; ++pos) {
@@ -1110,11 +1152,11 @@ static int process_slot(bbx_loader* L, int s) {
         if (!L->jpeg_roi) { y0 = 0; y1 = d->h; x0 = 0; x1 = d->w; }
         J.win[0] = (uint16_t)y0; J.win[1] = (uint16_t)y1; J.win[2] = (uint16_t)x0; J.win[3] = (uint16_t)x1;
       }
-      J.int_base = ti; J.blk_base = tb; J.bs_base = bs;
+      J.int_base = ti; J.blk_base = tb;
       ipre[pos] = ti; bpre[pos] = tb;
+      if (J.n_int) std::memcpy(starts + ti, jst[p][pos]->data(), (size_t)J.n_int * 4);
       ti += J.n_int; tb += J.n_blocks;
       if (J.n_int) {
-        bs += (uint64_t)pl.jpeg_bits_cap;
         mq = std::max(mq, (int32_t)d->h);
         mb = std::max(mb, J.n_blocks);
       }
@@ -1259,7 +1301,8 @@ static int process_slot(bbx_loader* L, int s) {
       J.jd = reinterpret_cast<const JpegDesc*>(jb);
       J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
       J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
-      J.istart = pl.d_istart; J.iend = pl.d_iend; J.isample = pl.d_isample; J.bits = pl.d_bits; J.coef = pl.d_coef; J.planes = pl.d_planes;
+      J.starts = reinterpret_cast<const uint32_t*>(jb + jpeg_block_bytes(L->batch));
+      J.coef = pl.d_coef; J.planes = pl.d_planes;
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
       J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
       J.coef_zeroed = 1;
@@ -1317,7 +1360,7 @@ static int process_slot(bbx_loader* L, int s) {
   return BBX_OK;
 }
 
-// codecs.decode_image for one JPEG blob: the batch decoder (J1-J4) run on a
+// codecs.decode_image for one JPEG blob: the batch decoder (J2-J4) run on a
 // batch of one, writing the (h, w, c) result straight into out_dev.
 static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len, uint8_t* out_dev, int device) {
   if (len < 4 || len > 0xFFFFFFFFll) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: missing SOI marker");
@@ -1330,30 +1373,27 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   Plan pl;
   pl.jpeg_blocks_cap = (int64_t)c * (2 * ((h + 15) / 16)) * (2 * ((w + 15) / 16));
   pl.jpeg_int_cap = (int64_t)((h + 7) / 8) * ((w + 7) / 8);
-  pl.jpeg_bits_cap = (len + (kJpegIntAlign + kJpegIntPad) * pl.jpeg_int_cap + 64 + 15) / 16 * 16;
   uint8_t desc[64] = {0};
   SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
   d->src = 0; d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = CODEC_JPEG;
   JpegDesc J{};
+  std::vector<uint32_t> starts;
   HostErr err;
-  bool ok = jpeg_prepare(&L, pl, pay, (uint32_t)len, d, &J, err, 0, 0);
+  bool ok = jpeg_prepare(&L, pl, pay, (uint32_t)len, d, &J, &starts, err, 0, 0);
   L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
   if (!ok) return fail(err.code, "%s", err.msg.c_str());
-  J.int_base = 0; J.blk_base = 0; J.bs_base = 0;
+  J.int_base = 0; J.blk_base = 0;
   J.win[0] = 0; J.win[1] = (uint16_t)h; J.win[2] = 0; J.win[3] = (uint16_t)w;
-  // device image: [desc 64][jd][prefixes][payload (+16 pad)] then tables, intervals, bits, coef, planes, status
+  // device image: [desc 64][jd][prefixes][payload (+16 pad)][tables][interval starts] then coef, planes, status
   const size_t o_jd = 64, o_ip = o_jd + sizeof(JpegDesc), o_bp = o_ip + 16, o_pay = o_bp + 16;
   const size_t o_hf = (o_pay + len + 16 + 255) / 256 * 256;
   const size_t o_q = o_hf + sizeof(JHuff) * L.jt.n_huff;
   const size_t o_is = (o_q + sizeof(JQuant) * L.jt.n_quant + 255) / 256 * 256;
-  const size_t o_ie = o_is + 4 * (size_t)J.n_int + 16;
-  const size_t o_isa = o_ie + 4 * (size_t)J.n_int + 16;
-  const size_t o_bs = (o_isa + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
-  const size_t o_cf = (o_bs + (size_t)pl.jpeg_bits_cap + 255) / 256 * 256;
+  const size_t o_cf = (o_is + 4 * (size_t)J.n_int + 16 + 255) / 256 * 256;
   const size_t o_pl = (o_cf + 128 * (size_t)J.n_blocks + 255) / 256 * 256;
   const size_t o_st = (o_pl + 64 * (size_t)J.n_blocks + 255) / 256 * 256;
   const size_t total = o_st + sizeof(SampleStatus);
-  std::vector<uint8_t> img(o_is, 0);
+  std::vector<uint8_t> img(o_cf, 0);
   std::memcpy(img.data(), desc, 64);
   std::memcpy(img.data() + o_jd, &J, sizeof J);
   const uint32_t ip[2] = {0, J.n_int};
@@ -1363,6 +1403,7 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   std::memcpy(img.data() + o_pay, pay, (size_t)len);
   std::memcpy(img.data() + o_hf, hh.data(), sizeof(JHuff) * L.jt.n_huff);
   std::memcpy(img.data() + o_q, hq.data(), sizeof(JQuant) * L.jt.n_quant);
+  std::memcpy(img.data() + o_is, starts.data(), 4 * (size_t)J.n_int);
   uint8_t* dev = nullptr;
   CK(cudaMalloc(&dev, total));
   cudaError_t e = cudaMemcpy(dev, img.data(), img.size(), cudaMemcpyHostToDevice);
@@ -1373,9 +1414,8 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   A.jd = reinterpret_cast<const JpegDesc*>(dev + o_jd);
   A.int_prefix = reinterpret_cast<const uint32_t*>(dev + o_ip);
   A.blk_prefix = reinterpret_cast<const uint64_t*>(dev + o_bp);
-  A.istart = reinterpret_cast<uint32_t*>(dev + o_is); A.iend = reinterpret_cast<uint32_t*>(dev + o_ie);
-  A.isample = reinterpret_cast<uint32_t*>(dev + o_isa);
-  A.bits = dev + o_bs; A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
+  A.starts = reinterpret_cast<const uint32_t*>(dev + o_is);
+  A.coef = reinterpret_cast<int16_t*>(dev + o_cf); A.planes = dev + o_pl;
   A.scratch = out_dev; A.scratch_bytes = (int64_t)h * w * c; A.exact_pitch = 1;   // (h, w, c) output, no row padding
   A.huff = reinterpret_cast<const JHuff*>(dev + o_hf); A.quant = reinterpret_cast<const JQuant*>(dev + o_q);
   A.n_huff = L.jt.n_huff;
@@ -1388,8 +1428,6 @@ static int jpeg_decode_one(int h, int w, int c, const uint8_t* pay, int64_t len,
   cudaFree(dev);
   if (rc || e != cudaSuccess) return fail(BBX_CUDA_ERROR, "jpeg decode failed: %s", cudaGetErrorString(e));
   if (st.kind == JST_BAD_CODE) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: bad Huffman code in restart interval %lld", (long long)st.value);
-  if (st.kind == JST_MARKER_COUNT) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: restart marker count %lld does not match the header", (long long)st.value);
-  if (st.kind == JST_MARKER_SEQ) return fail(BBX_CORRUPT_PAYLOAD, "jpeg: restart markers out of sequence");
   return BBX_OK;
 }
 
@@ -1626,9 +1664,7 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
       int64_t n = (int64_t)d->h * d->w * d->c;
       if (st.kind == 1) std::snprintf(buf, sizeof buf, "rle runs sum past %lld bytes", (long long)n);
       else if (st.kind == 2) std::snprintf(buf, sizeof buf, "rle runs sum to %lld bytes, expected %lld", (long long)st.value, (long long)n);
-      else if (st.kind == JST_BAD_CODE) std::snprintf(buf, sizeof buf, "jpeg: bad Huffman code in restart interval %lld", (long long)st.value);
-      else if (st.kind == JST_MARKER_COUNT) std::snprintf(buf, sizeof buf, "jpeg: restart marker count %lld does not match the header", (long long)st.value);
-      else std::snprintf(buf, sizeof buf, "jpeg: restart markers out of sequence");
+      else std::snprintf(buf, sizeof buf, "jpeg: bad Huffman code in restart interval %lld", (long long)st.value);
       best.pos = pos; best.plan = (int)p; best.code = BBX_CORRUPT_PAYLOAD; best.msg = buf;
       break;
     }
@@ -1708,11 +1744,7 @@ void bbx_loader_destroy(bbx_loader* L) {
     for (auto* p : pl.d_scratch) if (p) cudaFree(p);
     for (auto* p : pl.d_tables) if (p) cudaFree(p);
     if (pl.d_coef) cudaFree(pl.d_coef);
-    if (pl.d_bits) cudaFree(pl.d_bits);
     if (pl.d_planes) cudaFree(pl.d_planes);
-    if (pl.d_istart) cudaFree(pl.d_istart);
-    if (pl.d_iend) cudaFree(pl.d_iend);
-    if (pl.d_isample) cudaFree(pl.d_isample);
     if (pl.d_ticket) cudaFree(pl.d_ticket);
   }
   if (L->jt.h_huff) cudaFreeHost(L->jt.h_huff);

@@ -26,230 +26,6 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   return r;
 }
 
-// ------------------------------------------------------------------- J1
-// CTA per sample, kUnstuffWarps warps, each owning a contiguous run of
-// 16-byte chunks of the entropy-coded segment [scan_off, scan_end) (scan_end:
-// the EOI marker, found by the host).  Byte j is coded data unless it follows
-// 0xFF (stuffing 0x00 or a marker code) or is an 0xFF that starts a marker;
-// (0xFF, 0xD0..D7) is a restart marker: the interval ends, kJpegIntAlign-
-// aligned zero padding follows, and the next interval starts aligned.  A
-// lane's effect on the output cursor is x -> x + a, or x -> alignA(x + a) + c
-// once it holds a marker; that family is closed under composition, so
-//   pass 1: every warp composes the functions of its chunks (warp scans),
-//   pass 2: an exclusive scan over the warps gives each warp its start cursor,
-//   pass 3: every warp replays its chunks and writes bytes / interval bounds.
-constexpr int kUnstuffWarps = 8;
-constexpr int kUnstuffBuf = 1024;                  // per-warp output window of pass 3 (bytes)
-constexpr int kScanCache = 8;                      // rounds whose pass-1 scans pass 3 reuses (later rounds rescan)
-constexpr uint32_t kAlignMask = kJpegIntAlign - 1;
-
-__device__ __forceinline__ uint32_t align_int(uint32_t x) { return (x + kAlignMask) & ~kAlignMask; }
-
-struct CursorFn { uint32_t aligned, a, c; };   // aligned ? align_int(x + a) + c : x + a
-
-// c is a multiple of the alignment plus the bytes after the last marker, so
-// align(align(y) + c) == align(y) + align(c) keeps the family closed.
-__device__ __forceinline__ CursorFn compose(CursorFn f, CursorFn g) {   // g after f
-  if (!g.aligned) return f.aligned ? CursorFn{1u, f.a, f.c + g.a} : CursorFn{0u, f.a + g.a, 0u};
-  return f.aligned ? CursorFn{1u, f.a, align_int(f.c + g.a) + g.c} : CursorFn{1u, f.a + g.a, g.c};
-}
-__device__ __forceinline__ uint32_t apply(CursorFn f, uint32_t x) { return f.aligned ? align_int(x + f.a) + f.c : x + f.a; }
-
-struct ChunkMasks { uint32_t w[4]; uint32_t nxt, keep, rst, term; };
-
-// 4-bit mask of the bytes of w that __vcmpeq4 flagged (0xFF per equal byte).
-__device__ __forceinline__ uint32_t byte_bits(uint32_t eq) { return ((eq & 0x01010101u) * 0x10204080u) >> 28; }
-
-// Masks of the 16 bytes at `my` (16-byte aligned) restricted to [a_lo, a_hi),
-// byte-parallel (SWAR): data bytes to keep, RST markers, other markers.
-__device__ __forceinline__ ChunkMasks chunk_masks(uintptr_t my, uintptr_t a_lo, uintptr_t a_hi, int lane) {
-  ChunkMasks M;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (my < a_hi) v = ld_nc_v4(reinterpret_cast<const void*>(my));   // buffers carry >= 16 B of tail padding
-  M.w[0] = v.x; M.w[1] = v.y; M.w[2] = v.z; M.w[3] = v.w;
-  uint32_t prev = __shfl_up_sync(0xffffffffu, v.w >> 24, 1);
-  if (lane == 0) prev = (my > a_lo && my <= a_hi) ? *reinterpret_cast<const uint8_t*>(my - 1) : 0u;
-  uint32_t nxt = __shfl_down_sync(0xffffffffu, v.x & 0xFF, 1);
-  if (lane == 31) nxt = (my + 16 < a_hi) ? *reinterpret_cast<const uint8_t*>(my + 16) : 0u;
-  M.nxt = nxt;
-  uint32_t ff = 0, z = 0, rs = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    ff |= byte_bits(__vcmpeq4(M.w[q], 0xFFFFFFFFu)) << (4 * q);
-    z |= byte_bits(__vcmpeq4(M.w[q], 0u)) << (4 * q);
-    rs |= byte_bits(__vcmpeq4(M.w[q] & 0xF8F8F8F8u, 0xD0D0D0D0u)) << (4 * q);
-  }
-  // bytes of this chunk inside [a_lo, a_hi); the first has no predecessor, the last no successor
-  const int lo = my >= a_lo ? 0 : (int)min((uintptr_t)16, a_lo - my);
-  const int hi = my >= a_hi ? 0 : (int)min((uintptr_t)16, a_hi - my);
-  const uint32_t inr = lo < hi ? ((0xFFFFu >> (16 - hi)) & (0xFFFFu << lo)) : 0u;
-  const uint32_t first = (my <= a_lo && a_lo < my + 16) ? 1u << (a_lo - my) : 0u;
-  const uint32_t last = (a_hi > my && a_hi <= my + 16) ? 1u << (a_hi - 1 - my) : 0u;
-  const uint32_t prev_ff = ((ff << 1) | (prev == 0xFF ? 1u : 0u)) & ~first;
-  const uint32_t next_z = (z >> 1) | (nxt == 0 ? 0x8000u : 0u) | last;
-  const uint32_t next_rs = ((rs >> 1) | ((nxt & 0xF8) == 0xD0 ? 0x8000u : 0u)) & ~last;
-  const uint32_t next_ff = ((ff >> 1) | (nxt == 0xFF ? 0x8000u : 0u)) & ~last;
-  const uint32_t marker = ff & ~next_z;
-  M.keep = inr & ~prev_ff & ~marker & ~(ff & last);   // a trailing 0xFF is a fill byte
-  M.rst = inr & marker & next_rs;
-  M.term = inr & marker & ~next_ff & ~next_rs;
-  return M;
-}
-
-__device__ __forceinline__ CursorFn lane_fn(const ChunkMasks& M) {
-  if (M.rst == 0) return CursorFn{0u, (uint32_t)__popc(M.keep), 0u};
-  CursorFn f{0u, 0u, 0u};
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (M.rst >> j & 1) f = f.aligned ? CursorFn{1u, f.a, align_int(f.c) + kJpegIntPad} : CursorFn{1u, f.a, kJpegIntPad};
-    if (M.keep >> j & 1) { if (f.aligned) ++f.c; else ++f.a; }
-  }
-  return f;
-}
-
-__device__ __forceinline__ CursorFn warp_scan(CursorFn f, uint32_t& nr, int lane) {   // inclusive
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const CursorFn e{__shfl_up_sync(0xffffffffu, f.aligned, o), __shfl_up_sync(0xffffffffu, f.a, o),
-                     __shfl_up_sync(0xffffffffu, f.c, o)};
-    const uint32_t r = __shfl_up_sync(0xffffffffu, nr, o);
-    if (lane >= o) { f = compose(e, f); nr += r; }
-  }
-  return f;
-}
-
-__global__ void __launch_bounds__(32 * kUnstuffWarps) jpeg_unstuff_kernel(const JpegArgs A) {
-  const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const JpegDesc& J = A.jd[s];
-  const uint32_t nint = J.n_int;
-  if (nint == 0) return;
-  __shared__ CursorFn s_fn[kUnstuffWarps];
-  __shared__ uint32_t s_nr[kUnstuffWarps], s_x[kUnstuffWarps], s_k[kUnstuffWarps];
-  __shared__ int s_bad;
-  __shared__ __align__(16) uint8_t s_ob[kUnstuffWarps][kUnstuffBuf];
-  __shared__ uint2 s_scan[kUnstuffWarps][kScanCache][32];   // pass 1's per-lane inclusive scans (packed)
-  const uint8_t* base = A.payload + sdesc(A, s)->src;
-  uint8_t* out = A.bits + J.bs_base;
-  uint32_t* st = A.istart + J.int_base;
-  uint32_t* en = A.iend + J.int_base;
-  const uintptr_t ab = reinterpret_cast<uintptr_t>(base);
-  const uintptr_t a_lo = ab + J.scan_off, a_hi = ab + J.scan_end;
-  const uintptr_t c0 = a_lo & ~uintptr_t(15);
-  const uint32_t nch = (uint32_t)((a_hi - c0 + 15) >> 4);
-  const uint32_t rounds = (nch + 32 * kUnstuffWarps - 1) / (32 * kUnstuffWarps);
-  const uint32_t ch0 = warp * rounds * 32;
-  if (threadIdx.x == 0) s_bad = 0;
-  for (uint32_t k = threadIdx.x; k < nint; k += 32 * kUnstuffWarps) A.isample[J.int_base + k] = (uint32_t)s;
-  // pass 1: this warp's cursor function and marker count
-  CursorFn F{0u, 0u, 0u};
-  uint32_t NR = 0;
-  bool term = false;
-  for (uint32_t r = 0; r < rounds; ++r) {
-    const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
-    term |= M.term != 0;
-    uint32_t nr = __popc(M.rst);
-    const CursorFn inc = warp_scan(lane_fn(M), nr, lane);
-    if (r < kScanCache) s_scan[warp][r][lane] = make_uint2(inc.a | inc.aligned << 31, inc.c | nr << 16);
-    const CursorFn all{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
-                       __shfl_sync(0xffffffffu, inc.c, 31)};
-    F = compose(F, all);
-    NR += __shfl_sync(0xffffffffu, nr, 31);
-  }
-  if (lane == 0) { s_fn[warp] = F; s_nr[warp] = NR; }
-  if (__any_sync(0xffffffffu, term) && lane == 0) s_bad = 1;   // a non-RST marker inside the scan data
-  __syncthreads();
-  // pass 2: exclusive scan over the warps
-  if (threadIdx.x == 0) {
-    CursorFn P{0u, 0u, 0u};
-    uint32_t k = 0;
-    for (int w = 0; w < kUnstuffWarps; ++w) {
-      s_x[w] = apply(P, 0u);
-      s_k[w] = k;
-      P = compose(P, s_fn[w]);
-      k += s_nr[w];
-    }
-    const uint32_t xend = apply(P, 0u);
-    SampleStatus& S = A.status[s];
-    S.kind = 0; S.value = 0;
-    if (s_bad) { S.kind = JST_MARKER_COUNT; S.value = -1; }
-    else if (k != nint - 1) { S.kind = JST_MARKER_COUNT; S.value = k; }
-    else {
-      st[0] = 0;
-      en[nint - 1] = xend;
-      for (uint32_t z = xend; z < align_int(xend) + kJpegIntPad; ++z) out[z] = 0;
-    }
-  }
-  __syncthreads();
-  if (A.status[s].kind != 0) return;
-  // pass 3: replay, writing bytes and interval bounds.  A round's output (the
-  // warp's 512 input bytes minus stuffing, plus restart padding) is assembled
-  // in a zeroed shared-memory window aligned like the output, then written
-  // with 16-byte stores (byte stores only at the two partial edge chunks);
-  // a round too large for the window writes straight to global.
-  uint32_t xw = s_x[warp], kw = s_k[warp];
-  bool seq_bad = false;
-  uint8_t* ob = s_ob[warp];
-  for (uint32_t r = 0; r < rounds; ++r) {
-    const ChunkMasks M = chunk_masks(c0 + 16 * (uintptr_t)(ch0 + r * 32 + lane), a_lo, a_hi, lane);
-    const uint32_t nr = __popc(M.rst);
-    uint32_t nr_incl = nr, nr_all;
-    CursorFn exc, all;
-    if (r < kScanCache) {                            // pass 1's scan of this round, from shared memory
-      auto unpack = [](uint2 v) { return CursorFn{v.x >> 31, v.x & 0x7FFFFFFFu, v.y & 0xFFFFu}; };
-      const uint2 me = s_scan[warp][r][lane], lv = s_scan[warp][r][31];
-      const uint2 pv = lane ? s_scan[warp][r][lane - 1] : make_uint2(0u, 0u);
-      exc = unpack(pv);
-      all = unpack(lv);
-      nr_incl = me.y >> 16;
-      nr_all = lv.y >> 16;
-    } else {
-      const CursorFn inc = warp_scan(lane_fn(M), nr_incl, lane);
-      exc = CursorFn{__shfl_up_sync(0xffffffffu, inc.aligned, 1), __shfl_up_sync(0xffffffffu, inc.a, 1),
-                     __shfl_up_sync(0xffffffffu, inc.c, 1)};
-      if (lane == 0) exc = CursorFn{0u, 0u, 0u};
-      all = CursorFn{__shfl_sync(0xffffffffu, inc.aligned, 31), __shfl_sync(0xffffffffu, inc.a, 31),
-                     __shfl_sync(0xffffffffu, inc.c, 31)};
-      nr_all = __shfl_sync(0xffffffffu, nr_incl, 31);
-    }
-    const uint32_t xe = apply(all, xw), wb = xw & ~kAlignMask;   // round output [xw, xe); window base
-    uint32_t x = apply(exc, xw), k = kw + nr_incl - nr;
-    const bool staged = xe - wb <= (uint32_t)kUnstuffBuf;
-    if (staged) {
-      for (uint32_t c = lane; c < (xe - wb + 15) / 16; c += 32) reinterpret_cast<uint4*>(ob)[c] = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-    }
-    uint8_t* dst = staged ? ob - wb : out;           // byte x of the output goes to dst[x]
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (M.rst >> j & 1) {                          // interval k ends: zero tail, next one starts aligned
-        const uint32_t n = (j < 15 ? (M.w[(j + 1) >> 2] >> (((j + 1) & 3) * 8)) : M.nxt) & 7;
-        if (n != (k & 7)) seq_bad = true;
-        const uint32_t nx = align_int(x) + kJpegIntPad;
-        en[k] = x;
-        st[k + 1] = nx;
-        if (!staged) for (uint32_t z = x; z < nx; ++z) out[z] = 0;
-        x = nx;
-        ++k;
-      }
-      if (M.keep >> j & 1) dst[x++] = (uint8_t)(M.w[j >> 2] >> ((j & 3) * 8));
-    }
-    if (staged) {
-      __syncwarp();
-      const uint32_t h1 = min(align_int(xw), xe), t0 = max(xe & ~kAlignMask, h1);
-      for (uint32_t c = align_int(xw) / 16 + lane; c < t0 / 16; c += 32)   // whole chunks
-        reinterpret_cast<uint4*>(out)[c] = reinterpret_cast<const uint4*>(ob)[c - wb / 16];
-      if (lane < 16) {                               // partial edge chunks
-        if (xw + lane < h1) out[xw + lane] = ob[xw + lane - wb];
-        if (t0 + lane < xe) out[t0 + lane] = ob[t0 + lane - wb];
-      }
-      __syncwarp();
-    }
-    xw = xe;
-    kw += nr_all;
-  }
-  if (__any_sync(0xffffffffu, seq_bad) && lane == 0) A.status[s].kind = JST_MARKER_SEQ;
-}
-
 // ------------------------------------------------------------------- J2
 // Thread per restart interval (DC predictors restart at zero, T.81
 // F.2.1.3.1), one symbol per loop iteration whatever block / MCU it belongs
@@ -299,20 +75,27 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   // longest lane finishes; interval lengths vary ~4x within an image).  Key:
   // unstuffed bytes + 1 (0: outside the region of interest or a rejected
   // sample: never decoded) | position.
-  __shared__ uint32_t skey[kHuffThreads];
+  __shared__ uint32_t skey[kHuffThreads], ssamp[kHuffThreads];
   const uint32_t c0 = blockIdx.x * kHuffThreads;
   {
     const uint32_t t = c0 + threadIdx.x;
-    uint32_t key = 0;
+    uint32_t key = 0, si = 0;
     if (t < A.total_int) {
-      const uint32_t si = __ldg(&A.isample[t]);
-      if (A.status[si].kind == 0) {
-        const JpegDesc& J = A.jd[si];
-        if (jpeg_interval_live(J, jpeg_mcu_rect(J), t - J.int_base))
-          key = min(A.iend[t] - A.istart[t] + 1u, 0xFFFFFFu) << 8;
+      uint32_t lo = 0, hi = (uint32_t)A.count;       // the sample: int_prefix[si] <= t < int_prefix[si + 1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&A.int_prefix[mid]) <= t) lo = mid; else hi = mid;
+      }
+      si = lo;
+      const JpegDesc& J = A.jd[si];
+      const uint32_t k = t - J.int_base;
+      if (k < J.n_int && jpeg_interval_live(J, jpeg_mcu_rect(J), k)) {
+        const uint32_t e = k + 1 < J.n_int ? __ldg(&A.starts[t + 1]) : J.scan_end;
+        key = min(e - __ldg(&A.starts[t]) + 1u, 0xFFFFFFu) << 8;
       }
     }
     skey[threadIdx.x] = key | threadIdx.x;
+    ssamp[threadIdx.x] = si;
   }
   __syncthreads();
 #pragma unroll 1
@@ -328,13 +111,22 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     }
   const uint32_t mine = skey[threadIdx.x];
 
-  // per-lane decoder state of the current restart interval
-  const uint4* p16 = nullptr;
-  const uint4* plast = nullptr;
-  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;          // next stream words; nxt, nxt2 = the two chunks after them
-  uint4 nxt = make_uint4(0, 0, 0, 0), nxt2 = make_uint4(0, 0, 0, 0);   // (two loads in flight hide L2 latency)
+  // per-lane decoder state of the current restart interval.  The reader
+  // walks the stuffed entropy-coded bytes (T.81 F.1.2.3): a logical 32-bit
+  // word = 4 stream bytes at the interval's byte phase (one PRMT of two
+  // aligned words); words without 0xFF go straight into the bit buffer, any
+  // other word byte by byte -- 0xFF 0x00 is a data 0xFF, 0xFF + anything else
+  // is a marker (the next RSTn, EOI, or corruption) after which zeros are
+  // supplied (libjpeg's fill_bit_buffer rule; oracle/jpeg_oracle.c get_bit).
+  const uint4* p16 = nullptr;                        // last chunk loaded (nxt2)
+  const uint4* plast = nullptr;                      // chunk holding the sample's last scan byte
+  uint32_t lastn = 16;                               // scan bytes in *plast; later bytes read as 0xFF
+  uint4 cur = make_uint4(0, 0, 0, 0), nxt = cur, nxt2 = cur;   // two loads in flight hide L2 latency
+  uint32_t qa = 0, qb = 0, sel = 0x0123;            // window of two aligned words, PRMT selector
+  int wci = 0;                                       // next word of `cur`
+  bool carry = false, marker = false;               // pending 0xFF / marker reached
   uint64_t acc = 0;
-  int nb = 0, wi = 0;
+  int nb = 0;
   uint32_t m = 0, m1 = 0;                            // MCU counter / end
   int b = 0, bpm = 1, kk = 0, ci = 0, s = 0;
   uint32_t k = 0, sched = 0, tdc = 0, tac = 0;
@@ -342,16 +134,31 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   int pred0 = 0, pred1 = 0, pred2 = 0;
   int16_t* cb = nullptr;
 
+  auto ld_chunk = [&](const uint4* p) -> uint4 {
+    if (p > plast) return make_uint4(~0u, ~0u, ~0u, ~0u);
+    uint4 v = ld_nc_v4(p);
+    if (p == plast && lastn < 16) {                  // bytes past the scan data read as 0xFF (a marker)
+      const uint32_t n0 = min(lastn, 4u), n1 = lastn > 4 ? min(lastn - 4, 4u) : 0u,
+                     n2 = lastn > 8 ? min(lastn - 8, 4u) : 0u, n3 = lastn > 12 ? lastn - 12 : 0u;
+      auto keep = [](uint32_t w, uint32_t n) { return n >= 4 ? w : (w | (0xFFFFFFFFu << (8 * n))); };
+      v = make_uint4(keep(v.x, n0), keep(v.y, n1), keep(v.z, n2), keep(v.w, n3));
+    }
+    return v;
+  };
+  auto next_word = [&]() -> uint32_t {
+    const uint32_t w = wci == 0 ? cur.x : (wci == 1 ? cur.y : (wci == 2 ? cur.z : cur.w));
+    if (++wci == 4) { wci = 0; cur = nxt; nxt = nxt2; ++p16; nxt2 = ld_chunk(p16); }
+    return w;
+  };
   auto comp_tables = [&]() {                         // ci, tdc, tac of block b
     ci = (int)((sched >> (2 * b)) & 3u);
     const uint32_t ids = (uint32_t)(tabs >> (18 * ci));
     tdc = (ids & 511u) * TSTRIDE;
     tac = ((ids >> 9) & 511u) * TSTRIDE;
   };
-  // set up interval t; false when it has nothing to decode
-  auto start = [&](uint32_t t) -> bool {
-    s = (int)__ldg(&A.isample[t]);                  // written by J1 (no search over the prefix)
-    if (A.status[s].kind != 0) return false;         // J1 rejected the marker layout
+  // set up interval t of sample si; false when it has nothing to decode
+  auto start = [&](uint32_t t, int si) -> bool {
+    s = si;
     const JpegDesc& J = A.jd[s];
     k = t - J.int_base;
     const uint32_t total = (uint32_t)J.mcus_x * J.mcus_y;
@@ -364,38 +171,58 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     tabs = 0;
     for (int c = 0; c < J.ncomp; ++c) tabs |= (uint64_t)(J.comp[c].dc | (uint32_t)J.comp[c].ac << 9) << (18 * c);
     cb = A.coef + (J.blk_base + (uint64_t)m * bpm) * 64;
-    // 16-byte chunks of the interval (J1 aligned it and zero-padded its tail)
-    p16 = reinterpret_cast<const uint4*>(A.bits + J.bs_base + A.istart[t]);
-    plast = reinterpret_cast<const uint4*>(A.bits + J.bs_base + align_int(A.iend[t]) + kJpegIntPad - 16);
-    const uint4 c = ld_nc_v4(p16);
-    q0 = c.x; q1 = c.y; q2 = c.z; q3 = c.w;
-    p16 += p16 < plast ? 1 : 0;
-    nxt = ld_nc_v4(p16);
-    p16 += p16 < plast ? 1 : 0;
-    nxt2 = ld_nc_v4(p16);
-    wi = 0; acc = 0; nb = 0;
+    const uint8_t* base = A.payload + sdesc(A, s)->src;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(base + __ldg(&A.starts[t]));
+    const uintptr_t e = reinterpret_cast<uintptr_t>(base + J.scan_end);
+    plast = reinterpret_cast<const uint4*>((e - 1) & ~uintptr_t(15));
+    lastn = (uint32_t)(e - reinterpret_cast<uintptr_t>(plast));
+    p16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    cur = ld_chunk(p16);
+    nxt = ld_chunk(p16 + 1);
+    p16 += 2;
+    nxt2 = ld_chunk(p16);
+    wci = (int)((a >> 2) & 3);
+    const uint32_t ph = (uint32_t)(a & 3);
+    sel = (ph << 12) | ((ph + 1) << 8) | ((ph + 2) << 4) | (ph + 3);   // big-endian bytes ph..ph+3 of (qa, qb)
+    qa = next_word();
+    qb = next_word();
+    carry = marker = false;
+    acc = 0; nb = 0;
     b = 0; kk = 0;
     pred0 = pred1 = pred2 = 0;
     comp_tables();
     return true;
   };
-  bool active = (mine >> 8) != 0 && start(c0 + (mine & 0xFFu));
+  bool active = (mine >> 8) != 0 && start(c0 + (mine & 0xFFu), (int)ssamp[mine & 0xFFu]);
   while (__any_sync(0xffffffffu, active)) {
     if (!active) continue;
-    {                                                // predicated 32-bit refill
-      const bool need = nb <= 32;
-      const uint32_t wv = need ? __byte_perm(q0, 0, 0x0123) : 0u;
-      acc |= (uint64_t)wv << ((32 - nb) & 63);
-      nb += need ? 32 : 0;
-      wi += need ? 1 : 0;
-      q0 = need ? q1 : q0; q1 = need ? q2 : q1; q2 = need ? q3 : q2;
-      if (wi == 4) {
-        wi = 0;
-        q0 = nxt.x; q1 = nxt.y; q2 = nxt.z; q3 = nxt.w;
-        nxt = nxt2;
-        p16 += p16 < plast ? 1 : 0;
-        nxt2 = ld_nc_v4(p16);
+    while (nb <= 32) {                               // refill: >= 33 valid bits for the symbol(s) below
+      const uint32_t wv = __byte_perm(qa, qb, sel);
+      if (!(carry | marker) && __vcmpeq4(wv, 0xFFFFFFFFu) == 0) {
+        acc |= (uint64_t)wv << (32 - nb);
+        nb += 32;
+      } else {                                       // stuffing / marker: byte by byte
+        uint32_t o = 0;
+        int no = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t by = (wv >> (24 - 8 * j)) & 0xFFu;
+          if (marker) { o <<= 8; ++no; }
+          else if (carry) {
+            carry = false;
+            if (by == 0) { o = (o << 8) | 0xFFu; ++no; }
+            else { marker = true; o <<= 8; ++no; }
+          } else if (by == 0xFFu) {
+            carry = true;
+          } else {
+            o = (o << 8) | by; ++no;
+          }
+        }
+        if (no) acc |= (uint64_t)o << (64 - nb - 8 * no);
+        nb += 8 * no;
       }
+      qa = qb;
+      qb = next_word();
     }
     uint32_t e = tab[(kk ? tac : tdc) + (uint32_t)(acc >> (64 - kJpegFastBits))];
     bool bad = false;
@@ -801,7 +628,6 @@ static int sm_count() {                     // of the current device (cached per
 int launch_jpeg(const JpegArgs& A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (A.count <= 0 || A.total_int == 0) return 0;
-  jpeg_unstuff_kernel<<<A.count, 32 * kUnstuffWarps, 0, st>>>(A);
   const bool smem = A.n_huff <= kJpegSmemTables;
   const int hsmem = smem ? A.n_huff * (int)sizeof(JHuff::fast) + (A.n_huff * (10 * 4 + 256) + 15) / 16 * 16 : 0;
   // a thread per restart interval, CTAs of kHuffThreads consecutive intervals

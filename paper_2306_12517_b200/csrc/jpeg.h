@@ -1,19 +1,16 @@
 // JPEG codec (codec id 3): host header parse + device decoder.  Shared by
 // jpeg_host.cpp (parse, table build), jpeg.cu (kernels) and engine.cpp.
 //
+// Host (jpeg_prepare, once per sample, cached): header parse, and a scan of
+// the entropy-coded segment for its RSTn markers (T.81 B.2.5) -- count and
+// sequence checked, each restart interval's first byte recorded.
 // Device pipeline for the JPEG samples of one batch:
-//   J1 jpeg_unstuff_kernel   warp per sample: finds the RSTn markers of the
-//                            entropy-coded segment (T.81 B.2.5 / F.1.2.3),
-//                            drops marker and stuffing bytes and writes every
-//                            restart interval as a 4-byte-aligned plain
-//                            bitstream followed by kJpegIntPad zero bytes (so
-//                            J2 refills 32 bits per load, no 0xFF checks, no
-//                            end-of-data test)
-//   J2 jpeg_huffman_kernel   thread per restart interval: one flat loop, one
-//                            symbol per iteration (T.81 F.2.2), shared-memory
-//                            tables that resolve code + extra bits in one
-//                            lookup; coefficient blocks built in shared memory,
-//                            stored as int16[64] natural order
+//   J2 jpeg_huffman_kernel   thread per restart interval, reading the stuffed
+//                            bytes directly (0xFF00 -> 0xFF, marker -> zeros,
+//                            T.81 F.1.2.3): one flat loop, up to five symbols
+//                            per iteration (T.81 F.2.2), shared-memory tables
+//                            that resolve code + extra bits in one lookup;
+//                            coefficients stored as int16[64] in zig-zag order
 //   J3 jpeg_idct_kernel      thread per 8x8 block: dequantize + islow IDCT in
 //                            registers -> u8 component planes
 //   J4 jpeg_color_kernel     thread per 8 output pixels: fancy chroma
@@ -34,8 +31,6 @@ constexpr int kJpegFastBits = 11;         // Huffman lookahead bits (fast table)
 constexpr int kJpegMaxHuff = 512;         // device Huffman table pool entries
 constexpr int kJpegMaxQuant = 256;        // device quant table pool entries
 constexpr int kJpegSmemTables = 8;        // J2 stages the pool in smem when it holds at most this many
-constexpr int kJpegIntAlign = 16;         // restart intervals start 16-byte aligned in the J1 output
-constexpr int kJpegIntPad = 32;           // zero bytes (at least) J1 writes after every interval
 
 // Fast-table entry (u32) indexed by the next kJpegFastBits bits of the stream:
 //   bit 31 valid (code <= kJpegFastBits bits; else the maxcode search),
@@ -75,7 +70,7 @@ struct JpegDesc {                         // per sample, staged with the descrip
   uint32_t n_blocks;
   uint64_t blk_base;                      // first block in the batch coefficient buffer (MCU order:
                                           // block b of MCU m at blk_base + m * bpm + b)
-  uint64_t bs_base;                       // first byte of the sample's unstuffed bitstream
+  uint64_t reserved;
   uint64_t sched;                         // MCU block b: comp bits 4b..4b+1, v bit 4b+2, h bit 4b+3
   JComp comp[3];
   uint32_t plane_blk[3];                  // component c's pixel plane starts plane_blk[c] blocks into the sample's planes
@@ -138,8 +133,8 @@ BBX_HD inline bool jpeg_interval_live(const JpegDesc& J, const McuRect& R, uint3
   return true;
 }
 
-// Per-sample status kinds written by J1/J2 (SampleStatus::kind).
-enum : int32_t { JST_BAD_CODE = 3, JST_MARKER_COUNT = 4, JST_MARKER_SEQ = 5 };
+// Per-sample status kind written by J2 (SampleStatus::kind).
+enum : int32_t { JST_BAD_CODE = 3 };
 
 // Everything the JPEG kernels need for one batch of one plan.
 struct JpegArgs {
@@ -150,10 +145,7 @@ struct JpegArgs {
   const uint32_t* int_prefix;             // count + 1: exclusive prefix of n_int
   const uint64_t* blk_prefix;             // count + 1: exclusive prefix of n_blocks
   uint8_t* planes;                        // total blocks x 64: component planes (J3 -> J4)
-  uint32_t* istart;                       // per interval: bitstream start / end (sample-relative)
-  uint32_t* iend;
-  uint32_t* isample;                      // per interval: its sample (written by J1; J2 needs no search)
-  uint8_t* bits;                          // unstuffed bitstreams
+  const uint32_t* starts;                 // per interval: first entropy-coded byte (payload-relative, host scan)
   int16_t* coef;                          // total blocks x 64
   uint8_t* scratch;                       // count x scratch_bytes: decoded HWC u8
   int64_t scratch_bytes;
