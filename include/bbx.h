@@ -190,6 +190,8 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *   "jpeg_header_cache"     1: keep each JPEG sample's parsed header for later epochs
  *   "jpeg_header_prefetch"  1: parse the headers of this loader's samples up front
  *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
+ *   "compute_streams"       2: consecutive batches alternate between two CUDA streams, so
+ *                              one batch's kernels fill SMs the previous batch's tail leaves idle
  * Unknown names return BBX_INVALID_ARGUMENT. */
 bbx_status bbx_loader_set_option(bbx_loader* ld, const char* name, int64_t value);
 /* Samples whose JPEG headers the loader parses up front (before the first

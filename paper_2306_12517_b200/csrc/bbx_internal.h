@@ -18,6 +18,7 @@ constexpr int kDescHeader = 32;     // bytes before the per-sample params
 constexpr int kCwCols = 2;          // column-walker K1: output columns per thread
 constexpr int kCwStages = 2;   // column-walker K1: source-row pipeline stages
 constexpr int kThreads = 256;       // CTA size of the image kernels
+constexpr int kStreams = 2;         // compute streams a loader alternates its batches between
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
 

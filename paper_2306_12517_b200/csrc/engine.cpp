@@ -141,9 +141,10 @@ struct Plan {
   bool field_has_jpeg = false;
   int64_t jpeg_blocks_cap = 0;   // per sample: coefficient blocks (any sampling with factors <= 2)
   int64_t jpeg_int_cap = 0;      // per sample: restart intervals (<= MCUs)
-  int16_t* d_coef = nullptr;     // JPEG scratch shared by the slots (one compute stream orders them)
-  uint8_t* d_planes = nullptr;   // IDCT output: component planes
-  unsigned long long* d_ticket = nullptr;   // column-walker K1 tile ticket (2 x u64, zero between launches)
+  // per compute stream (batches alternate between kStreams streams; one stream orders its own)
+  int16_t* d_coef[kStreams] = {};           // JPEG coefficients
+  uint8_t* d_planes[kStreams] = {};         // IDCT output: component planes
+  unsigned long long* d_ticket[kStreams] = {};   // column-walker K1 tile ticket (2 x u64, zero between launches)
   void* d_lut = nullptr;
   std::vector<void*> outs;       // per slot
   std::vector<uint8_t*> d_scratch;
@@ -210,7 +211,9 @@ struct bbx_loader {
   int batch = 0, nslots = 0;
   std::vector<Plan> plans;
   std::vector<Slot> slots;
-  cudaStream_t copy_st{}, comp_st{};
+  cudaStream_t copy_st{}, comp_st[kStreams]{};   // batches alternate between the compute streams
+  uint64_t batch_seq = 0;             // batches launched (pipeline thread): picks the stream
+  int nstreams = kStreams;            // compute streams in use (option "compute_streams": 1 or 2)
   std::unique_ptr<Pool> pool;
   bool finalized = false;
   size_t slot_bytes = 0, desc_bytes = 0, idx_off = 0;
@@ -881,8 +884,10 @@ static int finalize(bbx_loader* L) {
   }
   for (auto& pl : L->plans) {
     if (pl.scalar || !pl.dev.cw) continue;
-    CK(cudaMalloc(&pl.d_ticket, 16));
-    CK(cudaMemset(pl.d_ticket, 0, 16));
+    for (int k = 0; k < kStreams; ++k) {
+      CK(cudaMalloc(&pl.d_ticket[k], 16));
+      CK(cudaMemset(pl.d_ticket[k], 0, 16));
+    }
   }
   for (auto& pl : L->plans) {
     if (pl.scalar || pl.dev.src_kind == SRC_ARRAY) continue;
@@ -902,8 +907,10 @@ static int finalize(bbx_loader* L) {
       pl.jcached.assign(L->ds->num_samples, 0);
     }
     const size_t blocks = (size_t)L->batch * pl.jpeg_blocks_cap, ints = (size_t)L->batch * pl.jpeg_int_cap;
-    CK(cudaMalloc(&pl.d_coef, blocks * 128 + 256));
-    CK(cudaMalloc(&pl.d_planes, blocks * 64 + 256));
+    for (int k = 0; k < kStreams; ++k) {
+      CK(cudaMalloc(&pl.d_coef[k], blocks * 128 + 256));
+      CK(cudaMalloc(&pl.d_planes[k], blocks * 64 + 256));
+    }
   }
   if (any_jpeg && !L->jt.d_huff) {
     JpegTables& T = L->jt;
@@ -1230,14 +1237,18 @@ static int process_slot(bbx_loader* L, int s) {
     CK(cudaEventRecord(S.h2d_t, L->copy_st));
     S.h2d_timed = true;
   }
-  CK(cudaStreamWaitEvent(L->comp_st, S.h2d_done, 0));
+  // consecutive batches go to alternating compute streams: one batch's kernels can
+  // fill the SMs that the previous batch's tail (e.g. the last Huffman lanes) leaves idle
+  const int sk = (int)(L->batch_seq++ % (uint64_t)L->nstreams);
+  cudaStream_t cs = L->comp_st[sk];
+  CK(cudaStreamWaitEvent(cs, S.h2d_done, 0));
   bool wait_release;
   {
     std::lock_guard<std::mutex> g(L->mu);
     wait_release = S.released_pending;
     S.released_pending = false;
   }
-  if (wait_release) CK(cudaStreamWaitEvent(L->comp_st, S.release, 0));
+  if (wait_release) CK(cudaStreamWaitEvent(cs, S.release, 0));
   int launches = 0;
   // profiling: every prof_every-th batch gets the CUDA-event window (sampling keeps
   // the events' own cost off most batches)
@@ -1245,9 +1256,9 @@ static int process_slot(bbx_loader* L, int s) {
   int64_t kbytes = 0, klaunch = 0;
   if (prof && !L->t_ref) {
     CK(cudaEventCreate(&L->t_ref));
-    CK(cudaEventRecord(L->t_ref, L->comp_st));
+    CK(cudaEventRecord(L->t_ref, cs));
   }
-  if (prof) CK(cudaEventRecord(S.k0, L->comp_st));
+  if (prof) CK(cudaEventRecord(S.k0, cs));
   int64_t d2h = 0;
   bool any_rle = false, any_jpeg = false;
   ScalarArgs SA{};
@@ -1275,7 +1286,7 @@ static int process_slot(bbx_loader* L, int s) {
       SA.cols[SA.n_fields] = pl.d_col;
       SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
       ++SA.n_fields;
-      if (SA.n_fields == 16) { if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed"); ++launches; SA.n_fields = 0; }
+      if (SA.n_fields == 16) { if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed"); ++launches; SA.n_fields = 0; }
       continue;
     }
     LaunchArgs A{};
@@ -1288,10 +1299,10 @@ static int process_slot(bbx_loader* L, int s) {
     A.status = S.d_status + (size_t)p * L->batch;
     A.count = count;
     if ((int)p == fused_plan) A.sc = SA;
-    A.ticket = pl.d_ticket;
+    A.ticket = pl.d_ticket[sk];
     if (count == 0) continue;
     if (S.plan_has_rle[p]) {
-      if (launch_rle_expand(pl.dev, A, L->comp_st)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      if (launch_rle_expand(pl.dev, A, cs)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       ++launches; any_rle = true;
     }
     if (S.plan_has_jpeg[p]) {
@@ -1302,18 +1313,18 @@ static int process_slot(bbx_loader* L, int s) {
       J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
       J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
       J.starts = reinterpret_cast<const uint32_t*>(jb + jpeg_block_bytes(L->batch));
-      J.coef = pl.d_coef; J.planes = pl.d_planes;
+      J.coef = pl.d_coef[sk]; J.planes = pl.d_planes[sk];
       J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
       J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
       J.coef_zeroed = 1;
       J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
       J.max_blocks = S.jpeg_max_blocks[p];
       // J2 stores only nonzero coefficients
-      CK(cudaMemsetAsync(pl.d_coef, 0, (size_t)S.jpeg_total_blk[p] * 128, L->comp_st));
-      if (launch_jpeg(J, L->comp_st)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      CK(cudaMemsetAsync(pl.d_coef[sk], 0, (size_t)S.jpeg_total_blk[p] * 128, cs));
+      if (launch_jpeg(J, cs)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       launches += 4; any_jpeg = true;
     }
-    int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, L->comp_st) : launch_image(pl.dev, A, L->comp_st);
+    int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, cs) : launch_image(pl.dev, A, cs);
     if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
       ++klaunch;
       const uint8_t* dblk = H + L->desc_off[p];
@@ -1331,20 +1342,20 @@ static int process_slot(bbx_loader* L, int s) {
     if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.cw) ? 1 : 2;   // K1 = prologue + tiles (column walker: one kernel)
   }
-  if (prof) CK(cudaEventRecord(S.k1, L->comp_st));
+  if (prof) CK(cudaEventRecord(S.k1, cs));
   S.timed = prof;
   S.timed_launches = klaunch;
   S.timed_bytes = kbytes;
   if (SA.n_fields && count && fused_plan < 0) {
-    if (launch_scalar_gather(SA, L->comp_st)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
+    if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
     ++launches;
   }
   if (any_rle || any_jpeg) {
     size_t nb = sizeof(SampleStatus) * L->batch * L->plans.size();
-    CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, L->comp_st));
+    CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, cs));
     d2h += (int64_t)nb;
   }
-  CK(cudaEventRecord(S.done, L->comp_st));
+  CK(cudaEventRecord(S.done, cs));
   S.used = true;
   {
     std::lock_guard<std::mutex> g(L->stats_mu);
@@ -1529,7 +1540,8 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   }
   L->pool = std::make_unique<Pool>(nt);
   if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
-      (e = cudaStreamCreateWithFlags(&L->comp_st, cudaStreamNonBlocking)) != cudaSuccess)
+      (e = cudaStreamCreateWithFlags(&L->comp_st[0], cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&L->comp_st[1], cudaStreamNonBlocking)) != cudaSuccess)
     return (bbx_status)fail(BBX_CUDA_ERROR, "stream create: %s", cudaGetErrorString(e));
   *out = L.release();
   return BBX_OK;
@@ -1710,7 +1722,8 @@ bbx_status bbx_loader_drain(bbx_loader* L) {
     for (auto& S : L->slots) if (S.state == 2) S.state = 0;
   }
   cudaSetDevice(L->device);
-  cudaError_t e1 = cudaStreamSynchronize(L->comp_st), e2 = cudaStreamSynchronize(L->copy_st);
+  cudaError_t e1 = cudaStreamSynchronize(L->comp_st[0]), e2 = cudaStreamSynchronize(L->copy_st);
+  if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(L->comp_st[1]);
   if (e1 != cudaSuccess || e2 != cudaSuccess)
     return (bbx_status)fail(BBX_CUDA_ERROR, "drain: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
   return BBX_OK;
@@ -1743,16 +1756,18 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (pl.d_col) cudaFree(pl.d_col);
     for (auto* p : pl.d_scratch) if (p) cudaFree(p);
     for (auto* p : pl.d_tables) if (p) cudaFree(p);
-    if (pl.d_coef) cudaFree(pl.d_coef);
-    if (pl.d_planes) cudaFree(pl.d_planes);
-    if (pl.d_ticket) cudaFree(pl.d_ticket);
+    for (int k = 0; k < kStreams; ++k) {
+      if (pl.d_coef[k]) cudaFree(pl.d_coef[k]);
+      if (pl.d_planes[k]) cudaFree(pl.d_planes[k]);
+      if (pl.d_ticket[k]) cudaFree(pl.d_ticket[k]);
+    }
   }
   if (L->jt.h_huff) cudaFreeHost(L->jt.h_huff);
   if (L->jt.h_quant) cudaFreeHost(L->jt.h_quant);
   if (L->jt.d_huff) cudaFree(L->jt.d_huff);
   if (L->jt.d_quant) cudaFree(L->jt.d_quant);
   if (L->copy_st) cudaStreamDestroy(L->copy_st);
-  if (L->comp_st) cudaStreamDestroy(L->comp_st);
+  for (cudaStream_t st : L->comp_st) if (st) cudaStreamDestroy(st);
   delete L;
 }
 
@@ -1781,6 +1796,10 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   else if (n == "jpeg_header_cache") L->jpeg_cache = value != 0;
   else if (n == "jpeg_roi") L->jpeg_roi = value != 0;
   else if (n == "jpeg_header_prefetch") L->jpeg_prefetch = value != 0;
+  else if (n == "compute_streams") {
+    if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);
+    L->nstreams = (int)value;
+  }
   else return (bbx_status)fail(BBX_INVALID_ARGUMENT, "unknown loader option '%s'", name);
   return BBX_OK;
 }
@@ -1807,7 +1826,7 @@ bbx_status bbx_loader_set_profiling(bbx_loader* L, int enabled) {
   L->last_k1_ms = -1.f;
   return BBX_OK;
 }
-void* bbx_loader_compute_stream(bbx_loader* L) { return L ? (void*)L->comp_st : nullptr; }
+void* bbx_loader_compute_stream(bbx_loader* L) { return L ? (void*)L->comp_st[0] : nullptr; }
 
 static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host, int64_t len,
                              uint8_t* out_dev, int device) {

@@ -38,7 +38,8 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
 // (the block buffer is pre-zeroed).  Block ends read the next block's
 // component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 256;           // 8 warps share one copy of the smem tables
-constexpr int kHuffCtasPerSm = 4;           // 32 warps per SM: <= 64 registers per thread
+constexpr int kHuffCtasPerSm = 3;           // 24 warps per SM (<= 85 registers): a B200 holds 113k lanes,
+                                            // more than a batch of 1024 ImageNet-sized JPEGs has intervals
 constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
 
   auto ld_chunk = [&](const uint4* p) -> uint4 {
     if (p > plast) return make_uint4(~0u, ~0u, ~0u, ~0u);
-    uint4 v = ld_nc_v4(p);
+    uint4 v = __ldg(p);                             // L1-allocating: the line's next chunks hit
     if (p == plast && lastn < 16) {                  // bytes past the scan data read as 0xFF (a marker)
       const uint32_t n0 = min(lastn, 4u), n1 = lastn > 4 ? min(lastn - 4, 4u) : 0u,
                      n2 = lastn > 8 ? min(lastn - 8, 4u) : 0u, n3 = lastn > 12 ? lastn - 12 : 0u;
@@ -147,7 +148,14 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   };
   auto next_word = [&]() -> uint32_t {
     const uint32_t w = wci == 0 ? cur.x : (wci == 1 ? cur.y : (wci == 2 ? cur.z : cur.w));
-    if (++wci == 4) { wci = 0; cur = nxt; nxt = nxt2; ++p16; nxt2 = ld_chunk(p16); }
+    if (++wci == 4) {
+      wci = 0; cur = nxt; nxt = nxt2; ++p16;
+      // the rotation reads nxt2, so the load it waits on must hit L1: the stream's
+      // line after next is prefetched when a chunk starts a 128-B line
+      if ((reinterpret_cast<uintptr_t>(p16) & 127) == 0 && p16 + 16 <= plast)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 16));
+      nxt2 = ld_chunk(p16);
+    }
     return w;
   };
   auto comp_tables = [&]() {                         // ci, tdc, tac of block b
@@ -177,6 +185,8 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     plast = reinterpret_cast<const uint4*>((e - 1) & ~uintptr_t(15));
     lastn = (uint32_t)(e - reinterpret_cast<uintptr_t>(plast));
     p16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    if (p16 + 8 <= plast) asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 8));
+    if (p16 + 16 <= plast) asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 16));
     cur = ld_chunk(p16);
     nxt = ld_chunk(p16 + 1);
     p16 += 2;
@@ -279,18 +289,23 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     const int pos = kk + run;
     if (v != 0 && !bad) cb[min(pos, 63)] = (int16_t)v;   // zig-zag order (J3 de-zigzags at compile time)
     kk = (e & kFastEob) ? 64 : pos + 1;
-    // a second AC symbol in the same iteration when the block continues, the bit
-    // buffer holds the 11-bit peek (a full entry consumes at most that) and its code + value resolve in the
-    // fast table; otherwise it is left for the next iteration
+    // more AC symbols in the same iteration while the block continues and the
+    // bit buffer holds the symbol: its code within the 11-bit peek, plus its
+    // extra bits (read here when the entry could not hold the value)
 #pragma unroll
     for (int extra = 0; extra < kExtraSymbols; ++extra) {
-      if (kk < 64 && !bad && nb >= kJpegFastBits) {   // a full entry never reads past the 11-bit peek
+      if (kk < 64 && !bad && nb >= kJpegFastBits) {
         const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
-        if ((e2 & (kFastValid | kFastFull)) == (kFastValid | kFastFull)) {
-          acc <<= (e2 >> 25) & 31;
-          nb -= (int)((e2 >> 25) & 31);
+        const bool full2 = (e2 & kFastFull) != 0;
+        const int l2 = (int)((e2 >> 25) & 31), sz2 = full2 ? 0 : (int)((e2 >> 16) & 15);
+        if ((e2 & kFastValid) && nb >= l2 + sz2) {
+          acc <<= l2;
+          const uint32_t hi2 = (uint32_t)(acc >> 32);
+          const int v2 = full2 ? (int)(int16_t)(e2 & 0xFFFF)
+                               : (int)__funnelshift_l(hi2, 0u, sz2) + ((int)((0xFFFFFFFFu << sz2) + 1u) & ~((int)hi2 >> 31));
+          acc <<= sz2;
+          nb -= l2 + sz2;
           const int pos2 = kk + (int)((e2 >> 21) & 15);
-          const int v2 = (int)(int16_t)(e2 & 0xFFFF);
           if (v2 != 0) cb[min(pos2, 63)] = (int16_t)v2;
           kk = (e2 & kFastEob) ? 64 : pos2 + 1;
         }
