@@ -15,8 +15,20 @@ enum ValueMode : int32_t { VAL_COPY = 0, VAL_FMA = 1, VAL_DIRECT = 2, VAL_LUT = 
 constexpr int kMaxRemaps = 12;
 constexpr int kMaxValueOps = 8;
 constexpr int kDescHeader = 32;     // bytes before the per-sample params
-constexpr int kCwCols = 2;          // column-walker K1: output columns per thread
-constexpr int kCwStages = 2;   // column-walker K1: source-row pipeline stages
+// column-walker K1 compile-time shape (the defaults are the measured best;
+// _build.build(defines=...) makes A/B builds for measurement scripts)
+#ifndef BBX_CW_STAGES
+#define BBX_CW_STAGES 2
+#endif
+#ifndef BBX_CW_ROWS
+#define BBX_CW_ROWS 16
+#endif
+#ifndef BBX_CW_RUN
+#define BBX_CW_RUN 3
+#endif
+constexpr int kCwStages = BBX_CW_STAGES;   // source-row pipeline stages
+constexpr int kCwRows = BBX_CW_ROWS;       // output rows per tile (fewer when a tile would span > 32 source rows)
+constexpr int kCwRun = BBX_CW_RUN;         // consecutive tiles per ticket
 constexpr int kThreads = 256;       // CTA size of the image kernels
 constexpr int kStreams = 2;         // compute streams a loader alternates its batches between
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
@@ -69,14 +81,14 @@ struct PlanDev {
   uint32_t linx_magic, liny_magic;         // for 2*canvas_w / 2*canvas_h (bilinear axes), 0 = use /
   int32_t h_tpc;                           // horizontal pass: threads per output column
   int32_t tab_stride;                      // K1 prologue table words per sample
-  // column-walker K1 (bilinear, 3 channels): a thread per output column walks the
-  // tile's rows; no horizontal-pass buffer, so tiles are taller and CTAs smaller
-  int32_t cw, cw_smem, cw_npair, cw_groups;
-  uint32_t cw_magic;                       // ceil(2^32 / cw_npair) when exact for every item index
+  // column-walker K1 (bilinear, 3 channels): a compute thread owns two output
+  // columns of every tile its CTA takes (image_kernel.cuh, image_cw_kernel)
+  int32_t cw, cw_smem, cw_npair;
   int32_t cw_warps;                        // compute warps per CTA (plus one copy-issuing warp)
-  int32_t cw_slots;                        // source rows one pipeline stage holds (even, <= 2 x rows_per_tile)
-  int32_t cw_rg;                           // rows per item of a full tile: ceil(rows_per_tile / cw_groups)
-  int32_t cw_run;                          // consecutive tiles a CTA takes per ticket (BBX_CW_RUN, default 3)
+  int32_t cw_slots;                        // source rows one pipeline stage holds (<= 32)
+  int32_t cw_run;                          // consecutive tiles a CTA takes per ticket
+  int32_t cw_affine;                       // f16/bf16 values as fma(u, cw_aff_a[c], cw_aff_b[c]) (host-proven exact)
+  float cw_aff_a[4], cw_aff_b[4];
   SmemLayout lay;
 };
 

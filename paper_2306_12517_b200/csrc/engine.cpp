@@ -270,6 +270,50 @@ static bool verify_fma_normalize(const PlanDev& P, int C) {
   return true;
 }
 
+// f16 / bf16 output of a u8 value chain through the column-walker K1: the
+// kernel forms y = fma(u, A_c, B_c) in f32 and rounds it to the output type
+// (cvt.rn.f16x2 / bf16x2).  The chain (x - m) / s ... is affine in u; the
+// coefficients are searched a few ulps around their double-precision values
+// until the result equals the exact value table (`lut`, the reference's IEEE
+// subtract + divide, pipeline.py:158-160) for every one of the 256 inputs of
+// every channel -- a proof by enumeration, as verify_fma_normalize.  No pair
+// found: the kernel keeps the table.
+static bool prove_affine(PlanDev& P, int C, const std::vector<uint8_t>& lut, int out_dt) {
+  for (int k = 0; k < C; ++k) {
+    double a = 1.0, b = 0.0;
+    for (int i = 0; i < P.n_vops; ++i) {
+      a = a / P.vop_std[i][k];
+      b = (b - P.vop_mean[i][k]) / P.vop_std[i][k];
+    }
+    const uint16_t* want = reinterpret_cast<const uint16_t*>(lut.data()) + (size_t)k * 256;
+    auto ok = [&](float A, float B) {
+      for (int v = 0; v < 256; ++v) {
+        const float y = std::fma((float)v, A, B);
+        const uint16_t got = out_dt == BBX_F16 ? f32_to_f16_bits(y) : f32_to_bf16_bits(y);
+        if (got != want[v]) return false;
+      }
+      return true;
+    };
+    bool found = false;
+    const float A0 = (float)a, B0 = (float)b;
+    float A = A0;
+    for (int da = 0; da <= 8 && !found; ++da) {
+      for (int sa = 0; sa < (da ? 2 : 1) && !found; ++sa) {
+        A = A0;
+        for (int i = 0; i < da; ++i) A = std::nextafter(A, sa ? -INFINITY : INFINITY);
+        for (int db = 0; db <= 32 && !found; ++db)
+          for (int sb = 0; sb < (db ? 2 : 1) && !found; ++sb) {
+            float B = B0;
+            for (int i = 0; i < db; ++i) B = std::nextafter(B, sb ? -INFINITY : INFINITY);
+            if (ok(A, B)) { P.cw_aff_a[k] = A; P.cw_aff_b[k] = B; found = true; }
+          }
+      }
+    }
+    if (!found) return false;
+  }
+  return true;
+}
+
 static int host_back_y(const PlanDev& P, const int32_t* prm, int y);
 
 // Integer bilinear axis rule (kernel lin_axis / oracle lin_axis), host copy.
@@ -447,12 +491,14 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
     P.lay = img_layout_host(P);
     P.h_tpc = std::max(1, kThreads / W);
     P.tab_stride = image_tab_stride(P);
-    // column-walker K1 for 3-channel bilinear decoders
+    // column-walker K1 for 3-channel bilinear decoders: a compute thread owns
+    // two output columns (OW <= 512: at most 8 compute warps), row tags are
+    // 16-bit absolute source rows (heights < 0xFFFE)
     P.cw = 0;
-    if (P.src_kind == SRC_RESAMPLE && C == 3) {
-      // rows per tile: 16, fewer when two pipeline stages of source rows would
-      // not leave room for 2 CTAs per SM (nslot = 2 x rows <= 64)
-      for (int rows : {16, 8, 4, 2}) {
+    if (P.src_kind == SRC_RESAMPLE && C == 3 && (P.value_mode == VAL_LUT || P.value_mode == VAL_COPY) &&
+        W <= 2 * 32 * 8 && f.info.max_height < 0xFFFE) {
+      // rows per tile: 16, fewer when a tile could span more than 32 source rows
+      for (int rows : {kCwRows, 16, 8, 4, 2}) {
         PlanDev Q = P;
         Q.rows_per_tile = std::min(rows, H);
         Q.tiles_per_sample = (H + Q.rows_per_tile - 1) / Q.rows_per_tile;
@@ -461,41 +507,19 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
         {   // stage slots: source rows any tile can span.  Rows_per_tile output
             // rows cover at most n canvas rows back through the y remaps, and n
             // canvas rows at most ceil((n - 1) * crop / canvas) + 2 source rows
-            // (two taps) with crop <= the field's max height; the prologue then
-            // always takes its contiguous-range branch with <= that many slots.
+            // (two taps) with crop <= the field's max height.
           int64_t n = Q.rows_per_tile;
           for (int i = Q.n_remaps - 1; i >= 0; --i)
             if (Q.remaps[i].kind == BBX_OP_RESIZE)
               n = ((n - 1) * Q.remaps[i].in_h + Q.remaps[i].out_h - 1) / Q.remaps[i].out_h + 1;
           const int64_t src = ((n - 1) * f.info.max_height + Q.canvas_h - 1) / Q.canvas_h + 2;
-          if (src > 64) continue;
-          Q.cw_slots = (int)((src + 1) & ~1LL);
+          if (src > 32) continue;
+          Q.cw_slots = (int)src;
         }
+        Q.cw_npair = (W + 1) / 2;
+        Q.cw_warps = (Q.cw_npair + 31) / 32;
+        Q.cw_run = kCwRun;
         Q.cw_smem = cw_smem_host(Q);
-        Q.cw_npair = (W + kCwCols - 1) / kCwCols;   // column groups
-        // items = column pairs x row groups; compute warps (<= 8) sized to the
-        // items so no warp idles at a tile: the fewest groups (longest row runs,
-        // most horizontal-sum reuse) that give >= 6 warps at >= 90 % lane use
-        {
-          int best_g = 1, best_w = 1;
-          double best_score = -1.0;
-          for (int g = 1; g <= Q.rows_per_tile; ++g) {
-            const int items = Q.cw_npair * g, w = std::min(8, (items + 31) / 32);
-            const int rounds = (items + 32 * w - 1) / (32 * w);
-            const double eff = (double)items / (rounds * 32.0 * w);
-            const bool ok = eff >= 0.9 && (w >= 6 || g == Q.rows_per_tile);
-            const double score = ok ? 2.0 : eff * std::min(1.0, w / 6.0);
-            if (score > best_score + 1e-9) { best_score = score; best_g = g; best_w = w; }
-            if (ok) break;
-          }
-          Q.cw_groups = best_g;
-          Q.cw_warps = best_w;
-        }
-        Q.cw_rg = (Q.rows_per_tile + Q.cw_groups - 1) / Q.cw_groups;
-        Q.cw_run = 3;
-        const uint64_t items = (uint64_t)Q.cw_npair * Q.cw_groups + kThreads;
-        Q.cw_magic = (Q.cw_npair > 1 && items * Q.cw_npair < (1ull << 32))
-                         ? (uint32_t)(((1ull << 32) + Q.cw_npair - 1) / Q.cw_npair) : 0u;
         if (Q.cw_smem <= 110 * 1024) { P = Q; P.cw = 1; break; }
       }
     }
@@ -517,6 +541,10 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       }
     CK(cudaMalloc(&pl.d_lut, lut.size()));
     CK(cudaMemcpy(pl.d_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+    if (P.cw && (out_dt == BBX_F16 || out_dt == BBX_BF16) && prove_affine(P, C, lut, out_dt)) {
+      P.cw_affine = 1;
+      P.cw_smem = cw_smem_host(P);   // no value table in shared memory
+    }
   }
   // one pass over the row table: exact staging capacity, RLE presence
   int64_t mx = 0;

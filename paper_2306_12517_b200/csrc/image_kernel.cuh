@@ -522,36 +522,52 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 }
 
 // ------------------------------------------------------- K1 (column walker)
-// Bilinear decoders, 3 channels.  Persistent CTAs (SMs x resident CTAs) walk the
-// batch's tiles (tile = rows_per_tile output rows of one sample), taking runs of
-// cw_run consecutive tiles from a global ticket that the last CTA re-zeroes, so
-// SMs that drew cheap samples take more.  Per CTA a two-stage shared-memory
-// pipeline: while the compute warps work on tile i out of one stage, the
-// source rows of tile i + 1 are landing in the other, moved by the copy engine
-// (one cp.async.bulk per tile: the tile's rows are consecutive rows of a
-// row-strided image; completion counted in bytes on the stage's "full"
-// mbarrier).  A dedicated copy warp takes the tickets, computes each tile's
-// geometry (column table once per sample, row taps) into a ring entry, issues
-// the copy once the compute warps have released the stage ("empty" mbarrier),
-// gathers the batch's scalar fields with tile 0 of each sample, and finally
-// posts a stop entry.
-// Compute: thread x owns output columns 2x, 2x + 1 and walks a run of the
-// tile's rows: the 2-tap horizontal sums of a source row are computed in
-// registers when a row first appears (one register set per slot parity, kept
-// for the next output row that reuses it), then the vertical blend, the value
-// table and the store.  Same integer arithmetic as image_kernel (bit-identical).
-__host__ __device__ inline int cw_nslot(const PlanDev& P) { return 2 * P.rows_per_tile; }   // table slots
+// Bilinear decoders (RandomResizedCrop / CenterCrop), 3 channels.
+//
+// Persistent CTAs (SMs x resident CTAs) walk the batch's tiles (tile =
+// rows_per_tile output rows of one sample), taking runs of cw_run consecutive
+// tiles from a global ticket that the last CTA re-zeroes, so SMs that drew
+// cheap samples take more.  A CTA is one copy warp plus ceil(OW / 64) compute
+// warps; compute thread x owns output columns 2x, 2x + 1 of EVERY tile the CTA
+// takes, so its per-column state survives from tile to tile of a sample.
+//
+// Copy warp: takes the tickets, writes each tile's geometry into a ring entry
+// (the column table once per sample; per output row the two source rows'
+// stage offsets, their absolute row numbers and the blend weight), then --
+// once the compute warps have released the stage ("empty" mbarrier) -- moves
+// the tile's source rows into it with cp.async.bulk (TMA 1-D, completion
+// counted in bytes on the stage's "full" mbarrier): one copy per row when the
+// window is narrower than the row stride (only the window's columns cross
+// L2 -> SMEM), else one copy for the whole row range.  It also gathers the
+// batch's scalar fields with tile 0 of each sample.
+//
+// Compute: the 2-tap horizontal sums of a source row are formed when the row
+// first appears for its parity (even / odd absolute row: the two taps of an
+// output row are always one of each), with byte-pair dot products (dp2a) on
+// funnel-shifted words, and kept in registers as
+//     nhe = -h(even row),  D = h(odd row) - h(even row),  Ce = 8192 h(even) + 2^23
+// so the vertical blend is ONE integer multiply-add per value,
+//     s = Ce + 4 w_odd D = 4 (w_even h_even + w_odd h_odd + 2^21),   u = s >> 24,
+// the same integer the tile kernel / oracle form ((w0 h0 + w1 h1 + 2^21) >> 22,
+// bit for bit).  Row tags are absolute source rows, so a row shared by two
+// consecutive tiles of a sample is not summed twice.  u -> output: f16 / bf16
+// through a per-channel f32 affine map fma(u, A, B) that the host proved equal
+// to the exact value table for all 256 inputs (packed f32x2 math, no shared-
+// memory table), else the table; packed 32-bit stores.
+enum CwMode : int { CW_COPY = 0, CW_LUT = 1, CW_AFFINE = 2 };
+constexpr uint32_t kCwFake = 0xFFFEu;       // tag of a weight-0 parity (never a real row: heights < 0xFFFE)
+constexpr uint32_t kCwReset = 0xFFFFFFFFu;  // tags after a sample change: match nothing
+
 __host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
 __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
-  return P.value_mode == VAL_LUT ? align_up(P.channels * 256 * out_size(P), 16) : 0;
+  return (P.value_mode == VAL_LUT && !P.cw_affine) ? align_up(P.channels * 256 * out_size(P), 16) : 0;
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16 * kCwStages; }
-// geometry ring (stages + 1 entries): tile id (16 B) | column table xt[owp] | rowtap[rows_per_tile] (uint2);
-// source-row stages (2): cw_slots x span_pad (whole rows at the image's row stride)
-__host__ __device__ inline int cw_stage_meta(const PlanDev& P) {
-  return 16 + align_up((tab_owp(P) + 2 * P.rows_per_tile) * 4, 16);   // [tile id, pad x3] | xt | rowtap
-}
+// ring entry (stages + 1 of them): header (16 B: tile id, sample, live, new-sample) | column table xt[owp] |
+// per output row uint4 {even row's stage offset, odd row's stage offset, tag_even | tag_odd << 16, 4 * w_odd}
+__host__ __device__ inline int cw_tap_off(const PlanDev& P) { return 16 + align_up(tab_owp(P) * 4, 16); }
+__host__ __device__ inline int cw_stage_meta(const PlanDev& P) { return cw_tap_off(P) + 16 * P.rows_per_tile; }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
   return cw_stage_off(P) + (kCwStages + 1) * cw_stage_meta(P) + kCwStages * cw_src_stage(P);
@@ -577,22 +593,77 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
 }
+// c + a.lo16 * b.byte0 + a.hi16 * b.byte1 (signed 16-bit weights, unsigned bytes); _hi: bytes 2, 3
+__device__ __forceinline__ int dp2a_lo(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp2a.lo.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp2a.hi.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+// (x - y) and fma(x, a, b) on f32 pairs, one instruction each (FADD2 / FFMA2; .rn: never contracted)
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long x, unsigned long long y) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(y));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long x, unsigned long long a,
+                                                     unsigned long long b) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(x), "l"(a), "l"(b));
+  return d;
+}
+// bits of the float 2^23 + (s >> 24): one IMAD.HI on the FMA pipe
+__device__ __forceinline__ uint32_t u8_magic(uint32_t s) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, 256, 0x4B000000;" : "=r"(d) : "r"(s));
+  return d;
+}
+template <typename OutT> __device__ __forceinline__ uint32_t cvt_pack2(unsigned long long y);
+template <> __device__ __forceinline__ uint32_t cvt_pack2<__half>(unsigned long long y) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "r"((uint32_t)(y >> 32)), "r"((uint32_t)y));
+  return d;
+}
+template <> __device__ __forceinline__ uint32_t cvt_pack2<__nv_bfloat16>(unsigned long long y) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "r"((uint32_t)(y >> 32)), "r"((uint32_t)y));
+  return d;
+}
 
-template <typename OutT, int kVal>
-__global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
-  constexpr int C = 3, NP = kCwCols;
+// Horizontal 2-tap sums of one source pixel's three channels: bytes a0 a1 a2 b0 b1 b2 at stage byte `a`
+// (b = the second tap's pixel, 3 bytes on; sel picks a's bytes twice when both taps are one column).
+struct CwTap {
+  uint32_t p1, p2;   // {a0, b0, a1, b1}, {a2, b2, -, -}
+};
+__device__ __forceinline__ CwTap cw_bytes(const uint8_t* stage, uint32_t a, uint32_t sel1, uint32_t sel2) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(stage + (a & ~3u));
+  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+  const uint32_t x = __funnelshift_r(w0, w1, a << 3), y = __funnelshift_r(w1, w2, a << 3);
+  return CwTap{__byte_perm(x, y, sel1), __byte_perm(x, y, sel2)};
+}
+
+template <typename OutT, int kMode>
+__global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
+  constexpr int C = 3;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ncw = P.cw_warps, nct = ncw * 32;          // compute warps 0..ncw-1; warp ncw issues the copies
+  const int ncw = P.cw_warps;                          // compute warps 0..ncw-1; warp ncw issues the copies
   const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
-  // nslot: source-row slots a stage holds (the host proves every tile's
-  // contiguous row range fits)
-  const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P);
+  const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P), span_pad = cw_span_pad(P);
+  const int tap_off = cw_tap_off(P);
+  // tickets: the first `nrun` hand out runs of cw_run consecutive tiles (sample-major
+  // order), the last ~2 x grid tiles go out one by one (a short tail); a CTA's
+  // first ticket is its block index, the rest come from a global counter
   const int total = A.count * tps, G = gridDim.x;
-  // tiles are handed out in runs of cw_run consecutive tiles (sample-major order)
-  // from a global ticket, so CTAs whose samples resample cheaply take more
-  const int run = P.cw_run, nruns = (total + run - 1) / run;
+  const int run = P.cw_run, tail = min(total, 2 * G), nrun = (total - tail) / run, head = nrun * run;
+  const int ntickets = nrun + (total - head);
   extern __shared__ __align__(16) uint8_t smem[];
-  OutT* lut = reinterpret_cast<OutT*>(smem);
   constexpr int NS = kCwStages, NR = kCwStages + 1;   // source stages; geometry ring entries
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[NS], empty[NS]
   uint64_t* empty = full + NS;
@@ -609,21 +680,26 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
   if (warp == ncw) {
     // ---- copy warp: tile k's geometry -> ring entry k % NR (free: iteration
     // k - 1 waited for tile k - 1 - NS), then, once the compute warps have
-    // released tile k - NS's stage, its source rows -> stage k % NS (nslot <= 64)
+    // released tile k - NS's stage, its source rows -> stage k % NS (nslot <= 32)
     int k = 0, m = 0, b = 0, ph = 0;                   // ph: parity of stage b's use count
     int t = 0, left = 0;                               // next tile, tiles left in the current run
-    int cur_s = -1, prev_m = 0, col_lo = 0, span_bytes = 0;   // the column table of sample cur_s sits in entry prev_m
+    int cur_s = -1, col_lo = 0, span_bytes = 0;        // the sample whose column table was last written
     for (;; ++k, m = m == NR - 1 ? 0 : m + 1) {
       if (k > 0 && ++b == NS) { b = 0; ph ^= 1; }
       if (left == 0) {
-        unsigned long long u = 0;
-        if (lane == 0) u = atomicAdd(&A.ticket[0], 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= (unsigned long long)nruns) {
+        unsigned long long u = blockIdx.x;
+        if (k > 0) {
+          if (lane == 0) u = G + atomicAdd(&A.ticket[0], 1ull);
+          u = __shfl_sync(0xffffffffu, u, 0);
+        }
+        if (u >= (unsigned long long)ntickets) {
           t = -1;
-        } else {
+        } else if (u < (unsigned long long)nrun) {
           t = (int)u * run;
-          left = min(run, total - t);
+          left = run;
+        } else {
+          t = head + (int)(u - nrun);
+          left = 1;
         }
       }
       int32_t* hdr = reinterpret_cast<int32_t*>(metas + m * meta);
@@ -645,43 +721,41 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
       const int s = t / tps, tile = t - s * tps;
       ++t;
       --left;
-      if (lane == 0) hdr[0] = t - 1;
       const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-      uint32_t tx = 0;
-      const uint8_t* src = nullptr;
+      const bool live = !d->skip && R > 0;
       if (tile == 0 && lane < A.sc.n_fields) {         // the batch's scalar fields, once per sample
         const int64_t i = A.sc.idx[s];
         A.sc.outs[lane][s] = A.sc.cols[lane][i];
       }
-      if (!d->skip && R > 0) {
-        // what sample_tables_kernel computes for the other K1 variants
+      int newxt = 0, ncopy = 0;
+      bool per_row = false;
+      const uint8_t* src0 = nullptr;                   // lane j: global address of slot j's first byte
+      uint32_t tx = 0, my_sz = 0;
+      if (live) {
         uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
-        uint2* rowtap = reinterpret_cast<uint2*>(xt + owp);
+        uint4* taps = reinterpret_cast<uint4*>(metas + m * meta + tap_off);
         const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
         const SrcRows S = src_rows_of(P, A, d, s);
         const int top = prm[0], ch = prm[2], sh = S.sh;
-        if (s != cur_s) {   // a CTA's tiles are consecutive: the column table is built once per sample
-          const int left = prm[1], cwd = prm[3];
+        if (s != cur_s) {   // a CTA's tiles of one sample are consecutive: the column table once per sample
+          const int lft = prm[1], cwd = prm[3];
           const int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
           int a0, a1, aw, b0, b1, bw;   // the composed maps are monotone: the end columns span the range
           lin_axis(min(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, a0, a1, aw);
           lin_axis(max(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, b0, b1, bw);
-          col_lo = (left + a0) >> sh;
-          const int col_hi = (left + b1) >> sh;
+          col_lo = (lft + a0) >> sh;
+          const int col_hi = (lft + b1) >> sh;
           span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
           for (int ox = lane; ox < OW; ox += 32) {
             int x0, x1, wx;
             lin_axis(back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
-            const int c0 = (left + x0) >> sh, c1 = (left + x1) >> sh;
+            const int c0 = (lft + x0) >> sh, c1 = (lft + x1) >> sh;
             xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
           }
           cur_s = s;
-        } else if (m != prev_m) {
-          const uint32_t* xp = reinterpret_cast<const uint32_t*>(metas + prev_m * meta + 16);
-          for (int ox = lane; ox < OW; ox += 32) xt[ox] = xp[ox];
+          newxt = 1;
         }
-        prev_m = m;
         int ya = 0, yb = 0, wy = 0;
         if (lane < R) {
           int y0, y1;
@@ -692,135 +766,194 @@ __global__ void __launch_bounds__(kThreads + 32, 3) image_cw_kernel(const PlanDe
         // rows [lo, hi] are contiguous and at most nslot of them (host bound,
         // engine.cpp plan_compile: cw_slots)
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
-        const int nvalid = min(hi - lo + 1, nslot);
-        // the tile's source rows [lo, lo + ncopy) are consecutive rows of one
-        // row-strided image: ONE bulk copy (16-byte aligned ends) from column
-        // col_lo of row lo to column col_hi of the last row; row j's column
-        // col_lo lands at byte j * rstride + shift of the stage
-        const int ncopy = max(0, min(nvalid, S.rows - lo));
-        const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)lo * S.rstride + (int64_t)col_lo * C);
-        const uintptr_t al = a & ~(uintptr_t)15;
-        const uint32_t rstr = (uint32_t)S.rstride, base0 = (uint32_t)(a - al);
-        if (span_bytes > 0 && ncopy > 0) {
-          tx = (uint32_t)((base0 + (uint64_t)(ncopy - 1) * rstr + span_bytes + 15) & ~(uint64_t)15);
-          src = reinterpret_cast<const uint8_t*>(al);
+        ncopy = span_bytes > 0 ? max(0, min(min(hi - lo + 1, nslot), S.rows - lo)) : 0;
+        const uint32_t rstr = (uint32_t)S.rstride;
+        // one copy per row when whole-row copies would move >= 25 % more bytes than the window
+        per_row = ncopy > 1 && 4ull * rstr > 5ull * (uint64_t)(span_bytes + 16);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)(lo + lane) * S.rstride + (int64_t)col_lo * C);
+        uint32_t my_base;                              // stage offset of slot `lane`'s column col_lo
+        if (per_row) {
+          const uintptr_t al = a & ~(uintptr_t)15;
+          my_base = (uint32_t)lane * span_pad + (uint32_t)(a - al);
+          my_sz = lane < ncopy ? (uint32_t)((a - al + span_bytes + 15) & ~(uintptr_t)15) : 0u;
+          src0 = reinterpret_cast<const uint8_t*>(al);
+          tx = __reduce_add_sync(0xffffffffu, my_sz);
+        } else {
+          const uintptr_t a0 = reinterpret_cast<uintptr_t>(S.base + (int64_t)lo * S.rstride + (int64_t)col_lo * C);
+          const uintptr_t al = a0 & ~(uintptr_t)15;
+          const uint32_t base0 = (uint32_t)(a0 - al);
+          my_base = base0 + (uint32_t)lane * rstr;
+          if (ncopy > 0) tx = (uint32_t)((base0 + (uint64_t)(ncopy - 1) * rstr + span_bytes + 15) & ~(uint64_t)15);
+          src0 = reinterpret_cast<const uint8_t*>(al);
         }
+        const int ra = lane < R ? ya - lo : 0, rb = lane < R ? yb - lo : 0;
+        const uint32_t ba = __shfl_sync(0xffffffffu, my_base, ra), bb = __shfl_sync(0xffffffffu, my_base, rb);
         if (lane < R) {
-          // Taps a, b of a row are consecutive slots (b == a at the bottom
-          // clamp), so one is even and one odd: the walker keeps one register
-          // set per slot parity and a row never moves between them.  When
-          // b == a the other parity gets slot a ^ 1 with weight 0.  Stored:
-          // x = byte base of the even slot's row | its weight << 20, y = byte
-          // base of the odd slot's row (bases identify slots: the walker's tags).
-          const uint32_t ra = (uint32_t)(ya - lo), rb = (uint32_t)(yb - lo);
-          uint32_t e, o, we;
-          if (ra == rb) { e = (ra & 1) ? ra ^ 1 : ra; o = (ra & 1) ? ra : ra ^ 1; we = (ra & 1) ? 0u : 2048u; }
-          else if (ra & 1) { e = rb; o = ra; we = (uint32_t)wy; }
-          else { e = ra; o = rb; we = 2048u - (uint32_t)wy; }
-          rowtap[lane] = make_uint2((base0 + e * rstr) | we << 20, base0 + o * rstr);
+          // the two taps are one even and one odd absolute row (yb == ya + 1), or one row twice (bottom /
+          // top clamp, or subsampled rows): that row takes all the weight, the other parity a fake tag
+          uint32_t be, bo, te, to, wo;
+          if (ya == yb) {
+            be = bo = ba;
+            if (ya & 1) { te = kCwFake; to = (uint32_t)ya; wo = 2048u; }
+            else { te = (uint32_t)ya; to = kCwFake; wo = 0u; }
+          } else if (ya & 1) {
+            bo = ba; be = bb; to = (uint32_t)ya; te = (uint32_t)yb; wo = 2048u - (uint32_t)wy;
+          } else {
+            be = ba; bo = bb; te = (uint32_t)ya; to = (uint32_t)yb; wo = (uint32_t)wy;
+          }
+          taps[lane] = make_uint4(be, bo, te | to << 16, 4u * wo);
         }
       }
-      if (k >= NS) mbar_wait(&empty[b], ph ^ 1);      // the previous use's release
-      uint8_t* srcbuf = stages + (size_t)b * sbytes;
-      __syncwarp();
       if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_tx(&full[b], tx);
-        if (tx) bulk_g2s(srcbuf, src, tx, &full[b]);
+        hdr[0] = t - 1; hdr[1] = s; hdr[2] = live ? 1 : 0; hdr[3] = newxt;
+      }
+      if (k >= NS) mbar_wait(&empty[b], ph ^ 1);      // the previous use's release
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      uint8_t* srcbuf = stages + (size_t)b * sbytes;
+      if (lane == 0) mbar_arrive_tx(&full[b], tx);
+      __syncwarp();
+      if (tx) {
+        if (per_row) {
+          if (lane < ncopy) bulk_g2s(srcbuf + (size_t)lane * span_pad, src0, my_sz, &full[b]);
+        } else if (lane == 0) {
+          bulk_g2s(srcbuf, src0, tx, &full[b]);
+        }
       }
     }
     return;
   }
 
-  // ---- compute warps: the value table (while the copy warp stages the first tiles)
-  if constexpr (kVal == VAL_LUT) {
+  // ---- compute warps
+  const OutT* lut = reinterpret_cast<const OutT*>(smem);
+  if constexpr (kMode == CW_LUT) {
     const uint4* g = reinterpret_cast<const uint4*>(A.lut);
-    uint4* l4 = reinterpret_cast<uint4*>(lut);
-    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += nct) l4[i] = g[i];
-    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");   // compute warps only
+    uint4* l4 = reinterpret_cast<uint4*>(smem);
+    for (int i = tid; i < C * 256 * (int)sizeof(OutT) / 16; i += ncw * 32) l4[i] = g[i];
+    asm volatile("bar.sync 1, %0;" ::"r"(ncw * 32) : "memory");   // compute warps only
   }
-  const int npair = P.cw_npair, groups = P.cw_groups;   // host-computed (engine.cpp plan_compile)
+  const int pr = tid, npair = P.cw_npair;
+  const bool act = pr < npair;
+  const int ox0 = 2 * pr;
+  const int nval = min(2, OW - ox0) * C;               // values this thread writes per row (6, or 3 at an odd edge)
   const size_t ostep = (size_t)OW * C;
+  const bool vec = nval == 6 && (OW & 1) == 0;
+  unsigned long long ab[3], bb[3];                     // affine map per value pair: channels (0,1) (2,0) (1,2)
+  if constexpr (kMode == CW_AFFINE) {
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      ab[p] = f2_pack(P.cw_aff_a[(2 * p) % 3], P.cw_aff_a[(2 * p + 1) % 3]);
+      bb[p] = f2_pack(P.cw_aff_b[(2 * p) % 3], P.cw_aff_b[(2 * p + 1) % 3]);
+    }
+  }
+  const unsigned long long magic2 = f2_pack(8388608.0f, 8388608.0f);
+  uint32_t off[2] = {0, 0}, wp[2] = {0, 0}, wn[2] = {0, 0}, sel1[2] = {0, 0}, sel2[2] = {0, 0};
+  int nhe[6], dd[6];
+  uint32_t ce[6];
+#pragma unroll
+  for (int v = 0; v < 6; ++v) { nhe[v] = 0; dd[v] = 0; ce[v] = 0; }
+  uint32_t tags = kCwReset;
   for (int m = 0, b = 0, ph = 0;; m = m == NR - 1 ? 0 : m + 1) {
     mbar_wait(&full[b], ph);
-    const int t = *reinterpret_cast<const volatile int32_t*>(metas + m * meta);
-    if (t < 0) break;                                  // the copy warp's stop entry
-    const int s = t / tps, tile = t - s * tps;
-    const uint32_t* xt = reinterpret_cast<const uint32_t*>(metas + m * meta + 16);
-    const uint2* rowtap = reinterpret_cast<const uint2*>(xt + owp);
-    const uint8_t* srcbuf = stages + (size_t)b * sbytes;
-    const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-    const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-    const bool live = !d->skip && R > 0;
-    if (live) {
-      OutT* out = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep;
-      const int rg = R == Rt ? P.cw_rg : (R + groups - 1) / groups;
-      for (int item = tid; item < npair * groups; item += nct) {
-        const int g = P.cw_magic ? (int)fast_div((uint32_t)item, P.cw_magic) : item / npair, pr = item - g * npair;
-        const int ra0 = g * rg, ra1 = min(R, ra0 + rg);
-        const int ox0 = pr * NP;
-        int off0[NP], off1[NP];
-        uint32_t w0[NP], w1[NP];
+    const int4 hd = *reinterpret_cast<const int4*>(metas + m * meta);   // ordered by the mbarrier wait (acquire)
+    if (hd.x < 0) break;                               // the copy warp's stop entry
+    if (hd.z && act) {
+      const uint8_t* ent = metas + m * meta;
+      if (hd.w) {                                      // first tile of a sample: its column table
+        const uint32_t* xt = reinterpret_cast<const uint32_t*>(ent + 16);
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const uint32_t e = xt[min(ox0 + q, OW - 1)];
-          off0[q] = (int)(e & 0xFFFFu);
-          off1[q] = (e >> 28) ? off0[q] : off0[q] + C;
-          w1[q] = (e >> 16) & 0xFFFu;
-          w0[q] = 2048u - w1[q];
+          const uint32_t w1 = (e >> 16) & 0xFFFu, w0 = 2048u - w1;
+          off[q] = e & 0xFFFFu;
+          wp[q] = w0 | w1 << 16;
+          wn[q] = ((0u - w0) & 0xFFFFu) | (0u - w1) << 16;
+          const bool same = (e >> 28) != 0;
+          sel1[q] = same ? 0x1100u : 0x4130u;
+          sel2[q] = same ? 0x0022u : 0x0052u;
         }
-        uint32_t tag_e = ~0u, tag_o = ~0u;             // rows (byte bases) whose sums are in he / ho
-        uint32_t he[NP * C], ho[NP * C];
+        tags = kCwReset;
+      }
+      const int s = hd.y, tile = hd.x - s * tps;
+      const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
+      const uint4* taps = reinterpret_cast<const uint4*>(ent + tap_off);
+      const uint8_t* stage = stages + (size_t)b * sbytes;
+      OutT* obase = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep + (size_t)ox0 * C;
+      auto rows = [&](auto kvec) {
+      constexpr bool kV = decltype(kvec)::value;
+      uint4 tn = taps[0];
+      OutT* o = obase;
+      for (int r = 0; r < R; ++r, o += ostep) {
+        const uint4 tp = tn;
+        if (r + 1 < R) tn = taps[r + 1];               // next row's taps, one row ahead
+        const uint32_t dt = tp.z ^ tags;
+        tags = tp.z;
+        if (dt & 0xFFFFu) {                            // a new even row
 #pragma unroll
-        for (int q = 0; q < NP * C; ++q) { he[q] = 0; ho[q] = 0; }
-        auto hsum = [&](uint32_t base, uint32_t* hv) {
-          const uint8_t* row = srcbuf + base;
-#pragma unroll
-          for (int q = 0; q < NP; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) hv[q * C + c] = w0[q] * row[off0[q] + c] + w1[q] * row[off1[q] + c];
-        };
-        const bool fullw = ox0 + NP <= OW;
-        OutT* o = out + (size_t)ra0 * ostep + (size_t)ox0 * C;
-        // NP pixels = 3 x NP values: three aligned stores of NP values each when
-        // every row of this thread starts on an NP-pixel boundary (OW % NP == 0)
-        constexpr int kVB = NP * (int)sizeof(OutT);
-        const bool vec = fullw && OW % NP == 0 && (reinterpret_cast<uintptr_t>(o) & (kVB - 1)) == 0;
-        const int nval = fullw ? NP * C : (OW - ox0) * C;
-        uint2 tn = rowtap[ra0];
-        for (int r = ra0; r < ra1; ++r, o += ostep) {
-          const uint2 tp = tn;
-          if (r + 1 < ra1) tn = rowtap[r + 1];         // next row's taps, one row ahead
-          const uint32_t be = tp.x & 0xFFFFFu, bo = tp.y, we = tp.x >> 20, wo = 2048u - we;
-          // taps only move forward: a parity's sums are recomputed when its row changes
-          if (be != tag_e) { hsum(be, he); tag_e = be; }
-          if (bo != tag_o) { hsum(bo, ho); tag_o = bo; }
-          OutT v[NP * C];
-#pragma unroll
-          for (int q = 0; q < NP * C; ++q) {
-            const uint32_t u = (we * he[q] + wo * ho[q] + (1u << 21)) >> 22;
-            if constexpr (kVal == VAL_LUT) v[q] = lut[(q % C) * 256 + u];
-            else v[q] = value_generic<OutT, kVal>(P, u, q % C);
-          }
-          if (vec) {
-            using VT = typename std::conditional<kVB == 2, uint16_t, typename std::conditional<kVB == 4, uint32_t,
-                       typename std::conditional<kVB == 8, uint2, uint4>::type>::type>::type;
-            VT wv[3];
-            memcpy(wv, v, sizeof v);
-            if constexpr (kVB == 4) {   // one asm block: three live source registers, no reuse hazard between the stores
-              asm volatile("st.global.b32 [%0], %1;\n\tst.global.b32 [%0+4], %2;\n\tst.global.b32 [%0+8], %3;"
-                           ::"l"(o), "r"(wv[0]), "r"(wv[1]), "r"(wv[2]));
-            } else {
-              VT* p = reinterpret_cast<VT*>(o);
-#pragma unroll
-              for (int q = 0; q < 3; ++q) p[q] = wv[q];
-            }
-            continue;
+          for (int q = 0; q < 2; ++q) {
+            const CwTap h = cw_bytes(stage, tp.x + off[q], sel1[q], sel2[q]);
+            const int n0 = dp2a_lo(wn[q], h.p1, 0), n1 = dp2a_hi(wn[q], h.p1, 0), n2 = dp2a_lo(wn[q], h.p2, 0);
+            dd[3 * q] += n0 - nhe[3 * q]; dd[3 * q + 1] += n1 - nhe[3 * q + 1]; dd[3 * q + 2] += n2 - nhe[3 * q + 2];
+            nhe[3 * q] = n0; nhe[3 * q + 1] = n1; nhe[3 * q + 2] = n2;
           }
 #pragma unroll
-          for (int q = 0; q < NP * C; ++q) if (q < nval) o[q] = v[q];
+          for (int v = 0; v < 6; ++v) ce[v] = (uint32_t)nhe[v] * 0xFFFFE000u + (1u << 23);   // -8192 nhe + 2^23
+        }
+        if (dt >> 16) {                                // a new odd row
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const CwTap h = cw_bytes(stage, tp.y + off[q], sel1[q], sel2[q]);
+            dd[3 * q] = dp2a_lo(wp[q], h.p1, nhe[3 * q]);
+            dd[3 * q + 1] = dp2a_hi(wp[q], h.p1, nhe[3 * q + 1]);
+            dd[3 * q + 2] = dp2a_lo(wp[q], h.p2, nhe[3 * q + 2]);
+          }
+        }
+        uint32_t u[6];                                 // 4 (w_e h_e + w_o h_o + 2^21): the value in bits 24..31
+#pragma unroll
+        for (int v = 0; v < 6; ++v) u[v] = ce[v] + tp.w * (uint32_t)dd[v];
+        if constexpr (kMode == CW_AFFINE) {
+          uint32_t pk[3];
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            const unsigned long long x = f2_pack(__uint_as_float(u8_magic(u[2 * p])),
+                                                 __uint_as_float(u8_magic(u[2 * p + 1])));
+            pk[p] = cvt_pack2<OutT>(f2_fma(f2_sub(x, magic2), ab[p], bb[p]));
+          }
+          if constexpr (kV) {
+            uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+            o32[0] = pk[0]; o32[1] = pk[1]; o32[2] = pk[2];
+          } else {
+#pragma unroll
+            for (int v = 0; v < 6; ++v)
+              if (v < nval) {
+                const uint16_t h = (uint16_t)(pk[v >> 1] >> (16 * (v & 1)));
+                memcpy(o + v, &h, 2);
+              }
+          }
+        } else {
+          OutT val[6];
+#pragma unroll
+          for (int v = 0; v < 6; ++v) {
+            if constexpr (kMode == CW_LUT) val[v] = lut[(v % 3) * 256 + (u[v] >> 24)];
+            else val[v] = (OutT)(u[v] >> 24);
+          }
+          if constexpr (kV && sizeof(OutT) <= 4) {
+            using PT = typename std::conditional<sizeof(OutT) == 1, uint16_t,
+                       typename std::conditional<sizeof(OutT) == 2, uint32_t, uint2>::type>::type;
+            PT w3[3];
+            memcpy(w3, val, sizeof w3);
+            PT* op = reinterpret_cast<PT*>(o);
+            op[0] = w3[0]; op[1] = w3[1]; op[2] = w3[2];
+          } else {
+#pragma unroll
+            for (int v = 0; v < 6; ++v)
+              if (v < nval) o[v] = val[v];
+          }
         }
       }
+      };
+      if (vec) rows(std::true_type{});
+      else rows(std::false_type{});
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
@@ -848,9 +981,11 @@ inline int persistent_ctas(const void* fn, int threads, int smem) {
 }
 template <typename OutT, bool kRes, int kVal, int kC, bool kVec>
 static int launch_img_t(const PlanDev& P, const LaunchArgs& A, cudaStream_t st) {
-  if constexpr (kRes && kC == 3) {
+  if constexpr (kRes && kC == 3 && (kVal == VAL_LUT || kVal == VAL_COPY)) {
     if (P.cw) {   // the copy warp computes the geometry: no prologue launch
-      auto k = image_cw_kernel<OutT, kVal == VAL_LUT ? VAL_LUT : kVal>;
+      auto k = image_cw_kernel<OutT, kVal == VAL_COPY ? CW_COPY : CW_LUT>;
+      if constexpr (sizeof(OutT) == 2)
+        if (P.cw_affine) k = image_cw_kernel<OutT, CW_AFFINE>;
       if (P.cw_smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, P.cw_smem);
       const int total = P.tiles_per_sample * A.count;
       const int threads = (P.cw_warps + 1) * 32;
