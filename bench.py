@@ -1,30 +1,46 @@
-"""Benchmark of the hot path on BASELINE.json configs[1]:
+"""Benchmark of the hot path (BASELINE.json metric: images/sec decode + RRC + flip + normalize).
+
+Headline workload: BASELINE.json configs[1] --
 
     ImageNet-shaped synthetic .bbox, RAW RGB max_res 256 (256x256x3),
     RandomResizedCrop 192 + RandomHorizontalFlip + NormalizeImage -> f16, batch 512
 
 One step = one batch of 512 images through the public Loader API.
 
-  value  : images/s with the heap resident in HBM (DeviceResident strategy):
-           per step the loader uploads indices + descriptors and runs the
-           fused kernel on payloads already in HBM.
-  e2e    : images/s through the same Loader with the OsCache strategy:
-           every step gathers the batch's payloads from the mmap'd file into
-           pinned memory and copies them H2D (inside the timed region), and
-           reads the step's labels back D2H.
-  roofline: the fused RRC kernel (K1), CUDA-event timed on the loader's
-           compute stream during the `value` run; algorithmic bytes =
-           sum over images of (source window bytes + output bytes).
+  value    : images/s with the heap resident in HBM (DeviceResident strategy):
+             per step the loader uploads indices + descriptors and runs the
+             fused kernel on payloads already in HBM.
+  e2e      : images/s through the same Loader with the OsCache strategy:
+             every step gathers the batch's payloads from the mmap'd file into
+             pinned memory and copies them H2D (inside the timed region), and
+             reads the step's labels back D2H.  e2e.frac_pcie = e2e over the
+             PCIe roofline (measured pinned H2D GB/s / H2D bytes per image).
+  roofline : the fused RRC kernel K1 (image_cw_kernel), CUDA events around
+             every launch on the loader's compute stream in a second timed pass
+             of the same workload with one compute stream (so launches do not
+             overlap); achieved = algorithmic bytes per launch (source window
+             bytes + output bytes) / mean launch time.
+  parity   : the last timed batch of every leg, copied back after the timed
+             region, compared bit for bit with the oracle (oracle/) on the same
+             indices, seed and epoch.
   cpu_baseline: the oracle C port (oracle/bbx_oracle.c) of the same chain on
-           the host cores, bounded sample (rank 0, N=1 only).
+             the host cores, bounded sample (rank 0, N=1 only).
 
-`--impl reference` times that CPU port alone on this config (the reference
-is pure Python/numpy and has no RRC; its own CPU path is what the port
-restates, tests/test_oracle.py pins it).
+The other BASELINE configs run as legs of the same invocation (`workloads`, and a
+compact per-leg summary in config["legs"]): configs[0] (CIFAR-shaped RAW, flip +
+normalize -> f32), configs[2] (JPEG q90 RRC-192 and RRC-160 -> f16, batch 1024),
+configs[3] (JPEG CenterCrop-224, sequential), configs[4] (JPEG RRC-192 quasi-random +
+float32 NDArray d=50,000).
+
+`--impl reference` times the reference's CPU path on the box's host cores on the
+same configs: the oracle C port (the reference is pure Python/numpy and has no
+RRC or JPEG; tests/test_oracle.py pins the port to it), plus the UNMODIFIED
+reference Loader (baseline/_ref, `pip install --target`) on the chains it can
+run -- configs[0]'s flip + normalize and the RandomCrop-192 proxy of configs[1].
 
 Under torchrun each rank runs its shard (distributed=True: rank r takes
-positions [r*512, (r+1)*512) of each global batch of N*512); no collective on
-the data path; timing is the max over ranks.
+positions [r*B, (r+1)*B) of each global batch of N*B); no collective on the
+data path; timing is the max over ranks.
 """
 
 from __future__ import annotations
@@ -47,77 +63,104 @@ C = 3
 OUT = 192
 MEAN = (123.675, 116.28, 103.53)
 STD = (58.395, 57.12, 57.375)
-CHAIN_SPEC = f"rrc:{OUT},{OUT}|flip:0.5|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}/f16"
-ORACLE_SPEC = f"rrc:{OUT},{OUT}|flip:0.5|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}|cast:f16"
+NORM = f"normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}/f16"
+CHAIN_SPEC = f"rrc:{OUT},{OUT}|flip:0.5|{NORM}"
 SEED = 3
-N_SAMPLES = int(os.environ.get("BBX_BENCH_SAMPLES", 8192))   # 1.6 GB file, > 126 MB L2 per batch stream
+N_SAMPLES = int(os.environ.get("BBX_BENCH_SAMPLES", 16384))   # 3.2 GB file (>= 16k)
 DATA_DIR = Path(os.environ.get("BBX_BENCH_DIR", "/tmp/bbx_bench"))
+JPEG_B = 1024
+JPEG_SAMPLES = int(os.environ.get("BBX_BENCH_JPEG_SAMPLES", 16384))
+RST_BLOCKS = 2                                    # restart interval (MCUs) the writer emits
+ND = 50000                                        # configs[4] float32 NDArray length (paper: d = 50,000)
+VAL_SPEC = f"center:224,224,{224 / 256}|{NORM}"
+CIFAR_SPEC = "flip:0.5|normalize:127.5,64"        # the reference's C1 chain
+C2_PROXY_SPEC = "decode|crop:192,192|flip:0.5|normalize:127.5,64"   # configs[1] in the reference's own transforms
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def dataset_path() -> Path:
-    return DATA_DIR / f"imagenet256_raw_{N_SAMPLES}.bbox"
+def oracle_spec(spec: str) -> str:
+    return spec.replace("/f16", "|cast:f16")
 
 
-JPEG_B = 1024
-JPEG_SAMPLES = int(os.environ.get("BBX_BENCH_JPEG_SAMPLES", 8192))
-RST_BLOCKS = int(os.environ.get("BBX_BENCH_RST_BLOCKS", 2))   # restart interval (MCUs) the writer emits
-ND = int(os.environ.get("BBX_BENCH_ND", 50000))               # configs[4] float32 NDArray length (paper: d = 50,000)
-VAL_SPEC = f"center:224,224,{224 / 256}|normpc:{','.join(map(str, MEAN))}/{','.join(map(str, STD))}/f16"
-
-
-def jpeg_dataset_path() -> Path:
-    return DATA_DIR / f"imagenet256_jpeg_q90_420_rstb{RST_BLOCKS}_{JPEG_SAMPLES}.bbox"
-
-
-def ensure_jpeg_dataset(rank: int, barrier, nd: int = 0) -> Path:
-    """configs[2..4]: ImageNet-shaped synthetic photos (longer side 256, shorter side
-    153-256), JPEG q90 4:2:0 with a restart marker every RST_BLOCKS MCUs; with
-    `nd`, plus the float32 NDArray field "x" of that length (configs[4])."""
-    import paper_2306_12517_b200 as bx
-
-    path = jpeg_dataset_path() if not nd else jpeg_dataset_path().with_name(
-        jpeg_dataset_path().stem + f"_nd{nd}.bbox")
+# ------------------------------------------------------------------ datasets
+def _write_once(path: Path, rank: int, barrier, make):
     if rank == 0 and not path.exists():
         DATA_DIR.mkdir(parents=True, exist_ok=True)
         tmp = path.with_suffix(".tmp")
         t0 = time.time()
-        bx.write_dataset(bx.PhotoLikeSource(JPEG_SAMPLES, H, W, C, seed=1, array_dim=nd), tmp,
-                         bx.WriterConfig(seed=1, compress_probability=1.0, compress_codec=bx.CodecId.JPEG,
-                                         jpeg=bx.JpegParams(90, "4:2:0", restart_blocks=RST_BLOCKS),
-                                         num_encode_workers=min(16, os.cpu_count() or 1)))
+        make(tmp)
         os.replace(tmp, path)
         log(f"wrote {path} ({path.stat().st_size / 1e6:.0f} MB) in {time.time() - t0:.1f}s")
     barrier()
     return path
 
 
-def ensure_dataset(rank: int, barrier) -> Path:
+def raw_dataset(rank: int, barrier) -> Path:
     import paper_2306_12517_b200 as bx
 
-    path = dataset_path()
-    if rank == 0 and not path.exists():
-        DATA_DIR.mkdir(parents=True, exist_ok=True)
-        tmp = path.with_suffix(".tmp")
-        t0 = time.time()
-        bx.write_dataset(bx.SyntheticImageSource(N_SAMPLES, H, W, C, seed=1), tmp, bx.WriterConfig(seed=1))
-        os.replace(tmp, path)
-        log(f"wrote {path} ({path.stat().st_size / 1e9:.2f} GB) in {time.time() - t0:.1f}s")
-    barrier()
-    return path
+    return _write_once(DATA_DIR / f"imagenet256_raw_{N_SAMPLES}.bbox", rank, barrier, lambda p: bx.write_dataset(
+        bx.SyntheticImageSource(N_SAMPLES, H, W, C, seed=1), p, bx.WriterConfig(seed=1)))
+
+
+def cifar_dataset(rank: int, barrier) -> Path:
+    import paper_2306_12517_b200 as bx
+
+    return _write_once(DATA_DIR / "cifar32_raw_50000.bbox", rank, barrier, lambda p: bx.write_dataset(
+        bx.SyntheticImageSource(50000, 32, 32, 3, seed=1), p, bx.WriterConfig(seed=1)))
+
+
+def jpeg_dataset(rank: int, barrier, nd: int = 0) -> Path:
+    """configs[2..4]: ImageNet-shaped synthetic photos (longer side 256, shorter side
+    153-256), JPEG q90 4:2:0 with a restart marker every RST_BLOCKS MCUs; with
+    `nd`, plus the float32 NDArray field "x" of that length (configs[4])."""
+    import paper_2306_12517_b200 as bx
+
+    name = f"imagenet256_jpeg_q90_420_rstb{RST_BLOCKS}_{JPEG_SAMPLES}" + (f"_nd{nd}" if nd else "") + ".bbox"
+    return _write_once(DATA_DIR / name, rank, barrier, lambda p: bx.write_dataset(
+        bx.PhotoLikeSource(JPEG_SAMPLES, H, W, C, seed=1, array_dim=nd), p,
+        bx.WriterConfig(seed=1, compress_probability=1.0, compress_codec=bx.CodecId.JPEG,
+                        jpeg=bx.JpegParams(90, "4:2:0", restart_blocks=RST_BLOCKS),
+                        num_encode_workers=min(16, os.cpu_count() or 1))))
+
+
+# ---------------------------------------------------------------- workloads
+# name -> (BASELINE config, description, chain, order, batch, dataset kind)
+LEGS = {
+    "raw": ("configs[1]", "ImageNet-shaped synthetic .bbox RAW 256x256x3, RandomResizedCrop 192 (scale 0.08-1, "
+                          "ratio 3/4-4/3, bilinear) + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC, random order",
+            CHAIN_SPEC, "random", B, "raw"),
+    "cifar": ("configs[0]", "CIFAR-10-shaped synthetic .bbox (50k x 32x32x3 RAW + IntField label), RandomFlip(0.5) + "
+                            "Normalize(127.5, 64) -> f32 NHWC, random order", CIFAR_SPEC, "random", B, "cifar"),
+    "jpeg": ("configs[2]", "JPEG q90 4:2:0 RandomResizedCrop 192 + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC, "
+                           "random order", CHAIN_SPEC, "random", JPEG_B, "jpeg"),
+    "jpeg160": ("configs[2]@160", "JPEG q90 4:2:0 RandomResizedCrop 160 + flip 0.5 + NormalizeImage(ImageNet) -> "
+                                  "f16 NHWC, random order", f"rrc:160,160|flip:0.5|{NORM}", "random", JPEG_B, "jpeg"),
+    "val": ("configs[3]", "JPEG validation path: CenterCrop 224 (ratio 224/256) + NormalizeImage(ImageNet) -> f16 "
+                          "NHWC, sequential order", VAL_SPEC, "sequential", JPEG_B, "jpeg"),
+    "ndarray": ("configs[4]", "JPEG RRC-192 + flip + normalize -> f16, QUASI_RANDOM order (distributed=True "
+                              "sharding under torchrun), plus a float32 NDArray field d=50,000 (sparse-regression "
+                              "case study)", CHAIN_SPEC, "quasi-random", JPEG_B, "ndarray"),
+}
+
+
+def leg_dataset(kind: str, rank: int, barrier) -> Path:
+    if kind == "raw":
+        return raw_dataset(rank, barrier)
+    if kind == "cifar":
+        return cifar_dataset(rank, barrier)
+    return jpeg_dataset(rank, barrier, ND if kind == "ndarray" else 0)
 
 
 class ClockSampler:
-    """nvidia-smi/NVML clocks and throttle reasons during the timed region."""
+    """NVML SM clocks and throttle reasons, sampled every 2 ms during the timed regions."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
-        self.device = device
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -144,10 +187,11 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if self._nv is not None:
+            self._stop.clear()
             self._th = threading.Thread(target=self._run, daemon=True)
             self._th.start()
         return self
@@ -164,19 +208,20 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def make_loader(path, device, rank, world, strategy, slot_count=3, batch=B, chain=CHAIN_SPEC, order="random"):
+def make_loader(path, device, rank, world, strategy, chain, order, batch, slot_count=3, options=None):
     import paper_2306_12517_b200 as bx
 
     ds = bx.open_dataset(path, strategy)
     cfg = bx.LoaderConfig(batch_size=batch, order=bx.OrderKind(order), seed=SEED, slot_count=slot_count,
                           pipelines={"image": bx.parse_pipeline(chain)}, device=device,
-                          distributed=world > 1, rank=rank, world_size=world)
+                          distributed=world > 1, rank=rank, world_size=world, options=options)
     return ds, bx.Loader(ds, cfg)
 
 
 def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
-    """W warm-up steps, then exactly `steps` steps bracketed by barrier + sync;
-    returns (device seconds max over ranks, d2h bytes per step)."""
+    """W warm-up steps, then exactly `steps` steps bracketed by barrier + sync.
+    Returns (device seconds max over ranks, d2h bytes per step, last timed batch
+    copied to the host after the timed region: (indices, {field: ndarray}))."""
     import torch
 
     warm = loader.iterate_steps(warmup)
@@ -193,6 +238,7 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
     d2h = 0
     start.record(stream)
     it = loader.iterate_steps(steps, start_epoch=1)   # submitted inside the timed region (pipeline fill included)
+    b = None
     for _ in range(steps):
         b = next(it)
         if read_back:   # the step's result back on the host (labels of the batch)
@@ -200,34 +246,46 @@ def timed_run(loader, steps, warmup, barrier, reduce_max, read_back: bool):
             d2h += lab.numel() * lab.element_size()
     end.record(stream)
     torch.cuda.synchronize()
+    secs = start.elapsed_time(end) * 1e-3
+    last = (list(b.indices), {k: b[k].cpu().numpy() for k in b.arrays}) if b is not None else None
     barrier()
     it.close()
-    secs = start.elapsed_time(end) * 1e-3
-    return reduce_max(secs), d2h / steps
+    return reduce_max(secs), d2h / steps, last
 
 
-def cpu_baseline(path, seconds_budget: float = 15.0, batch=B, what="RRC-192+flip+normalize->f16",
-                 spec=None, order="random"):
-    """Oracle C port on the host cores, bounded sample (whole batches)."""
+def oracle_ops(spec: str, field: dict):
+    from oracle import oracle as O
+
+    ops = O.parse_spec(oracle_spec(spec))
+    if ops[0]["kind"] not in ("decode", "arrayread", "rrc", "center"):
+        ops = O.default_ops(field) + ops
+    return ops
+
+
+def parity_check(path, chain, last, epoch) -> dict:
+    """The last timed batch vs the oracle on the same indices, seed and epoch:
+    images (and arrays) bit for bit, labels exactly."""
     import numpy as np
 
     from oracle import oracle as O
 
+    if last is None:
+        return {"parity_ok": None}
+    idx, arrays = last
     f = O.OracleFile(path)
-    field = f.fields[0]
-    ops = O.parse_spec(spec or ORACLE_SPEC)
-    threads = os.cpu_count() or 1
-    page_map = [f.primary_page(i) for i in range(f.num_samples)] if order == "quasi-random" else None
-    batches = O.epoch_batches(order, SEED, 0, f.num_samples, batch, page_map)
-    done, t0 = 0, time.perf_counter()
-    out = None
-    while time.perf_counter() - t0 < seconds_budget and done < len(batches):
-        out = O.run_field_batch(f, field, 0, ops, batches[done], SEED, 0, threads, out=out)
-        done += 1
-    el = time.perf_counter() - t0
-    return {"value": done * batch / el, "unit": "images/s", "cores": threads, "kind": "port",
-            "sample": f"{done} batches x {batch} images of {path.name} ({what}), "
-                      f"{threads} threads, {el:.1f}s"}
+    ok, checked = True, []
+    for fi, fd in enumerate(f.fields):
+        name = fd["name"]
+        if name not in arrays:
+            continue
+        if fd["kind"] in ("int", "float"):
+            want = np.array([f.cell(i, fd) for i in idx], dtype="<i8" if fd["kind"] == "int" else "<f8")
+        else:
+            ops = oracle_ops(chain, fd) if name == "image" else O.default_ops(fd)
+            want = O.run_field_batch(f, fd, fi, ops, idx, SEED, epoch, os.cpu_count() or 1)
+        ok &= bool(np.array_equal(np.asarray(arrays[name]), want))
+        checked.append(name)
+    return {"parity_ok": ok, "parity_checked": checked, "parity_batch": len(idx), "parity_epoch": epoch}
 
 
 def h2d_peak_gbs(device) -> float:
@@ -247,128 +305,12 @@ def h2d_peak_gbs(device) -> float:
     return best
 
 
-def oracle_spec(spec: str) -> str:
-    return spec.replace("/f16", "|cast:f16")
-
-
-JPEG_LEGS = {
-    "jpeg": ("configs[2]", "RandomResizedCrop 192 + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC, random order",
-             CHAIN_SPEC, "random", 0),
-    "val": ("configs[3]", "validation path: CenterCrop 224 (ratio 224/256) + NormalizeImage(ImageNet) -> f16 NHWC, "
-                          "sequential order", VAL_SPEC, "sequential", 0),
-    "ndarray": ("configs[4]", "QUASI_RANDOM order (distributed=True sharding under torchrun) RRC-192 + flip + "
-                              "normalize -> f16, plus a float32 NDArray field of the sparse-regression case study",
-                CHAIN_SPEC, "quasi-random", ND),
-}
-
-
-CIFAR_SPEC = "flip:0.5|normalize:127.5,64"           # the reference's C1 chain
-
-
-def cifar_workload(args, device, rank, world, barrier, reduce_max):
-    """configs[0]: CIFAR-10-shaped .bbox (50k x 32x32x3 RAW + label), RandomFlip(0.5) +
-    Normalize(127.5, 64) -> f32 NHWC, batch 512, random order (the reference-pinned chain)."""
-    import paper_2306_12517_b200 as bx
-
-    path = DATA_DIR / "cifar32_raw_50000.bbox"
-    if rank == 0 and not path.exists():
-        DATA_DIR.mkdir(parents=True, exist_ok=True)
-        tmp = path.with_suffix(".tmp")
-        bx.write_dataset(bx.SyntheticImageSource(50000, 32, 32, 3, seed=1), tmp, bx.WriterConfig(seed=1))
-        os.replace(tmp, path)
-    barrier()
-    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=B, chain=CIFAR_SPEC)
-    ld.set_profiling(True)
-    secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
-    st = ld.stats()
-    ld.shutdown()
-    ds.close()
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=B, chain=CIFAR_SPEC)
-    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
-    st2 = ld2.stats()
-    ld2.shutdown()
-    ds2.close()
-    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
-    out = {"workload": "configs[0]: CIFAR-10-shaped synthetic .bbox (50k x 32x32x3 RAW + IntField label), "
-                       "RandomFlip(0.5) + Normalize(127.5, 64) -> f32 NHWC, random order",
-           "batch_per_gpu": B, "num_samples": 50000,
-           "value": world * args.steps * B / secs, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
-           "device_ms_per_batch": st["kernel_seconds"] / max(st["batches"], 1) * 1e3,
-           "e2e": {"value": world * args.steps * B / e2e_secs, "unit": "images/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_secs / args.steps * 1e3},
-           "gpu_launches": int(st["kernel_launches"])}
-    if world == 1 and rank == 0:
-        try:
-            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 3, B, "flip + normalize -> f32",
-                                               spec="decode|" + CIFAR_SPEC)
-        except Exception as e:
-            out["cpu_baseline"] = {"value": None, "error": str(e)}
-    return out
-
-
-def jpeg_workload(args, device, rank, world, barrier, reduce_max, leg="jpeg"):
-    """configs[2..4] on the synthetic JPEG .bbox, batch 1024 per GPU: `value` with the
-    compressed heap resident in HBM, `e2e` staging every batch from host RAM."""
-    import paper_2306_12517_b200 as bx
-
-    name, desc, chain, order, nd = JPEG_LEGS[leg]
-    path = ensure_jpeg_dataset(rank, barrier, nd)
-    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), batch=JPEG_B, chain=chain,
-                         order=order, slot_count=int(os.environ.get("BBX_BENCH_SLOTS", "6")))
-    ld.set_profiling(True)
-    with ClockSampler(device) as clk:
-        secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
-    st = ld.stats()
-    ld.shutdown()
-    ds.close()
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), batch=JPEG_B, slot_count=4, chain=chain,
-                           order=order)
-    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
-    st2 = ld2.stats()
-    ld2.shutdown()
-    ds2.close()
-    value = world * args.steps * JPEG_B / secs
-    e2e = world * args.steps * JPEG_B / e2e_secs
-    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
-    kern_s = st["kernel_seconds"] / max(st["timed_batches"], 1)   # one timed window (memset + J1-J4 + K1 [+ array]) per batch
-    h2d_img = h2d / JPEG_B
-    hbm_peak, _ = peaks()
-    pcie = h2d_peak_gbs(device)
-    out_px = 224 * 224 if leg == "val" else OUT * OUT
-    # per image: compressed read + unstuffed bits (w+r) + coef (w+r) + planes (w+r) + RGB (w+r) + output (+ array)
-    comp = h2d_img - 4 * nd
-    hbm_img = comp * 3 + 2 * 1.5 * H * W * 2 + 2 * 1.5 * H * W + 2 * H * W * C + out_px * C * 2 + 2 * 4 * nd
-    roof_pcie = pcie * 1e9 / max(h2d_img, 1.0)
-    roof_hbm = hbm_peak * 1e9 / hbm_img
-    out = {
-        "workload": f"{name}: ImageNet-shaped synthetic JPEG .bbox (q90, 4:2:0, RST every {RST_BLOCKS} MCUs, longer "
-                    f"side 256){f', + float32 NDArray d={nd}' if nd else ''}; {desc}",
-        "batch_per_gpu": JPEG_B, "num_samples": JPEG_SAMPLES, "h2d_bytes_per_image": h2d_img,
-        "value": value, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
-        "device_ms_per_batch": kern_s * 1e3,
-        "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
-        "gpu_idle_ms_per_step": st["gap_seconds"] / max(st["timed_batches"], 1) * 1e3,
-        "gpu_idle_h2d_ms_per_step": st["h2d_late_seconds"] / max(st["timed_batches"], 1) * 1e3,
-        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_secs / args.steps * 1e3,
-                "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
-                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9},
-        "roofline": {"pcie_h2d_peak_gbs": pcie, "hbm_peak_gbs": hbm_peak,
-                     "pcie_images_per_s": roof_pcie, "hbm_images_per_s": roof_hbm,
-                     "binding": "pcie" if roof_pcie < roof_hbm else "hbm",
-                     "e2e_frac": e2e / min(roof_pcie, roof_hbm), "value_frac_hbm": value / roof_hbm,
-                     "note": "Huffman decode is serial integer work per restart interval; neither bandwidth binds "
-                             "the device path (profiles/ has the per-kernel split)"},
-        "gpu_launches": int(st["kernel_launches"]), "clocks": clk.summary(),
-    }
-    if world == 1 and rank == 0:
-        try:
-            out["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds / 3, JPEG_B,
-                                               "JPEG decode (oracle restatement of libjpeg-turbo) + the same chain; "
-                                               "restatement, not the reference", spec=oracle_spec(chain), order=order)
-        except Exception as e:
-            out["cpu_baseline"] = {"value": None, "error": str(e)}
-    return out
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def load_traffic():
@@ -381,12 +323,205 @@ def load_traffic():
     return None
 
 
-def peaks():
-    p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+def cpu_port(path, spec, order, batch, seconds, threads=None, epoch=0) -> dict:
+    """The oracle C port of one leg on the host cores: whole batches for about
+    `seconds` (bounded sample)."""
+    from oracle import oracle as O
+
+    f = O.OracleFile(path)
+    field = f.fields[0]
+    ops = oracle_ops(spec, field)
+    threads = threads or os.cpu_count() or 1
+    page_map = [f.primary_page(i) for i in range(f.num_samples)] if order == "quasi-random" else None
+    batches = O.epoch_batches(order, SEED, epoch, f.num_samples, batch, page_map)
+    done, t0, out = 0, time.perf_counter(), None
+    while (time.perf_counter() - t0 < seconds or done == 0) and done < len(batches):
+        out = O.run_field_batch(f, field, 0, ops, batches[done], SEED, epoch, threads, out=out)
+        done += 1
+    el = time.perf_counter() - t0
+    return {"value": done * batch / el, "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{done} batches x {batch} images of {path.name}, oracle C port, {threads} threads, {el:.1f}s"}
+
+
+def reference_loader(path, spec, batch, seconds) -> dict:
+    """The UNMODIFIED reference Loader (baseline/_ref) on a chain it supports:
+    best of num_workers in {1, cpu_count}, a bounded sample each."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "bbox").exists():
+        return {"value": None, "unavailable": "baseline/_ref not installed"}
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import bbox
+
+    best = None
+    for workers in sorted({1, os.cpu_count() or 1}):
+        ds = bbox.open_dataset(path, bbox.OsCache())
+        try:
+            cfg = bbox.LoaderConfig(batch_size=batch, num_workers=workers, order=bbox.OrderKind.RANDOM, seed=SEED,
+                                    pipelines={"image": bbox.parse_pipeline(spec)})
+            loader = bbox.Loader(ds, cfg)
+            it = iter(loader.iterate_epoch(0))
+            next(it)                                     # warm-up batch
+            n, t0 = 0, time.perf_counter()
+            for b in it:
+                n += b.size
+                if time.perf_counter() - t0 > seconds:
+                    break
+            el = time.perf_counter() - t0
+        finally:
+            ds.close()
+        v = n / el
+        if best is None or v > best["value"]:
+            best = {"value": v, "unit": "images/s", "cores": workers, "kind": "reference",
+                    "sample": f"{n} images of {path.name} through bbox.Loader (unmodified, baseline/_ref), "
+                              f"pipeline '{spec}', num_workers={workers}, {el:.1f}s"}
+    return best
+
+
+def run_leg(name, args, device, rank, world, barrier, reduce_max, detail_roofline=False) -> dict:
+    """One BASELINE config: `value` (heap in HBM), `e2e` (host RAM -> H2D each
+    step), parity of the last timed batch, the CPU port beside it."""
+    import paper_2306_12517_b200 as bx
+
+    cfg_name, desc, chain, order, batch, kind = LEGS[name]
+    path = leg_dataset(kind, rank, barrier)
+    slots = 6
+    out = {"workload": f"{cfg_name}: {desc}", "batch_per_gpu": batch, "global_batch": batch * world,
+           "num_samples": 50000 if kind == "cifar" else (N_SAMPLES if kind == "raw" else JPEG_SAMPLES)}
+
+    # ---- value: heap resident in HBM
+    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device), chain, order, batch, slots)
+    ld.set_profiling(4)   # device windows on every 4th batch: the events' cost stays off the other steps
+    clk = ClockSampler(device)
+    with clk:
+        secs, _, last = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
+    st = ld.stats()
+    epoch_last = 1 + (args.steps - 1) // ld.batches_per_epoch()   # the timed stream starts at epoch 1
+    ld.shutdown()
+    ds.close()
+    value = world * args.steps * batch / secs
+    out.update({"value": value, "unit": "images/s", "ms_per_step": secs / args.steps * 1e3,
+                "device_ms_per_batch": st["kernel_seconds"] / max(st["timed_batches"], 1) * 1e3,
+                "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
+                "gpu_launches": int(st["kernel_launches"])})
+    if rank == 0:
+        try:
+            out.update(parity_check(path, chain, last, epoch_last))
+        except Exception as e:
+            out.update({"parity_ok": False, "parity_error": str(e)[:200]})
+
+    # ---- e2e: payloads staged from host RAM (mmap -> pinned -> H2D) every step
+    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(), chain, order, batch, 4)
+    with clk:
+        e2e_secs, d2h, _ = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
+    st2 = ld2.stats()
+    ld2.shutdown()
+    ds2.close()
+    e2e = world * args.steps * batch / e2e_secs
+    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
+    pcie = h2d_peak_gbs(device)
+    roof_pcie = pcie * 1e9 / max(h2d / batch, 1.0)
+    out["e2e"] = {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                  "ms_per_step": e2e_secs / args.steps * 1e3, "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9,
+                  "pcie_h2d_peak_gbs": pcie, "pcie_roofline_images_per_s": roof_pcie,
+                  "frac_pcie": e2e / world / roof_pcie,
+                  "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
+                  "path": "Loader(OsCache): host RAM -> pinned slot -> H2D -> kernels"}
+    out["clocks"] = clk.summary()
+
+    # ---- K1 alone: one compute stream, every launch timed (roofline)
+    if detail_roofline:
+        ds3, ld3 = make_loader(path, device, rank, world, bx.DeviceResident(device), chain, order, batch, slots,
+                               options={"compute_streams": 1})
+        ld3.set_profiling(1)
+        timed_run(ld3, args.steps, args.warmup, barrier, reduce_max, read_back=False)
+        st3 = ld3.stats()
+        ld3.shutdown()
+        ds3.close()
+        kern_s = st3["kernel_seconds"] / max(st3["kernel_timed"], 1)
+        kern_bytes = st3["kernel_bytes"] / max(st3["kernel_timed"], 1)
+        peak, peak_src = peaks()
+        achieved = kern_bytes / kern_s / 1e9 if st3["kernel_timed"] else 0.0
+        out["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                           "frac": achieved / peak if peak else None, "traffic": load_traffic(),
+                           "kernel": "image_cw_kernel<__half, CW_AFFINE> (K1)", "kernel_us": kern_s * 1e6,
+                           "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src,
+                           "launches_timed": int(st3["kernel_timed"]),
+                           "how": "CUDA events around every K1 launch on its stream, a second timed pass of the same "
+                                  "workload with one compute stream (no overlapping launches)"}
+    if kind in ("jpeg", "ndarray"):
+        out["device_note"] = ("JPEG path: Huffman decode is serial integer work per restart interval; the binding "
+                              "roofline end to end is PCIe (e2e.frac_pcie); profiles/ has the per-kernel split")
+    if world == 1 and rank == 0:
+        try:
+            out["cpu_baseline"] = cpu_port(path, chain, order, batch, args.cpu_seconds / 4)
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    return out
+
+
+def compact(leg: dict) -> dict:
+    e = leg.get("e2e") or {}
+    cb = leg.get("cpu_baseline") or {}
+    return {"value": round(leg.get("value") or 0), "e2e": round(e.get("value") or 0),
+            "e2e_frac_pcie": round(e.get("frac_pcie") or 0, 3), "ms_step": round(leg.get("ms_per_step") or 0, 4),
+            "parity_ok": leg.get("parity_ok"), "cpu": round(cb["value"]) if cb.get("value") else None}
+
+
+def reference_arm(args, rank):
+    """--impl reference: the reference's CPU path on this box's host cores."""
+    if rank != 0:
+        return
+    noop = lambda: None  # noqa: E731
+    path = raw_dataset(0, noop)
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+
+    f = O.OracleFile(path)
+    ops = O.parse_spec(oracle_spec(CHAIN_SPEC))
+    batches = O.epoch_batches("random", SEED, 0, f.num_samples, B)
+    out = None
+    for g in range(args.warmup):
+        out = O.run_field_batch(f, f.fields[0], 0, ops, batches[g % len(batches)], SEED, 0, threads, out=out)
+    t0 = time.perf_counter()
+    for g in range(args.steps):
+        out = O.run_field_batch(f, f.fields[0], 0, ops, batches[(args.warmup + g) % len(batches)], SEED, 0,
+                                threads, out=out)
+    el = time.perf_counter() - t0
+    v = args.steps * B / el
+    legs = {}
+    for name in [w for w in args.workloads.split(",") if w in LEGS and w != "raw"]:
+        cfg_name, _, chain, order, batch, kind = LEGS[name]
+        p = leg_dataset(kind, 0, noop)
+        try:
+            legs[cfg_name] = {"port": cpu_port(p, chain, order, batch, args.cpu_seconds / 4)}
+        except Exception as e:
+            legs[cfg_name] = {"port": {"value": None, "error": str(e)[:200]}}
+    # the unmodified reference Loader on the chains it runs
+    try:
+        legs.setdefault("configs[0]", {})["reference_loader"] = reference_loader(
+            cifar_dataset(0, noop), "decode|" + CIFAR_SPEC, B, args.cpu_seconds / 4)
+    except Exception as e:
+        legs.setdefault("configs[0]", {})["reference_loader"] = {"value": None, "error": str(e)[:200]}
+    try:
+        legs["configs[1]-proxy RandomCrop-192"] = {"reference_loader": reference_loader(
+            path, C2_PROXY_SPEC, B, args.cpu_seconds / 4)}
+    except Exception as e:
+        legs["configs[1]-proxy RandomCrop-192"] = {"reference_loader": {"value": None, "error": str(e)[:200]}}
+    summary = {k: {kk: (round(vv["value"]) if vv.get("value") else None) for kk, vv in d.items()}
+               for k, d in legs.items()}
+    print(json.dumps({
+        "impl": "reference", "metric": "images/sec decode+RRC+flip+normalize", "value": v, "unit": "images/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} batches x {B} images (configs[1]), oracle C port of the reference "
+                                   f"chain + RRC extension, {threads} threads"},
+        "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "workloads": legs,
+        "config": {"workload": "configs[1]: " + LEGS["raw"][1], "batch_per_gpu": B, "num_samples": N_SAMPLES,
+                   "legs": summary},
+    }))
 
 
 def main():
@@ -395,27 +530,27 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--workloads", default="raw,cifar,jpeg,val,ndarray",
-                    help="raw (configs[1], the headline), cifar (configs[0]), jpeg (configs[2]), val (configs[3]), "
-                         "ndarray (configs[4])")
+    ap.add_argument("--cpu-seconds", type=float, default=16.0)
+    ap.add_argument("--workloads", default="raw,cifar,jpeg,jpeg160,val,ndarray",
+                    help="comma list of " + ", ".join(f"{k} ({v[0]})" for k, v in LEGS.items()))
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
 
     import torch
 
     dist = None
+    torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo",
-                                device_id=torch.device("cuda", local) if args.impl == "ours" else None)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if dist is not None:
@@ -424,140 +559,35 @@ def main():
     def reduce_max(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.impl == "ours" else "cpu")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    config = {"workload": "configs[1]: ImageNet-shaped synthetic .bbox RAW 256x256x3, RandomResizedCrop 192 "
-                          "(scale 0.08-1, ratio 3/4-4/3, bilinear) + flip 0.5 + NormalizeImage(ImageNet) -> f16 NHWC",
-              "batch_per_gpu": B, "global_batch": B * world, "num_samples": N_SAMPLES, "order": "random",
-              "out_dtype": "f16", "l2_policy": "inputs larger than L2: each step reads ~100 MB of payload and "
-                                               "writes 113 MB of output; 6 output slots rotate",
-              "timing": "timed steps come from a fresh iterator created inside the timed region (the warm-up "
-                        "iterator and its prefetched batches are drained first): pipeline fill included"}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        path = ensure_dataset(0, lambda: None)
-        from oracle import oracle as O
-
-        f = O.OracleFile(path)
-        ops = O.parse_spec(ORACLE_SPEC)
-        threads = os.cpu_count() or 1
-        batches = O.epoch_batches("random", SEED, 0, f.num_samples, B)
-        out = None
-        for g in range(args.warmup):
-            out = O.run_field_batch(f, f.fields[0], 0, ops, batches[g % len(batches)], SEED, 0, threads, out=out)
-        t0 = time.perf_counter()
-        for g in range(args.steps):
-            out = O.run_field_batch(f, f.fields[0], 0, ops, batches[(args.warmup + g) % len(batches)], SEED, 0,
-                                    threads, out=out)
-        el = time.perf_counter() - t0
-        v = args.steps * B / el
-        print(json.dumps({
-            "impl": "reference", "metric": "images/sec decode+RRC+flip+normalize", "value": v, "unit": "images/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+    names = [w for w in args.workloads.split(",") if w in LEGS]
+    legs = {}
+    for n in names:
+        legs[n] = run_leg(n, args, local, rank, world, barrier, reduce_max, detail_roofline=(n == "raw"))
+    if rank == 0:
+        head = legs.get("raw") or legs[names[0]]
+        config = {"workload": head["workload"], "batch_per_gpu": head["batch_per_gpu"],
+                  "global_batch": head["global_batch"], "num_samples": head["num_samples"],
+                  "l2_policy": "inputs larger than L2: each step reads ~50 MB of source windows and writes 113 MB of "
+                               "output into one of 6 rotating slots",
+                  "timing": "timed steps come from a fresh iterator created inside the timed region (the warm-up "
+                            "iterator and its prefetched batches are drained first): pipeline fill included",
+                  "legs": {LEGS[n][0]: compact(legs[n]) for n in names}}
+        line = {
+            "metric": "images/sec decode+RRC+flip+normalize", "value": head["value"], "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (SyntheticImageSource pattern RAW / PhotoLikeSource JPEG, writer seed 1)",
+            "e2e": head["e2e"], "roofline": head.get("roofline"), "cpu_baseline": head.get("cpu_baseline"),
+            "gpu_launches": head["gpu_launches"], "clocks": head.get("clocks"),
+            "parity_ok": all(legs[n].get("parity_ok") for n in names),
+            "workloads": {LEGS[n][0]: legs[n] for n in names},
             "config": config,
-            "cpu_baseline": {"value": v, "unit": "images/s", "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} batches x {B} images, oracle C port, {threads} threads"},
-            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }))
-        return
-
-    import paper_2306_12517_b200 as bx
-
-    device = local
-    torch.cuda.set_device(device)
-    legs = [w for w in args.workloads.split(",") if w in JPEG_LEGS]
-    if "raw" not in args.workloads.split(","):   # JPEG legs alone (profiling runs)
-        res = {JPEG_LEGS[w][0]: jpeg_workload(args, device, rank, world, barrier, reduce_max, w) for w in legs}
-        if rank == 0:
-            print(json.dumps({"workloads": res}))
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-    path = ensure_dataset(rank, barrier)
-
-    # ---- value: heap resident in HBM
-    ds, ld = make_loader(path, device, rank, world, bx.DeviceResident(device),
-                         slot_count=int(os.environ.get("BBX_BENCH_SLOTS", "6")))
-    ld.set_profiling(int(os.environ.get("BBX_BENCH_PROFILE_EVERY", "4")))   # K1 windows on every 4th batch
-    with ClockSampler(device) as clk:
-        secs, _ = timed_run(ld, args.steps, args.warmup, barrier, reduce_max, read_back=False)
-    st = ld.stats()
-    ld.shutdown()
-    ds.close()
-    value = world * args.steps * B / secs
-    kern_s = st["kernel_seconds"] / max(st["kernel_timed"], 1)
-    kern_bytes = st["kernel_bytes"] / max(st["kernel_timed"], 1)
-    achieved = kern_bytes / kern_s / 1e9 if st["kernel_timed"] else 0.0
-    peak, peak_src = peaks()
-
-    # ---- e2e: payloads staged from host (mmap -> pinned -> H2D) every step
-    ds2, ld2 = make_loader(path, device, rank, world, bx.OsCache(),
-                           slot_count=int(os.environ.get("BBX_BENCH_E2E_SLOTS", "4")))
-    e2e_secs, d2h = timed_run(ld2, args.steps, args.warmup, barrier, reduce_max, read_back=True)
-    st2 = ld2.stats()
-    ld2.shutdown()
-    ds2.close()
-    e2e = world * args.steps * B / e2e_secs
-    h2d = st2["h2d_bytes"] / max(st2["batches"], 1)
-
-    # ---- e2e, zero-copy: K1 reads each window straight from the pinned host heap over PCIe
-    ds3, ld3 = make_loader(path, device, rank, world, bx.OsCache(zero_copy=True))
-    zc_secs, zc_d2h = timed_run(ld3, args.steps, args.warmup, barrier, reduce_max, read_back=True)
-    st3 = ld3.stats()
-    ld3.shutdown()
-    ds3.close()
-    zc_bytes = (st3["zero_copy_bytes"] + st3["h2d_bytes"]) / max(st3["batches"], 1)
-    e2e_zc = {"value": world * args.steps * B / zc_secs, "unit": "images/s", "h2d_bytes_per_step": int(zc_bytes),
-              "d2h_bytes_per_step": int(zc_d2h), "ms_per_step": zc_secs / args.steps * 1e3,
-              "h2d_gbs": zc_bytes / (zc_secs / args.steps) / 1e9,
-              "path": "Loader(OsCache(zero_copy=True)): pinned host heap -> PCIe reads inside K1 (no CPU gather, "
-                      "no staging copy)"}
-
-    jpeg = {}
-    if "cifar" in args.workloads.split(","):
-        jpeg["configs[0]"] = cifar_workload(args, device, rank, world, barrier, reduce_max)
-    for w in legs:
-        jpeg[JPEG_LEGS[w][0]] = jpeg_workload(args, device, rank, world, barrier, reduce_max, w)
-    jpeg = jpeg or None
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
-    line = {
-        "metric": "images/sec decode+RRC+flip+normalize", "value": value, "unit": "images/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (SyntheticImageSource pattern, 256x256x3 RAW, writer seed 1)",
-        "config": config,
-        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "ms_per_step": e2e_secs / args.steps * 1e3, "path": "Loader(OsCache): host RAM -> H2D -> K1",
-                "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
-                "h2d_gbs": h2d / (e2e_secs / args.steps) / 1e9,
-                "staging": ("copy-engine DMA (batched 2-D) from the pinned host heap" if st2["dma_batches"]
-                            else "cpu gather into pinned slot + one H2D")},
-        "e2e_zero_copy": e2e_zc,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": load_traffic(),
-                     "kernel": "image_cw_kernel<half, 3> (K1: persistent column walker, bulk-copy pipeline)", "kernel_us": kern_s * 1e6,
-                     "algorithmic_bytes_per_launch": kern_bytes, "peak_source": peak_src},
-        "gpu_launches": int(st["kernel_launches"]),
-        "host_prep_ms_per_step": st["stage_seconds"] / max(st["batches"], 1) * 1e3,
-        "clocks": clk.summary(),
-    }
-    if world == 1:
-        try:
-            line["cpu_baseline"] = cpu_baseline(path, args.cpu_seconds)
-        except Exception as e:   # the baseline must not sink the GPU line
-            line["cpu_baseline"] = {"value": None, "error": str(e)}
-    if jpeg is not None:
-        line["workloads"] = jpeg
-    print(json.dumps(line))
+        }
+        print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
 

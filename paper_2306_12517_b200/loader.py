@@ -53,6 +53,7 @@ class LoaderConfig:
     rank: int | None = None
     world_size: int | None = None
     staging_threads: int = 0           # host gather threads (0 = automatic)
+    options: dict | None = None        # engine tuning options (include/bbx.h bbx_loader_set_option); defaults = measured best
 
     def check(self) -> None:
         if self.batch_size < 1:
@@ -279,6 +280,8 @@ class Loader:
         self._handle = h
         if isinstance(strategy, OsCache) and getattr(strategy, "zero_copy", False):
             _lib.check(L.bbx_loader_set_zero_copy(h, 1))
+        for name, value in (config.options or {}).items():
+            _lib.check(L.bbx_loader_set_option(h, str(name).encode(), int(value)))
         field_index = {f.name: i for i, f in enumerate(schema)}
         self._field_index = field_index
         pipelines = dict(config.pipelines or {})

@@ -1,10 +1,18 @@
-# Bench both workloads, then the ncu launch list and one full capture of a named kernel.
-# env: STEPS (30), KERNEL (regex for the full capture, default jpeg_huffman_kernel), WL (jpeg)
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# The driver's two bench arms (N=1), as the round-end run does them.
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 900 python bench.py --steps ${STEPS:-30} --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
-cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
-if [ "${NCU:-1}" = "1" ]; then
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${WL:-jpeg}.csv python bench.py --workloads ${WL:-jpeg} --steps 3 --warmup 3 --cpu-seconds 0.5 > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KERNEL:-jpeg_huffman_kernel} -s 4 -c 1 -o gpurun_out/prof_full -f python bench.py --workloads ${WL:-jpeg} --steps 3 --warmup 3 --cpu-seconds 0.5 > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
-fi
+timeout 1200 python bench.py --gpus 1 --steps ${STEPS:-20} --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --gpus 1 --steps ${STEPS:-20} --warmup 5 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+python - <<'PY'
+import json
+for f in ["gpurun_out/bench.json", "gpurun_out/bench_ref.json"]:
+    try:
+        d = json.loads(open(f).read().splitlines()[-1])
+        print(f, round(d["value"]), "e2e", round(d["e2e"]["value"]), "parity", d.get("parity_ok"),
+              "roof", (d.get("roofline") or {}).get("frac"))
+        print(json.dumps(d["config"].get("legs")))
+    except Exception as e:
+        print(f, "ERR", e)
+PY
+tail -n 3 gpurun_out/bench.err gpurun_out/bench_ref.err
