@@ -217,6 +217,13 @@ enum { BBX_CODEC_RAW = 0, BBX_CODEC_RLE = 1, BBX_CODEC_SUBSAMPLE2 = 2, BBX_CODEC
 bbx_status bbx_decode_image(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host,
                             int64_t len, uint8_t* out_dev, int device);
 
+/* The host half of the JPEG decode of one blob, without device work: header
+ * (baseline sequential Huffman, 8-bit, 1 or 3 components, sampling <= 2),
+ * dims == the cell's (h, w, c), Huffman tables, restart-marker count and
+ * sequence.  BBX_OK or BBX_CORRUPT_PAYLOAD with the decoder's message.
+ * validate_file (format.py:476-548, extended to codec 3) calls it per sample. */
+bbx_status bbx_jpeg_check(int32_t h, int32_t w, int32_t c, const uint8_t* payload, int64_t len);
+
 const char* bbx_last_error(void);
 const char* bbx_version(void);
 

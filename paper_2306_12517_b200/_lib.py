@@ -110,6 +110,7 @@ def _bind(L):
         "bbx_loader_set_option": (c_i32, [c_vp, ctypes.c_char_p, c_i64]),
         "bbx_loader_prefetch_headers": (c_i32, [c_vp, c_vp, c_i64]),
         "bbx_decode_image": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.c_int]),
+        "bbx_jpeg_check": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -127,7 +128,7 @@ EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_cl
             "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",
             "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling",
             "bbx_loader_set_zero_copy", "bbx_loader_set_option", "bbx_loader_prefetch_headers",
-            "bbx_decode_image")
+            "bbx_decode_image", "bbx_jpeg_check")
 
 
 def last_error() -> str:

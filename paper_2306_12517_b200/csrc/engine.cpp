@@ -1925,4 +1925,26 @@ bbx_status bbx_decode_image(int32_t h, int32_t w, int32_t c, int32_t codec, cons
   return (bbx_status)decode_image_impl(h, w, c, codec, payload_host, len, out_dev, device);
 }
 
+bbx_status bbx_jpeg_check(int32_t h, int32_t w, int32_t c, const uint8_t* payload, int64_t len) {
+  if (len < 4 || len > 0xFFFFFFFFll) return (bbx_status)fail(BBX_CORRUPT_PAYLOAD, "jpeg: missing SOI marker");
+  if (h < 1 || w < 1 || h > 65535 || w > 65535 || c < 1 || c > 255)
+    return (bbx_status)fail(BBX_SCHEMA_MISMATCH, "image dims out of range");
+  bbx_loader L;                                  // only its table registry is used (no device work)
+  std::vector<JHuff> hh(kJpegMaxHuff);
+  std::vector<JQuant> hq(kJpegMaxQuant);
+  L.jt.h_huff = hh.data(); L.jt.h_quant = hq.data();
+  Plan pl;
+  pl.jpeg_blocks_cap = (int64_t)c * (2 * ((h + 15) / 16)) * (2 * ((w + 15) / 16));
+  pl.jpeg_int_cap = (int64_t)((h + 7) / 8) * ((w + 7) / 8);
+  uint8_t desc[64] = {0};
+  SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
+  d->len = (uint32_t)len; d->h = (uint16_t)h; d->w = (uint16_t)w; d->c = (uint8_t)c; d->codec = CODEC_JPEG;
+  JpegDesc J{};
+  std::vector<uint32_t> starts;
+  HostErr err;
+  const bool ok = jpeg_prepare(&L, pl, payload, (uint32_t)len, d, &J, &starts, err, 0, 0);
+  L.jt.h_huff = nullptr; L.jt.h_quant = nullptr;
+  return ok ? BBX_OK : (bbx_status)fail(err.code, "%s", err.msg.c_str());
+}
+
 }  // extern "C"

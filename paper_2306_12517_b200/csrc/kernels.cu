@@ -155,6 +155,48 @@ __global__ void __launch_bounds__(kThreads) array_kernel(const PlanDev P, const 
     }
   }
 }
+// FIXED_ARRAY chains without remaps or value ops (ArrayRead alone, pipeline.py:
+// 128-129): a straight copy of each sample's payload into its output row,
+// 16-byte aligned stores; the source is read as aligned 16-byte chunks and
+// realigned with funnel shifts (its misalignment is uniform per sample).
+template <int kQ>
+__device__ __forceinline__ uint4 realign(const uint4 a, const uint4 b, uint32_t r) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  return make_uint4(__funnelshift_r(w[kQ], w[kQ + 1], r), __funnelshift_r(w[kQ + 1], w[kQ + 2], r),
+                    __funnelshift_r(w[kQ + 2], w[kQ + 3], r), __funnelshift_r(w[kQ + 3], w[kQ + 4], r));
+}
+__global__ void __launch_bounds__(kThreads) array_copy_kernel(const PlanDev P, const LaunchArgs A) {
+  const int s = blockIdx.y;
+  const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
+  if (d->skip) return;
+  const int64_t len = P.out_sample_elems * P.src_elem;
+  const uint8_t* src = A.payload + d->src;
+  uint8_t* dst = reinterpret_cast<uint8_t*>(A.out) + (size_t)s * len;
+  const int64_t al = (16 - (int64_t)(reinterpret_cast<uintptr_t>(dst) & 15)) & 15, head = al < len ? al : len;
+  const int64_t nchunk = (len - head) >> 4;
+  const int64_t tail0 = head + nchunk * 16;
+  const int64_t t0 = (int64_t)blockIdx.x * kThreads + threadIdx.x, step = (int64_t)gridDim.x * kThreads;
+  if (t0 < head) dst[t0] = src[t0];
+  if (t0 < len - tail0) dst[tail0 + t0] = src[tail0 + t0];
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(src + head);
+  const int sh = (int)(a0 & 15);
+  const uint4* s4 = reinterpret_cast<const uint4*>(a0 - sh);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  const uint32_t r = (uint32_t)(sh & 3) * 8;
+  switch (sh >> 2) {   // uniform per sample
+#define BBX_COPY_CASE(Q)                                                                   \
+    case Q:                                                                               \
+      for (int64_t c = t0; c < nchunk; c += step) {                                       \
+        const uint4 lo = ld_nc_v4(s4 + c);                                                \
+        const uint4 hi = sh ? ld_nc_v4(s4 + c + 1) : lo;                                  \
+        d4[c] = realign<Q>(lo, hi, r);                                                    \
+      }                                                                                   \
+      break;
+    BBX_COPY_CASE(0) BBX_COPY_CASE(1) BBX_COPY_CASE(2) BBX_COPY_CASE(3)
+#undef BBX_COPY_CASE
+  }
+}
+
 // ------------------------------------------------------------------ launch
 
 int image_smem_bytes(const PlanDev& P) { return img_layout(P).total; }
@@ -189,7 +231,12 @@ int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream) {
   int64_t tiles = (P.out_sample_elems + kThreads * 8 - 1) / (kThreads * 8);
   if (tiles > 65535) tiles = 65535;
   dim3 grid((unsigned)tiles, A.count);
-  if (P.value_mode == VAL_COPY) {
+  if (P.value_mode == VAL_COPY && !P.has_remaps_3d) {
+    const int64_t chunks = (P.out_sample_elems * P.src_elem + 15) / 16;
+    dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>((chunks + kThreads * 4 - 1) / (kThreads * 4), 65535)),
+           A.count);
+    array_copy_kernel<<<g, kThreads, 0, st>>>(P, A);
+  } else if (P.value_mode == VAL_COPY) {
     array_kernel<false, float><<<grid, kThreads, 0, st>>>(P, A);
   } else {
     switch (P.out_dtype) {

@@ -276,3 +276,22 @@ def test_zero_copy_payloads_match_oracle(tmp_path, chain):
         st = ld.stats()
     ds.close()
     assert st["zero_copy_bytes"] > 0 and st["h2d_bytes"] < st["zero_copy_bytes"]
+
+
+@pytest.mark.parametrize("strategy", ["os", "resident", "zero_copy"])
+def test_array_copy_kernel_alignments(tmp_path, strategy):
+    """ArrayRead with no transform is a straight copy (array_copy_kernel: 16-B
+    stores, source realigned per sample): odd lengths and every source
+    misalignment, staged / HBM-resident / zero-copy payloads."""
+    rs = np.random.default_rng(3)
+    schema = [bx.array_field("a", np.uint8, (1001,)), bx.array_field("b", np.float32, (7, 111)),
+              bx.array_field("c", np.int64, (3,)), bx.array_field("d", np.uint8, (17,)), bx.int_field("label")]
+    samples = [{"a": rs.integers(0, 256, 1001, dtype=np.uint8), "b": rs.normal(size=(7, 111)).astype(np.float32),
+                "c": rs.integers(-2**60, 2**60, 3, dtype=np.int64), "d": rs.integers(0, 256, 17, dtype=np.uint8),
+                "label": i} for i in range(37)]
+    path = tmp_path / "arrays.bbox"
+    bx.write_dataset(bx.InMemorySource(schema, samples), path, bx.WriterConfig(page_size=65536, seed=1))
+    strat = {"os": bx.OsCache(), "resident": bx.DeviceResident(), "zero_copy": bx.OsCache(zero_copy=True)}[strategy]
+    got = run_gpu(path, 8, "random", seed=2, epoch=1, strategy=strat)
+    want = list(O.loader_batches(path, 8, "random", 2, 1))
+    assert_same(got, want)
