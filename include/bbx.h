@@ -177,6 +177,8 @@ typedef struct {
   double  gap_seconds;        /* profiling: compute-stream idle between consecutive timed batches */
   double  h2d_late_seconds;   /* profiling: part of that idle time spent waiting for the batch's H2D */
   int64_t timed_batches;      /* profiling: batches whose kernel window (kernel_seconds) was timed */
+  int64_t page_fetches;       /* page pool: pages fetched H2D (reader.py CacheStats.fetch_count) */
+  int64_t page_reloads;       /* page pool: fetches of a page already fetched this epoch (reload_count) */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
  * RLE / JPEG fields, kernels read each sample's payload window straight from
@@ -194,6 +196,20 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *                              one batch's kernels fill SMs the previous batch's tail leaves idle
  * Unknown names return BBX_INVALID_ARGUMENT. */
 bbx_status bbx_loader_set_option(bbx_loader* ld, const char* name, int64_t value);
+/* HBM page pool -- ProcessCacheStrategy (reader.py:152-297 ProcessCache,
+ * loader.py:273-291,444-445): `capacity_pages` heap pages live in device memory.
+ * Each epoch's plan (bbx_loader_plan_epoch, called before the epoch's first
+ * submit, in epoch order) is the reference's PageSchedule: the trace of every
+ * batch's samples' distinct pages, farthest-next-use eviction; a batch touching
+ * more pages than the capacity fails with BBX_CAPACITY_TOO_SMALL ("batch
+ * touches N pages, cache holds K").  Submitted batches then execute the plan
+ * in order: each planned fetch copies one page H2D (mmap -> pinned -> pool
+ * slot, `fetch_latency_s` spun first), and kernels read payloads from the pool.
+ * Fetch / reload counts are the plan's (stats page_fetches / page_reloads).
+ * Call set_page_pool before the first submit. */
+bbx_status bbx_loader_set_page_pool(bbx_loader* ld, int64_t capacity_pages, double fetch_latency_s);
+bbx_status bbx_loader_plan_epoch(bbx_loader* ld, const int64_t* idx, const int32_t* batch_len, int32_t n_batches,
+                                 int64_t* planned_fetches, int64_t* planned_reloads);
 /* Samples whose JPEG headers the loader parses up front (before the first
  * submit).  A distributed rank passes its shard of the first epoch so that
  * ranks do not each parse every header; others are parsed on first sight

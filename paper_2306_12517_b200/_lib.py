@@ -42,7 +42,7 @@ class LoaderStats(ctypes.Structure):
                 ("kernel_launches", c_i64), ("stage_seconds", c_dbl), ("wait_seconds", c_dbl),
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
                 ("dma_batches", c_i64), ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
-                ("timed_batches", c_i64)]
+                ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64)]
 
 
 # bbx_status -> exception class (errors.py:4-57)
@@ -111,6 +111,8 @@ def _bind(L):
         "bbx_loader_prefetch_headers": (c_i32, [c_vp, c_vp, c_i64]),
         "bbx_decode_image": (c_i32, [c_i32, c_i32, c_i32, c_i32, c_vp, c_i64, c_vp, ctypes.c_int]),
         "bbx_jpeg_check": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_i64]),
+        "bbx_loader_set_page_pool": (c_i32, [c_vp, c_i64, c_dbl]),
+        "bbx_loader_plan_epoch": (c_i32, [c_vp, c_vp, c_vp, c_i32, P(c_i64), P(c_i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -128,7 +130,7 @@ EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_cl
             "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",
             "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling",
             "bbx_loader_set_zero_copy", "bbx_loader_set_option", "bbx_loader_prefetch_headers",
-            "bbx_decode_image", "bbx_jpeg_check")
+            "bbx_decode_image", "bbx_jpeg_check", "bbx_loader_set_page_pool", "bbx_loader_plan_epoch")
 
 
 def last_error() -> str:

@@ -25,6 +25,8 @@
 #include <emmintrin.h>
 #endif
 #include <unordered_map>
+#include <deque>
+#include <set>
 
 #include "engine.h"
 #include "jpeg.h"
@@ -170,6 +172,7 @@ struct Slot {
   bool timed = false;
   int64_t timed_launches = 0, timed_bytes = 0;
   bool released_pending = false, used = false;
+  uint64_t serial = 0;             // batches this ring slot has launched (page-pool reuse guards)
   // job
   int state = 0;                 // 0 idle, 1 queued, 2 launched
   int count = 0;
@@ -199,6 +202,45 @@ struct JpegTables {
   std::unordered_multimap<uint64_t, int> hmap, qmap;
   std::vector<std::vector<uint8_t>> hkey, qkey;
   std::mutex mu;                 // headers are parsed on the staging pool
+};
+
+// One epoch's page plan (reader.py:96-145 PageSchedule over the trace loader.py:
+// 276-291 builds): the batches' samples, and per batch its trace positions
+// (the distinct heap pages of each sample, ascending) with the plan's fetch /
+// eviction steps.  An eviction whose victim this same batch already used is
+// "deferred": the batch's kernels read every page of the batch at once, so
+// the victim's buffer is recycled after them (a spare physical page slot
+// holds the incoming page meanwhile).
+struct PageStep {
+  int64_t page;
+  int64_t victim;      // -1: no eviction
+  uint8_t fetch, deferred, reload;
+};
+struct PagePlan {
+  std::vector<int64_t> idx;           // samples, batch after batch
+  std::vector<int64_t> batch_off;     // first sample of batch b in idx (n_batches + 1 entries)
+  std::vector<int64_t> trace_off;     // first trace position of sample k (idx.size() + 1 entries)
+  std::vector<PageStep> trace;
+  int64_t phys_needed = 0;            // capacity + most deferred evictions of one batch
+  int64_t fetches = 0, reloads = 0;
+  int32_t next = 0;                   // next batch to execute
+};
+constexpr int kPageBufs = 4;          // pinned host page buffers (fetch staging)
+struct PagePool {
+  int64_t capacity = 0;               // capacity_pages (0: no page pool)
+  double fetch_latency_s = 0.0;       // reader.py ProcessCache fetch_latency_s (spin before each fetch)
+  int64_t phys = 0;                   // physical page slots allocated in d_pool
+  uint8_t* d_pool = nullptr;
+  std::deque<PagePlan> plans;         // installed epochs, executed in submission order (bbx_loader_plan_epoch)
+  std::vector<int64_t> slot_of;       // heap page -> physical slot (-1: not resident)
+  std::vector<int64_t> page_in;       // physical slot -> heap page (-1: free)
+  std::vector<int32_t> user_ring;     // physical slot -> ring slot of the last batch that read it (-1: none)
+  std::vector<uint64_t> user_serial;  //   ... and that batch's serial (the ring slot's, at submission)
+  std::vector<int64_t> free_list;
+  uint8_t* h_buf = nullptr;           // kPageBufs x page_size pinned
+  cudaEvent_t buf_ev[kPageBufs]{};
+  bool buf_used[kPageBufs] = {};
+  int buf_next = 0;
 };
 
 }  // namespace bbx
@@ -231,6 +273,9 @@ struct bbx_loader {
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
+  // HBM page pool (ProcessCacheStrategy with capacity < num_pages): executes the
+  // reference's Belady PageSchedule (reader.py:96-145) batch by batch
+  PagePool pp;
   // pipeline thread
   std::thread th;
   std::mutex mu;
@@ -1029,6 +1074,221 @@ static void gather_rows(uint8_t* dst, uint32_t dst_stride, const uint8_t* src, u
 #endif
 }
 
+// ------------------------------------------------------------------ page pool
+// Distinct heap pages of sample i, ascending (reader.py:414-424 sample_pages).
+// Pages outside the heap are left out (the sample fails at its descriptor).
+static void sample_pages(const bbx_dataset* ds, int64_t i, std::vector<int64_t>& out) {
+  out.clear();
+  const int64_t ps = ds->page_size, np = (ds->alloc_table_offset - ds->heap_offset) / ps;
+  auto add = [&](uint64_t off, uint64_t len) {
+    if (!len) return;
+    const int64_t a = ((int64_t)off - ds->heap_offset) / ps, b = ((int64_t)(off + len - 1) - ds->heap_offset) / ps;
+    for (int64_t q = std::max<int64_t>(a, 0); q <= std::min<int64_t>(b, np - 1); ++q) out.push_back(q);
+  };
+  for (const Field& f : ds->fields) {
+    const uint8_t* c = ds->rows + i * ds->row_width + f.info.cell_offset;
+    uint64_t off, len;
+    if (f.info.kind == 2) { std::memcpy(&off, c, 8); add(off, (uint64_t)f.array_nbytes); }
+    else if (f.info.kind == 3 || f.info.kind == 4) { std::memcpy(&off, c, 8); std::memcpy(&len, c + 8, 8); add(off, len); }
+  }
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+}
+
+// The epoch's page plan: the trace loader.py:276-291 builds (each batch's
+// samples' pages, in batch order), the CapacityTooSmall check of loader.py:
+// 286-289, and the farthest-next-use schedule of reader.py:112-141 (victim =
+// the resident page with the largest (next use, page)); fetch / reload counts
+// are the schedule's planned ones.
+static int plan_epoch(bbx_loader* L, const int64_t* idx, const int32_t* blen, int32_t nb, PagePlan& P) {
+  const bbx_dataset* ds = L->ds;
+  const int64_t K = L->pp.capacity, np = (ds->alloc_table_offset - ds->heap_offset) / ds->page_size;
+  std::vector<int64_t> pg, stamp((size_t)np, -1);
+  P.batch_off.assign(1, 0);
+  int64_t k = 0;
+  for (int32_t b = 0; b < nb; ++b) {
+    int64_t distinct = 0;
+    for (int32_t j = 0; j < blen[b]; ++j, ++k) {
+      const int64_t i = idx[k];
+      P.idx.push_back(i);
+      P.trace_off.push_back((int64_t)P.trace.size());
+      if (i >= 0 && i < ds->num_samples) sample_pages(ds, i, pg); else pg.clear();
+      for (int64_t q : pg) {
+        P.trace.push_back(PageStep{q, -1, 0, 0, 0});
+        if (stamp[q] != b) { stamp[q] = b; ++distinct; }
+      }
+    }
+    if (distinct > K)
+      return fail(BBX_CAPACITY_TOO_SMALL, "batch touches %lld pages, cache holds %lld", (long long)distinct,
+                  (long long)K);
+    P.batch_off.push_back(k);
+  }
+  P.trace_off.push_back((int64_t)P.trace.size());
+  const int64_t T = (int64_t)P.trace.size(), INF = T + 1;
+  std::vector<int64_t> next_use((size_t)T), last_seen((size_t)np, INF);
+  for (int64_t t = T - 1; t >= 0; --t) {
+    next_use[t] = last_seen[P.trace[t].page];
+    last_seen[P.trace[t].page] = t;
+  }
+  std::set<std::pair<int64_t, int64_t>> res;        // (next use, page) of the resident pages
+  std::vector<int64_t> cur((size_t)np, -1), last_pos((size_t)np, -1);
+  std::vector<uint8_t> seen((size_t)np, 0);
+  P.phys_needed = K;
+  for (int32_t b = 0; b < nb; ++b) {
+    const int64_t t0 = P.trace_off[P.batch_off[b]], t1 = P.trace_off[P.batch_off[b + 1]];
+    int64_t deferred = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      PageStep& st = P.trace[t];
+      const int64_t q = st.page;
+      if (cur[q] >= 0) {
+        res.erase({cur[q], q});
+      } else {
+        if ((int64_t)res.size() >= K) {
+          auto it = std::prev(res.end());
+          const int64_t v = it->second;
+          res.erase(it);
+          cur[v] = -1;
+          st.victim = v;
+          st.deferred = last_pos[v] >= t0 ? 1 : 0;   // read by this batch's kernels: recycle after them
+          deferred += st.deferred;
+        }
+        st.fetch = 1;
+        st.reload = seen[q];
+        seen[q] = 1;
+        ++P.fetches;
+        P.reloads += st.reload;
+      }
+      cur[q] = next_use[t];
+      res.insert({cur[q], q});
+      last_pos[q] = t;
+    }
+    P.phys_needed = std::max(P.phys_needed, K + deferred);
+  }
+  return BBX_OK;
+}
+
+// Fetch heap page `page` into physical pool slot `ph`: once the last batch that
+// read the slot is done, the page's bytes go mmap -> pinned page buffer (the
+// staging pool's threads) -> H2D on the copy stream (reader.py:379-384 _fetch_page,
+// with the strategy's fetch latency spun before it as in reader.py:247-248).
+static int fetch_page(bbx_loader* L, int64_t page, int64_t ph) {
+  PagePool& PP = L->pp;
+  const bbx_dataset* ds = L->ds;
+  if (PP.user_ring[ph] >= 0 && L->slots[PP.user_ring[ph]].serial == PP.user_serial[ph])
+    CK(cudaStreamWaitEvent(L->copy_st, L->slots[PP.user_ring[ph]].done, 0));
+  const int k = PP.buf_next;
+  PP.buf_next = (k + 1) % kPageBufs;
+  if (PP.buf_used[k]) CK(cudaEventSynchronize(PP.buf_ev[k]));
+  if (PP.fetch_latency_s > 0) {
+    const auto until = std::chrono::steady_clock::now() + std::chrono::duration<double>(PP.fetch_latency_s);
+    while (std::chrono::steady_clock::now() < until) {}
+  }
+  const int64_t ps = ds->page_size, off = ds->heap_offset + page * ps;
+  const int64_t len = std::min<int64_t>(ps, ds->alloc_table_offset - off);
+  uint8_t* dst = PP.h_buf + (size_t)k * ps;
+  const int64_t chunk = 1 << 20, n = (len + chunk - 1) / chunk;
+  L->pool->parallel_for(n, [&](int64_t c) {
+    const int64_t a = c * chunk, m = std::min(chunk, len - a);
+    std::memcpy(dst + a, ds->map + off + a, (size_t)m);
+  });
+  CK(cudaMemcpyAsync(PP.d_pool + (size_t)ph * ps, dst, (size_t)len, cudaMemcpyHostToDevice, L->copy_st));
+  CK(cudaEventRecord(PP.buf_ev[k], L->copy_st));
+  PP.buf_used[k] = true;
+  std::lock_guard<std::mutex> g(L->stats_mu);
+  L->stats.page_fetches += 1;
+  L->stats.h2d_bytes += len;
+  return BBX_OK;
+}
+
+// This batch's part of the installed plan: its fetches / evictions in trace
+// order, and the pool address of every sample payload that lies in one page
+// (addr[p][pos]; null: staged like an OsCache payload -- oversized blobs).
+static int page_batch(bbx_loader* L, Slot& S, int count, std::vector<std::vector<const uint8_t*>>& addr,
+                      std::vector<int64_t>& read_slots, std::vector<int64_t>& deferred) {
+  PagePool& PP = L->pp;
+  const bbx_dataset* ds = L->ds;
+  PagePlan* Pp;
+  {
+    std::lock_guard<std::mutex> g(L->mu);
+    if (PP.plans.empty()) return fail(BBX_INVALID_ARGUMENT, "page pool: batch submitted without an epoch plan");
+    Pp = &PP.plans.front();
+  }
+  PagePlan& P = *Pp;
+  const int32_t b = P.next;
+  const int64_t k0 = P.batch_off[b], k1 = P.batch_off[b + 1];
+  if (k1 - k0 != count || std::memcmp(&P.idx[k0], S.idx.data(), (size_t)count * 8))
+    return fail(BBX_INVALID_ARGUMENT, "page pool: batch does not follow the installed epoch plan");
+  const int64_t ps = ds->page_size;
+  if (b == 0) {   // epoch start: the reference's install() starts from an empty cache (reader.py:196-208)
+    if (PP.phys < P.phys_needed) {
+      for (int k = 0; k < kStreams; ++k) CK(cudaStreamSynchronize(L->comp_st[k]));
+      CK(cudaStreamSynchronize(L->copy_st));
+      if (PP.d_pool) CK(cudaFree(PP.d_pool));
+      PP.d_pool = nullptr;
+      CK(cudaMalloc(&PP.d_pool, (size_t)P.phys_needed * ps));
+      PP.phys = P.phys_needed;
+      PP.page_in.assign((size_t)PP.phys, -1);
+      PP.user_ring.assign((size_t)PP.phys, -1);
+      PP.user_serial.assign((size_t)PP.phys, 0);
+    }
+    for (int64_t ph = 0; ph < PP.phys; ++ph)
+      if (PP.page_in[ph] >= 0) { PP.slot_of[PP.page_in[ph]] = -1; PP.page_in[ph] = -1; }
+    PP.free_list.clear();
+    for (int64_t ph = PP.phys - 1; ph >= 0; --ph) PP.free_list.push_back(ph);
+  }
+  int64_t reloads = 0;
+  for (int64_t k = k0; k < k1; ++k) {
+    const int pos = (int)(k - k0);
+    for (int64_t t = P.trace_off[k]; t < P.trace_off[k + 1]; ++t) {
+      const PageStep& st = P.trace[t];
+      if (st.fetch) {
+        int64_t ph;
+        if (st.victim >= 0) {
+          const int64_t vp = PP.slot_of[st.victim];
+          PP.slot_of[st.victim] = -1;
+          PP.page_in[vp] = -1;
+          if (st.deferred) {
+            deferred.push_back(vp);
+            if (PP.free_list.empty()) return fail(BBX_INVALID_ARGUMENT, "page pool: no spare page slot");
+            ph = PP.free_list.back();
+            PP.free_list.pop_back();
+          } else {
+            ph = vp;
+          }
+        } else {
+          if (PP.free_list.empty()) return fail(BBX_INVALID_ARGUMENT, "page pool: no free page slot");
+          ph = PP.free_list.back();
+          PP.free_list.pop_back();
+        }
+        if (int r = fetch_page(L, st.page, ph)) return r;
+        PP.slot_of[st.page] = ph;
+        PP.page_in[ph] = st.page;
+        reloads += st.reload;
+      }
+      read_slots.push_back(PP.slot_of[st.page]);
+    }
+    const int64_t i = S.idx[pos];
+    if (i < 0 || i >= ds->num_samples) continue;
+    for (size_t p = 0; p < L->plans.size(); ++p) {
+      const Plan& pl = L->plans[p];
+      if (pl.scalar) continue;
+      const Field& f = ds->fields[pl.field_index];
+      uint64_t off, len;
+      if (f.info.kind == 4) { const ImageCell c = image_cell(ds, i, f); off = c.offset; len = c.length; }
+      else { off = u64_cell(ds, i, f); len = (uint64_t)f.array_nbytes; }
+      if (!len || (int64_t)off < ds->heap_offset || off + len > (uint64_t)ds->alloc_table_offset) continue;
+      const int64_t q = ((int64_t)off - ds->heap_offset) / ps;
+      if (q != ((int64_t)(off + len - 1) - ds->heap_offset) / ps || PP.slot_of[q] < 0) continue;
+      addr[p][pos] = PP.d_pool + (size_t)PP.slot_of[q] * ps + ((int64_t)off - ds->heap_offset - q * ps);
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(L->stats_mu);
+    L->stats.page_reloads += reloads;
+  }
+  return BBX_OK;
+}
+
 static int process_slot(bbx_loader* L, int s) {
   Slot& S = L->slots[s];
   const bbx_dataset* ds = L->ds;
@@ -1038,6 +1298,7 @@ static int process_slot(bbx_loader* L, int s) {
   int64_t zc_bytes = 0;
   // the pinned slot may still be the source of the previous H2D
   if (S.used) CK(cudaEventSynchronize(S.h2d_done));
+  ++S.serial;
   S.herr = HostErr{};
   S.plan_has_rle.assign(L->plans.size(), 0);
   S.plan_has_jpeg.assign(L->plans.size(), 0);
@@ -1059,6 +1320,14 @@ static int process_slot(bbx_loader* L, int s) {
       reinterpret_cast<int64_t*>(H + L->idx_off)[pos] = 0;   // keep device gathers in bounds
     }
   }
+  // page pool: this batch's fetches, and where each payload sits in the pool
+  std::vector<std::vector<const uint8_t*>> pool_addr;
+  std::vector<int64_t> pool_read, pool_deferred;
+  if (L->pp.capacity) {
+    pool_addr.assign(L->plans.size(), std::vector<const uint8_t*>((size_t)count, nullptr));
+    if (int r = page_batch(L, S, count, pool_addr, pool_read, pool_deferred)) return r;
+  }
+  const uint8_t* stage_dev = S.d_stage + L->pay_base;   // device address of the staged payload region
   // descriptors + payload plan (serial: ~100 ns per sample per field)
   struct Copy { const uint8_t* src; uint8_t* dst; uint32_t row_bytes, rows, src_stride, dst_stride; };
   std::vector<Copy> copies;
@@ -1098,6 +1367,10 @@ static int process_slot(bbx_loader* L, int s) {
         if (L->jpeg_cache && pl.jcached[i]) { jds[pos] = pl.jcache[i]; jst[p][pos] = &pl.jstarts[i]; }
         else jparse.push_back({(int)p, pos, i, off, len});
         S.plan_has_jpeg[p] = 1;
+      }
+      if (!pool_addr.empty() && pool_addr[p][pos]) {   // in the HBM page pool (offset from the staged base)
+        d->src = (uint64_t)(pool_addr[p][pos] - stage_dev);
+        continue;
       }
       if (resident) {
         d->src = off;                                   // absolute file offset; base = heap - heap_offset
@@ -1385,6 +1658,14 @@ static int process_slot(bbx_loader* L, int s) {
   }
   CK(cudaEventRecord(S.done, cs));
   S.used = true;
+  if (L->pp.capacity) {   // the pool slots this batch reads are recycled only after S.done
+    PagePool& PP = L->pp;
+    for (int64_t ph : pool_read) { PP.user_ring[ph] = s; PP.user_serial[ph] = S.serial; }
+    for (int64_t ph : pool_deferred) { PP.user_ring[ph] = s; PP.user_serial[ph] = S.serial; PP.free_list.push_back(ph); }
+    std::lock_guard<std::mutex> g(L->mu);
+    PagePlan& P = PP.plans.front();
+    if (++P.next == (int32_t)P.batch_off.size() - 1) PP.plans.pop_front();
+  }
   {
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.batches += 1;
@@ -1748,6 +2029,7 @@ bbx_status bbx_loader_drain(bbx_loader* L) {
       return true;
     });
     for (auto& S : L->slots) if (S.state == 2) S.state = 0;
+    L->pp.plans.clear();   // an abandoned stream's remaining page plan
   }
   cudaSetDevice(L->device);
   cudaError_t e1 = cudaStreamSynchronize(L->comp_st[0]), e2 = cudaStreamSynchronize(L->copy_st);
@@ -1766,6 +2048,11 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (L->th.joinable()) L->th.join();
   }
   cudaSetDevice(L->device);
+  if (L->pp.d_pool) cudaFree(L->pp.d_pool);
+  if (L->pp.h_buf) {
+    cudaFreeHost(L->pp.h_buf);
+    for (int k = 0; k < kPageBufs; ++k) cudaEventDestroy(L->pp.buf_ev[k]);
+  }
   for (auto& S : L->slots) {
     if (S.h_stage) cudaFreeHost(S.h_stage);
     if (S.d_stage) cudaFree(S.d_stage);
@@ -1923,6 +2210,44 @@ static int decode_image_impl(int32_t h, int32_t w, int32_t c, int32_t codec, con
 bbx_status bbx_decode_image(int32_t h, int32_t w, int32_t c, int32_t codec, const uint8_t* payload_host, int64_t len,
                             uint8_t* out_dev, int device) {
   return (bbx_status)decode_image_impl(h, w, c, codec, payload_host, len, out_dev, device);
+}
+
+static int set_page_pool_impl(bbx_loader* L, int64_t capacity_pages, double fetch_latency_s) {
+  if (!L) return fail(BBX_INVALID_ARGUMENT, "null loader");
+  if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "page pool: set before the first submit");
+  if (capacity_pages < 1)
+    return (bbx_status)fail(BBX_CAPACITY_TOO_SMALL, "capacity_pages must be >= 1, got %lld", (long long)capacity_pages);
+  if (L->ds->d_heap || L->zero_copy)
+    return (bbx_status)fail(BBX_INVALID_ARGUMENT, "page pool: the heap is already device-resident / zero-copy");
+  CK(cudaSetDevice(L->device));
+  PagePool& PP = L->pp;
+  PP.capacity = capacity_pages;
+  PP.fetch_latency_s = fetch_latency_s > 0 ? fetch_latency_s : 0.0;
+  const int64_t np = (L->ds->alloc_table_offset - L->ds->heap_offset) / L->ds->page_size;
+  PP.slot_of.assign((size_t)std::max<int64_t>(np, 1), -1);
+  if (!PP.h_buf) {
+    CK(cudaHostAlloc(&PP.h_buf, (size_t)kPageBufs * L->ds->page_size, cudaHostAllocDefault));
+    for (int k = 0; k < kPageBufs; ++k) CK(cudaEventCreateWithFlags(&PP.buf_ev[k], cudaEventDisableTiming));
+  }
+  return BBX_OK;
+}
+bbx_status bbx_loader_set_page_pool(bbx_loader* L, int64_t capacity_pages, double fetch_latency_s) {
+  return (bbx_status)set_page_pool_impl(L, capacity_pages, fetch_latency_s);
+}
+
+bbx_status bbx_loader_plan_epoch(bbx_loader* L, const int64_t* idx, const int32_t* batch_len, int32_t n_batches,
+                                 int64_t* planned_fetches, int64_t* planned_reloads) {
+  if (!L || (n_batches > 0 && (!idx || !batch_len))) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
+  if (!L->pp.capacity) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "page pool: not enabled");
+  PagePlan P;
+  if (int r = plan_epoch(L, idx, batch_len, n_batches, P)) return (bbx_status)r;
+  if (planned_fetches) *planned_fetches = P.fetches;
+  if (planned_reloads) *planned_reloads = P.reloads;
+  if (n_batches > 0) {
+    std::lock_guard<std::mutex> g(L->mu);
+    L->pp.plans.push_back(std::move(P));
+  }
+  return BBX_OK;
 }
 
 bbx_status bbx_jpeg_check(int32_t h, int32_t w, int32_t c, const uint8_t* payload, int64_t len) {

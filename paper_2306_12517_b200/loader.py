@@ -261,8 +261,8 @@ class Loader:
             raise SchemaMismatch("no batchable fields selected")
 
         strategy = self.dataset.strategy
-        if isinstance(strategy, DeviceResident) or (
-                isinstance(strategy, ProcessCacheStrategy) and strategy.capacity_pages >= self.dataset.num_pages):
+        self.page_pool = isinstance(strategy, ProcessCacheStrategy)
+        if isinstance(strategy, DeviceResident):
             if isinstance(strategy, DeviceResident) and strategy.device is not None and \
                     int(strategy.device) != self.device:
                 raise ValueError(f"DeviceResident(device={strategy.device}) but the loader runs on cuda:{self.device}: "
@@ -280,6 +280,9 @@ class Loader:
         self._handle = h
         if isinstance(strategy, OsCache) and getattr(strategy, "zero_copy", False):
             _lib.check(L.bbx_loader_set_zero_copy(h, 1))
+        if self.page_pool:   # HBM page pool executing the reference's PageSchedule (reader.py:96-297)
+            strategy.check()
+            _lib.check(L.bbx_loader_set_page_pool(h, int(strategy.capacity_pages), float(strategy.fetch_latency_s)))
         for name, value in (config.options or {}).items():
             _lib.check(L.bbx_loader_set_option(h, str(name).encode(), int(value)))
         field_index = {f.name: i for i, f in enumerate(schema)}
@@ -467,9 +470,8 @@ class _EpochRun:
                 break
             if self._steps is not None:
                 bl = bl[:self._steps - len(self.batch_lists)]
-            strategy = self.loader.dataset.strategy
-            if isinstance(strategy, ProcessCacheStrategy):
-                self._check_capacity(bl, strategy.capacity_pages)
+            if self.loader.page_pool:
+                self._plan_pages(bl)
             self.batch_lists += bl
             self.batch_epochs += [self._next_epoch] * len(bl)
             self._next_epoch += 1
@@ -477,14 +479,16 @@ class _EpochRun:
                 self._exhausted = True
         return g < len(self.batch_lists)
 
-    def _check_capacity(self, batches, capacity: int) -> None:
-        ds = self.loader.dataset
-        for batch in batches:
-            pages: set = set()
-            for i in batch:
-                pages.update(ds.sample_pages(int(i)))
-            if len(pages) > capacity:
-                raise CapacityTooSmall(f"batch touches {len(pages)} pages, cache holds {capacity}")
+    def _plan_pages(self, batches) -> None:
+        """The epoch's page plan (loader.py:273-291): trace, CapacityTooSmall check
+        and the Belady schedule, computed natively and queued ahead of the epoch's
+        batches (bbx_loader_plan_epoch)."""
+        idx = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int64) for b in batches])
+                                   if batches else np.zeros(0, dtype=np.int64))
+        lens = np.ascontiguousarray(np.array([len(b) for b in batches], dtype=np.int32))
+        fetches, reloads = ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(_lib.lib().bbx_loader_plan_epoch(self.loader.handle, idx.ctypes.data, lens.ctypes.data, len(batches),
+                                                    ctypes.byref(fetches), ctypes.byref(reloads)))
 
     def _submit(self, g: int) -> None:
         ld = self.loader
@@ -511,6 +515,7 @@ class _EpochRun:
             ld._headers_named = True
             mine = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int64) for b in self.batch_lists]))
             _lib.check(L.bbx_loader_prefetch_headers(ld.handle, mine.ctypes.data, len(mine)))
+        pool_base = ld.stats() if ld.page_pool else None   # page-pool counters at the stream's start
         for g in range(S - 1):
             if self._ensure(g):
                 self._submit(g)
@@ -549,6 +554,10 @@ class _EpochRun:
                 arrays[fd.name] = t
             self.stats.batches += 1
             self.stats.samples += count
+            if pool_base is not None:   # the executed fetches (loader.py:443-445)
+                now = ld.stats()
+                self.stats.page_fetches = max(0, now["page_fetches"] - pool_base["page_fetches"])
+                self.stats.page_reloads = max(0, now["page_reloads"] - pool_base["page_reloads"])
             yield Batch(arrays, indices.tolist(), g)
             g += 1
 

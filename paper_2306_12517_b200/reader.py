@@ -9,9 +9,10 @@ the device loader stages payloads from, plus a Python mmap for metadata
 * Direct(read_latency_s)       accepted for API compatibility; staging reads
                                the same mmap (latency injection is a CPU-
                                benchmark device of the reference)
-* ProcessCacheStrategy(cap)    pages cached in HBM: with capacity >= num_pages
-                               the whole heap is made device-resident; a batch
-                               touching more pages than `cap` raises
+* ProcessCacheStrategy(cap)    an HBM page pool of `cap` heap pages executing
+                               the reference's Belady PageSchedule per epoch
+                               (reader.py:96-297; csrc/engine.cpp page pool):
+                               page_fetches / page_reloads as the reference's,
                                CapacityTooSmall as in loader.py:286-289
 * DeviceResident(device=None)  extension: the heap lives in HBM (B200 180 GB),
                                batches read payloads from HBM, no H2D per epoch
