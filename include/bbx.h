@@ -179,6 +179,7 @@ typedef struct {
   int64_t timed_batches;      /* profiling: batches whose kernel window (kernel_seconds) was timed */
   int64_t page_fetches;       /* page pool: pages fetched H2D (reader.py CacheStats.fetch_count) */
   int64_t page_reloads;       /* page pool: fetches of a page already fetched this epoch (reload_count) */
+  int64_t io_reads;           /* Direct strategy: payload preads (reader.py io_read_count) */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
  * RLE / JPEG fields, kernels read each sample's payload window straight from
@@ -192,6 +193,9 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *   "jpeg_header_cache"     1: keep each JPEG sample's parsed header for later epochs
  *   "jpeg_header_prefetch"  1: parse the headers of this loader's samples up front
  *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
+ *   "direct_io"             0: Direct strategy -- every payload read is one pread of the whole
+ *                              payload (reader.py:368-372), no window staging, no DMA
+ *   "read_latency_ns"       0: Direct: latency spun before each read (reader.py:369-370)
  *   "compute_streams"       2: consecutive batches alternate between two CUDA streams, so
  *                              one batch's kernels fill SMs the previous batch's tail leaves idle
  * Unknown names return BBX_INVALID_ARGUMENT. */

@@ -1,43 +1,3 @@
-# INTEGRATION — binding libbbx from the reference (`bbox`, Python)
-
-The reference is a pure-Python package, so its FFI for this path is `ctypes`.  A
-maintainer of `bbox` who wants the B200 path behind the existing API adds one module —
-a loader whose `__init__` builds device plans from the same `LoaderConfig` and whose
-`iterate_epoch` hands each batch's indices to `bbx_loader_submit`.  This repo's
-`paper_2306_12517_b200/_lib.py` + `loader.py` are exactly that binding; the minimal
-form is below.
-
-## Entry points ↔ reference interfaces
-
-| C ABI (`include/bbx.h`) | replaces (reference, `pkg/src/bbox/`) |
-|---|---|
-| `bbx_dataset_open` / `_close` / `_header` / `_field` / `_row` | `reader.open_dataset`, `Dataset.__init__` (reader.py:323-366, 535-546), `format.decode_header` (format.py:298-337), `Dataset.row_bytes` (reader.py:383-386) |
-| `bbx_dataset_make_resident` | (extension) `DeviceResident`: the whole heap in HBM |
-| `bbx_loader_set_page_pool` / `bbx_loader_plan_epoch` | `ProcessCacheStrategy` + `ProcessCache` (reader.py:67-77, 152-297) executing `PageSchedule` (reader.py:96-145) as planned by `_EpochRun.__init__` (loader.py:273-291); counts as `EpochStats.page_fetches/page_reloads` (loader.py:443-445) |
-| `bbx_loader_set_option("direct_io" / "read_latency_ns")` | `Direct(read_latency_s)` reads (reader.py:61-65, 368-372) |
-| `bbx_jpeg_check` | `validate_file`'s per-cell codec check (format.py:542-543), extended to codec 3 |
-| `bbx_dataset_page_map` | `Dataset.primary_page` (reader.py:430-437) |
-| `bbx_epoch_order` | `TraversalOrder.epoch_indices` (traversal.py:84-104), `_quasi_epoch` (45-73), `Rng.shuffle` (rng.py:75-79) |
-| `bbx_loader_create` / `_add_field` / `_add_scalar` / `_bind` | `Loader.__init__` plan building (loader.py:153-198), `PipelinePlan` (pipeline.py:312-361) |
-| `bbx_loader_submit` | `_EpochRun._next_task` + `_process_position` for a whole batch (loader.py:301-347) |
-| `bbx_loader_wait` | `BatchRing.consume` + first-error re-raise (pipeline.py:509-524, loader.py:397-402) |
-| `bbx_loader_release` | `BatchRing.end_consume` (pipeline.py:484-488) |
-| `bbx_loader_stream_wait` | (new) consumer stream ordering, no host round trip |
-| `bbx_loader_drain` / `_destroy` | `_EpochRun.stop` / `Loader.shutdown` (loader.py:232-242, 427-447) |
-| `bbx_decode_image` | `codecs.decode_image` (codecs.py:91-128); codec 3 = JPEG (extension) |
-| `bbx_last_error` + status codes | `errors.py:4-57` exception classes |
-
-## The ctypes module a `bbox` maintainer would add (`bbox/gpu.py`)
-
-Committed as `integration/bbox_gpu.py` and exercised for real by
-`tests/test_gpu_integration.py`: the test imports the UNMODIFIED reference package
-(`baseline/_ref`, installed with `pip install --no-index --no-build-isolation --no-deps
---target baseline/_ref`), builds the reference's own `LoaderConfig`, transform
-instances (`bbox.parse_pipeline`) and `TraversalOrder` batches, runs them through this
-module, and compares every batch with the reference Loader's golden batches
-(`tests/golden/loader_batches.npz`) -- bit-exact.
-
-```python
 """The ctypes module a `bbox` maintainer adds to put the B200 path behind the
 reference's own API (INTEGRATION.md): `GpuLoader` takes the reference's
 `LoaderConfig` and its `Decode` / `RandomCrop` / `RandomFlip` / `Resize` /
@@ -161,29 +121,3 @@ class GpuLoader:
             _L.bbx_loader_destroy(self.ld)
             _L.bbx_dataset_close(self.ds)
             self.ld = self.ds = None
-```
-
-The full declaration table of every entry point is in `paper_2306_12517_b200/_lib.py`.  Building `libbbx.so`: `python -c "import
-__graft_entry__ as g; g.build()"` (nvcc `-gencode arch=compute_100a,code=sm_100a`, g++ for
-the host engine; no CMake, no runtime JIT).
-
-## JPEG (codec id 3) — what a `bbox` maintainer adds
-
-The reference stops at codec 2 (`codecs.py:25-28`) and its validator rejects anything
-higher (`format.py:542-543`).  To carry JPEG payloads through the same `.bbox` layout:
-
-1. `codecs.py`: `CodecId.JPEG = 3`; `encode_image(..., CodecId.JPEG)` returns the JFIF
-   bytes (this repo's `codecs.encode_jpeg`: Pillow, quality 90, 4:2:0, a restart marker
-   every 4 MCUs by default — `JpegParams`).  Restart intervals are the device decoder's
-   unit of parallelism; they cost ~0.7 % in file size at q90.
-2. `format.py:542`: accept `cell.codec == 3` and check the payload with `bbx_jpeg_check`
-   (this repo's `paper_2306_12517_b200/validate.py` is that validator: the reference's
-   checks and texts, vectorised, plus the JPEG payload check).
-3. Nothing changes in the loader binding above: `bbx_loader_add_field` on a field that
-   holds JPEG cells allocates the decoder's scratch, and every `Decode` /
-   `RandomResizedCrop` / `CenterCrop` chain on it decodes on the GPU first.  Corrupt
-   streams raise `CorruptPayload` with a `jpeg: ...` reason at the sample's position
-   (host-side header checks) or at batch wait (device-side marker / Huffman checks).
-
-Cells stay `(offset, length, h, w, c, codec)`; `h, w, c` must equal the SOF header's
-dimensions (checked per sample).

@@ -42,7 +42,8 @@ class LoaderStats(ctypes.Structure):
                 ("kernel_launches", c_i64), ("stage_seconds", c_dbl), ("wait_seconds", c_dbl),
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
                 ("dma_batches", c_i64), ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
-                ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64)]
+                ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64),
+                ("io_reads", c_i64)]
 
 
 # bbx_status -> exception class (errors.py:4-57)

@@ -17,6 +17,7 @@
 // of g+1 and the kernels of g.  With a device-resident heap
 // (bbx_dataset_make_resident) steps 2-3 shrink to the descriptor upload.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -273,6 +274,8 @@ struct bbx_loader {
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
+  bool direct_io = false;             // Direct strategy (reader.py:61-65,368-372): one pread per payload read
+  int64_t read_latency_ns = 0;        //   ... with the strategy's read latency spun before each read
   // HBM page pool (ProcessCacheStrategy with capacity < num_pages): executes the
   // reference's Belady PageSchedule (reader.py:96-145) batch by batch
   PagePool pp;
@@ -1517,7 +1520,26 @@ static int process_slot(bbx_loader* L, int s) {
     }
   }
   // gather mode: mmap page cache -> pinned slot (row segments for windows)
-  if (!dma_done && !copies.empty()) {
+  if (!dma_done && !copies.empty() && L->direct_io) {   // Direct: pread each payload (whole, unwindowed)
+    std::atomic<int> io_err{0};
+    L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
+      const Copy& c = copies[k];
+      if (L->read_latency_ns > 0) {
+        const auto until = std::chrono::steady_clock::now() + std::chrono::nanoseconds(L->read_latency_ns);
+        while (std::chrono::steady_clock::now() < until) {}
+      }
+      const off_t at = (off_t)(c.src - ds->map);
+      size_t done = 0;
+      while (done < c.row_bytes) {
+        const ssize_t r = ::pread(ds->fd, c.dst + done, c.row_bytes - done, at + (off_t)done);
+        if (r <= 0) { io_err = 1; break; }
+        done += (size_t)r;
+      }
+    });
+    if (io_err) return fail(BBX_INVALID_FILE, "%s: short read", ds->path.c_str());
+    std::lock_guard<std::mutex> g(L->stats_mu);
+    L->stats.io_reads += (int64_t)copies.size();
+  } else if (!dma_done && !copies.empty()) {
     const uint8_t* map_end = ds->map + ds->map_len;
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
@@ -2111,6 +2133,8 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   else if (n == "jpeg_header_cache") L->jpeg_cache = value != 0;
   else if (n == "jpeg_roi") L->jpeg_roi = value != 0;
   else if (n == "jpeg_header_prefetch") L->jpeg_prefetch = value != 0;
+  else if (n == "direct_io") { L->direct_io = value != 0; if (L->direct_io) { L->window_staging = false; L->dma_allowed = false; } }
+  else if (n == "read_latency_ns") L->read_latency_ns = value > 0 ? value : 0;
   else if (n == "compute_streams") {
     if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);
     L->nstreams = (int)value;

@@ -31,7 +31,7 @@ from . import _lib
 from . import pipeline as pl
 from .errors import CapacityTooSmall, SchemaMismatch, ShutdownError, SpecMismatch
 from .format import FieldKind
-from .reader import Dataset, DeviceResident, OsCache, ProcessCacheStrategy, open_dataset
+from .reader import Dataset, DeviceResident, Direct, OsCache, ProcessCacheStrategy, open_dataset
 from .traversal import OrderKind, TraversalOrder
 
 DEFAULT_SLOT_COUNT = 3
@@ -262,6 +262,7 @@ class Loader:
 
         strategy = self.dataset.strategy
         self.page_pool = isinstance(strategy, ProcessCacheStrategy)
+        self.direct_io = isinstance(strategy, Direct)
         if isinstance(strategy, DeviceResident):
             if isinstance(strategy, DeviceResident) and strategy.device is not None and \
                     int(strategy.device) != self.device:
@@ -280,6 +281,9 @@ class Loader:
         self._handle = h
         if isinstance(strategy, OsCache) and getattr(strategy, "zero_copy", False):
             _lib.check(L.bbx_loader_set_zero_copy(h, 1))
+        if isinstance(strategy, Direct):   # one pread per payload, the strategy's latency first
+            _lib.check(L.bbx_loader_set_option(h, b"direct_io", 1))
+            _lib.check(L.bbx_loader_set_option(h, b"read_latency_ns", int(strategy.read_latency_s * 1e9)))
         if self.page_pool:   # HBM page pool executing the reference's PageSchedule (reader.py:96-297)
             strategy.check()
             _lib.check(L.bbx_loader_set_page_pool(h, int(strategy.capacity_pages), float(strategy.fetch_latency_s)))
@@ -516,6 +520,7 @@ class _EpochRun:
             mine = np.ascontiguousarray(np.concatenate([np.asarray(b, dtype=np.int64) for b in self.batch_lists]))
             _lib.check(L.bbx_loader_prefetch_headers(ld.handle, mine.ctypes.data, len(mine)))
         pool_base = ld.stats() if ld.page_pool else None   # page-pool counters at the stream's start
+        io_seen = ld.stats()["io_reads"] if ld.direct_io else 0
         for g in range(S - 1):
             if self._ensure(g):
                 self._submit(g)
@@ -554,6 +559,10 @@ class _EpochRun:
                 arrays[fd.name] = t
             self.stats.batches += 1
             self.stats.samples += count
+            if ld.direct_io:            # Direct: the loader's preads count as the dataset's reads
+                io_now = ld.stats()["io_reads"]
+                ld.dataset.io_read_count += io_now - io_seen
+                io_seen = io_now
             if pool_base is not None:   # the executed fetches (loader.py:443-445)
                 now = ld.stats()
                 self.stats.page_fetches = max(0, now["page_fetches"] - pool_base["page_fetches"])

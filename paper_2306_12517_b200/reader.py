@@ -6,9 +6,10 @@ the device loader stages payloads from, plus a Python mmap for metadata
 
 * OsCache(pinned=None)         page-cache mmap (default; reference OsCache);
                                small heaps are also held pinned for DMA
-* Direct(read_latency_s)       accepted for API compatibility; staging reads
-                               the same mmap (latency injection is a CPU-
-                               benchmark device of the reference)
+* Direct(read_latency_s)       every heap read is one pread (+ the latency
+                               spun first), counted in io_read_count, as
+                               reader.py:61-65,368-372; the loader stages each
+                               payload with one pread (loader option direct_io)
 * ProcessCacheStrategy(cap)    an HBM page pool of `cap` heap pages executing
                                the reference's Belady PageSchedule per epoch
                                (reader.py:96-297; csrc/engine.cpp page pool):
@@ -23,6 +24,7 @@ from __future__ import annotations
 import ctypes
 import mmap
 import os
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -93,7 +95,7 @@ class Dataset:
         self.num_samples = self.header.num_samples
         self.num_pages = self.header.num_pages
         self._row_width = self.header.row_width
-        self.io_read_count = 0
+        self.io_read_count = 1 if isinstance(self.strategy, Direct) else 0   # the row table (reader.py:343-346)
         self.cache = None
         handle = ctypes.c_void_p()
         _lib.check(_lib.lib().bbx_dataset_open(self.path.encode(), ctypes.byref(handle)), f"{self.path}: ")
@@ -196,6 +198,14 @@ class Dataset:
     def heap_read(self, offset: int, length: int, blocking: bool = False) -> np.ndarray:
         if length == 0:
             return np.empty(0, dtype=np.uint8)
+        if isinstance(self.strategy, Direct):   # reader.py:368-372: pread copy, latency first
+            if self.strategy.read_latency_s:
+                end = time.perf_counter() + self.strategy.read_latency_s
+                while time.perf_counter() < end:
+                    pass
+            self.io_read_count += 1
+            with open(self.path, "rb", buffering=0) as fh:
+                return np.frombuffer(os.pread(fh.fileno(), length, offset), dtype=np.uint8)
         return self._view[offset:offset + length]
 
     # -- random access ------------------------------------------------------------

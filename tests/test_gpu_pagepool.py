@@ -96,3 +96,37 @@ def test_pool_stream_across_epochs_vs_oracle(tmp_path, chain):
         want += list(O.loader_batches(path, 16, "random", 11, e, pipelines={"image": spec}))
     for (gi, gimg), (wi, wa) in zip(got, want[:60]):
         assert gi == wi and np.array_equal(gimg, wa["image"])
+
+
+def test_direct_strategy_preads_with_latency(tmp_path):
+    """Direct(read_latency_s) (reader.py:61-65,368-372): one counted pread per
+    payload read, the latency spun first; batches identical to the oracle."""
+    import time
+
+    path = tmp_path / "d.bbox"
+    bx.write_dataset(bx.SyntheticImageSource(64, 24, 20, 3, seed=4), path,
+                     bx.WriterConfig(seed=1, page_size=65536, compress_probability=0.5))
+    lat = 0.002
+    ds = bx.open_dataset(path, bx.Direct(read_latency_s=lat))
+    assert ds.io_read_count == 1
+    cfg = bx.LoaderConfig(batch_size=16, order=bx.OrderKind.RANDOM, seed=5,
+                          pipelines={"image": bx.parse_pipeline("crop:16,16|flip:0.5")})
+    t0 = time.perf_counter()
+    with bx.Loader(ds, cfg) as loader:
+        got = [(list(b.indices), b["image"].cpu().numpy()) for b in loader.iterate_epoch(0)]
+    el = time.perf_counter() - t0
+    assert ds.io_read_count == 1 + 64
+    assert el >= 64 * lat / (os_cpu := __import__("os").cpu_count() or 1)   # spun on the staging threads
+    want = list(O.loader_batches(path, 16, "random", 5, 0, pipelines={"image": "crop:16,16|flip:0.5"}))
+    for (gi, gimg), (wi, wa) in zip(got, want):
+        assert gi == wi and np.array_equal(gimg, wa["image"])
+    before = ds.io_read_count
+    s = ds.get_sample(3)
+    assert ds.io_read_count == before + 1 and np.array_equal(s["image"], O.decode(*_cell4(ds, 3)))
+    ds.close()
+
+
+def _cell4(ds, i):
+    c = ds.cells(i)[0]
+    raw = np.frombuffer(open(ds.path, "rb").read()[c.offset:c.offset + c.length], dtype=np.uint8)
+    return c.height, c.width, c.channels, c.codec, raw
