@@ -426,6 +426,8 @@ def run_leg(name, args, device, rank, world, barrier, reduce_max, detail_rooflin
                   "pcie_h2d_peak_gbs": pcie, "pcie_roofline_images_per_s": roof_pcie,
                   "frac_pcie": e2e / world / roof_pcie,
                   "host_stage_ms_per_step": st2["stage_seconds"] / max(st2["batches"], 1) * 1e3,
+                  "numa_node": int(st2["numa_node"]), "staging_threads": int(st2["staging_threads"]),
+                  "staging_cpus": int(st2["staging_cpus"]),
                   "path": "Loader(OsCache): host RAM -> pinned slot -> H2D -> kernels"}
     out["clocks"] = clk.summary()
 

@@ -180,6 +180,9 @@ typedef struct {
   int64_t page_fetches;       /* page pool: pages fetched H2D (reader.py CacheStats.fetch_count) */
   int64_t page_reloads;       /* page pool: fetches of a page already fetched this epoch (reload_count) */
   int64_t io_reads;           /* Direct strategy: payload preads (reader.py io_read_count) */
+  int64_t numa_node;          /* the GPU's NUMA node (-1: unknown); staging threads + pinned slots live there */
+  int64_t staging_threads;    /* host gather threads */
+  int64_t staging_cpus;       /* CPUs those threads are bound to (this rank's slice of the node; 0: unbound) */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
  * RLE / JPEG fields, kernels read each sample's payload window straight from

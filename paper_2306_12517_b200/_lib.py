@@ -43,7 +43,7 @@ class LoaderStats(ctypes.Structure):
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
                 ("dma_batches", c_i64), ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
                 ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64),
-                ("io_reads", c_i64)]
+                ("io_reads", c_i64), ("numa_node", c_i64), ("staging_threads", c_i64), ("staging_cpus", c_i64)]
 
 
 # bbx_status -> exception class (errors.py:4-57)

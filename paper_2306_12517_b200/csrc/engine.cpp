@@ -56,6 +56,75 @@ Pool::~Pool() {
   cv_.notify_all();
   for (auto& t : workers_) t.join();
 }
+static bool set_affinity(pthread_t th, const std::vector<int>& cpus) {
+  if (cpus.empty()) return false;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  for (int c : cpus) if (c >= 0 && c < CPU_SETSIZE) CPU_SET(c, &set);
+  return pthread_setaffinity_np(th, sizeof set, &set) == 0;
+}
+void Pool::pin(const std::vector<int>& cpus) {
+  for (auto& t : workers_) set_affinity(t.native_handle(), cpus);
+}
+
+// NUMA placement.  The CPUs of the GPU's NUMA node (sysfs: the
+// PCI device's numa_node, the node's cpulist) that this process may run on;
+// with several ranks per node (torchrun LOCAL_RANK / LOCAL_WORLD_SIZE, GPUs
+// spread evenly over the nodes) each rank takes its own slice of them.
+// Empty when the topology is unknown (the threads then float).
+static std::vector<int> parse_cpulist(const std::string& s) {
+  std::vector<int> out;
+  size_t i = 0;
+  while (i < s.size()) {
+    char* end = nullptr;
+    const long a = std::strtol(s.c_str() + i, &end, 10);
+    if (end == s.c_str() + i) break;
+    long b = a;
+    i = (size_t)(end - s.c_str());
+    if (i < s.size() && s[i] == '-') { b = std::strtol(s.c_str() + i + 1, &end, 10); i = (size_t)(end - s.c_str()); }
+    for (long c = a; c <= b; ++c) out.push_back((int)c);
+    while (i < s.size() && (s[i] == ',' || s[i] == '\n' || s[i] == ' ')) ++i;
+  }
+  return out;
+}
+static std::string read_small(const std::string& path) {
+  FILE* f = std::fopen(path.c_str(), "r");
+  if (!f) return "";
+  char buf[4096];
+  const size_t n = std::fread(buf, 1, sizeof buf - 1, f);
+  std::fclose(f);
+  buf[n] = 0;
+  return buf;
+}
+static std::vector<int> gpu_local_cpus(int device, int* node_out) {
+  *node_out = -1;
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) { cudaGetLastError(); return {}; }
+  std::string id(bus);
+  for (auto& ch : id) ch = (char)std::tolower((unsigned char)ch);
+  const std::string ns = read_small("/sys/bus/pci/devices/" + id + "/numa_node");
+  if (ns.empty()) return {};
+  const int node = std::atoi(ns.c_str());
+  if (node < 0) return {};
+  *node_out = node;
+  std::vector<int> cpus = parse_cpulist(read_small("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist"));
+  cpu_set_t allowed;
+  if (sched_getaffinity(0, sizeof allowed, &allowed) == 0)
+    cpus.erase(std::remove_if(cpus.begin(), cpus.end(), [&](int c) { return c >= CPU_SETSIZE || !CPU_ISSET(c, &allowed); }),
+               cpus.end());
+  int nodes = 0;
+  for (int k = 0; k < 64; ++k)
+    if (!read_small("/sys/devices/system/node/node" + std::to_string(k) + "/cpulist").empty()) ++nodes;
+  const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+  const char* lr = std::getenv("LOCAL_RANK");
+  if (lws && lr && nodes > 0 && !cpus.empty()) {
+    const int per_node = std::max(1, std::atoi(lws) / nodes), slice = std::atoi(lr) % per_node;
+    const size_t n = cpus.size() / (size_t)per_node;
+    if (n > 0) cpus = std::vector<int>(cpus.begin() + (size_t)slice * n, cpus.begin() + (size_t)(slice + 1) * n);
+  }
+  return cpus;
+}
+
 void Pool::work(Job& job) {
   for (int64_t i; (i = job.next.fetch_add(1)) < job.n;) {
     (*job.fn)(i);
@@ -274,6 +343,8 @@ struct bbx_loader {
   bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
   bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
+  std::vector<int> local_cpus;        // the GPU's NUMA-node CPUs (this rank's slice); empty: unknown
+  int numa_node = -1;
   bool direct_io = false;             // Direct strategy (reader.py:61-65,368-372): one pread per payload read
   int64_t read_latency_ns = 0;        //   ... with the strategy's read latency spun before each read
   // HBM page pool (ProcessCacheStrategy with capacity < num_pages): executes the
@@ -909,7 +980,20 @@ static size_t jpeg_block_bytes(int B) { return jpeg_bprefix_off(B) + (size_t)(B 
 
 
 
+static int finalize_impl(bbx_loader* L);
+// Pinned staging memory is allocated (and first touched) with the calling
+// thread bound to the GPU's NUMA node, so the pages sit next to the GPU's PCIe
+// root: the gather writes them and the DMA reads them without crossing sockets.
 static int finalize(bbx_loader* L) {
+  if (L->finalized || L->local_cpus.empty()) return finalize_impl(L);
+  cpu_set_t old;
+  const bool have_old = pthread_getaffinity_np(pthread_self(), sizeof old, &old) == 0;
+  set_affinity(pthread_self(), L->local_cpus);
+  const int r = finalize_impl(L);
+  if (have_old) pthread_setaffinity_np(pthread_self(), sizeof old, &old);
+  return r;
+}
+static int finalize_impl(bbx_loader* L) {
   if (L->finalized) return BBX_OK;
   CK(cudaSetDevice(L->device));
   // slot layout: [idx: B*8][desc blocks per plan][one compact payload region]
@@ -1029,6 +1113,30 @@ static int finalize(bbx_loader* L) {
       }
     }
   }
+  // Staged loaders read payloads from the mmap: populate its page tables once,
+  // in parallel on the staging threads, when the file comfortably fits in RAM
+  // (MADV_POPULATE_READ), so batches do not pay a minor fault per 4 KiB page on
+  // the first touch of every sample (the OS page cache keeps the data; only the
+  // process's mapping is filled in).  Once per dataset.
+  if (!resident && !L->direct_io) {
+    bbx_dataset* ds = L->ds;
+    std::lock_guard<std::mutex> g(ds->reg_mu);
+    const long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
+    if (!ds->populated && (double)ds->map_len < 0.25 * (double)pages * (double)psz) {
+      const int64_t chunk = 64ll << 20, n = ((int64_t)ds->map_len + chunk - 1) / chunk;
+      L->pool->parallel_for(n, [&](int64_t c) {
+        const int64_t a = c * chunk, m = std::min<int64_t>(chunk, (int64_t)ds->map_len - a);
+#ifndef MADV_POPULATE_READ
+#define MADV_POPULATE_READ 22
+#endif
+        if (madvise((void*)(ds->map + a), (size_t)m, MADV_POPULATE_READ) != 0) {   // older kernels: touch
+          volatile uint8_t sink = 0;
+          for (int64_t q = 0; q < m; q += psz) sink ^= ds->map[a + q];
+        }
+      });
+      ds->populated = true;
+    }
+  }
   // Page-lock the mmap'd file once per dataset so the copy engine reads
   // payloads straight out of the page cache (no CPU gather).  Only when the
   // file comfortably fits in RAM; otherwise payloads are gathered by the pool.
@@ -1050,6 +1158,7 @@ static int finalize(bbx_loader* L) {
     L->dma = ds->dma_base() != nullptr;
   }
   L->th = std::thread(pipeline_loop, L);
+  set_affinity(L->th.native_handle(), L->local_cpus);
   L->finalized = true;
   return BBX_OK;
 }
@@ -1869,7 +1978,10 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) hc = std::max(1u, hc / (unsigned)std::max(1, std::atoi(e)));
     nt = (int)std::min<unsigned>(16, hc);
   }
+  L->local_cpus = gpu_local_cpus(device, &L->numa_node);
+  if (!L->local_cpus.empty()) nt = std::min<int>(nt, (int)L->local_cpus.size());
   L->pool = std::make_unique<Pool>(nt);
+  L->pool->pin(L->local_cpus);   // staging threads on the GPU's NUMA node
   if ((e = cudaStreamCreateWithFlags(&L->copy_st, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&L->comp_st[0], cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&L->comp_st[1], cudaStreamNonBlocking)) != cudaSuccess)
@@ -2147,6 +2259,9 @@ bbx_status bbx_loader_get_stats(const bbx_loader* L, bbx_loader_stats* out) {
   if (!L || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
   std::lock_guard<std::mutex> g(const_cast<bbx_loader*>(L)->stats_mu);
   *out = L->stats;
+  out->numa_node = L->numa_node;
+  out->staging_threads = L->pool ? L->pool->size() : 0;
+  out->staging_cpus = (int64_t)L->local_cpus.size();
   return BBX_OK;
 }
 bbx_status bbx_loader_reset_stats(bbx_loader* L) {

@@ -79,6 +79,7 @@ struct bbx_dataset {
   int resident_device = -1;
   uint8_t* d_heap = nullptr;   // device copy of [heap_offset, alloc_table_offset)
   bool host_registered = false; // the mmap is page-locked for DMA (cudaHostRegister)
+  bool populated = false;        // the mmap's page tables were filled in (staged loaders, engine.cpp finalize)
   uint8_t* h_heap = nullptr;     // pinned host copy of the heap (bbx_dataset_pin_host)
   uint8_t* h_heap_dev = nullptr; // its device-mapped address (zero-copy reads over PCIe)
   // DMA-able host address of file offset o: dma_base + o (registered mmap or pinned copy)
@@ -115,6 +116,8 @@ class Pool {
   // Runs fn(i) for i in [0, n) on the pool (and the caller); returns when done.
   void parallel_for(int64_t n, const std::function<void(int64_t)>& fn);
   int size() const { return (int)workers_.size() + 1; }
+  // Restrict the worker threads to `cpus` (NUMA placement of the staging gather).
+  void pin(const std::vector<int>& cpus);
 
  private:
   // One parallel_for call.  Each call owns its counters, so a worker that wakes
