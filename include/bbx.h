@@ -172,7 +172,6 @@ typedef struct {
   double kernel_seconds;
   int64_t kernel_timed;       /* kernel launches that were timed */
   int64_t kernel_bytes;       /* algorithmic bytes of the timed launches */
-  int64_t dma_batches;        /* batches whose payloads the copy engine read from the registered mmap */
   int64_t zero_copy_bytes;    /* payload bytes kernels read straight from pinned host memory over PCIe */
   double  gap_seconds;        /* profiling: compute-stream idle between consecutive timed batches */
   double  h2d_late_seconds;   /* profiling: part of that idle time spent waiting for the batch's H2D */
@@ -192,12 +191,11 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
 /* Loader tuning options (before the first submit; the defaults are the
  * measured-best settings):
  *   "window_staging"        1: stage only the rows x columns a RAW sample's chain reads
- *   "dma"                   1: let the copy engine read a registered host heap directly
  *   "jpeg_header_cache"     1: keep each JPEG sample's parsed header for later epochs
  *   "jpeg_header_prefetch"  1: parse the headers of this loader's samples up front
  *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
  *   "direct_io"             0: Direct strategy -- every payload read is one pread of the whole
- *                              payload (reader.py:368-372), no window staging, no DMA
+ *                              payload (reader.py:368-372), no window staging
  *   "read_latency_ns"       0: Direct: latency spun before each read (reader.py:369-370)
  *   "compute_streams"       2: consecutive batches alternate between two CUDA streams, so
  *                              one batch's kernels fill SMs the previous batch's tail leaves idle

@@ -41,7 +41,7 @@ class LoaderStats(ctypes.Structure):
     _fields_ = [("batches", c_i64), ("samples", c_i64), ("h2d_bytes", c_i64), ("d2h_bytes", c_i64),
                 ("kernel_launches", c_i64), ("stage_seconds", c_dbl), ("wait_seconds", c_dbl),
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
-                ("dma_batches", c_i64), ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
+                ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
                 ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64),
                 ("io_reads", c_i64), ("numa_node", c_i64), ("staging_threads", c_i64), ("staging_cpus", c_i64)]
 

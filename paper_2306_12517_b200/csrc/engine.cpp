@@ -340,8 +340,6 @@ struct bbx_loader {
   const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
   bool zc = false;                    // payload_dev is host memory (zero-copy)
   size_t pay_base = 0;                // start of the compact payload region
-  bool dma = false;                   // payloads DMA'd straight from the registered mmap (no CPU gather)
-  bool dma_allowed = true;           // DMA when the dataset exposes a DMA-able host copy
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
   std::vector<int> local_cpus;        // the GPU's NUMA-node CPUs (this rank's slice); empty: unknown
   int numa_node = -1;
@@ -1137,26 +1135,6 @@ static int finalize_impl(bbx_loader* L) {
       ds->populated = true;
     }
   }
-  // Page-lock the mmap'd file once per dataset so the copy engine reads
-  // payloads straight out of the page cache (no CPU gather).  Only when the
-  // file comfortably fits in RAM; otherwise payloads are gathered by the pool.
-  if (!resident && L->dma_allowed) {
-    bbx_dataset* ds = L->ds;
-    std::lock_guard<std::mutex> g(ds->reg_mu);
-    if (!ds->host_registered) {
-      long pages = sysconf(_SC_PHYS_PAGES), psz = sysconf(_SC_PAGE_SIZE);
-      double ram = (double)pages * (double)psz;
-      cudaError_t re = cudaErrorMemoryAllocation;
-      if (ram > 0 && (double)ds->map_len < 0.25 * ram)
-        re = cudaHostRegister((void*)ds->map, ds->map_len, cudaHostRegisterReadOnly | cudaHostRegisterPortable);
-      if (re == cudaSuccess) {
-        ds->host_registered = true;
-      } else {
-        cudaGetLastError();   // clear a refused registration; fall back to the gather pool
-      }
-    }
-    L->dma = ds->dma_base() != nullptr;
-  }
   L->th = std::thread(pipeline_loop, L);
   set_affinity(L->th.native_handle(), L->local_cpus);
   L->finalized = true;
@@ -1598,38 +1576,8 @@ static int process_slot(bbx_loader* L, int s) {
       T.up_quant = T.n_quant;
     }
   }
-  // DMA mode: the copy engine reads every payload / window straight from the
-  // registered mmap (one batched 2-D copy call); descriptors go in one H2D.
-  bool dma_done = false;
-  if (L->dma && !copies.empty()) {
-    std::vector<cudaMemcpy3DBatchOp> ops(copies.size());
-    for (size_t k = 0; k < copies.size(); ++k) {
-      const Copy& c = copies[k];
-      cudaMemcpy3DBatchOp& op = ops[k];
-      std::memset(&op, 0, sizeof op);
-      op.src.type = cudaMemcpyOperandTypePointer;
-      op.src.op.ptr.ptr = (void*)(L->ds->dma_base() + (c.src - L->ds->map));
-      op.src.op.ptr.rowLength = c.rows == 1 ? 0 : c.src_stride;
-      op.dst.type = cudaMemcpyOperandTypePointer;
-      op.dst.op.ptr.ptr = S.d_stage + (c.dst - S.h_stage);
-      op.dst.op.ptr.rowLength = 0;
-      op.extent = make_cudaExtent(c.row_bytes, c.rows, 1);
-      op.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      op.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    }
-    if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
-    CK(cudaMemcpyAsync(S.d_stage, S.h_stage, L->desc_bytes, cudaMemcpyHostToDevice, L->copy_st));
-    size_t fail_idx = 0;
-    cudaError_t e = cudaMemcpy3DBatchAsync(ops.size(), ops.data(), &fail_idx, 0, L->copy_st);
-    if (e == cudaSuccess) {
-      dma_done = true;
-    } else {
-      cudaGetLastError();
-      L->dma = false;   // unsupported here: gather on the host from now on
-    }
-  }
   // gather mode: mmap page cache -> pinned slot (row segments for windows)
-  if (!dma_done && !copies.empty() && L->direct_io) {   // Direct: pread each payload (whole, unwindowed)
+  if (!copies.empty() && L->direct_io) {   // Direct: pread each payload (whole, unwindowed)
     std::atomic<int> io_err{0};
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
@@ -1648,7 +1596,7 @@ static int process_slot(bbx_loader* L, int s) {
     if (io_err) return fail(BBX_INVALID_FILE, "%s: short read", ds->path.c_str());
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.io_reads += (int64_t)copies.size();
-  } else if (!dma_done && !copies.empty()) {
+  } else if (!copies.empty()) {
     const uint8_t* map_end = ds->map + ds->map_len;
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
@@ -1658,10 +1606,8 @@ static int process_slot(bbx_loader* L, int s) {
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // H2D on the copy stream (after the previous kernels reading d_stage)
   const size_t bytes = resident ? L->desc_bytes : cursor;
-  if (!dma_done) {
-    if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
-    CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
-  }
+  if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
+  CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
   CK(cudaEventRecord(S.h2d_done, L->copy_st));
   S.h2d_timed = false;
   if (L->profiling && L->prof_every == 1) {   // idle-gap attribution needs every batch timed
@@ -1805,7 +1751,6 @@ static int process_slot(bbx_loader* L, int s) {
     L->stats.d2h_bytes += d2h;
     L->stats.kernel_launches += launches;
     L->stats.stage_seconds += t1 - t0;
-    L->stats.dma_batches += dma_done ? 1 : 0;
     L->stats.zero_copy_bytes += zc_bytes;
   }
   return BBX_OK;
@@ -2241,11 +2186,10 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   if (L->finalized) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "loader already started");
   const std::string n(name);
   if (n == "window_staging") L->window_staging = value != 0;
-  else if (n == "dma") L->dma_allowed = value != 0;
   else if (n == "jpeg_header_cache") L->jpeg_cache = value != 0;
   else if (n == "jpeg_roi") L->jpeg_roi = value != 0;
   else if (n == "jpeg_header_prefetch") L->jpeg_prefetch = value != 0;
-  else if (n == "direct_io") { L->direct_io = value != 0; if (L->direct_io) { L->window_staging = false; L->dma_allowed = false; } }
+  else if (n == "direct_io") { L->direct_io = value != 0; if (L->direct_io) { L->window_staging = false; } }
   else if (n == "read_latency_ns") L->read_latency_ns = value > 0 ? value : 0;
   else if (n == "compute_streams") {
     if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);

@@ -78,12 +78,9 @@ struct bbx_dataset {
   const uint8_t* rows = nullptr;
   int resident_device = -1;
   uint8_t* d_heap = nullptr;   // device copy of [heap_offset, alloc_table_offset)
-  bool host_registered = false; // the mmap is page-locked for DMA (cudaHostRegister)
   bool populated = false;        // the mmap's page tables were filled in (staged loaders, engine.cpp finalize)
   uint8_t* h_heap = nullptr;     // pinned host copy of the heap (bbx_dataset_pin_host)
   uint8_t* h_heap_dev = nullptr; // its device-mapped address (zero-copy reads over PCIe)
-  // DMA-able host address of file offset o: dma_base + o (registered mmap or pinned copy)
-  const uint8_t* dma_base() const { return h_heap ? h_heap - heap_offset : (host_registered ? map : nullptr); }
   std::mutex reg_mu;
   ~bbx_dataset() {
     if (map) munmap((void*)map, map_len);

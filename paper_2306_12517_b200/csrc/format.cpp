@@ -130,7 +130,6 @@ int dataset_open(const char* path, bbx_dataset** out) {
 void dataset_close(bbx_dataset* ds) {
   if (!ds) return;
   if (ds->d_heap) { cudaSetDevice(ds->resident_device); cudaFree(ds->d_heap); }
-  if (ds->host_registered) cudaHostUnregister((void*)ds->map);
   if (ds->h_heap) cudaFreeHost(ds->h_heap);
   delete ds;   // ~bbx_dataset unmaps and closes
 }
