@@ -544,19 +544,25 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 // Compute: the 2-tap horizontal sums of a source row are formed when the row
 // first appears for its parity (even / odd absolute row: the two taps of an
 // output row are always one of each), with byte-pair dot products (dp2a) on
-// funnel-shifted words, and kept in registers as
-//     nhe = -h(even row),  D = h(odd row) - h(even row),  Ce = 8192 h(even) + 2^23
-// so the vertical blend is ONE integer multiply-add per value,
-//     s = Ce + 4 w_odd D = 4 (w_even h_even + w_odd h_odd + 2^21),   u = s >> 24,
+// funnel-shifted words, and kept in registers (h_even, h_odd per value).  The
+// copy warp mirrors which rows the compute warps hold and flags, per output row,
+// the parities whose row is new, so the compute loop does no tag bookkeeping.
+// The vertical blend is two integer multiply-adds per value,
+//     s = 4 w_even h_even + 4 w_odd h_odd + 2^23 = 4 (w_even h_even + w_odd h_odd + 2^21),  u = s >> 24,
 // the same integer the tile kernel / oracle form ((w0 h0 + w1 h1 + 2^21) >> 22,
-// bit for bit).  Row tags are absolute source rows, so a row shared by two
-// consecutive tiles of a sample is not summed twice.  u -> output: f16 / bf16
-// through a per-channel f32 affine map fma(u, A, B) that the host proved equal
-// to the exact value table for all 256 inputs (packed f32x2 math, no shared-
-// memory table), else the table; packed 32-bit stores.
+// bit for bit).  When a sample's row stride is a multiple of 4 every staged row
+// has the same byte phase mod 4, so the column table carries it and a tap's
+// bytes are three aligned shared loads at row + column offset.  u -> output:
+// f16 / bf16 through a per-channel f32 affine map fma(u, A, B) that the host
+// proved equal to the exact value table for all 256 inputs (packed f32x2 math,
+// no shared-memory table), else the table; packed 32-bit stores.
 enum CwMode : int { CW_COPY = 0, CW_LUT = 1, CW_AFFINE = 2 };
-constexpr uint32_t kCwFake = 0xFFFEu;       // tag of a weight-0 parity (never a real row: heights < 0xFFFE)
-constexpr uint32_t kCwReset = 0xFFFFFFFFu;  // tags after a sample change: match nothing
+constexpr int kK1Unroll = 2;                // row loop unroll (A/B: 1 / 2 / 4 -> 45.3 / 44.9 / 45.1 us under ncu)
+// one bulk copy per source row when the window is narrower than half the row stride,
+// else one copy of the whole row range (fewer serialised copy issues in the copy warp)
+constexpr int kCwPerRowNum = 8, kCwPerRowDen = 4;
+constexpr uint32_t kCwFake = 0xFFFEu;       // a parity with weight 0 in this output row (never a real row: heights < 0xFFFE)
+constexpr uint32_t kCwNone = 0xFFFFFFFFu;   // no source row held (start of a sample)
 
 __host__ __device__ inline int cw_span_pad(const PlanDev& P) { return align_up(P.src_row_w * P.channels, 16) + 32; }
 __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
@@ -637,24 +643,12 @@ template <> __device__ __forceinline__ uint32_t cvt_pack2<__nv_bfloat16>(unsigne
   return d;
 }
 
-// Horizontal 2-tap sums of one source pixel's three channels: bytes a0 a1 a2 b0 b1 b2 at stage byte `a`
-// (b = the second tap's pixel, 3 bytes on; sel picks a's bytes twice when both taps are one column).
-struct CwTap {
-  uint32_t p1, p2;   // {a0, b0, a1, b1}, {a2, b2, -, -}
-};
-__device__ __forceinline__ CwTap cw_bytes(const uint8_t* stage, uint32_t a, uint32_t sel1, uint32_t sel2) {
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(stage + (a & ~3u));
-  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-  const uint32_t x = __funnelshift_r(w0, w1, a << 3), y = __funnelshift_r(w1, w2, a << 3);
-  return CwTap{__byte_perm(x, y, sel1), __byte_perm(x, y, sel2)};
-}
-
 template <typename OutT, int kMode>
 __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, const LaunchArgs A) {
   constexpr int C = 3;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = P.cw_warps;                          // compute warps 0..ncw-1; warp ncw issues the copies
-  const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile, owp = tab_owp(P);
+  const int OW = P.out_w, tps = P.tiles_per_sample, Rt = P.rows_per_tile;
   const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P), span_pad = cw_span_pad(P);
   const int tap_off = cw_tap_off(P);
   // tickets: the first `nrun` hand out runs of cw_run consecutive tiles (sample-major
@@ -668,7 +662,8 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + cw_bar_off(P));   // full[NS], empty[NS]
   uint64_t* empty = full + NS;
   uint8_t* metas = smem + cw_stage_off(P);              // geometry ring: tile k uses entry k % NR
-  uint8_t* stages = metas + NR * meta;                  // source rows: tile k uses stage k % NS
+  const uint32_t stage0 = (uint32_t)(cw_stage_off(P) + NR * meta);   // source rows: tile k uses stage k % NS
+  uint8_t* stages = smem + stage0;
 
   if (tid == 0) {
 #pragma unroll
@@ -682,18 +677,29 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
     // k - 1 waited for tile k - 1 - NS), then, once the compute warps have
     // released tile k - NS's stage, its source rows -> stage k % NS (nslot <= 32)
     int k = 0, m = 0, b = 0, ph = 0;                   // ph: parity of stage b's use count
-    int t = 0, left = 0;                               // next tile, tiles left in the current run
+    int left = 0, s = 0, tile = 0, t_id = 0;           // the run being handed out: tiles left, next tile
     int cur_s = -1, col_lo = 0, span_bytes = 0;        // the sample whose column table was last written
+    bool aligned = false;                              // its rows share one byte phase mod 4
+    int bx0 = 0, bxs = 1, by0 = 0;                     // its x / y maps when they are affine (no Resize)
+    uint32_t held_e = kCwNone, held_o = kCwNone;       // mirror: the source rows whose sums the compute warps hold
+    int loaded_s = -1, top = 0, ch = 0;                // the sample whose descriptor fields are cached below
+    bool s_skip = true;
+    SrcRows S{};
+    bool affine = true;                                // crops / flips only: back_x, back_y are +-1 slopes
+    for (int i = 0; i < P.n_remaps; ++i) affine = affine && P.remaps[i].kind != BBX_OP_RESIZE;
+    // the next run's ticket is fetched while the current run is handed out
+    unsigned long long next_u = blockIdx.x;
     for (;; ++k, m = m == NR - 1 ? 0 : m + 1) {
       if (k > 0 && ++b == NS) { b = 0; ph ^= 1; }
+      bool done = false;
       if (left == 0) {
-        unsigned long long u = blockIdx.x;
-        if (k > 0) {
-          if (lane == 0) u = G + atomicAdd(&A.ticket[0], 1ull);
-          u = __shfl_sync(0xffffffffu, u, 0);
-        }
+        const unsigned long long u = next_u;
+        if (lane == 0) next_u = G + atomicAdd(&A.ticket[0], 1ull);   // consumed when this run ends
+        next_u = __shfl_sync(0xffffffffu, next_u, 0);
+        int t;
         if (u >= (unsigned long long)ntickets) {
-          t = -1;
+          done = true;
+          t = 0;
         } else if (u < (unsigned long long)nrun) {
           t = (int)u * run;
           left = run;
@@ -701,9 +707,12 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
           t = head + (int)(u - nrun);
           left = 1;
         }
+        s = t / tps;
+        tile = t - s * tps;
+        t_id = t;
       }
       int32_t* hdr = reinterpret_cast<int32_t*>(metas + m * meta);
-      if (t < 0) {                                     // no tiles left: a stop entry for the compute warps
+      if (done) {                                      // no tiles left: a stop entry for the compute warps
         if (k >= NS) mbar_wait(&empty[b], ph ^ 1);
         if (lane == 0) {
           hdr[0] = -1;
@@ -718,15 +727,24 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         }
         break;
       }
-      const int s = t / tps, tile = t - s * tps;
-      ++t;
+      const int this_id = t_id, this_tile = tile;
+      const int cs = s;
       --left;
-      const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)s * P.desc_stride);
-      const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
-      const bool live = !d->skip && R > 0;
-      if (tile == 0 && lane < A.sc.n_fields) {         // the batch's scalar fields, once per sample
-        const int64_t i = A.sc.idx[s];
-        A.sc.outs[lane][s] = A.sc.cols[lane][i];
+      ++t_id;
+      if (++tile == tps) { tile = 0; ++s; }
+      const SampleDesc* d = reinterpret_cast<const SampleDesc*>(A.desc + (size_t)cs * P.desc_stride);
+      const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
+      if (cs != loaded_s) {                            // the sample's descriptor, once per sample
+        s_skip = d->skip != 0;
+        S = src_rows_of(P, A, d, cs);
+        top = prm[0]; ch = prm[2];
+        loaded_s = cs;
+      }
+      const int r0 = this_tile * Rt, R = min(Rt, P.out_h - r0);
+      const bool live = !s_skip && R > 0;
+      if (this_tile == 0 && lane < A.sc.n_fields) {    // the batch's scalar fields, once per sample
+        const int64_t i = A.sc.idx[cs];
+        A.sc.outs[lane][cs] = A.sc.cols[lane][i];
       }
       int newxt = 0, ncopy = 0;
       bool per_row = false;
@@ -735,31 +753,40 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
       if (live) {
         uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
         uint4* taps = reinterpret_cast<uint4*>(metas + m * meta + tap_off);
-        const int32_t* prm = reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(d) + kDescHeader);
-        const SrcRows S = src_rows_of(P, A, d, s);
-        const int top = prm[0], ch = prm[2], sh = S.sh;
-        if (s != cur_s) {   // a CTA's tiles of one sample are consecutive: the column table once per sample
+        const int sh = S.sh;
+        if (cs != cur_s) {   // a CTA's tiles of one sample are consecutive: the column table once per sample
           const int lft = prm[1], cwd = prm[3];
-          const int xa = back_x(P, prm, 0), xb = back_x(P, prm, OW - 1);
+          if (affine) {
+            bx0 = back_x(P, prm, 0);
+            bxs = back_x(P, prm, 1) - bx0;
+            by0 = back_y(P, prm, 0);
+          }
+          const int xa = affine ? bx0 : back_x(P, prm, 0), xb = affine ? bx0 + bxs * (OW - 1) : back_x(P, prm, OW - 1);
           int a0, a1, aw, b0, b1, bw;   // the composed maps are monotone: the end columns span the range
           lin_axis(min(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, a0, a1, aw);
           lin_axis(max(xa, xb), P.canvas_w, cwd, P.lin32, P.linx_magic, b0, b1, bw);
           col_lo = (lft + a0) >> sh;
           const int col_hi = (lft + b1) >> sh;
           span_bytes = col_hi >= col_lo ? (col_hi - col_lo + 1) * C : 0;
+          // a row stride that is a multiple of 4 gives every staged row of the sample the
+          // same byte phase mod 4 (the stage keeps the global phase mod 16): the column
+          // table then carries it, and row offsets are word aligned
+          aligned = (S.rstride & 3) == 0;
+          const uint32_t ph4 = aligned ? (uint32_t)((reinterpret_cast<uintptr_t>(S.base) + (uintptr_t)col_lo * C) & 3u) : 0u;
           for (int ox = lane; ox < OW; ox += 32) {
             int x0, x1, wx;
-            lin_axis(back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
+            lin_axis(affine ? bx0 + bxs * ox : back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
             const int c0 = (lft + x0) >> sh, c1 = (lft + x1) >> sh;
-            xt[ox] = (uint32_t)((c0 - col_lo) * C) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+            xt[ox] = ((uint32_t)((c0 - col_lo) * C) + ph4) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
           }
-          cur_s = s;
+          cur_s = cs;
           newxt = 1;
+          held_e = held_o = kCwNone;
         }
         int ya = 0, yb = 0, wy = 0;
         if (lane < R) {
           int y0, y1;
-          lin_axis(back_y(P, prm, r0 + lane), P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
+          lin_axis(affine ? by0 + r0 + lane : back_y(P, prm, r0 + lane), P.canvas_h, ch, P.lin32, P.liny_magic, y0, y1, wy);
           ya = (top + y0) >> sh;
           yb = (top + y1) >> sh;
         }
@@ -769,7 +796,7 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         ncopy = span_bytes > 0 ? max(0, min(min(hi - lo + 1, nslot), S.rows - lo)) : 0;
         const uint32_t rstr = (uint32_t)S.rstride;
         // one copy per row when whole-row copies would move >= 25 % more bytes than the window
-        per_row = ncopy > 1 && 4ull * rstr > 5ull * (uint64_t)(span_bytes + 16);
+        per_row = ncopy > 1 && (uint64_t)kCwPerRowDen * rstr > (uint64_t)kCwPerRowNum * (uint64_t)(span_bytes + 16);
         const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)(lo + lane) * S.rstride + (int64_t)col_lo * C);
         uint32_t my_base;                              // stage offset of slot `lane`'s column col_lo
         if (per_row) {
@@ -786,26 +813,43 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
           if (ncopy > 0) tx = (uint32_t)((base0 + (uint64_t)(ncopy - 1) * rstr + span_bytes + 15) & ~(uint64_t)15);
           src0 = reinterpret_cast<const uint8_t*>(al);
         }
+        if (aligned) my_base &= ~3u;                   // the phase is in the column table
         const int ra = lane < R ? ya - lo : 0, rb = lane < R ? yb - lo : 0;
         const uint32_t ba = __shfl_sync(0xffffffffu, my_base, ra), bb = __shfl_sync(0xffffffffu, my_base, rb);
+        // the two taps are one even and one odd absolute row (yb == ya + 1), or one row twice (bottom /
+        // top clamp, or subsampled rows): that row takes all the weight, the other parity none
+        uint32_t be = 0, bo = 0, te = kCwFake, to = kCwFake, wo = 0;
         if (lane < R) {
-          // the two taps are one even and one odd absolute row (yb == ya + 1), or one row twice (bottom /
-          // top clamp, or subsampled rows): that row takes all the weight, the other parity a fake tag
-          uint32_t be, bo, te, to, wo;
           if (ya == yb) {
             be = bo = ba;
-            if (ya & 1) { te = kCwFake; to = (uint32_t)ya; wo = 2048u; }
-            else { te = (uint32_t)ya; to = kCwFake; wo = 0u; }
+            if (ya & 1) { to = (uint32_t)ya; wo = 2048u; }
+            else te = (uint32_t)ya;
           } else if (ya & 1) {
             bo = ba; be = bb; to = (uint32_t)ya; te = (uint32_t)yb; wo = 2048u - (uint32_t)wy;
           } else {
             be = ba; bo = bb; te = (uint32_t)ya; to = (uint32_t)yb; wo = (uint32_t)wy;
           }
-          taps[lane] = make_uint4(be, bo, te | to << 16, 4u * wo);
+        }
+        // new-row flags: a row is summed when it differs from the one the compute
+        // warps hold for its parity (the last real row before it, this tile or the
+        // sample's previous tiles in this CTA)
+        const uint32_t me = __ballot_sync(0xffffffffu, te != kCwFake), mo = __ballot_sync(0xffffffffu, to != kCwFake);
+        const uint32_t below = (1u << lane) - 1u, je = me & below, jo = mo & below;
+        const uint32_t pe_l = __shfl_sync(0xffffffffu, te, je ? 31 - __clz(je) : 0);
+        const uint32_t po_l = __shfl_sync(0xffffffffu, to, jo ? 31 - __clz(jo) : 0);
+        const uint32_t pe = je ? pe_l : held_e, po = jo ? po_l : held_o;
+        const uint32_t he_l = __shfl_sync(0xffffffffu, te, me ? 31 - __clz(me) : 0);
+        const uint32_t ho_l = __shfl_sync(0xffffffffu, to, mo ? 31 - __clz(mo) : 0);
+        if (me) held_e = he_l;
+        if (mo) held_o = ho_l;
+        if (lane < R) {
+          const uint32_t fl = (te != kCwFake && te != pe ? 1u : 0u) | (to != kCwFake && to != po ? 2u : 0u);
+          const uint32_t sb = stage0 + (uint32_t)b * (uint32_t)sbytes;
+          taps[lane] = make_uint4(sb + be, sb + bo, fl, 4u * wo);
         }
       }
       if (lane == 0) {
-        hdr[0] = t - 1; hdr[1] = s; hdr[2] = live ? 1 : 0; hdr[3] = newxt;
+        hdr[0] = this_id; hdr[1] = cs; hdr[2] = live ? 1 : 0; hdr[3] = newxt | (aligned ? 2 : 0);
       }
       if (k >= NS) mbar_wait(&empty[b], ph ^ 1);      // the previous use's release
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -847,113 +891,110 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
     }
   }
   const unsigned long long magic2 = f2_pack(8388608.0f, 8388608.0f);
-  uint32_t off[2] = {0, 0}, wp[2] = {0, 0}, wn[2] = {0, 0}, sel1[2] = {0, 0}, sel2[2] = {0, 0};
-  int nhe[6], dd[6];
-  uint32_t ce[6];
+  // per owned column q: byte offset of its left tap in a staged row (word offset + shift
+  // when the sample's rows are word aligned), tap weights, byte selectors
+  uint32_t off[2] = {0, 0}, shf[2] = {0, 0}, wp[2] = {0, 0}, sel1[2] = {0, 0}, sel2[2] = {0, 0};
+  uint32_t he[6], ho[6];                               // horizontal sums of the held even / odd source row
 #pragma unroll
-  for (int v = 0; v < 6; ++v) { nhe[v] = 0; dd[v] = 0; ce[v] = 0; }
-  uint32_t tags = kCwReset;
+  for (int v = 0; v < 6; ++v) { he[v] = 0; ho[v] = 0; }
+  bool al = false;
   for (int m = 0, b = 0, ph = 0;; m = m == NR - 1 ? 0 : m + 1) {
     mbar_wait(&full[b], ph);
     const int4 hd = *reinterpret_cast<const int4*>(metas + m * meta);   // ordered by the mbarrier wait (acquire)
     if (hd.x < 0) break;                               // the copy warp's stop entry
     if (hd.z && act) {
       const uint8_t* ent = metas + m * meta;
-      if (hd.w) {                                      // first tile of a sample: its column table
+      if (hd.w & 1) {                                  // first tile of a sample: its column table
         const uint32_t* xt = reinterpret_cast<const uint32_t*>(ent + 16);
+        al = (hd.w & 2) != 0;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const uint32_t e = xt[min(ox0 + q, OW - 1)];
           const uint32_t w1 = (e >> 16) & 0xFFFu, w0 = 2048u - w1;
-          off[q] = e & 0xFFFFu;
+          const uint32_t o = e & 0xFFFFu;
+          off[q] = al ? (o & ~3u) : o;
+          shf[q] = (o & 3u) * 8u;
           wp[q] = w0 | w1 << 16;
-          wn[q] = ((0u - w0) & 0xFFFFu) | (0u - w1) << 16;
           const bool same = (e >> 28) != 0;
           sel1[q] = same ? 0x1100u : 0x4130u;
           sel2[q] = same ? 0x0022u : 0x0052u;
         }
-        tags = kCwReset;
       }
       const int s = hd.y, tile = hd.x - s * tps;
       const int r0 = tile * Rt, R = min(Rt, P.out_h - r0);
       const uint4* taps = reinterpret_cast<const uint4*>(ent + tap_off);
-      const uint8_t* stage = stages + (size_t)b * sbytes;
       OutT* obase = reinterpret_cast<OutT*>(A.out) + ((size_t)s * P.out_h + r0) * ostep + (size_t)ox0 * C;
-      auto rows = [&](auto kvec) {
-      constexpr bool kV = decltype(kvec)::value;
-      uint4 tn = taps[0];
-      OutT* o = obase;
-      for (int r = 0; r < R; ++r, o += ostep) {
-        const uint4 tp = tn;
-        if (r + 1 < R) tn = taps[r + 1];               // next row's taps, one row ahead
-        const uint32_t dt = tp.z ^ tags;
-        tags = tp.z;
-        if (dt & 0xFFFFu) {                            // a new even row
+      auto rows = [&](auto kvec, auto kal) {
+        constexpr bool kV = decltype(kvec)::value, kA = decltype(kal)::value;
+        // the three channel sums of column q's two taps in the row at smem byte `a`
+        auto sums = [&](uint32_t row, int q, uint32_t* h) {
+          const uint32_t a = row + off[q];
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(smem + (kA ? a : (a & ~3u)));
+          const uint32_t sa = kA ? shf[q] : (a << 3);
+          const uint32_t x = __funnelshift_r(w[0], w[1], sa), y = __funnelshift_r(w[1], w[2], sa);
+          const uint32_t p1 = __byte_perm(x, y, sel1[q]), p2 = __byte_perm(x, y, sel2[q]);   // {a0 b0 a1 b1}, {a2 b2}
+          h[0] = (uint32_t)dp2a_lo(wp[q], p1, 0);
+          h[1] = (uint32_t)dp2a_hi(wp[q], p1, 0);
+          h[2] = (uint32_t)dp2a_lo(wp[q], p2, 0);
+        };
+        OutT* o = obase;
+#pragma unroll (kK1Unroll)
+        for (int r = 0; r < R; ++r, o += ostep) {
+          const uint4 tp = taps[r];
+          if (tp.z & 1u) { sums(tp.x, 0, he); sums(tp.x, 1, he + 3); }   // a new even source row
+          if (tp.z & 2u) { sums(tp.y, 0, ho); sums(tp.y, 1, ho + 3); }   // a new odd source row
+          const uint32_t wo4 = tp.w, we4 = 8192u - tp.w;
+          uint32_t u[6];                               // 4 (w_e h_e + w_o h_o + 2^21): the value in bits 24..31
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const CwTap h = cw_bytes(stage, tp.x + off[q], sel1[q], sel2[q]);
-            const int n0 = dp2a_lo(wn[q], h.p1, 0), n1 = dp2a_hi(wn[q], h.p1, 0), n2 = dp2a_lo(wn[q], h.p2, 0);
-            dd[3 * q] += n0 - nhe[3 * q]; dd[3 * q + 1] += n1 - nhe[3 * q + 1]; dd[3 * q + 2] += n2 - nhe[3 * q + 2];
-            nhe[3 * q] = n0; nhe[3 * q + 1] = n1; nhe[3 * q + 2] = n2;
-          }
+          for (int v = 0; v < 6; ++v) u[v] = he[v] * we4 + ho[v] * wo4 + (1u << 23);
+          if constexpr (kMode == CW_AFFINE) {
+            uint32_t pk[3];
 #pragma unroll
-          for (int v = 0; v < 6; ++v) ce[v] = (uint32_t)nhe[v] * 0xFFFFE000u + (1u << 23);   // -8192 nhe + 2^23
-        }
-        if (dt >> 16) {                                // a new odd row
+            for (int p = 0; p < 3; ++p) {
+              const unsigned long long x = f2_pack(__uint_as_float(u8_magic(u[2 * p])),
+                                                   __uint_as_float(u8_magic(u[2 * p + 1])));
+              pk[p] = cvt_pack2<OutT>(f2_fma(f2_sub(x, magic2), ab[p], bb[p]));
+            }
+            if constexpr (kV) {
+              uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+              o32[0] = pk[0]; o32[1] = pk[1]; o32[2] = pk[2];
+            } else {
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const CwTap h = cw_bytes(stage, tp.y + off[q], sel1[q], sel2[q]);
-            dd[3 * q] = dp2a_lo(wp[q], h.p1, nhe[3 * q]);
-            dd[3 * q + 1] = dp2a_hi(wp[q], h.p1, nhe[3 * q + 1]);
-            dd[3 * q + 2] = dp2a_lo(wp[q], h.p2, nhe[3 * q + 2]);
-          }
-        }
-        uint32_t u[6];                                 // 4 (w_e h_e + w_o h_o + 2^21): the value in bits 24..31
-#pragma unroll
-        for (int v = 0; v < 6; ++v) u[v] = ce[v] + tp.w * (uint32_t)dd[v];
-        if constexpr (kMode == CW_AFFINE) {
-          uint32_t pk[3];
-#pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            const unsigned long long x = f2_pack(__uint_as_float(u8_magic(u[2 * p])),
-                                                 __uint_as_float(u8_magic(u[2 * p + 1])));
-            pk[p] = cvt_pack2<OutT>(f2_fma(f2_sub(x, magic2), ab[p], bb[p]));
-          }
-          if constexpr (kV) {
-            uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
-            o32[0] = pk[0]; o32[1] = pk[1]; o32[2] = pk[2];
+              for (int v = 0; v < 6; ++v)
+                if (v < nval) {
+                  const uint16_t h = (uint16_t)(pk[v >> 1] >> (16 * (v & 1)));
+                  memcpy(o + v, &h, 2);
+                }
+            }
           } else {
+            OutT val[6];
 #pragma unroll
-            for (int v = 0; v < 6; ++v)
-              if (v < nval) {
-                const uint16_t h = (uint16_t)(pk[v >> 1] >> (16 * (v & 1)));
-                memcpy(o + v, &h, 2);
-              }
-          }
-        } else {
-          OutT val[6];
+            for (int v = 0; v < 6; ++v) {
+              if constexpr (kMode == CW_LUT) val[v] = lut[(v % 3) * 256 + (u[v] >> 24)];
+              else val[v] = (OutT)(u[v] >> 24);
+            }
+            if constexpr (kV && sizeof(OutT) <= 4) {
+              using PT = typename std::conditional<sizeof(OutT) == 1, uint16_t,
+                         typename std::conditional<sizeof(OutT) == 2, uint32_t, uint2>::type>::type;
+              PT w3[3];
+              memcpy(w3, val, sizeof w3);
+              PT* op = reinterpret_cast<PT*>(o);
+              op[0] = w3[0]; op[1] = w3[1]; op[2] = w3[2];
+            } else {
 #pragma unroll
-          for (int v = 0; v < 6; ++v) {
-            if constexpr (kMode == CW_LUT) val[v] = lut[(v % 3) * 256 + (u[v] >> 24)];
-            else val[v] = (OutT)(u[v] >> 24);
-          }
-          if constexpr (kV && sizeof(OutT) <= 4) {
-            using PT = typename std::conditional<sizeof(OutT) == 1, uint16_t,
-                       typename std::conditional<sizeof(OutT) == 2, uint32_t, uint2>::type>::type;
-            PT w3[3];
-            memcpy(w3, val, sizeof w3);
-            PT* op = reinterpret_cast<PT*>(o);
-            op[0] = w3[0]; op[1] = w3[1]; op[2] = w3[2];
-          } else {
-#pragma unroll
-            for (int v = 0; v < 6; ++v)
-              if (v < nval) o[v] = val[v];
+              for (int v = 0; v < 6; ++v)
+                if (v < nval) o[v] = val[v];
+            }
           }
         }
-      }
       };
-      if (vec) rows(std::true_type{});
-      else rows(std::false_type{});
+      if (vec) {
+        if (al) rows(std::true_type{}, std::true_type{});
+        else rows(std::true_type{}, std::false_type{});
+      } else {
+        if (al) rows(std::false_type{}, std::true_type{});
+        else rows(std::false_type{}, std::false_type{});
+      }
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
