@@ -30,7 +30,8 @@ constexpr int kCwStages = BBX_CW_STAGES;   // source-row pipeline stages
 constexpr int kCwRows = BBX_CW_ROWS;       // output rows per tile (fewer when a tile would span > 32 source rows)
 constexpr int kCwRun = BBX_CW_RUN;         // consecutive tiles per ticket
 constexpr int kThreads = 256;       // CTA size of the image kernels
-constexpr int kStreams = 2;         // compute streams a loader alternates its batches between
+constexpr int kStreams = 2;         // compute streams a loader alternates its batches between (A/B, configs[2]:
+                                    // 3 streams +3 % value but -20 % e2e, 4 streams slower on both)
 constexpr int kSmemTarget = 56 * 1024;   // 4 CTAs of 256 threads per SM
 constexpr int kSmemBudget = 200 * 1024;
 

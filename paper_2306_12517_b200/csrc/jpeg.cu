@@ -38,8 +38,8 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
 // (the block buffer is pre-zeroed).  Block ends read the next block's
 // component / offset / tables from a per-thread slot table in shared memory.
 constexpr int kHuffThreads = 256;           // 8 warps share one copy of the smem tables
-constexpr int kHuffCtasPerSm = 3;           // 24 warps per SM (<= 85 registers): a B200 holds 113k lanes,
-                                            // more than a batch of 1024 ImageNet-sized JPEGs has intervals
+constexpr int kHuffCtasPerSm = 3;           // a batch of 1024 ImageNet-sized JPEGs has ~110k intervals: ~3 CTAs
+                                            // per SM hold all of them at once (4 / 5 measured the same)
 constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
@@ -71,11 +71,14 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
       slow[i] = v;
     }
   }
-  // This CTA's intervals [c0, c0 + kHuffThreads), ordered longest first so
-  // that each warp decodes intervals of similar length (a warp runs until its
-  // longest lane finishes; interval lengths vary ~4x within an image).  Key:
-  // unstuffed bytes + 1 (0: outside the region of interest or a rejected
-  // sample: never decoded) | position.
+  // This CTA's intervals [c0, c0 + kHuffThreads) (A/B: taking every gridDim.x-th
+  // interval instead balances the CTAs -- J2 alone 295 -> 280 us -- but lowers the
+  // batch rate of the two-stream pipeline, 2.29 -> 2.24 M img/s, whose
+  // overlapping batches fill the SMs a contiguous J2 leaves idle at its end),
+  // ordered longest first so that each warp decodes intervals of similar length
+  // (a warp runs until its longest lane finishes; interval lengths vary ~4x
+  // within an image).  Key: stream bytes + 1 (0: outside the
+  // region of interest or a rejected sample: never decoded) | position.
   __shared__ uint32_t skey[kHuffThreads], ssamp[kHuffThreads];
   const uint32_t c0 = blockIdx.x * kHuffThreads;
   {
@@ -119,12 +122,10 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   // other word byte by byte -- 0xFF 0x00 is a data 0xFF, 0xFF + anything else
   // is a marker (the next RSTn, EOI, or corruption) after which zeros are
   // supplied (libjpeg's fill_bit_buffer rule; oracle/jpeg_oracle.c get_bit).
-  const uint4* p16 = nullptr;                        // last chunk loaded (nxt2)
-  const uint4* plast = nullptr;                      // chunk holding the sample's last scan byte
-  uint32_t lastn = 16;                               // scan bytes in *plast; later bytes read as 0xFF
-  uint4 cur = make_uint4(0, 0, 0, 0), nxt = cur, nxt2 = cur;   // two loads in flight hide L2 latency
+  const uint32_t* wp = nullptr;                      // next aligned stream word to load
+  uintptr_t wend = 0;                                // end of the sample's scan data (exclusive)
+  uint32_t qn = 0;                                   // the word loaded one refill ahead
   uint32_t qa = 0, qb = 0, sel = 0x0123;            // window of two aligned words, PRMT selector
-  int wci = 0;                                       // next word of `cur`
   bool carry = false, marker = false;               // pending 0xFF / marker reached
   uint64_t acc = 0;
   int nb = 0;
@@ -135,27 +136,22 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   int pred0 = 0, pred1 = 0, pred2 = 0;
   int16_t* cb = nullptr;
 
-  auto ld_chunk = [&](const uint4* p) -> uint4 {
-    if (p > plast) return make_uint4(~0u, ~0u, ~0u, ~0u);
-    uint4 v = __ldg(p);                             // L1-allocating: the line's next chunks hit
-    if (p == plast && lastn < 16) {                  // bytes past the scan data read as 0xFF (a marker)
-      const uint32_t n0 = min(lastn, 4u), n1 = lastn > 4 ? min(lastn - 4, 4u) : 0u,
-                     n2 = lastn > 8 ? min(lastn - 8, 4u) : 0u, n3 = lastn > 12 ? lastn - 12 : 0u;
-      auto keep = [](uint32_t w, uint32_t n) { return n >= 4 ? w : (w | (0xFFFFFFFFu << (8 * n))); };
-      v = make_uint4(keep(v.x, n0), keep(v.y, n1), keep(v.z, n2), keep(v.w, n3));
-    }
-    return v;
+  // one aligned stream word: a predicated L1-allocating load (no branch, so the
+  // lanes of a warp never diverge on it); bytes past the scan data read as 0xFF
+  // (a marker), and no byte past the word holding the last one is loaded
+  auto ld_word = [&](const uint32_t* p) -> uint32_t {
+    const intptr_t rem = (intptr_t)(wend - reinterpret_cast<uintptr_t>(p));
+    uint32_t w = ~0u;
+    if (rem > 0) w = __ldg(p);
+    return rem >= 4 ? w : (w | (~0u << (8 * (int)max(rem, (intptr_t)0))));
   };
-  auto next_word = [&]() -> uint32_t {
-    const uint32_t w = wci == 0 ? cur.x : (wci == 1 ? cur.y : (wci == 2 ? cur.z : cur.w));
-    if (++wci == 4) {
-      wci = 0; cur = nxt; nxt = nxt2; ++p16;
-      // the rotation reads nxt2, so the load it waits on must hit L1: the stream's
-      // line after next is prefetched when a chunk starts a 128-B line
-      if ((reinterpret_cast<uintptr_t>(p16) & 127) == 0 && p16 + 16 <= plast)
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 16));
-      nxt2 = ld_chunk(p16);
-    }
+  auto next_word = [&]() -> uint32_t {               // the next window word; the one after is loaded now
+    const uint32_t w = qn;
+    qn = ld_word(wp);
+    ++wp;
+    // the stream two lines ahead goes into L1 when a word starts a 128-B line
+    if ((reinterpret_cast<uintptr_t>(wp) & 127) == 0 && reinterpret_cast<uintptr_t>(wp + 64) < wend)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(wp + 64));
     return w;
   };
   auto comp_tables = [&]() {                         // ci, tdc, tac of block b
@@ -181,17 +177,12 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     cb = A.coef + (J.blk_base + (uint64_t)m * bpm) * 64;
     const uint8_t* base = A.payload + sdesc(A, s)->src;
     const uintptr_t a = reinterpret_cast<uintptr_t>(base + __ldg(&A.starts[t]));
-    const uintptr_t e = reinterpret_cast<uintptr_t>(base + J.scan_end);
-    plast = reinterpret_cast<const uint4*>((e - 1) & ~uintptr_t(15));
-    lastn = (uint32_t)(e - reinterpret_cast<uintptr_t>(plast));
-    p16 = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
-    if (p16 + 8 <= plast) asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 8));
-    if (p16 + 16 <= plast) asm volatile("prefetch.global.L1 [%0];" ::"l"(p16 + 16));
-    cur = ld_chunk(p16);
-    nxt = ld_chunk(p16 + 1);
-    p16 += 2;
-    nxt2 = ld_chunk(p16);
-    wci = (int)((a >> 2) & 3);
+    wend = reinterpret_cast<uintptr_t>(base + J.scan_end);
+    wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    if (reinterpret_cast<uintptr_t>(wp + 32) < wend) asm volatile("prefetch.global.L1 [%0];" ::"l"(wp + 32));
+    if (reinterpret_cast<uintptr_t>(wp + 64) < wend) asm volatile("prefetch.global.L1 [%0];" ::"l"(wp + 64));
+    qn = ld_word(wp);
+    ++wp;
     const uint32_t ph = (uint32_t)(a & 3);
     sel = (ph << 12) | ((ph + 1) << 8) | ((ph + 2) << 4) | (ph + 3);   // big-endian bytes ph..ph+3 of (qa, qb)
     qa = next_word();
@@ -649,6 +640,7 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   const unsigned hgrid = (unsigned)(((uint64_t)A.total_int + kHuffThreads - 1) / kHuffThreads);
   if (smem) {
     cudaFuncSetAttribute(jpeg_huffman_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
+    cudaFuncSetAttribute(jpeg_huffman_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     jpeg_huffman_kernel<true><<<hgrid, kHuffThreads, hsmem, st>>>(A);
   } else {
     cudaFuncSetAttribute(jpeg_huffman_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, hsmem);
