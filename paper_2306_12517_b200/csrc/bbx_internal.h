@@ -90,6 +90,9 @@ struct PlanDev {
   int32_t cw_run;                          // consecutive tiles a CTA takes per ticket
   int32_t cw_affine;                       // f16/bf16 values as fma(u, cw_aff_a[c], cw_aff_b[c]) (host-proven exact)
   float cw_aff_a[4], cw_aff_b[4];
+  // the same maps as the f32 pairs a compute thread's packed values use: channels (0,1) (2,0) (1,2)
+  alignas(8) float cw_pair_a[6];
+  alignas(8) float cw_pair_b[6];
   SmemLayout lay;
 };
 

@@ -428,6 +428,7 @@ static bool prove_affine(PlanDev& P, int C, const std::vector<uint8_t>& lut, int
     }
     if (!found) return false;
   }
+  for (int v = 0; v < 6; ++v) { P.cw_pair_a[v] = P.cw_aff_a[v % 3]; P.cw_pair_b[v] = P.cw_aff_b[v % 3]; }
   return true;
 }
 

@@ -594,6 +594,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t tx) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(tx) : "memory");
+}
 // 1-D bulk copy global -> shared (16-byte aligned ends, size a multiple of 16)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -749,12 +752,11 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
       int newxt = 0, ncopy = 0;
       bool per_row = false;
       const uint8_t* src0 = nullptr;                   // lane j: global address of slot j's first byte
-      uint32_t tx = 0, my_sz = 0;
+      uint32_t tx = 0, my_sz = 0, my_base_out = 0;
+      int ra = 0, rb = 0, ya_out = 0, yb_out = 0, wy_out = 0;
       if (live) {
-        uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
-        uint4* taps = reinterpret_cast<uint4*>(metas + m * meta + tap_off);
         const int sh = S.sh;
-        if (cs != cur_s) {   // a CTA's tiles of one sample are consecutive: the column table once per sample
+        if (cs != cur_s) {   // a CTA's tiles of one sample are consecutive: its column range once per sample
           const int lft = prm[1], cwd = prm[3];
           if (affine) {
             bx0 = back_x(P, prm, 0);
@@ -772,13 +774,6 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
           // same byte phase mod 4 (the stage keeps the global phase mod 16): the column
           // table then carries it, and row offsets are word aligned
           aligned = (S.rstride & 3) == 0;
-          const uint32_t ph4 = aligned ? (uint32_t)((reinterpret_cast<uintptr_t>(S.base) + (uintptr_t)col_lo * C) & 3u) : 0u;
-          for (int ox = lane; ox < OW; ox += 32) {
-            int x0, x1, wx;
-            lin_axis(affine ? bx0 + bxs * ox : back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
-            const int c0 = (lft + x0) >> sh, c1 = (lft + x1) >> sh;
-            xt[ox] = ((uint32_t)((c0 - col_lo) * C) + ph4) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
-          }
           cur_s = cs;
           newxt = 1;
           held_e = held_o = kCwNone;
@@ -795,7 +790,7 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
         ncopy = span_bytes > 0 ? max(0, min(min(hi - lo + 1, nslot), S.rows - lo)) : 0;
         const uint32_t rstr = (uint32_t)S.rstride;
-        // one copy per row when whole-row copies would move >= 25 % more bytes than the window
+        // one copy per row when the window is under half the row stride (kCwPerRowNum / Den)
         per_row = ncopy > 1 && (uint64_t)kCwPerRowDen * rstr > (uint64_t)kCwPerRowNum * (uint64_t)(span_bytes + 16);
         const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)(lo + lane) * S.rstride + (int64_t)col_lo * C);
         uint32_t my_base;                              // stage offset of slot `lane`'s column col_lo
@@ -814,7 +809,42 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
           src0 = reinterpret_cast<const uint8_t*>(al);
         }
         if (aligned) my_base &= ~3u;                   // the phase is in the column table
-        const int ra = lane < R ? ya - lo : 0, rb = lane < R ? yb - lo : 0;
+        ra = lane < R ? ya - lo : 0;
+        rb = lane < R ? yb - lo : 0;
+        my_base_out = my_base;
+        ya_out = ya; yb_out = yb; wy_out = wy;
+      }
+      // the tile's source rows go out first (the compute warps' release of tile
+      // k - NS's stage), the rest of its geometry is written while they are in
+      // flight; the full barrier completes on the bytes AND the arrive below
+      if (k >= NS) mbar_wait(&empty[b], ph ^ 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint8_t* srcbuf = stages + (size_t)b * sbytes;
+      if (tx) {
+        if (lane == 0) mbar_expect_tx(&full[b], tx);
+        __syncwarp();
+        if (per_row) {
+          if (lane < ncopy) bulk_g2s(srcbuf + (size_t)lane * span_pad, src0, my_sz, &full[b]);
+        } else if (lane == 0) {
+          bulk_g2s(srcbuf, src0, tx, &full[b]);
+        }
+      }
+      if (live) {
+        const int sh = S.sh;
+        if (newxt) {                                   // the column table of a new sample
+          uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
+          const int lft = prm[1], cwd = prm[3];
+          const uint32_t ph4 = aligned ? (uint32_t)((reinterpret_cast<uintptr_t>(S.base) + (uintptr_t)col_lo * C) & 3u) : 0u;
+          for (int ox = lane; ox < OW; ox += 32) {
+            int x0, x1, wx;
+            lin_axis(affine ? bx0 + bxs * ox : back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
+            const int c0 = (lft + x0) >> sh, c1 = (lft + x1) >> sh;
+            xt[ox] = ((uint32_t)((c0 - col_lo) * C) + ph4) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
+          }
+        }
+        uint4* taps = reinterpret_cast<uint4*>(metas + m * meta + tap_off);
+        const int ya = ya_out, yb = yb_out, wy = wy_out;
+        const uint32_t my_base = my_base_out;
         const uint32_t ba = __shfl_sync(0xffffffffu, my_base, ra), bb = __shfl_sync(0xffffffffu, my_base, rb);
         // the two taps are one even and one odd absolute row (yb == ya + 1), or one row twice (bottom /
         // top clamp, or subsampled rows): that row takes all the weight, the other parity none
@@ -851,19 +881,8 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
       if (lane == 0) {
         hdr[0] = this_id; hdr[1] = cs; hdr[2] = live ? 1 : 0; hdr[3] = newxt | (aligned ? 2 : 0);
       }
-      if (k >= NS) mbar_wait(&empty[b], ph ^ 1);      // the previous use's release
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      uint8_t* srcbuf = stages + (size_t)b * sbytes;
-      if (lane == 0) mbar_arrive_tx(&full[b], tx);
-      __syncwarp();
-      if (tx) {
-        if (per_row) {
-          if (lane < ncopy) bulk_g2s(srcbuf + (size_t)lane * span_pad, src0, my_sz, &full[b]);
-        } else if (lane == 0) {
-          bulk_g2s(srcbuf, src0, tx, &full[b]);
-        }
-      }
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[b])) : "memory");
     }
     return;
   }
@@ -886,8 +905,8 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
   if constexpr (kMode == CW_AFFINE) {
 #pragma unroll
     for (int p = 0; p < 3; ++p) {
-      ab[p] = f2_pack(P.cw_aff_a[(2 * p) % 3], P.cw_aff_a[(2 * p + 1) % 3]);
-      bb[p] = f2_pack(P.cw_aff_b[(2 * p) % 3], P.cw_aff_b[(2 * p + 1) % 3]);
+      ab[p] = reinterpret_cast<const unsigned long long*>(P.cw_pair_a)[p];   // distinct 64-bit pairs: no
+      bb[p] = reinterpret_cast<const unsigned long long*>(P.cw_pair_b)[p];   // per-row re-pairing of 3 floats
     }
   }
   const unsigned long long magic2 = f2_pack(8388608.0f, 8388608.0f);
