@@ -594,6 +594,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ uint4 lds_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(smem_u32(p)));
+  return v;
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t tx) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(tx) : "memory");
 }
@@ -959,7 +964,7 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         OutT* o = obase;
 #pragma unroll (kK1Unroll)
         for (int r = 0; r < R; ++r, o += ostep) {
-          const uint4 tp = taps[r];
+          const uint4 tp = lds_v4(taps + r);             // one 128-bit load (the compiler splits a plain one)
           if (tp.z & 1u) { sums(tp.x, 0, he); sums(tp.x, 1, he + 3); }   // a new even source row
           if (tp.z & 2u) { sums(tp.y, 0, ho); sums(tp.y, 1, ho + 3); }   // a new odd source row
           const uint32_t wo4 = tp.w, we4 = 8192u - tp.w;
