@@ -558,9 +558,10 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 // no shared-memory table), else the table; packed 32-bit stores.
 enum CwMode : int { CW_COPY = 0, CW_LUT = 1, CW_AFFINE = 2 };
 constexpr int kK1Unroll = 2;                // row loop unroll (A/B: 1 / 2 / 4 -> 45.3 / 44.9 / 45.1 us under ncu)
-// one bulk copy per source row when the window is narrower than half the row stride,
-// else one copy of the whole row range (fewer serialised copy issues in the copy warp)
-constexpr int kCwPerRowNum = 8, kCwPerRowDen = 4;
+// one bulk copy per source row when whole-row copies would move >= 25 % more bytes than
+// the window, else one copy of the whole row range (A/B: thresholds 5/4, 6/4, 8/4 take
+// the same time; 5/4 keeps the DRAM read side at 1.18x the window vs 1.32x at 8/4)
+constexpr int kCwPerRowNum = 5, kCwPerRowDen = 4;
 constexpr uint32_t kCwFake = 0xFFFEu;       // a parity with weight 0 in this output row (never a real row: heights < 0xFFFE)
 constexpr uint32_t kCwNone = 0xFFFFFFFFu;   // no source row held (start of a sample)
 
@@ -660,8 +661,9 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
   const int nslot = P.cw_slots, meta = cw_stage_meta(P), sbytes = cw_src_stage(P), span_pad = cw_span_pad(P);
   const int tap_off = cw_tap_off(P);
   // tickets: the first `nrun` hand out runs of cw_run consecutive tiles (sample-major
-  // order), the last ~2 x grid tiles go out one by one (a short tail); a CTA's
-  // first ticket is its block index, the rest come from a global counter
+  // order), the last ~2 x grid tiles go out one by one (a short tail; half tiles were
+  // measured slower, 43 -> 50 us: each half re-sums its first rows and the column
+  // table); a CTA's first ticket is its block index, the rest come from a global counter
   const int total = A.count * tps, G = gridDim.x;
   const int run = P.cw_run, tail = min(total, 2 * G), nrun = (total - tail) / run, head = nrun * run;
   const int ntickets = nrun + (total - head);
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         const int lo = __shfl_sync(0xffffffffu, ya, 0), hi = __shfl_sync(0xffffffffu, yb, R - 1);
         ncopy = span_bytes > 0 ? max(0, min(min(hi - lo + 1, nslot), S.rows - lo)) : 0;
         const uint32_t rstr = (uint32_t)S.rstride;
-        // one copy per row when the window is under half the row stride (kCwPerRowNum / Den)
+        // one copy per row when the row stride exceeds kCwPerRowNum / kCwPerRowDen x the window
         per_row = ncopy > 1 && (uint64_t)kCwPerRowDen * rstr > (uint64_t)kCwPerRowNum * (uint64_t)(span_bytes + 16);
         const uintptr_t a = reinterpret_cast<uintptr_t>(S.base + (int64_t)(lo + lane) * S.rstride + (int64_t)col_lo * C);
         uint32_t my_base;                              // stage offset of slot `lane`'s column col_lo
