@@ -254,13 +254,13 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
         }
       }
       const int size = kk ? (sym & 15) : sym, run = kk ? (sym >> 4) : 0;
-      e = kFastValid | (uint32_t)len << 25 | (uint32_t)size << 16 | (uint32_t)run << 21 |
-          ((kk && size == 0 && run != 15) ? kFastEob : 0u);
+      const uint32_t adv = (kk && size == 0 && run != 15) ? 64u : (uint32_t)run + 1u;
+      e = kFastValid | (uint32_t)len << 25 | adv << kFastAdvShift | (uint32_t)size;
     }
     // common tail: consume the code (or code + extra bits), then any extra bits still pending
     const int used = (int)((e >> 25) & 31);
     acc <<= used;
-    const int size = (e & kFastFull) ? 0 : (int)((e >> 16) & 15);
+    const int size = (e & kFastFull) ? 0 : (int)(e & 15u);
     const uint32_t hi = (uint32_t)(acc >> 32);
     const uint32_t bits = __funnelshift_l(hi, 0u, size);               // top `size` bits (0 when size == 0)
     const int sgn = (int)hi >> 31;                                      // leading extra bit 1: positive
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
                             : (int)bits + ((int)((0xFFFFFFFFu << size) + 1u) & ~sgn);   // EXTEND (F.2.2.1)
     acc <<= size;
     nb -= used + size;
-    const int run = (int)((e >> 21) & 15);
+    const int adv = (int)((e >> kFastAdvShift) & kFastAdvMask);
     if (kk == 0) {                                   // DC: prediction per component
       int p = ci == 0 ? pred0 : pred1;
       p = ci == 2 ? pred2 : p;
@@ -277,28 +277,23 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
       pred1 = ci == 1 ? v : pred1;
       pred2 = ci == 2 ? v : pred2;
     }
-    const int pos = kk + run;
+    const int pos = kk + adv - 1;
     if (v != 0 && !bad) cb[min(pos, 63)] = (int16_t)v;   // zig-zag order (J3 de-zigzags at compile time)
-    kk = (e & kFastEob) ? 64 : pos + 1;
+    kk += adv;                                       // an end of block advances past 63
     // more AC symbols in the same iteration while the block continues and the
-    // bit buffer holds the symbol: its code within the 11-bit peek, plus its
-    // extra bits (read here when the entry could not hold the value)
+    // bit buffer holds the symbol with its value: code + extra bits within the
+    // 11-bit peek (entries that need more extra bits wait for the next iteration)
 #pragma unroll
     for (int extra = 0; extra < kExtraSymbols; ++extra) {
       if (kk < 64 && !bad && nb >= kJpegFastBits) {
         const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
-        const bool full2 = (e2 & kFastFull) != 0;
-        const int l2 = (int)((e2 >> 25) & 31), sz2 = full2 ? 0 : (int)((e2 >> 16) & 15);
-        if ((e2 & kFastValid) && nb >= l2 + sz2) {
+        if (e2 & kFastFull) {
+          const int l2 = (int)((e2 >> 25) & 31), adv2 = (int)((e2 >> kFastAdvShift) & kFastAdvMask);
           acc <<= l2;
-          const uint32_t hi2 = (uint32_t)(acc >> 32);
-          const int v2 = full2 ? (int)(int16_t)(e2 & 0xFFFF)
-                               : (int)__funnelshift_l(hi2, 0u, sz2) + ((int)((0xFFFFFFFFu << sz2) + 1u) & ~((int)hi2 >> 31));
-          acc <<= sz2;
-          nb -= l2 + sz2;
-          const int pos2 = kk + (int)((e2 >> 21) & 15);
+          nb -= l2;
+          const int v2 = (int)(int16_t)(e2 & 0xFFFF), pos2 = kk + adv2 - 1;
           if (v2 != 0) cb[min(pos2, 63)] = (int16_t)v2;
-          kk = (e2 & kFastEob) ? 64 : pos2 + 1;
+          kk += adv2;
         }
       }
     }

@@ -35,11 +35,14 @@ constexpr int kJpegSmemTables = 8;        // J2 stages the pool in smem when it 
 // Fast-table entry (u32) indexed by the next kJpegFastBits bits of the stream:
 //   bit 31 valid (code <= kJpegFastBits bits; else the maxcode search),
 //   bit 30 full: code + extra bits fit, bits 0..15 hold the decoded value
-//          (EXTENDed coefficient, or the DC difference),
+//          (EXTENDed coefficient, or the DC difference); not full: bits 0..3
+//          hold the extra bits still to read,
 //   bits 25..29 bits to consume (full: code + extra; else the code only),
-//   bits 21..24 zero run, bit 20 end of block (AC size 0, run < 15),
-//   bits 16..19 extra bits still to read (entries that are not full)
-constexpr uint32_t kFastValid = 1u << 31, kFastFull = 1u << 30, kFastEob = 1u << 20;
+//   bits 16..22 zig-zag advance: run + 1 (1 for DC), 64 for end of block
+//          (AC size 0, run < 15) -- the coefficient lands at k + advance - 1
+constexpr uint32_t kFastValid = 1u << 31, kFastFull = 1u << 30;
+constexpr int kFastAdvShift = 16;
+constexpr uint32_t kFastAdvMask = 127u;
 
 struct JHuff {                            // one Huffman table, device form
   uint32_t fast[1 << kJpegFastBits];

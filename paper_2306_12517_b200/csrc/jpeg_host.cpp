@@ -133,13 +133,13 @@ bool jpeg_build_huff(const JpegHeader::Huff& t, bool is_ac, JHuff* o) {
       const int sh = F - l;
       const bool eob = is_ac && size == 0 && run != 15;           // EOB / ZRL: jdhuff.c rule
       for (int f = 0; f < (1 << sh); ++f) {
-        uint32_t e = kFastValid | (uint32_t)run << 21 | (eob ? kFastEob : 0u);
+        uint32_t e = kFastValid | (uint32_t)(eob ? 64 : run + 1) << kFastAdvShift;
         if (l + size <= F) {                                        // value fits: decode it here
           const int bits = size ? (f >> (sh - size)) & ((1 << size) - 1) : 0;
           const int v = size ? (bits < (1 << (size - 1)) ? bits - (1 << size) + 1 : bits) : 0;
-          e |= kFastFull | (uint32_t)(l + size) << 25 | (uint32_t)(uint16_t)(int16_t)v;
+          e = (e & ~0xFFFFu) | kFastFull | (uint32_t)(l + size) << 25 | (uint32_t)(uint16_t)(int16_t)v;
         } else {
-          e |= (uint32_t)l << 25 | (uint32_t)size << 16;
+          e |= (uint32_t)l << 25 | (uint32_t)size;
         }
         o->fast[(code << sh) | f] = e;
       }
