@@ -194,6 +194,8 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *   "jpeg_header_cache"     1: keep each JPEG sample's parsed header for later epochs
  *   "jpeg_header_prefetch"  1: parse the headers of this loader's samples up front
  *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
+ *   "parallel_desc_min"     256: batches of at least this many samples whose chains draw
+ *                              RandomResizedCrop windows build their descriptors on the pool
  *   "direct_io"             0: Direct strategy -- every payload read is one pread of the whole
  *                              payload (reader.py:368-372), no window staging
  *   "read_latency_ns"       0: Direct: latency spun before each read (reader.py:369-370)

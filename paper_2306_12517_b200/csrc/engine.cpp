@@ -341,6 +341,7 @@ struct bbx_loader {
   bool zc = false;                    // payload_dev is host memory (zero-copy)
   size_t pay_base = 0;                // start of the compact payload region
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
+  int64_t par_desc_min = 256;         // batches of at least this many samples fill descriptors on the pool
   std::vector<int> local_cpus;        // the GPU's NUMA-node CPUs (this rank's slice); empty: unknown
   int numa_node = -1;
   bool direct_io = false;             // Direct strategy (reader.py:61-65,368-372): one pread per payload read
@@ -1433,11 +1434,16 @@ static int process_slot(bbx_loader* L, int s) {
   // one compact payload region for every plan: [pay_base, cursor)
   const size_t pay_base = L->pay_base;
   size_t cursor = pay_base;
-  // descriptors (RNG draws + cell checks, ~65 ns per sample and field) are filled on
-  // the staging pool for large batches: the pipeline thread is otherwise the
-  // bound of an HBM-resident batch (K1 takes ~45 us per 512 images)
+  // descriptors (RNG draws + cell checks) of large batches whose chains draw
+  // RandomResizedCrop windows (~60 ns per sample: log / exp / sqrt per attempt) are
+  // filled on the staging pool: the pipeline thread is otherwise the bound of an
+  // HBM-resident configs[1] batch (measured 31.5 -> 25 us per 512).  Cheaper chains
+  // (~20 ns per sample) stay serial: waking the pool costs more (configs[0]: 10 vs 22 us).
   constexpr int kDescChunk = 64;
-  const bool par_desc = count >= 4 * kDescChunk;
+  bool rrc_draws = false;
+  for (const Plan& pl : L->plans)
+    for (const Draw& dr : pl.draws) rrc_draws = rrc_draws || dr.kind == BBX_OP_RRC;
+  const bool par_desc = rrc_draws && count >= L->par_desc_min && count > kDescChunk;
   std::vector<uint64_t> d_off;
   std::vector<uint32_t> d_len;
   std::vector<uint8_t> d_ok;
@@ -2220,6 +2226,7 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   else if (n == "jpeg_header_prefetch") L->jpeg_prefetch = value != 0;
   else if (n == "direct_io") { L->direct_io = value != 0; if (L->direct_io) { L->window_staging = false; } }
   else if (n == "read_latency_ns") L->read_latency_ns = value > 0 ? value : 0;
+  else if (n == "parallel_desc_min") L->par_desc_min = value;
   else if (n == "compute_streams") {
     if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);
     L->nstreams = (int)value;

@@ -77,12 +77,20 @@ class EpochStats:
 class Batch:
     """A lease on one ring slot's device tensors; valid until the next batch."""
 
-    __slots__ = ("arrays", "indices", "index")
+    __slots__ = ("arrays", "_idx", "_list", "index")
 
     def __init__(self, arrays: dict, indices, index: int):
         self.arrays = arrays
-        self.indices = indices
+        self._idx = indices          # list or int64 ndarray; `indices` is a list, as the reference's
+        self._list = indices if isinstance(indices, list) else None
         self.index = index
+
+    @property
+    def indices(self) -> list:
+        """The batch's sample indices (a list, loader.py:411), built on first access."""
+        if self._list is None:
+            self._list = self._idx.tolist()
+        return self._list
 
     def __getitem__(self, name: str):
         return self.arrays[name]
@@ -92,7 +100,7 @@ class Batch:
 
     @property
     def size(self) -> int:
-        return len(self.indices)
+        return len(self._idx)
 
     def keys(self):
         return self.arrays.keys()
@@ -567,7 +575,7 @@ class _EpochRun:
                 now = ld.stats()
                 self.stats.page_fetches = max(0, now["page_fetches"] - pool_base["page_fetches"])
                 self.stats.page_reloads = max(0, now["page_reloads"] - pool_base["page_reloads"])
-            yield Batch(arrays, indices.tolist(), g)
+            yield Batch(arrays, indices, g)   # the list is built only if the consumer reads it
             g += 1
 
     def stop(self) -> None:
