@@ -147,7 +147,11 @@ bbx_status bbx_loader_submit(bbx_loader* ld, int32_t slot, const int64_t* idx, i
                              uint64_t epoch);
 /* Block until `slot` is filled (BatchRing.consume, pipeline.py:509-524).
  * On a per-sample failure returns its code, *bad_pos = lowest failing
- * position and bbx_last_error() = the reference's inner message. */
+ * position and bbx_last_error() = the reference's inner message.  The host
+ * waits for the slot's device work only when the batch has device-detected
+ * sample errors to read (RLE / JPEG fields) or is profiled; otherwise it
+ * returns once the batch is queued, and bbx_loader_stream_wait orders the
+ * consumer's stream after it. */
 bbx_status bbx_loader_wait(bbx_loader* ld, int32_t slot, int64_t* bad_pos);
 /* Make `stream` (a cudaStream_t) wait for slot's device work: no host block. */
 bbx_status bbx_loader_stream_wait(bbx_loader* ld, int32_t slot, void* stream);
@@ -155,6 +159,15 @@ bbx_status bbx_loader_stream_wait(bbx_loader* ld, int32_t slot, void* stream);
  * pipeline.py:484-488): work queued on `stream` so far must finish before
  * the slot is overwritten.  stream may be NULL (legacy default stream). */
 bbx_status bbx_loader_release(bbx_loader* ld, int32_t slot, void* stream);
+/* One consumer step in one call (the Python iterator's per-batch sequence):
+ * release_slot >= 0: bbx_loader_release(release_slot, stream); submit_slot >= 0:
+ * bbx_loader_submit(submit_slot, idx, count, seed, epoch); then
+ * bbx_loader_wait(wait_slot, bad_pos) and, when that succeeds,
+ * bbx_loader_stream_wait(wait_slot, stream).  Returns the first failing
+ * status (a wait failure carries bad_pos as bbx_loader_wait does). */
+bbx_status bbx_loader_step(bbx_loader* ld, int32_t release_slot, int32_t submit_slot, const int64_t* idx,
+                           int32_t count, uint64_t seed, uint64_t epoch, int32_t wait_slot, void* stream,
+                           int64_t* bad_pos);
 /* Wait for every submitted batch (used on shutdown / abandoned epochs). */
 bbx_status bbx_loader_drain(bbx_loader* ld);
 
@@ -182,6 +195,7 @@ typedef struct {
   int64_t numa_node;          /* the GPU's NUMA node (-1: unknown); staging threads + pinned slots live there */
   int64_t staging_threads;    /* host gather threads */
   int64_t staging_cpus;       /* CPUs those threads are bound to (this rank's slice of the node; 0: unbound) */
+  double  pipeline_seconds;   /* pipeline-thread time per batch: descriptors, staging, H2D and launch calls */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
  * RLE / JPEG fields, kernels read each sample's payload window straight from
@@ -196,6 +210,8 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *   "jpeg_roi"              1: entropy-decode / IDCT only the MCUs the chain reads
  *   "parallel_desc_min"     256: batches of at least this many samples whose chains draw
  *                              RandomResizedCrop windows build their descriptors on the pool
+ *   "cuda_graphs"           1: a full HBM-resident batch without per-sample device status
+ *                              is captured once per (slot, compute stream) and replayed as a graph
  *   "direct_io"             0: Direct strategy -- every payload read is one pread of the whole
  *                              payload (reader.py:368-372), no window staging
  *   "read_latency_ns"       0: Direct: latency spun before each read (reader.py:369-370)

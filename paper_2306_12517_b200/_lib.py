@@ -43,7 +43,8 @@ class LoaderStats(ctypes.Structure):
                 ("kernel_seconds", c_dbl), ("kernel_timed", c_i64), ("kernel_bytes", c_i64),
                 ("zero_copy_bytes", c_i64), ("gap_seconds", c_dbl), ("h2d_late_seconds", c_dbl),
                 ("timed_batches", c_i64), ("page_fetches", c_i64), ("page_reloads", c_i64),
-                ("io_reads", c_i64), ("numa_node", c_i64), ("staging_threads", c_i64), ("staging_cpus", c_i64)]
+                ("io_reads", c_i64), ("numa_node", c_i64), ("staging_threads", c_i64), ("staging_cpus", c_i64),
+                ("pipeline_seconds", c_dbl)]
 
 
 # bbx_status -> exception class (errors.py:4-57)
@@ -102,6 +103,7 @@ def _bind(L):
         "bbx_loader_wait": (c_i32, [c_vp, c_i32, P(c_i64)]),
         "bbx_loader_stream_wait": (c_i32, [c_vp, c_i32, c_vp]),
         "bbx_loader_release": (c_i32, [c_vp, c_i32, c_vp]),
+        "bbx_loader_step": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i32, c_u64, c_u64, c_i32, c_vp, P(c_i64)]),
         "bbx_loader_drain": (c_i32, [c_vp]),
         "bbx_loader_get_stats": (c_i32, [c_vp, P(LoaderStats)]),
         "bbx_loader_reset_stats": (c_i32, [c_vp]),
@@ -128,7 +130,7 @@ EXPORTED = ("bbx_last_error", "bbx_version", "bbx_dataset_open", "bbx_dataset_cl
             "bbx_dataset_page_map",
             "bbx_epoch_order", "bbx_loader_create", "bbx_loader_destroy", "bbx_loader_add_field",
             "bbx_loader_add_scalar", "bbx_loader_bind", "bbx_loader_submit", "bbx_loader_wait",
-            "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_drain", "bbx_loader_get_stats",
+            "bbx_loader_stream_wait", "bbx_loader_release", "bbx_loader_step", "bbx_loader_drain", "bbx_loader_get_stats",
             "bbx_loader_reset_stats", "bbx_loader_compute_stream", "bbx_loader_set_profiling",
             "bbx_loader_set_zero_copy", "bbx_loader_set_option", "bbx_loader_prefetch_headers",
             "bbx_decode_image", "bbx_jpeg_check", "bbx_loader_set_page_pool", "bbx_loader_plan_epoch")

@@ -238,6 +238,10 @@ struct Slot {
   cudaEvent_t h2d_done{}, done{}, release{};
   cudaEvent_t h2d_t{};             // profiling: timed copy of h2d_done
   bool h2d_timed = false;
+  bool h2d_on_compute = false;     // the last H2D ran on the batch's compute stream (no h2d_done record)
+  cudaGraphExec_t gexec[kStreams] = {};   // the slot's captured batch per compute stream (resident, full batch)
+  int glaunches[kStreams] = {};           // kernels in that graph
+  int last_stream = -1;            // compute stream of the slot's last batch
   cudaEvent_t k0{}, k1{};          // profiling: around the transform kernels
   bool timed = false;
   int64_t timed_launches = 0, timed_bytes = 0;
@@ -342,6 +346,7 @@ struct bbx_loader {
   size_t pay_base = 0;                // start of the compact payload region
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
   int64_t par_desc_min = 256;         // batches of at least this many samples fill descriptors on the pool
+  bool use_graphs = true;             // replay full resident batches as CUDA graphs (option "cuda_graphs")
   std::vector<int> local_cpus;        // the GPU's NUMA-node CPUs (this rank's slice); empty: unknown
   int numa_node = -1;
   bool direct_io = false;             // Direct strategy (reader.py:61-65,368-372): one pread per payload read
@@ -1389,7 +1394,7 @@ static int process_slot(bbx_loader* L, int s) {
   CK(cudaSetDevice(L->device));
   int64_t zc_bytes = 0;
   // the pinned slot may still be the source of the previous H2D
-  if (S.used) CK(cudaEventSynchronize(S.h2d_done));
+  if (S.used) CK(cudaEventSynchronize(S.h2d_on_compute ? S.done : S.h2d_done));
   ++S.serial;
   S.herr = HostErr{};
   S.plan_has_rle.assign(L->plans.size(), 0);
@@ -1639,136 +1644,204 @@ static int process_slot(bbx_loader* L, int s) {
     });
   }
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
-  // H2D on the copy stream (after the previous kernels reading d_stage)
-  const size_t bytes = resident ? L->desc_bytes : cursor;
-  if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
-  CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
-  CK(cudaEventRecord(S.h2d_done, L->copy_st));
-  S.h2d_timed = false;
-  if (L->profiling && L->prof_every == 1) {   // idle-gap attribution needs every batch timed
-    if (!S.h2d_t) CK(cudaEventCreate(&S.h2d_t));
-    CK(cudaEventRecord(S.h2d_t, L->copy_st));
-    S.h2d_timed = true;
-  }
   // consecutive batches go to alternating compute streams: one batch's kernels can
   // fill the SMs that the previous batch's tail (e.g. the last Huffman lanes) leaves idle
   const int sk = (int)(L->batch_seq++ % (uint64_t)L->nstreams);
   cudaStream_t cs = L->comp_st[sk];
-  CK(cudaStreamWaitEvent(cs, S.h2d_done, 0));
-  bool wait_release;
-  {
-    std::lock_guard<std::mutex> g(L->mu);
-    wait_release = S.released_pending;
-    S.released_pending = false;
-  }
-  if (wait_release) CK(cudaStreamWaitEvent(cs, S.release, 0));
-  int launches = 0;
+  const size_t bytes = resident ? L->desc_bytes : cursor;
+  // A resident RAW / RLE / array batch uploads only its indices + descriptors (tens of KB): that copy
+  // goes on the compute stream itself, ordered after the slot's previous kernels by
+  // the stream (or one event wait when they ran on the other stream) -- three fewer
+  // API calls on the pipeline thread, which bounds the small-image legs.  Payload
+  // batches copy on the copy stream so the H2D overlaps the previous batches' kernels.
+  bool jpeg_plan = false;   // JPEG tables are uploaded on the copy stream ahead of its H2D
+  for (const Plan& pl : L->plans) jpeg_plan = jpeg_plan || pl.field_has_jpeg;
+  const bool h2d_compute = resident && !jpeg_plan && !(L->profiling && L->prof_every == 1);
   // profiling: every prof_every-th batch gets the CUDA-event window (sampling keeps
   // the events' own cost off most batches)
   const bool prof = L->profiling && (L->prof_seq++ % (uint64_t)L->prof_every) == 0;
-  int64_t kbytes = 0, klaunch = 0;
-  if (prof && !L->t_ref) {
-    CK(cudaEventCreate(&L->t_ref));
-    CK(cudaEventRecord(L->t_ref, cs));
-  }
-  if (prof) CK(cudaEventRecord(S.k0, cs));
-  int64_t d2h = 0;
-  bool any_rle = false, any_jpeg = false;
-  ScalarArgs SA{};
-  SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
-  SA.count = count;
-  // up to 16 scalar fields ride along with the first image plan's K1 launch (the
-  // column walker's copy warp, or tile 0 of the tile kernel, gathers them);
-  // otherwise, or beyond that, scalar_gather_kernel
-  int n_scalar = 0, fused_plan = -1;
-  for (const Plan& pl : L->plans) n_scalar += pl.scalar ? 1 : 0;
-  if (n_scalar > 0 && n_scalar <= 16 && count > 0)   // an image plan's K1 (either variant) carries them
-    for (size_t p = 0; p < L->plans.size(); ++p)
-      if (!L->plans[p].scalar && L->plans[p].dev.src_kind != SRC_ARRAY) { fused_plan = (int)p; break; }
-  if (fused_plan >= 0)
-    for (const Plan& pl : L->plans)
+  bool any_status = false;   // device-detected sample errors to read back (RLE / JPEG)
+  for (size_t p = 0; p < L->plans.size(); ++p) any_status = any_status || S.plan_has_rle[p] || S.plan_has_jpeg[p];
+  int launches = 0;
+  int64_t kbytes = 0, klaunch = 0, d2h = 0;
+  // The batch's stream work: H2D, waits, kernels, status read-back, `done` record.
+  // cap: recorded into a CUDA graph instead of issued (stream capture).
+  auto enqueue = [&](bool cap) -> int {
+    if (h2d_compute) {
+      if (!cap && S.used && S.last_stream != sk) CK(cudaStreamWaitEvent(cs, S.done, 0));
+      CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, cs));
+      S.h2d_timed = false;
+    } else {
+      // H2D on the copy stream (after the previous kernels reading d_stage)
+      if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
+      CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
+      CK(cudaEventRecord(S.h2d_done, L->copy_st));
+      S.h2d_timed = false;
+      if (L->profiling && L->prof_every == 1) {   // idle-gap attribution needs every batch timed
+        if (!S.h2d_t) CK(cudaEventCreate(&S.h2d_t));
+        CK(cudaEventRecord(S.h2d_t, L->copy_st));
+        S.h2d_timed = true;
+      }
+      CK(cudaStreamWaitEvent(cs, S.h2d_done, 0));
+    }
+    S.h2d_on_compute = h2d_compute;
+    S.last_stream = sk;
+    bool wait_release;
+    {
+      std::lock_guard<std::mutex> g(L->mu);
+      wait_release = S.released_pending;
+      S.released_pending = false;
+    }
+    // a captured batch always waits on the slot's release event (a no-op when the
+    // consumer has not recorded a newer one): the graph is replayed every batch
+    if (cap) CK(cudaStreamWaitEvent(cs, S.release, cudaEventWaitExternal));
+    else if (wait_release) CK(cudaStreamWaitEvent(cs, S.release, 0));
+    launches = 0;
+    kbytes = 0; klaunch = 0;
+    if (prof && !L->t_ref) {
+      CK(cudaEventCreate(&L->t_ref));
+      CK(cudaEventRecord(L->t_ref, cs));
+    }
+    if (prof) CK(cudaEventRecord(S.k0, cs));
+    d2h = 0;
+    ScalarArgs SA{};
+    SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
+    SA.count = count;
+    // up to 16 scalar fields ride along with the first image plan's K1 launch (the
+    // column walker's copy warp, or tile 0 of the tile kernel, gathers them);
+    // otherwise, or beyond that, scalar_gather_kernel
+    int n_scalar = 0, fused_plan = -1;
+    for (const Plan& pl : L->plans) n_scalar += pl.scalar ? 1 : 0;
+    if (n_scalar > 0 && n_scalar <= 16 && count > 0)   // an image plan's K1 (either variant) carries them
+      for (size_t p = 0; p < L->plans.size(); ++p)
+        if (!L->plans[p].scalar && L->plans[p].dev.src_kind != SRC_ARRAY) { fused_plan = (int)p; break; }
+    if (fused_plan >= 0)
+      for (const Plan& pl : L->plans)
+        if (pl.scalar) {
+          SA.cols[SA.n_fields] = pl.d_col;
+          SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
+          ++SA.n_fields;
+        }
+    for (size_t p = 0; p < L->plans.size(); ++p) {
+      Plan& pl = L->plans[p];
       if (pl.scalar) {
+        if (fused_plan >= 0) continue;
         SA.cols[SA.n_fields] = pl.d_col;
         SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
         ++SA.n_fields;
+        if (SA.n_fields == 16) { if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed"); ++launches; SA.n_fields = 0; }
+        continue;
       }
-  for (size_t p = 0; p < L->plans.size(); ++p) {
-    Plan& pl = L->plans[p];
-    if (pl.scalar) {
-      if (fused_plan >= 0) continue;
-      SA.cols[SA.n_fields] = pl.d_col;
-      SA.outs[SA.n_fields] = reinterpret_cast<uint64_t*>(pl.outs[s]);
-      ++SA.n_fields;
-      if (SA.n_fields == 16) { if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed"); ++launches; SA.n_fields = 0; }
-      continue;
-    }
-    LaunchArgs A{};
-    A.desc = S.d_stage + L->desc_off[p];
-    A.payload = resident ? (const uint8_t*)(L->payload_dev - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
-    A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
-    A.tables = pl.d_tables.empty() ? nullptr : pl.d_tables[s];
-    A.lut = pl.d_lut;
-    A.out = pl.outs[s];
-    A.status = S.d_status + (size_t)p * L->batch;
-    A.count = count;
-    if ((int)p == fused_plan) A.sc = SA;
-    A.ticket = pl.d_ticket[sk];
-    if (count == 0) continue;
-    if (S.plan_has_rle[p]) {
-      if (launch_rle_expand(pl.dev, A, cs)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      ++launches; any_rle = true;
-    }
-    if (S.plan_has_jpeg[p]) {
-      JpegArgs J{};
-      const uint8_t* jb = S.d_stage + L->jpeg_off[p];
-      J.desc = A.desc; J.desc_stride = pl.dev.desc_stride; J.payload = A.payload;
-      J.jd = reinterpret_cast<const JpegDesc*>(jb);
-      J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
-      J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
-      J.starts = reinterpret_cast<const uint32_t*>(jb + jpeg_block_bytes(L->batch));
-      J.coef = pl.d_coef[sk]; J.planes = pl.d_planes[sk];
-      J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
-      J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
-      J.coef_zeroed = 1;
-      J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
-      J.max_blocks = S.jpeg_max_blocks[p];
-      // J2 stores only nonzero coefficients
-      CK(cudaMemsetAsync(pl.d_coef[sk], 0, (size_t)S.jpeg_total_blk[p] * 128, cs));
-      if (launch_jpeg(J, cs)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      launches += 4; any_jpeg = true;
-    }
-    int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, cs) : launch_image(pl.dev, A, cs);
-    if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
-      ++klaunch;
-      const uint8_t* dblk = H + L->desc_off[p];
-      for (int pos = 0; pos < count; ++pos) {
-        const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
-        if (d->skip) continue;
-        const int32_t* prm = reinterpret_cast<const int32_t*>(dblk + (size_t)pos * pl.dev.desc_stride + kDescHeader);
-        int64_t rd;
-        if (pl.dev.src_kind == SRC_RESAMPLE) rd = (int64_t)prm[2] * prm[3] * pl.dev.channels;
-        else if (pl.dev.src_kind == SRC_ARRAY) rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems * pl.dev.src_elem);
-        else rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems);
-        kbytes += rd + pl.out_sample_bytes;
+      LaunchArgs A{};
+      A.desc = S.d_stage + L->desc_off[p];
+      A.payload = resident ? (const uint8_t*)(L->payload_dev - ds->heap_offset) : (const uint8_t*)(S.d_stage + L->pay_base);
+      A.scratch = pl.d_scratch.empty() ? nullptr : pl.d_scratch[s];
+      A.tables = pl.d_tables.empty() ? nullptr : pl.d_tables[s];
+      A.lut = pl.d_lut;
+      A.out = pl.outs[s];
+      A.status = S.d_status + (size_t)p * L->batch;
+      A.count = count;
+      if ((int)p == fused_plan) A.sc = SA;
+      A.ticket = pl.d_ticket[sk];
+      if (count == 0) continue;
+      if (S.plan_has_rle[p]) {
+        if (launch_rle_expand(pl.dev, A, cs)) return fail(BBX_CUDA_ERROR, "rle launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        ++launches;
       }
+      if (S.plan_has_jpeg[p]) {
+        JpegArgs J{};
+        const uint8_t* jb = S.d_stage + L->jpeg_off[p];
+        J.desc = A.desc; J.desc_stride = pl.dev.desc_stride; J.payload = A.payload;
+        J.jd = reinterpret_cast<const JpegDesc*>(jb);
+        J.int_prefix = reinterpret_cast<const uint32_t*>(jb + jpeg_iprefix_off(L->batch));
+        J.blk_prefix = reinterpret_cast<const uint64_t*>(jb + jpeg_bprefix_off(L->batch));
+        J.starts = reinterpret_cast<const uint32_t*>(jb + jpeg_block_bytes(L->batch));
+        J.coef = pl.d_coef[sk]; J.planes = pl.d_planes[sk];
+        J.scratch = A.scratch; J.scratch_bytes = pl.dev.scratch_bytes;
+        J.huff = L->jt.d_huff; J.quant = L->jt.d_quant; J.n_huff = L->jt.n_huff; J.status = A.status; J.count = count;
+        J.coef_zeroed = 1;
+        J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
+        J.max_blocks = S.jpeg_max_blocks[p];
+        // J2 stores only nonzero coefficients
+        CK(cudaMemsetAsync(pl.d_coef[sk], 0, (size_t)S.jpeg_total_blk[p] * 128, cs));
+        if (launch_jpeg(J, cs)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        launches += 4;
+      }
+      int rc = pl.dev.src_kind == SRC_ARRAY ? launch_array(pl.dev, A, cs) : launch_image(pl.dev, A, cs);
+      if (prof) {   // algorithmic bytes: source bytes the chain needs + output bytes
+        ++klaunch;
+        const uint8_t* dblk = H + L->desc_off[p];
+        for (int pos = 0; pos < count; ++pos) {
+          const SampleDesc* d = reinterpret_cast<const SampleDesc*>(dblk + (size_t)pos * pl.dev.desc_stride);
+          if (d->skip) continue;
+          const int32_t* prm = reinterpret_cast<const int32_t*>(dblk + (size_t)pos * pl.dev.desc_stride + kDescHeader);
+          int64_t rd;
+          if (pl.dev.src_kind == SRC_RESAMPLE) rd = (int64_t)prm[2] * prm[3] * pl.dev.channels;
+          else if (pl.dev.src_kind == SRC_ARRAY) rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems * pl.dev.src_elem);
+          else rd = std::min<int64_t>(d->len, pl.dev.out_sample_elems);
+          kbytes += rd + pl.out_sample_bytes;
+        }
+      }
+      if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.cw) ? 1 : 2;   // K1 = prologue + tiles (column walker: one kernel)
     }
-    if (rc) return fail(BBX_CUDA_ERROR, "kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.cw) ? 1 : 2;   // K1 = prologue + tiles (column walker: one kernel)
+    if (prof) CK(cudaEventRecord(S.k1, cs));
+    S.timed = prof;
+    S.timed_launches = klaunch;
+    S.timed_bytes = kbytes;
+    if (SA.n_fields && count && fused_plan < 0) {
+      if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
+      ++launches;
+    }
+    if (any_status) {
+      size_t nb = sizeof(SampleStatus) * L->batch * L->plans.size();
+      CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, cs));
+      d2h += (int64_t)nb;
+    }
+    if (cap) CK(cudaEventRecordWithFlags(S.done, cs, cudaEventRecordExternal));
+    else CK(cudaEventRecord(S.done, cs));
+    return 0;
+  };
+  // A full-size resident batch without per-sample device status has the same stream
+  // work every time: it is captured once per (slot, compute stream) into a CUDA graph
+  // and replayed with one cudaGraphLaunch (the host pipeline thread -- ~5 API calls
+  // and 1-2 launches per batch otherwise -- bounds the small-image legs).
+  const bool graph_ok = L->use_graphs && h2d_compute && !prof && !any_status && count == L->batch && !L->pp.capacity;
+  if (graph_ok && S.gexec[sk]) {
+    if (S.used && S.last_stream != sk) CK(cudaStreamWaitEvent(cs, S.done, 0));
+    {
+      std::lock_guard<std::mutex> g(L->mu);
+      S.released_pending = false;
+    }
+    CK(cudaGraphLaunch(S.gexec[sk], cs));
+    S.h2d_on_compute = true;
+    S.last_stream = sk;
+    launches = S.glaunches[sk];
+    S.timed = false;
+  } else if (graph_ok) {
+    if (S.used && S.last_stream != sk) CK(cudaStreamWaitEvent(cs, S.done, 0));
+    bool captured = false;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const int r = enqueue(true);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+      if (r == 0 && ec == cudaSuccess && g && cudaGraphInstantiate(&S.gexec[sk], g, 0) == cudaSuccess) {
+        captured = true;
+        S.glaunches[sk] = launches;
+      }
+      if (g) cudaGraphDestroy(g);
+    }
+    if (captured) {
+      CK(cudaGraphLaunch(S.gexec[sk], cs));
+    } else {                                           // capture unsupported here: plain launches from now on
+      cudaGetLastError();
+      S.gexec[sk] = nullptr;
+      L->use_graphs = false;
+      if (int r = enqueue(false)) return r;
+    }
+  } else {
+    if (int r = enqueue(false)) return r;
   }
-  if (prof) CK(cudaEventRecord(S.k1, cs));
-  S.timed = prof;
-  S.timed_launches = klaunch;
-  S.timed_bytes = kbytes;
-  if (SA.n_fields && count && fused_plan < 0) {
-    if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
-    ++launches;
-  }
-  if (any_rle || any_jpeg) {
-    size_t nb = sizeof(SampleStatus) * L->batch * L->plans.size();
-    CK(cudaMemcpyAsync(S.h_status, S.d_status, nb, cudaMemcpyDeviceToHost, cs));
-    d2h += (int64_t)nb;
-  }
-  CK(cudaEventRecord(S.done, cs));
   S.used = true;
   if (L->pp.capacity) {   // the pool slots this batch reads are recycled only after S.done
     PagePool& PP = L->pp;
@@ -1873,7 +1946,13 @@ static void pipeline_loop(bbx_loader* L) {
       s = L->queue.front();
       L->queue.pop_front();
     }
+    const auto p0 = std::chrono::steady_clock::now();
     int rc = process_slot(L, s);
+    const double pdt = std::chrono::duration<double>(std::chrono::steady_clock::now() - p0).count();
+    {
+      std::lock_guard<std::mutex> g(L->stats_mu);
+      L->stats.pipeline_seconds += pdt;
+    }
     {
       std::lock_guard<std::mutex> g(L->mu);
       Slot& S = L->slots[s];
@@ -2054,7 +2133,14 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
   }
   cudaSetDevice(L->device);
   if (S.fatal) return (bbx_status)fail(S.fatal, "%s", S.fatal_msg.c_str());
-  cudaError_t e = cudaEventSynchronize(S.done);
+  // The host waits for the batch's device work only when it has something to read
+  // back: per-sample device status (RLE / JPEG) or a profiling window.  Otherwise the
+  // batch is complete as far as the host knows (host-side sample errors are final),
+  // and the consumer's stream is ordered after it by bbx_loader_stream_wait -- the
+  // consumer keeps slot_count - 1 batches queued on the GPU instead of syncing per step.
+  bool need_sync = S.timed;
+  for (size_t p = 0; p < L->plans.size(); ++p) need_sync = need_sync || S.plan_has_rle[p] || S.plan_has_jpeg[p];
+  cudaError_t e = need_sync ? cudaEventSynchronize(S.done) : cudaSuccess;
   {
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.wait_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -2119,6 +2205,18 @@ bbx_status bbx_loader_stream_wait(bbx_loader* L, int32_t slot, void* stream) {
   return BBX_OK;
 }
 
+bbx_status bbx_loader_step(bbx_loader* L, int32_t release_slot, int32_t submit_slot, const int64_t* idx,
+                           int32_t count, uint64_t seed, uint64_t epoch, int32_t wait_slot, void* stream,
+                           int64_t* bad_pos) {
+  if (bad_pos) *bad_pos = -1;
+  if (release_slot >= 0)
+    if (bbx_status r = bbx_loader_release(L, release_slot, stream)) return r;
+  if (submit_slot >= 0)
+    if (bbx_status r = bbx_loader_submit(L, submit_slot, idx, count, seed, epoch)) return r;
+  if (bbx_status r = bbx_loader_wait(L, wait_slot, bad_pos)) return r;
+  return bbx_loader_stream_wait(L, wait_slot, stream);
+}
+
 bbx_status bbx_loader_release(bbx_loader* L, int32_t slot, void* stream) {
   if (!L || slot < 0 || slot >= L->nslots) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "bad slot");
   if (!L->finalized) return BBX_OK;
@@ -2173,6 +2271,8 @@ void bbx_loader_destroy(bbx_loader* L) {
     if (S.d_status) cudaFree(S.d_status);
     if (S.h_status) cudaFreeHost(S.h_status);
     if (&S == &L->slots[0] && L->t_ref) { cudaEventDestroy(L->t_ref); L->t_ref = nullptr; }
+    for (int k = 0; k < kStreams; ++k)
+      if (S.gexec[k]) cudaGraphExecDestroy(S.gexec[k]);
     if (S.h2d_done) cudaEventDestroy(S.h2d_done);
     if (S.h2d_t) cudaEventDestroy(S.h2d_t);
     if (S.done) cudaEventDestroy(S.done);
@@ -2227,6 +2327,7 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   else if (n == "direct_io") { L->direct_io = value != 0; if (L->direct_io) { L->window_staging = false; } }
   else if (n == "read_latency_ns") L->read_latency_ns = value > 0 ? value : 0;
   else if (n == "parallel_desc_min") L->par_desc_min = value;
+  else if (n == "cuda_graphs") L->use_graphs = value != 0;
   else if (n == "compute_streams") {
     if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);
     L->nstreams = (int)value;

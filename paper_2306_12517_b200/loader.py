@@ -533,17 +533,26 @@ class _EpochRun:
             if self._ensure(g):
                 self._submit(g)
         g = 0
+        bad = ctypes.c_int64(-1)
+        bad_ref = ctypes.byref(bad)
+        seed = ld.config.seed & 0xFFFFFFFFFFFFFFFF
+        step = L.bbx_loader_step
         while self._ensure(g):
             if self._stopped:
                 raise ShutdownError("epoch stopped")
-            if self._ensure(g + S - 1):
-                if g >= 1:
-                    L.bbx_loader_release(ld.handle, (g - 1) % S, sp)
-                self._submit(g + S - 1)
             slot = g % S
-            bad = ctypes.c_int64(-1)
+            # release the previous lease, submit batch g + S - 1, wait for batch g and
+            # order the consumer's stream after it: one call (bbx_loader_step)
+            rel, sub, nidx, ep, iptr = -1, -1, 0, 0, None
+            if self._ensure(g + S - 1):
+                rel = (g - 1) % S if g >= 1 else -1
+                sub = (g + S - 1) % S
+                sidx = np.ascontiguousarray(self.batch_lists[g + S - 1], dtype=np.int64)
+                nidx, ep = len(sidx), self.batch_epochs[g + S - 1] & 0xFFFFFFFFFFFFFFFF
+                iptr = sidx.ctypes.data if nidx else None
+                self._inflight.add(sub)
             t0 = time.perf_counter()
-            rc = L.bbx_loader_wait(ld.handle, slot, ctypes.byref(bad))
+            rc = step(ld.handle, rel, sub, iptr, nidx, seed, ep, slot, sp, bad_ref)
             self.stats.consumer_blocked_s += time.perf_counter() - t0
             self._inflight.discard(slot)
             indices = self.batch_lists[g]
@@ -553,7 +562,6 @@ class _EpochRun:
                 if bad.value >= 0:
                     raise exc(f"sample {int(indices[bad.value])} failed: {msg}")
                 raise exc(msg)
-            _lib.check(L.bbx_loader_stream_wait(ld.handle, slot, sp))
             count = len(indices)
             arrays = {}
             for fd in ld._fields:

@@ -33,7 +33,7 @@ for leg, path, chain in (("configs[0]", bench.cifar_dataset(0, noop), bench.CIFA
         el = time.perf_counter() - t0
         st = ld.stats()
         print(f"{leg} parallel_desc_min={pmin}: step {el / 300 * 1e6:.1f} us, consumer in next() {t_next / 300 * 1e6:.1f} us, "
-              f"pipeline desc/stage {st['stage_seconds'] / max(st['batches'], 1) * 1e6:.1f} us, wait {st['wait_seconds'] / 300 * 1e6:.1f} us")
+              f"pipeline {st['pipeline_seconds'] / max(st['batches'], 1) * 1e6:.1f} us (desc/stage {st['stage_seconds'] / max(st['batches'], 1) * 1e6:.1f}), wait {st['wait_seconds'] / 300 * 1e6:.1f} us")
         it.close()
         ld.shutdown()
         ds.close()
