@@ -200,6 +200,7 @@ struct Draw {        // one RNG-consuming op, in chain order (host program)
   int in_h, in_w, h, w;
   double p;
   double scale[2], ratio[2];
+  double log_ratio[2];   // RRC: log(ratio), computed once at plan time
 };
 
 struct Plan {
@@ -472,6 +473,7 @@ static int plan_compile(bbx_loader* L, int field_index, const bbx_op* ops, int n
       P.src_kind = SRC_RESAMPLE; H = s0.h; W = s0.w;
       Draw d{}; d.kind = s0.kind; d.slot = 0; d.h = s0.h; d.w = s0.w; d.p = s0.p;
       d.scale[0] = s0.scale[0]; d.scale[1] = s0.scale[1]; d.ratio[0] = s0.ratio[0]; d.ratio[1] = s0.ratio[1];
+      d.log_ratio[0] = std::log(d.ratio[0]); d.log_ratio[1] = std::log(d.ratio[1]);
       if (s0.kind == BBX_OP_RRC && !(d.scale[0] > 0 && d.scale[0] <= d.scale[1] && d.ratio[0] > 0 && d.ratio[0] <= d.ratio[1]))
         return fail(BBX_SPEC_MISMATCH, "random-resized-crop needs 0 < scale[0] <= scale[1] and 0 < ratio[0] <= ratio[1]");
       if (s0.kind == BBX_OP_CENTERCROP && !(d.p > 0 && d.p <= 1.0))
@@ -798,7 +800,7 @@ static bool fill_desc(const bbx_dataset* ds, const Plan& pl, int64_t i, uint64_t
     switch (dr.kind) {
       case BBX_OP_RRC: {
         int t, l, hh, ww;
-        rrc_window(r, d->h, d->w, dr.scale, dr.ratio, &t, &l, &hh, &ww);
+        rrc_window(r, d->h, d->w, dr.scale, dr.ratio, &t, &l, &hh, &ww, dr.log_ratio);
         prm[0] = t; prm[1] = l; prm[2] = hh; prm[3] = ww;
         break;
       }

@@ -102,7 +102,7 @@ int epoch_order(int kind, uint64_t seed, uint64_t epoch, int64_t n, const int64_
 
 // RandomResizedCrop / CenterCrop windows (extension decoders).
 void rrc_window(Rng& r, int h, int w, const double scale[2], const double ratio[2], int* top, int* left, int* ch,
-                int* cw);
+                int* cw, const double* log_ratio = nullptr);
 void center_window(int h, int w, double ratio, int* top, int* left, int* ch, int* cw);
 
 // ---- fixed-size worker pool for payload gathers

@@ -82,9 +82,10 @@ int epoch_order(int kind, uint64_t seed, uint64_t epoch, int64_t n, const int64_
 // FFCV get_random_crop with bbox Rng draws; identical expression order to
 // oracle/bbx_oracle.c:or_rrc_window so the same libm gives the same window.
 void rrc_window(Rng& r, int h, int w, const double scale[2], const double ratio[2], int* top, int* left, int* ch,
-                int* cw) {
+                int* cw, const double* log_ratio) {
   double area = (double)h * (double)w;
-  double lr0 = std::log(ratio[0]), lr1 = std::log(ratio[1]);
+  // log(ratio) is a per-op constant: the loader passes it precomputed (same libm value)
+  double lr0 = log_ratio ? log_ratio[0] : std::log(ratio[0]), lr1 = log_ratio ? log_ratio[1] : std::log(ratio[1]);
   for (int attempt = 0; attempt < 10; ++attempt) {
     double target = area * (scale[0] + (scale[1] - scale[0]) * r.uniform());
     double aspect = std::exp(lr0 + (lr1 - lr0) * r.uniform());

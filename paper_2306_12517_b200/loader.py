@@ -214,10 +214,12 @@ def shard_batches(global_batches: list, rank: int, world_size: int, batch_size: 
 
 
 class _Field:
-    __slots__ = ("name", "plan_id", "outs", "nchw", "scalar", "contiguous")
+    __slots__ = ("name", "plan_id", "outs", "nchw", "scalar", "contiguous", "views")
 
     def __init__(self, name, plan_id, outs, nchw, scalar, contiguous=False):
         self.name, self.plan_id, self.outs, self.nchw, self.scalar = name, plan_id, outs, nchw, scalar
+        # per-slot views made once (indexing a tensor costs microseconds per batch)
+        self.views = [outs[k].permute(0, 3, 1, 2) if nchw else outs[k] for k in range(outs.shape[0])]
         self.contiguous = contiguous
 
 
@@ -564,14 +566,13 @@ class _EpochRun:
                 raise exc(msg)
             count = len(indices)
             arrays = {}
+            full = count == ld.config.batch_size
             for fd in ld._fields:
-                t = fd.outs[slot]
-                if count != t.shape[0]:                  # full batches hand out the slot tensor itself
+                t = fd.views[slot]                       # full batches hand out the slot tensor itself
+                if not full:
                     t = t[:count]
-                if fd.nchw:
-                    t = t.permute(0, 3, 1, 2)
-                    if fd.contiguous:                    # ToTorchImage(channels_last=False)
-                        t = t.contiguous()
+                if fd.contiguous:                        # ToTorchImage(channels_last=False)
+                    t = t.contiguous()
                 arrays[fd.name] = t
             self.stats.batches += 1
             self.stats.samples += count
