@@ -134,15 +134,26 @@ void Pool::work(Job& job) {
     }
   }
 }
+// A worker that just finished a job polls for the next one for a short while before
+// sleeping on the condition variable: batches arrive every few tens of microseconds,
+// and a futex wake-up costs about as much as a batch's descriptor work.
+static constexpr auto kPoolSpin = std::chrono::microseconds(60);
+static inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+  __builtin_ia32_pause();
+#endif
+}
 void Pool::run() {
   uint64_t seen = 0;
   for (;;) {
+    const auto until = std::chrono::steady_clock::now() + kPoolSpin;
+    while (gen_.load(std::memory_order_acquire) == seen && std::chrono::steady_clock::now() < until) cpu_relax();
     std::shared_ptr<Job> job;
     {
       std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      cv_.wait(lk, [&] { return stop_ || gen_.load() != seen; });
       if (stop_) return;
-      seen = gen_;
+      seen = gen_.load();
       job = job_;
     }
     if (job) work(*job);
@@ -157,10 +168,13 @@ void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
   {
     std::lock_guard<std::mutex> g(mu_);
     job_ = job;
-    ++gen_;
+    gen_.fetch_add(1, std::memory_order_release);
   }
   cv_.notify_all();
   work(*job);
+  // the caller's share is done: poll the stragglers briefly, then sleep
+  const auto until = std::chrono::steady_clock::now() + kPoolSpin;
+  while (job->done.load(std::memory_order_acquire) < n && std::chrono::steady_clock::now() < until) cpu_relax();
   std::unique_lock<std::mutex> lk(mu_);
   done_cv_.wait(lk, [&] { return job->done.load() >= n; });
   if (job_ == job) job_.reset();

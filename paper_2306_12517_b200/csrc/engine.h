@@ -131,7 +131,7 @@ class Pool {
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   std::shared_ptr<Job> job_;
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};   // bumped per job; spinning workers poll it without the lock
   bool stop_ = false;
 };
 
