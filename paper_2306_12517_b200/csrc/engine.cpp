@@ -1778,8 +1778,6 @@ static int process_slot(bbx_loader* L, int s) {
         J.coef_zeroed = 1;
         J.total_int = S.jpeg_total_int[p]; J.total_blocks = S.jpeg_total_blk[p]; J.max_quads = S.jpeg_max_quads[p];
         J.max_blocks = S.jpeg_max_blocks[p];
-        // J2 stores only nonzero coefficients
-        CK(cudaMemsetAsync(pl.d_coef[sk], 0, (size_t)S.jpeg_total_blk[p] * 128, cs));
         if (launch_jpeg(J, cs)) return fail(BBX_CUDA_ERROR, "jpeg launch failed: %s", cudaGetErrorString(cudaGetLastError()));
         launches += 4;
       }

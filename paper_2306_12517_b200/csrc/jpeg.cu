@@ -41,6 +41,13 @@ constexpr int kHuffThreads = 256;           // 8 warps share one copy of the sme
 constexpr int kHuffCtasPerSm = 3;           // a batch of 1024 ImageNet-sized JPEGs has ~110k intervals: ~3 CTAs
                                             // per SM hold all of them at once (4 / 5 measured the same)
 constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
+// Each lane assembles its current 8x8 block in shared memory and writes it to the
+// coefficient buffer as eight 16-byte stores when the block ends: scattered 2-byte
+// global stores of single coefficients kept the L1 busy with one sector per lane per
+// coefficient, and the buffer needed a memset first.  144-byte lane stride: the
+// 16-byte reads of 8 consecutive lanes hit distinct bank quads.
+constexpr int kBlkStride = 144;
+__host__ __device__ constexpr int huff_blk_bytes() { return kHuffThreads * kBlkStride; }
 constexpr int kMaxBpm = 12;                 // blocks per MCU with sampling factors <= 2
 
 
@@ -53,12 +60,19 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
   constexpr int TW = 1 << kJpegFastBits;
   constexpr uint32_t TSTRIDE = kSmem ? TW : (uint32_t)(sizeof(JHuff) / 4);
   const int tabs_bytes = kSmem ? A.n_huff * TW * 4 : 0;
-  const uint32_t* tab = kSmem ? reinterpret_cast<const uint32_t*>(hsm) : reinterpret_cast<const uint32_t*>(A.huff);
+  const uint32_t* tab = kSmem ? reinterpret_cast<const uint32_t*>(hsm + huff_blk_bytes())
+                              : reinterpret_cast<const uint32_t*>(A.huff);
   // long codes (12..16 bits): per table maxcode[12..16], valoff[12..16] (int32) and vals[256] in smem
   constexpr int kSlowBytes = 10 * 4 + 256;
-  uint8_t* slow = hsm + tabs_bytes;
+  uint8_t* slow = hsm + huff_blk_bytes() + tabs_bytes;
+  int16_t* myblk = reinterpret_cast<int16_t*>(hsm + threadIdx.x * kBlkStride);   // this lane's block
+  {
+    uint4* z = reinterpret_cast<uint4*>(myblk);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) z[j] = make_uint4(0, 0, 0, 0);
+  }
   if (kSmem) {
-    uint32_t* st = reinterpret_cast<uint32_t*>(hsm);
+    uint32_t* st = reinterpret_cast<uint32_t*>(hsm + huff_blk_bytes());
     const int n = A.n_huff * TW;
     for (int i = threadIdx.x; i < n; i += kHuffThreads) st[i] = __ldg(&A.huff[i / TW].fast[i % TW]);
     for (int i = threadIdx.x; i < A.n_huff * kSlowBytes; i += kHuffThreads) {
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
       pred2 = ci == 2 ? v : pred2;
     }
     const int pos = kk + adv - 1;
-    if (v != 0 && !bad) cb[min(pos, 63)] = (int16_t)v;   // zig-zag order (J3 de-zigzags at compile time)
+    if (v != 0 && !bad) myblk[min(pos, 63)] = (int16_t)v;   // zig-zag order (J3 de-zigzags at compile time)
     kk += adv;                                       // an end of block advances past 63
     // more AC symbols in the same iteration while the block continues and the
     // bit buffer holds the symbol with its value: code + extra bits within the
@@ -292,12 +306,19 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
           acc <<= l2;
           nb -= l2;
           const int v2 = (int)(int16_t)(e2 & 0xFFFF), pos2 = kk + adv2 - 1;
-          if (v2 != 0) cb[min(pos2, 63)] = (int16_t)v2;
+          if (v2 != 0) myblk[min(pos2, 63)] = (int16_t)v2;
           kk += adv2;
         }
       }
     }
     if (kk >= 64 || bad) {                           // block done: blocks are stored in decode order
+      uint4* z = reinterpret_cast<uint4*>(myblk);
+      uint4* dst = reinterpret_cast<uint4*>(cb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        dst[j] = z[j];
+        z[j] = make_uint4(0, 0, 0, 0);
+      }
       cb += 64;
       kk = 0;
       if (++b == bpm) { b = 0; ++m; }
@@ -630,7 +651,8 @@ int launch_jpeg(const JpegArgs& A, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (A.count <= 0 || A.total_int == 0) return 0;
   const bool smem = A.n_huff <= kJpegSmemTables;
-  const int hsmem = smem ? A.n_huff * (int)sizeof(JHuff::fast) + (A.n_huff * (10 * 4 + 256) + 15) / 16 * 16 : 0;
+  const int hsmem = huff_blk_bytes() +
+                    (smem ? A.n_huff * (int)sizeof(JHuff::fast) + (A.n_huff * (10 * 4 + 256) + 15) / 16 * 16 : 0);
   // a thread per restart interval, CTAs of kHuffThreads consecutive intervals
   const unsigned hgrid = (unsigned)(((uint64_t)A.total_int + kHuffThreads - 1) / kHuffThreads);
   if (smem) {
