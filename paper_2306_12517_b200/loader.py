@@ -12,6 +12,12 @@ else on the device), slot_count ring slots of device output tensors, and a
 prefetch depth of slot_count - 1 batches.  Batch arrays are CUDA tensors,
 channels-last (NHWC), exactly the reference's numpy shapes and dtypes.
 
+Stream semantics (as FFCV's loader): a yielded batch's device work is ordered
+before the work queued afterwards on the CUDA stream that was current when the
+iteration started (bbx_loader_stream_wait); the host does not wait for it unless
+the batch has device-detected sample errors to read (RLE / JPEG fields).  Work on
+another stream must wait on that stream (e.g. `other.wait_stream(current)`).
+
 Extensions: `distributed=True` shards every global batch of
 world_size * batch_size positions by rank; `device`.
 """
