@@ -56,3 +56,19 @@ def test_graph_replay_matches_oracle(tmp_path, chain):
         for f in ("image", "label"):
             assert np.array_equal(ga[f], wa[f]), (k, f)
             assert np.array_equal(oa[f], wa[f]), (k, f)
+
+
+def test_graph_replay_with_partial_batches(tmp_path):
+    """50 samples in batches of 8: six full (graph) batches and a short one (plain
+    launches) per epoch, interleaved on the same slots across epochs."""
+    path = _dataset(tmp_path, n=50)
+    chain = f"rrc:16,20|flip:0.5|{NORM}/bf16"
+    got = _run(path, chain, 7 * 3, 8, 4, graphs=True)
+    want = []
+    for e in range(2, 5):
+        want += list(O.loader_batches(path, 8, "random", 9, e, pipelines={"image": oracle_spec(chain)}))
+    assert len(got) == len(want) == 21
+    for k, ((gi, ga), (wi, wa)) in enumerate(zip(got, want)):
+        assert gi == list(wi), k
+        for f in ("image", "label"):
+            assert np.array_equal(ga[f], wa[f]), (k, f)
