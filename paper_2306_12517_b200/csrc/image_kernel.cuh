@@ -663,7 +663,8 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
   // tickets: the first `nrun` hand out runs of cw_run consecutive tiles (sample-major
   // order), the last ~2 x grid tiles go out one by one (a short tail; half tiles were
   // measured slower, 43 -> 50 us: each half re-sums its first rows and the column
-  // table); a CTA's first ticket is its block index, the rest come from a global counter
+  // table; handing out the tallest crop windows first made no difference); a CTA's
+  // first ticket is its block index, the rest come from a global counter
   const int total = A.count * tps, G = gridDim.x;
   const int run = P.cw_run, tail = min(total, 2 * G), nrun = (total - tail) / run, head = nrun * run;
   const int ntickets = nrun + (total - head);
