@@ -1680,6 +1680,12 @@ static int process_slot(bbx_loader* L, int s) {
   for (size_t p = 0; p < L->plans.size(); ++p) any_status = any_status || S.plan_has_rle[p] || S.plan_has_jpeg[p];
   int launches = 0;
   int64_t kbytes = 0, klaunch = 0, d2h = 0;
+  bool wait_release;   // the consumer released the slot since its last batch: order after that
+  {
+    std::lock_guard<std::mutex> g(L->mu);
+    wait_release = S.released_pending;
+    S.released_pending = false;
+  }
   // The batch's stream work: H2D, waits, kernels, status read-back, `done` record.
   // cap: recorded into a CUDA graph instead of issued (stream capture).
   auto enqueue = [&](bool cap) -> int {
@@ -1702,12 +1708,6 @@ static int process_slot(bbx_loader* L, int s) {
     }
     S.h2d_on_compute = h2d_compute;
     S.last_stream = sk;
-    bool wait_release;
-    {
-      std::lock_guard<std::mutex> g(L->mu);
-      wait_release = S.released_pending;
-      S.released_pending = false;
-    }
     // a captured batch always waits on the slot's release event (a no-op when the
     // consumer has not recorded a newer one): the graph is replayed every batch
     if (cap) CK(cudaStreamWaitEvent(cs, S.release, cudaEventWaitExternal));
@@ -1823,10 +1823,6 @@ static int process_slot(bbx_loader* L, int s) {
   const bool graph_ok = L->use_graphs && h2d_compute && !prof && !any_status && count == L->batch && !L->pp.capacity;
   if (graph_ok && S.gexec[sk]) {
     if (S.used && S.last_stream != sk) CK(cudaStreamWaitEvent(cs, S.done, 0));
-    {
-      std::lock_guard<std::mutex> g(L->mu);
-      S.released_pending = false;
-    }
     CK(cudaGraphLaunch(S.gexec[sk], cs));
     S.h2d_on_compute = true;
     S.last_stream = sk;
