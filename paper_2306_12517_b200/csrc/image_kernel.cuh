@@ -705,7 +705,14 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
       bool done = false;
       if (left == 0) {
         const unsigned long long u = next_u;
-        if (lane == 0) next_u = G + atomicAdd(&A.ticket[0], 1ull);   // consumed when this run ends
+        if (lane == 0) {   // consumed when this run ends
+          // every CTA fetches once per run it starts plus once more (the ticket that stops
+          // it): the launch's last fetch is number ntickets + G, after which no CTA touches
+          // the counter again -- that fetch re-zeroes it for the next launch
+          const unsigned long long old = atomicAdd(&A.ticket[0], 1ull);
+          if (old == (unsigned long long)ntickets + (unsigned long long)G - 1ull) A.ticket[0] = 0;
+          next_u = G + old;
+        }
         next_u = __shfl_sync(0xffffffffu, next_u, 0);
         int t;
         if (u >= (unsigned long long)ntickets) {
@@ -728,13 +735,6 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
         if (lane == 0) {
           hdr[0] = -1;
           mbar_arrive_tx(&full[b], 0);
-          // the last CTA to finish re-zeroes the ticket for the next launch
-          __threadfence();
-          if (atomicAdd(&A.ticket[1], 1ull) == (unsigned long long)gridDim.x - 1) {
-            A.ticket[0] = 0;
-            A.ticket[1] = 0;
-            __threadfence();
-          }
         }
         break;
       }
