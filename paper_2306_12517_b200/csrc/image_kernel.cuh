@@ -571,9 +571,9 @@ __host__ __device__ inline int cw_lut_bytes(const PlanDev& P) {
 }
 __host__ __device__ inline int cw_bar_off(const PlanDev& P) { return cw_lut_bytes(P); }
 __host__ __device__ inline int cw_stage_off(const PlanDev& P) { return cw_bar_off(P) + 16 * kCwStages; }
-// ring entry (stages + 1 of them): header (16 B: tile id, sample, live, new-sample) | column table xt[owp] |
+// ring entry (stages + 1 of them): header (16 B: first row, sample, live, new-sample) | the sample's column parameters (32 B) |
 // per output row uint4 {even row's stage offset, odd row's stage offset, tag_even | tag_odd << 16, 4 * w_odd}
-__host__ __device__ inline int cw_tap_off(const PlanDev& P) { return 16 + align_up(tab_owp(P) * 4, 16); }
+__host__ __device__ inline int cw_tap_off(const PlanDev&) { return 48; }
 __host__ __device__ inline int cw_stage_meta(const PlanDev& P) { return cw_tap_off(P) + 16 * P.rows_per_tile; }
 __host__ __device__ inline int cw_src_stage(const PlanDev& P) { return P.cw_slots * cw_span_pad(P); }
 __host__ __device__ inline int cw_smem_bytes(const PlanDev& P) {
@@ -839,16 +839,11 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
       }
       if (live) {
         const int sh = S.sh;
-        if (newxt) {                                   // the column table of a new sample
-          uint32_t* xt = reinterpret_cast<uint32_t*>(metas + m * meta + 16);
-          const int lft = prm[1], cwd = prm[3];
+        if (newxt && lane == 0) {                      // a new sample: the parameters of its column taps
+          int32_t* cp = reinterpret_cast<int32_t*>(metas + m * meta + 16);
           const uint32_t ph4 = aligned ? (uint32_t)((reinterpret_cast<uintptr_t>(S.base) + (uintptr_t)col_lo * C) & 3u) : 0u;
-          for (int ox = lane; ox < OW; ox += 32) {
-            int x0, x1, wx;
-            lin_axis(affine ? bx0 + bxs * ox : back_x(P, prm, ox), P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
-            const int c0 = (lft + x0) >> sh, c1 = (lft + x1) >> sh;
-            xt[ox] = ((uint32_t)((c0 - col_lo) * C) + ph4) | ((uint32_t)wx << 16) | (c1 == c0 ? (1u << 28) : 0u);
-          }
+          reinterpret_cast<int4*>(cp)[0] = make_int4(prm[1], prm[3], affine ? bx0 : INT32_MIN, bxs);
+          reinterpret_cast<int4*>(cp)[1] = make_int4(col_lo, (int)ph4, sh, cs);
         }
         uint4* taps = reinterpret_cast<uint4*>(metas + m * meta + tap_off);
         const int ya = ya_out, yb = yb_out, wy = wy_out;
@@ -931,18 +926,25 @@ __global__ void __launch_bounds__(9 * 32, 2) image_cw_kernel(const PlanDev P, co
     if (hd.x < 0) break;                               // the copy warp's stop entry
     if (hd.z && act) {
       const uint8_t* ent = metas + m * meta;
-      if (hd.w & 1) {                                  // first tile of a sample: its column table
-        const uint32_t* xt = reinterpret_cast<const uint32_t*>(ent + 16);
+      if (hd.w & 1) {                                  // first tile of a sample: this thread's two column taps
+        const int4 c0v = *reinterpret_cast<const int4*>(ent + 16), c1v = *reinterpret_cast<const int4*>(ent + 32);
+        const int lft = c0v.x, cwd = c0v.y, bx0 = c0v.z, bxs = c0v.w, col_lo = c1v.x, sh = c1v.z;
+        const uint32_t ph4 = (uint32_t)c1v.y;
+        const int32_t* prm = bx0 == INT32_MIN   // crops / flips / resizes: the generic map from the descriptor
+            ? reinterpret_cast<const int32_t*>(A.desc + (size_t)c1v.w * P.desc_stride + kDescHeader) : nullptr;
         al = (hd.w & 2) != 0;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const uint32_t e = xt[min(ox0 + q, OW - 1)];
-          const uint32_t w1 = (e >> 16) & 0xFFFu, w0 = 2048u - w1;
-          const uint32_t o = e & 0xFFFFu;
+          const int ox = min(ox0 + q, OW - 1);
+          int x0, x1, wx;
+          lin_axis(prm ? back_x(P, prm, ox) : bx0 + bxs * ox, P.canvas_w, cwd, P.lin32, P.linx_magic, x0, x1, wx);
+          const int cc0 = (lft + x0) >> sh, cc1 = (lft + x1) >> sh;
+          const uint32_t w1 = (uint32_t)wx, w0 = 2048u - w1;
+          const uint32_t o = (uint32_t)((cc0 - col_lo) * C) + ph4;
           off[q] = al ? (o & ~3u) : o;
           shf[q] = (o & 3u) * 8u;
           wp[q] = w0 | w1 << 16;
-          const bool same = (e >> 28) != 0;
+          const bool same = cc1 == cc0;
           sel1[q] = same ? 0x1100u : 0x4130u;
           sel2[q] = same ? 0x0022u : 0x0052u;
         }
