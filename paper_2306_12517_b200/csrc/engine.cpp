@@ -1661,8 +1661,11 @@ static int process_slot(bbx_loader* L, int s) {
   }
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // consecutive batches go to alternating compute streams: one batch's kernels can
-  // fill the SMs that the previous batch's tail (e.g. the last Huffman lanes) leaves idle
-  const int sk = (int)(L->batch_seq++ % (uint64_t)L->nstreams);
+  // fill the SMs that the previous batch's tail (e.g. the last Huffman lanes) leaves idle.
+  // The stream is a function of the slot (consecutive batches use consecutive slots), so
+  // each slot's captured graph is reused by every later iterator of the loader.
+  const int sk = s % L->nstreams;
+  ++L->batch_seq;
   cudaStream_t cs = L->comp_st[sk];
   const size_t bytes = resident ? L->desc_bytes : cursor;
   // A resident RAW / RLE / array batch uploads only its indices + descriptors (tens of KB): that copy
