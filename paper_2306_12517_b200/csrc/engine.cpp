@@ -1475,16 +1475,31 @@ static int process_slot(bbx_loader* L, int s) {
     const bool image = ds->fields[pl.field_index].info.kind == 4;
     JpegDesc* jds = pl.field_has_jpeg ? reinterpret_cast<JpegDesc*>(H + L->jpeg_off[p]) : nullptr;
     if (jds) { std::memset(jds, 0, sizeof(JpegDesc) * count); jst[p].assign(count, nullptr); }
+    // HBM-resident payloads need nothing from the per-position pass below but the
+    // payload offset and the RLE flag: the pool sets them too, and that pass is skipped
+    const bool finish_in_pool = par_desc && resident && !L->zc && pool_addr.empty() && !pl.field_has_jpeg;
     if (par_desc) {
       d_off.assign(count, 0); d_len.assign(count, 0); d_ok.assign(count, 0);
       const int64_t nchunk = (count + kDescChunk - 1) / kDescChunk;
       std::vector<HostErr> cerr((size_t)nchunk);
+      std::vector<uint8_t> crle((size_t)nchunk, 0);
       L->pool->parallel_for(nchunk, [&](int64_t c) {
         for (int pos = (int)(c * kDescChunk), e = std::min(count, pos + kDescChunk); pos < e; ++pos) {
           const int64_t i = S.idx[pos];
-          if (i < 0 || i >= ds->num_samples) continue;
-          d_ok[pos] = fill_desc(ds, pl, i, S.seed, S.epoch, dblk + (size_t)pos * pl.dev.desc_stride, &d_off[pos],
-                                &d_len[pos], cerr[c], pos, (int)p) ? 1 : 0;
+          uint8_t* desc = dblk + (size_t)pos * pl.dev.desc_stride;
+          if (i < 0 || i >= ds->num_samples) {
+            if (finish_in_pool) {
+              std::memset(desc, 0, pl.dev.desc_stride);
+              reinterpret_cast<SampleDesc*>(desc)->skip = 1;
+            }
+            continue;
+          }
+          d_ok[pos] = fill_desc(ds, pl, i, S.seed, S.epoch, desc, &d_off[pos], &d_len[pos], cerr[c], pos, (int)p) ? 1 : 0;
+          if (finish_in_pool && d_ok[pos]) {
+            SampleDesc* d = reinterpret_cast<SampleDesc*>(desc);
+            d->src = d_off[pos];                        // absolute file offset; base = heap - heap_offset
+            if (d->codec == CODEC_RLE && image) crle[c] = 1;
+          }
         }
       });
       for (const HostErr& e : cerr)   // chunks are in position order: the first error is the lowest
@@ -1492,6 +1507,10 @@ static int process_slot(bbx_loader* L, int s) {
           if (S.herr.pos < 0 || e.pos < S.herr.pos || (e.pos == S.herr.pos && e.plan < S.herr.plan)) S.herr = e;
           break;
         }
+      if (finish_in_pool) {
+        for (uint8_t f : crle) S.plan_has_rle[p] |= f;
+        continue;
+      }
     }
     for (int pos = 0; pos < count; ++pos) {
       int64_t i = S.idx[pos];
