@@ -526,20 +526,23 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 //
 // Persistent CTAs (SMs x resident CTAs) walk the batch's tiles (tile =
 // rows_per_tile output rows of one sample), taking runs of cw_run consecutive
-// tiles from a global ticket that the last CTA re-zeroes, so SMs that drew
-// cheap samples take more.  A CTA is one copy warp plus ceil(OW / 64) compute
-// warps; compute thread x owns output columns 2x, 2x + 1 of EVERY tile the CTA
-// takes, so its per-column state survives from tile to tile of a sample.
+// tiles from a global ticket counter (the launch's last fetch re-zeroes it), so
+// SMs that drew cheap samples take more.  A CTA is one copy warp plus
+// ceil(OW / 64) compute warps; compute thread x owns output columns 2x, 2x + 1 of
+// EVERY tile the CTA takes, so its per-column state survives from tile to tile of
+// a sample.
 //
-// Copy warp: takes the tickets, writes each tile's geometry into a ring entry
-// (the column table once per sample; per output row the two source rows'
-// stage offsets, their absolute row numbers and the blend weight), then --
-// once the compute warps have released the stage ("empty" mbarrier) -- moves
-// the tile's source rows into it with cp.async.bulk (TMA 1-D, completion
-// counted in bytes on the stage's "full" mbarrier): one copy per row when the
-// window is narrower than the row stride (only the window's columns cross
-// L2 -> SMEM), else one copy for the whole row range.  It also gathers the
-// batch's scalar fields with tile 0 of each sample.
+// Copy warp: takes the tickets (the next run's is fetched while the current run is
+// handed out); per tile, once the compute warps have released the stage ("empty"
+// mbarrier), it moves the tile's source rows into it with cp.async.bulk (TMA 1-D,
+// completion counted in bytes on the stage's "full" mbarrier: one copy per row when
+// whole-row copies would move >= 25 % more than the window, else one copy for the
+// row range), and while they are in flight writes the tile's geometry into a ring
+// entry: on a sample's first tile its column parameters (the compute threads derive
+// their own two columns' taps from them), per output row the smem offsets of its
+// even and odd source rows, the odd weight and the new-row flags; the arrive on
+// "full" comes after.  It also gathers the batch's scalar fields with tile 0 of each
+// sample.
 //
 // Compute: the 2-tap horizontal sums of a source row are formed when the row
 // first appears for its parity (even / odd absolute row: the two taps of an
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 4) image_kernel(const PlanDev P, con
 //     s = 4 w_even h_even + 4 w_odd h_odd + 2^23 = 4 (w_even h_even + w_odd h_odd + 2^21),  u = s >> 24,
 // the same integer the tile kernel / oracle form ((w0 h0 + w1 h1 + 2^21) >> 22,
 // bit for bit).  When a sample's row stride is a multiple of 4 every staged row
-// has the same byte phase mod 4, so the column table carries it and a tap's
+// has the same byte phase mod 4, so the column offsets carry it and a tap's
 // bytes are three aligned shared loads at row + column offset.  u -> output:
 // f16 / bf16 through a per-channel f32 affine map fma(u, A, B) that the host
 // proved equal to the exact value table for all 256 inputs (packed f32x2 math,
