@@ -472,6 +472,7 @@ def compact(leg: dict) -> dict:
     cb = leg.get("cpu_baseline") or {}
     return {"value": round(leg.get("value") or 0), "e2e": round(e.get("value") or 0),
             "e2e_frac_pcie": round(e.get("frac_pcie") or 0, 3), "ms_step": round(leg.get("ms_per_step") or 0, 4),
+            "dev_ms": round(leg.get("device_ms_per_batch") or 0, 4),
             "parity_ok": leg.get("parity_ok"), "cpu": round(cb["value"]) if cb.get("value") else None}
 
 
@@ -538,6 +539,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
+    ap.add_argument("--details", default=None, help="write every leg's full record to this JSON file")
     ap.add_argument("--workloads", default="raw,cifar,jpeg,jpeg160,val,ndarray",
                     help="comma list of " + ", ".join(f"{k} ({v[0]})" for k, v in LEGS.items()))
     args = ap.parse_args()
@@ -591,9 +593,13 @@ def main():
             "e2e": head["e2e"], "roofline": head.get("roofline"), "cpu_baseline": head.get("cpu_baseline"),
             "gpu_launches": head["gpu_launches"], "clocks": head.get("clocks"),
             "parity_ok": all(legs[n].get("parity_ok") for n in names),
-            "workloads": {LEGS[n][0]: legs[n] for n in names},
             "config": config,
         }
+        # the line stays short enough for a log tail to show it whole; every leg's full
+        # record (its own e2e / cpu_baseline / clocks / rooflines) goes to --details
+        if args.details:
+            with open(args.details, "w") as fh:
+                json.dump(dict(line, workloads={LEGS[n][0]: legs[n] for n in names}), fh, indent=1)
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
