@@ -1402,6 +1402,34 @@ static int page_batch(bbx_loader* L, Slot& S, int count, std::vector<std::vector
   return BBX_OK;
 }
 
+// A profiled batch's kernel window (events k0 / k1 on its compute stream), added
+// to the stats once its events have completed.  The host never waits for them on
+// the batch's own step (that would drain the GPU queue, and the next profiled
+// launch would then be timed from an idle GPU, host launch latency included): they
+// are read when the slot is reused, or by bbx_loader_get_stats.  Caller holds
+// stats_mu; k1 has completed.
+static void collect_timing(bbx_loader* L, Slot& S) {
+  if (!S.timed) return;
+  S.timed = false;
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, S.k0, S.k1) != cudaSuccess) { cudaGetLastError(); return; }
+  float a0 = 0.f, a1 = 0.f;   // absolute k0 / k1 against the loader's reference event
+  if (L->t_ref && cudaEventElapsedTime(&a0, L->t_ref, S.k0) == cudaSuccess &&
+      cudaEventElapsedTime(&a1, L->t_ref, S.k1) == cudaSuccess) {
+    if (L->prof_every == 1 && L->last_k1_ms >= 0.f && a0 > L->last_k1_ms) {
+      L->stats.gap_seconds += (a0 - L->last_k1_ms) * 1e-3;
+      float ah = 0.f;   // of that gap: the part spent waiting for this batch's H2D (host-late staging)
+      if (S.h2d_timed && cudaEventElapsedTime(&ah, L->t_ref, S.h2d_t) == cudaSuccess && ah > L->last_k1_ms)
+        L->stats.h2d_late_seconds += (std::min(ah, a0) - L->last_k1_ms) * 1e-3;
+    }
+    L->last_k1_ms = a1;
+  }
+  L->stats.kernel_seconds += ms * 1e-3;
+  L->stats.timed_batches += 1;
+  L->stats.kernel_timed += S.timed_launches;
+  L->stats.kernel_bytes += S.timed_bytes;
+}
+
 static int process_slot(bbx_loader* L, int s) {
   Slot& S = L->slots[s];
   const bbx_dataset* ds = L->ds;
@@ -1411,6 +1439,11 @@ static int process_slot(bbx_loader* L, int s) {
   int64_t zc_bytes = 0;
   // the pinned slot may still be the source of the previous H2D
   if (S.used) CK(cudaEventSynchronize(S.h2d_on_compute ? S.done : S.h2d_done));
+  if (S.used) {   // the slot's previous batch: its profiling window, if it had one
+    CK(cudaEventSynchronize(S.done));
+    std::lock_guard<std::mutex> g(L->stats_mu);
+    collect_timing(L, S);
+  }
   ++S.serial;
   S.herr = HostErr{};
   S.plan_has_rle.assign(L->plans.size(), 0);
@@ -1822,9 +1855,12 @@ static int process_slot(bbx_loader* L, int s) {
       launches += (pl.dev.src_kind == SRC_ARRAY || pl.dev.cw) ? 1 : 2;   // K1 = prologue + tiles (column walker: one kernel)
     }
     if (prof) CK(cudaEventRecord(S.k1, cs));
-    S.timed = prof;
-    S.timed_launches = klaunch;
-    S.timed_bytes = kbytes;
+    {
+      std::lock_guard<std::mutex> g(L->stats_mu);   // read by bbx_loader_get_stats on the consumer thread
+      S.timed = prof;
+      S.timed_launches = klaunch;
+      S.timed_bytes = kbytes;
+    }
     if (SA.n_fields && count && fused_plan < 0) {
       if (launch_scalar_gather(SA, cs)) return fail(BBX_CUDA_ERROR, "scalar gather launch failed");
       ++launches;
@@ -2170,33 +2206,12 @@ bbx_status bbx_loader_wait(bbx_loader* L, int32_t slot, int64_t* bad_pos) {
   // batch is complete as far as the host knows (host-side sample errors are final),
   // and the consumer's stream is ordered after it by bbx_loader_stream_wait -- the
   // consumer keeps slot_count - 1 batches queued on the GPU instead of syncing per step.
-  bool need_sync = S.timed;
+  bool need_sync = false;
   for (size_t p = 0; p < L->plans.size(); ++p) need_sync = need_sync || S.plan_has_rle[p] || S.plan_has_jpeg[p];
   cudaError_t e = need_sync ? cudaEventSynchronize(S.done) : cudaSuccess;
   {
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.wait_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    if (e == cudaSuccess && S.timed) {
-      float ms = 0.f;
-      if (cudaEventElapsedTime(&ms, S.k0, S.k1) == cudaSuccess) {
-        float a0 = 0.f, a1 = 0.f;   // absolute k0 / k1 against the loader's reference event
-        if (L->t_ref && cudaEventElapsedTime(&a0, L->t_ref, S.k0) == cudaSuccess &&
-            cudaEventElapsedTime(&a1, L->t_ref, S.k1) == cudaSuccess) {
-          if (L->prof_every == 1 && L->last_k1_ms >= 0.f && a0 > L->last_k1_ms) {
-            L->stats.gap_seconds += (a0 - L->last_k1_ms) * 1e-3;
-            float ah = 0.f;   // of that gap: the part spent waiting for this batch's H2D (host-late staging)
-            if (S.h2d_timed && cudaEventElapsedTime(&ah, L->t_ref, S.h2d_t) == cudaSuccess && ah > L->last_k1_ms)
-              L->stats.h2d_late_seconds += (std::min(ah, a0) - L->last_k1_ms) * 1e-3;
-          }
-          L->last_k1_ms = a1;
-        }
-        L->stats.kernel_seconds += ms * 1e-3;
-        L->stats.timed_batches += 1;
-        L->stats.kernel_timed += S.timed_launches;
-        L->stats.kernel_bytes += S.timed_bytes;
-      }
-      S.timed = false;
-    }
   }
   if (e != cudaSuccess) return (bbx_status)fail(BBX_CUDA_ERROR, "batch failed on device: %s", cudaGetErrorString(e));
   // merge host-detected and device-detected per-sample failures: lowest position wins
@@ -2370,7 +2385,13 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
 
 bbx_status bbx_loader_get_stats(const bbx_loader* L, bbx_loader_stats* out) {
   if (!L || !out) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null argument");
-  std::lock_guard<std::mutex> g(const_cast<bbx_loader*>(L)->stats_mu);
+  bbx_loader* M = const_cast<bbx_loader*>(L);
+  std::lock_guard<std::mutex> g(M->stats_mu);
+  if (L->finalized) {
+    cudaSetDevice(L->device);
+    for (auto& S : M->slots)   // profiled batches not yet read: wait for their windows
+      if (S.timed && cudaEventSynchronize(S.k1) == cudaSuccess) collect_timing(M, S);
+  }
   *out = L->stats;
   out->numa_node = L->numa_node;
   out->staging_threads = L->pool ? L->pool->size() : 0;
@@ -2381,6 +2402,7 @@ bbx_status bbx_loader_reset_stats(bbx_loader* L) {
   if (!L) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "null loader");
   std::lock_guard<std::mutex> g(L->stats_mu);
   L->stats = bbx_loader_stats{};
+  for (auto& S : L->slots) S.timed = false;   // windows of batches before the reset are not counted
   L->last_k1_ms = -1.f;
   return BBX_OK;
 }
