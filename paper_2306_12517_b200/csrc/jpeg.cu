@@ -479,6 +479,16 @@ __device__ __forceinline__ uint32_t ycc_g(int Y, int cb, int cr) {
   return (uint32_t)min(max(Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16), 0), 255);
 }
 __device__ __forceinline__ uint32_t ycc_b(int Y, int cb) { return (uint32_t)min(max(Y + ((116130 * cb + 32768) >> 16), 0), 255); }
+__device__ __forceinline__ int ycc_r_raw(int Y, int cr) { return Y + ((91881 * cr + 32768) >> 16); }
+__device__ __forceinline__ int ycc_g_raw(int Y, int cb, int cr) { return Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16); }
+__device__ __forceinline__ int ycc_b_raw(int Y, int cb) { return Y + ((116130 * cb + 32768) >> 16); }
+// four s32 -> u8 with saturation, packed little-endian p0 p1 p2 p3 (two cvt.pack.sat)
+__device__ __forceinline__ uint32_t pack4_sat(int p0, int p1, int p2, int p3) {
+  uint32_t t, d;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(t) : "r"(p3), "r"(p2));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(p1), "r"(p0), "r"(t));
+  return d;
+}
 
 template <int N>
 __device__ __forceinline__ void store_px(uint8_t* o, const uint32_t (&px)[N], int n) {   // first n bytes, packed
@@ -614,13 +624,25 @@ __global__ void __launch_bounds__(kColorThreads) jpeg_color_kernel(const JpegArg
           u[c][2 * k + 1] = ((3 * cs[1 + k] + cs[2 + k] + 7) >> 4) - 128;
         }
       }
-      uint32_t px[24];
+      // R, G, B unclamped; the clamp to [0, 255] is the saturation of the byte packing
+      int v[24];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int Y = (int)(((k < 4 ? y8.x : y8.y) >> (8 * (k & 3))) & 0xFF), cb = u[0][k], cr = u[1][k];
-        px[3 * k] = ycc_r(Y, cr); px[3 * k + 1] = ycc_g(Y, cb, cr); px[3 * k + 2] = ycc_b(Y, cb);
+        v[3 * k] = ycc_r_raw(Y, cr); v[3 * k + 1] = ycc_g_raw(Y, cb, cr); v[3 * k + 2] = ycc_b_raw(Y, cb);
       }
-      store_px(out + (size_t)y * pitch + (size_t)x0 * 3, px, 3 * min(8, w - x0));
+      uint8_t* const o = out + (size_t)y * pitch + (size_t)x0 * 3;
+      if (x0 + 8 <= w && (reinterpret_cast<uintptr_t>(o) & 7) == 0) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          *reinterpret_cast<uint2*>(o + 8 * q) = make_uint2(pack4_sat(v[8 * q], v[8 * q + 1], v[8 * q + 2], v[8 * q + 3]),
+                                                            pack4_sat(v[8 * q + 4], v[8 * q + 5], v[8 * q + 6], v[8 * q + 7]));
+      } else {
+        uint32_t px[24];
+#pragma unroll
+        for (int i = 0; i < 24; ++i) px[i] = (uint32_t)min(max(v[i], 0), 255);
+        store_px(o, px, 3 * min(8, w - x0));
+      }
       yy += dyy; qq += dqq; if (qq >= no) { qq -= no; ++yy; }
     }
     return;
