@@ -337,6 +337,13 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
 // Dequantize + islow IDCT (13-bit constants, 2 pass-1 bits, 32-bit modular
 // arithmetic as oracle/jpeg_oracle.c) of one 8x8 block in registers.
 
+// four s32 -> u8 with saturation, packed little-endian p0 p1 p2 p3 (two cvt.pack.sat)
+__device__ __forceinline__ uint32_t pack4_sat(int p0, int p1, int p2, int p3) {
+  uint32_t t, d;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(t) : "r"(p3), "r"(p2));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(p1), "r"(p0), "r"(t));
+  return d;
+}
 __device__ __forceinline__ uint32_t range_out(int v) {   // post-IDCT range_limit[v & 1023]
   int s = ((v & 1023) ^ 512) - 512 + 128;
   return (uint32_t)min(max(s, 0), 255);
@@ -407,18 +414,20 @@ __device__ __forceinline__ void idct_block(const int16_t* coef, const uint16_t* 
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     int* x = w + r * 8;
-    uint32_t o[8];
+    uint2 row;
     if ((x[1] | x[2] | x[3] | x[4] | x[5] | x[6] | x[7]) == 0) {
       const uint32_t v = range_out((int)((uint32_t)x[0] + 16u) >> 5);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = v;
+      row.x = row.y = v * 0x01010101u;
     } else {
       idct_1d<false>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7]);
+      // range_limit[v & 1023] = clamp(((v & 1023) ^ 512) - 512 + 128, 0, 255): the clamp is
+      // the saturation of the byte packing
+      int q[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = range_out(x[j]);
+      for (int j = 0; j < 8; ++j) q[j] = ((x[j] & 1023) ^ 512) - 384;
+      row = make_uint2(pack4_sat(q[0], q[1], q[2], q[3]), pack4_sat(q[4], q[5], q[6], q[7]));
     }
-    *reinterpret_cast<uint2*>(dst + (size_t)r * stride) =
-        make_uint2(o[0] | o[1] << 8 | o[2] << 16 | o[3] << 24, o[4] | o[5] << 8 | o[6] << 16 | o[7] << 24);
+    *reinterpret_cast<uint2*>(dst + (size_t)r * stride) = row;
   }
 }
 
@@ -482,13 +491,6 @@ __device__ __forceinline__ uint32_t ycc_b(int Y, int cb) { return (uint32_t)min(
 __device__ __forceinline__ int ycc_r_raw(int Y, int cr) { return Y + ((91881 * cr + 32768) >> 16); }
 __device__ __forceinline__ int ycc_g_raw(int Y, int cb, int cr) { return Y + ((-22554 * cb + 32768 - 46802 * cr) >> 16); }
 __device__ __forceinline__ int ycc_b_raw(int Y, int cb) { return Y + ((116130 * cb + 32768) >> 16); }
-// four s32 -> u8 with saturation, packed little-endian p0 p1 p2 p3 (two cvt.pack.sat)
-__device__ __forceinline__ uint32_t pack4_sat(int p0, int p1, int p2, int p3) {
-  uint32_t t, d;
-  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(t) : "r"(p3), "r"(p2));
-  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(p1), "r"(p0), "r"(t));
-  return d;
-}
 
 template <int N>
 __device__ __forceinline__ void store_px(uint8_t* o, const uint32_t (&px)[N], int n) {   // first n bytes, packed
