@@ -41,7 +41,8 @@ constexpr int kHuffThreads = 256;           // 8 warps share one copy of the sme
 constexpr int kHuffCtasPerSm = 3;           // a batch of 1024 ImageNet-sized JPEGs has ~110k intervals: ~3 CTAs
                                             // per SM hold all of them at once (4 / 5 measured the same)
 constexpr int kExtraSymbols = 4;   // AC symbols decoded after the first in one iteration
-                                   // (A/B, configs[2] value: 2 / 4 / 6 / 8 -> 2.65 / 2.73 / 2.65 / 2.51 M img/s)
+                                   // (A/B, configs[2] value: 2 / 4 / 6 / 8 -> 2.65 / 2.73 / 2.65 / 2.51 M img/s;
+                                   // branch-free extras: 3 / 4 / 5 / 6 -> J2 324 / 313 / 316 / 334 us under ncu)
 // Each lane assembles its current 8x8 block in shared memory and writes it to the
 // coefficient buffer as eight 16-byte stores when the block ends: scattered 2-byte
 // global stores of single coefficients kept the L1 busy with one sector per lane per
@@ -217,22 +218,22 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
       if (!(carry | marker) && __vcmpeq4(wv, 0xFFFFFFFFu) == 0) {
         acc |= (uint64_t)wv << (32 - nb);
         nb += 32;
-      } else {                                       // stuffing / marker: byte by byte
+      } else if (marker) {                           // past a marker: zeros (acc's low bits are zero)
+        nb += 32;
+      } else {                                       // a 0xFF in the word: byte by byte, branch-free
         uint32_t o = 0;
         int no = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint32_t by = (wv >> (24 - 8 * j)) & 0xFFu;
-          if (marker) { o <<= 8; ++no; }
-          else if (carry) {
-            carry = false;
-            if (by == 0) { o = (o << 8) | 0xFFu; ++no; }
-            else { marker = true; o <<= 8; ++no; }
-          } else if (by == 0xFFu) {
-            carry = true;
-          } else {
-            o = (o << 8) | by; ++no;
-          }
+          // after a 0xFF: 0x00 is a data 0xFF, anything else a marker (zeros from there on)
+          const bool mk = marker | (carry & (by != 0));
+          const bool emit = mk | carry | (by != 0xFFu);
+          const uint32_t ob = mk ? 0u : (carry ? 0xFFu : by);
+          carry = !mk && !carry && by == 0xFFu;
+          marker = mk;
+          o = emit ? (o << 8) | ob : o;
+          no += emit ? 1 : 0;
         }
         if (no) acc |= (uint64_t)o << (64 - nb - 8 * no);
         nb += 8 * no;
@@ -297,20 +298,19 @@ __global__ void __launch_bounds__(kHuffThreads, kHuffCtasPerSm) jpeg_huffman_ker
     kk += adv;                                       // an end of block advances past 63
     // more AC symbols in the same iteration while the block continues and the
     // bit buffer holds the symbol with its value: code + extra bits within the
-    // 11-bit peek (entries that need more extra bits wait for the next iteration)
+    // 11-bit peek (entries that need more extra bits wait for the next iteration).
+    // Branch-free: every lane looks its entry up and consumes nothing when it may
+    // not (nested ifs diverged per symbol: J2 354 -> 320 us under ncu)
 #pragma unroll
     for (int extra = 0; extra < kExtraSymbols; ++extra) {
-      if (kk < 64 && !bad && nb >= kJpegFastBits) {
-        const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
-        if (e2 & kFastFull) {
-          const int l2 = (int)((e2 >> 25) & 31), adv2 = (int)((e2 >> kFastAdvShift) & kFastAdvMask);
-          acc <<= l2;
-          nb -= l2;
-          const int v2 = (int)(int16_t)(e2 & 0xFFFF), pos2 = kk + adv2 - 1;
-          if (v2 != 0) myblk[min(pos2, 63)] = (int16_t)v2;
-          kk += adv2;
-        }
-      }
+      const uint32_t e2 = tab[tac + (uint32_t)(acc >> (64 - kJpegFastBits))];
+      const bool ok = (e2 & kFastFull) && kk < 64 && !bad && nb >= kJpegFastBits;
+      const int l2 = ok ? (int)((e2 >> 25) & 31) : 0, adv2 = ok ? (int)((e2 >> kFastAdvShift) & kFastAdvMask) : 0;
+      acc <<= l2;
+      nb -= l2;
+      const int v2 = (int)(int16_t)(e2 & 0xFFFF), pos2 = kk + adv2 - 1;
+      if (ok && v2 != 0) myblk[min(pos2, 63)] = (int16_t)v2;
+      kk += adv2;
     }
     if (kk >= 64 || bad) {                           // block done: blocks are stored in decode order
       uint4* z = reinterpret_cast<uint4*>(myblk);
