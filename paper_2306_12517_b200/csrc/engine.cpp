@@ -126,9 +126,11 @@ static std::vector<int> gpu_local_cpus(int device, int* node_out) {
 }
 
 void Pool::work(Job& job) {
-  for (int64_t i; (i = job.next.fetch_add(1)) < job.n;) {
-    (*job.fn)(i);
-    if (job.done.fetch_add(1) + 1 == job.n) {
+  const int64_t g = job.grain;
+  for (int64_t i; (i = job.next.fetch_add(g)) < job.n;) {
+    const int64_t e = std::min(job.n, i + g);
+    for (int64_t k = i; k < e; ++k) (*job.fn)(k);
+    if (job.done.fetch_add(e - i) + (e - i) == job.n) {
       std::lock_guard<std::mutex> g(mu_);
       done_cv_.notify_all();
     }
@@ -159,12 +161,13 @@ void Pool::run() {
     if (job) work(*job);
   }
 }
-void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn) {
+void Pool::parallel_for(int64_t n, const std::function<void(int64_t)>& fn, int64_t grain) {
   if (n <= 0) return;
   if (workers_.empty() || n == 1) { for (int64_t i = 0; i < n; ++i) fn(i); return; }
   auto job = std::make_shared<Job>();
   job->fn = &fn;
   job->n = n;
+  job->grain = std::max<int64_t>(1, grain);
   {
     std::lock_guard<std::mutex> g(mu_);
     job_ = job;
@@ -1706,10 +1709,16 @@ static int process_slot(bbx_loader* L, int s) {
     L->stats.io_reads += (int64_t)copies.size();
   } else if (!copies.empty()) {
     const uint8_t* map_end = ds->map + ds->map_len;
+    // small payloads (CIFAR-sized: ~3 KB) are claimed several at a time, ~16 KB per claim
+    // (A/B, configs[0] e2e: per-item claims 4.3-5.1, 16 KB 5.2-5.7, 64 KB 4.4-5.5 M img/s;
+    // the larger payloads of configs[1] / [2] keep one copy per claim)
+    constexpr int64_t kGatherGrainBytes = 16384;
+    const int64_t per_copy = (int64_t)(cursor - pay_base) / (int64_t)copies.size();
+    const int64_t grain = std::min<int64_t>(64, std::max<int64_t>(1, kGatherGrainBytes / std::max<int64_t>(per_copy, 1)));
     L->pool->parallel_for((int64_t)copies.size(), [&](int64_t k) {
       const Copy& c = copies[k];
       gather_rows(c.dst, c.dst_stride, c.src, c.src_stride, c.row_bytes, c.rows, map_end);
-    });
+    }, grain);
   }
   double t1 = (double)std::chrono::steady_clock::now().time_since_epoch().count() * 1e-9;
   // consecutive batches go to alternating compute streams: one batch's kernels can

@@ -111,7 +111,9 @@ class Pool {
   explicit Pool(int n);
   ~Pool();
   // Runs fn(i) for i in [0, n) on the pool (and the caller); returns when done.
-  void parallel_for(int64_t n, const std::function<void(int64_t)>& fn);
+  // fn(0) .. fn(n - 1) on the workers and the caller; indices are claimed `grain` at a
+  // time (tiny items: one shared-counter round trip per item costs more than the item)
+  void parallel_for(int64_t n, const std::function<void(int64_t)>& fn, int64_t grain = 1);
   int size() const { return (int)workers_.size() + 1; }
   // Restrict the worker threads to `cpus` (NUMA placement of the staging gather).
   void pin(const std::vector<int>& cpus);
@@ -122,8 +124,9 @@ class Pool {
   // claim indices of the next call (workers hold a shared_ptr to the job).
   struct Job {
     const std::function<void(int64_t)>* fn = nullptr;
-    int64_t n = 0;
-    std::atomic<int64_t> next{0}, done{0};
+    int64_t n = 0, grain = 1;
+    alignas(64) std::atomic<int64_t> next{0};   // claimed by every worker
+    alignas(64) std::atomic<int64_t> done{0};   // polled by the caller
   };
   void run();
   void work(Job& job);
