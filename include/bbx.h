@@ -198,9 +198,11 @@ typedef struct {
   double  pipeline_seconds;   /* pipeline-thread time per batch: descriptors, staging, H2D and launch calls */
 } bbx_loader_stats;
 /* Zero-copy payloads: with a pinned host heap (bbx_dataset_pin_host) and no
- * RLE / JPEG fields, kernels read each sample's payload window straight from
- * host memory over PCIe -- no CPU gather, no staging copy.  Call before the
- * first submit; ignored when the plan cannot use it. */
+ * RLE / JPEG fields, each sample's payload window comes straight from host
+ * memory over PCIe -- no CPU gather, no staging copy: a gather kernel pulls the
+ * batch's rows into the slot's HBM region (option "zc_gather", default), or K1
+ * reads them itself ("zc_gather" 0).  Call before the first submit; ignored when
+ * the plan cannot use it. */
 bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
 /* Loader tuning options (before the first submit; the defaults are the
  * measured-best settings):
@@ -217,6 +219,8 @@ bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
  *   "read_latency_ns"       0: Direct: latency spun before each read (reader.py:369-370)
  *   "compute_streams"       2: consecutive batches alternate between two CUDA streams, so
  *                              one batch's kernels fill SMs the previous batch's tail leaves idle
+ *   "zc_gather"             1: zero-copy payloads are gathered into HBM by a kernel before K1
+ *                              (0: K1 reads the mapped host heap directly; fewer reads in flight)
  * Unknown names return BBX_INVALID_ARGUMENT. */
 bbx_status bbx_loader_set_option(bbx_loader* ld, const char* name, int64_t value);
 /* HBM page pool -- ProcessCacheStrategy (reader.py:152-297 ProcessCache,

@@ -144,7 +144,19 @@ struct LaunchArgs {
   unsigned long long* ticket;  // column-walker K1: [0] next tile run, [1] CTAs done (self-resetting, zero between launches)
 };
 
+// One payload copy of a batch gathered by the device from the pinned, mapped host
+// heap (zero-copy gather): `rows` rows of `row_bytes`, source rows `src_stride`
+// apart from heap offset `src`, destination rows `dst_stride` (16-byte multiple)
+// apart from slot offset `dst` (16-byte aligned).
+struct GatherCopy {
+  uint64_t src, dst;
+  uint32_t row_bytes, rows, src_stride, dst_stride;
+};
+static_assert(sizeof(GatherCopy) == 32, "GatherCopy layout");
+
 // kernels.cu
+int launch_host_gather(const uint8_t* heap, uint64_t heap_bytes, uint8_t* slot, const GatherCopy* copies, int n,
+                       void* stream);
 int launch_rle_expand(const PlanDev& P, const LaunchArgs& A, void* stream);
 int launch_image(const PlanDev& P, const LaunchArgs& A, void* stream);
 int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream);

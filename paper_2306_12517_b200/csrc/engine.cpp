@@ -250,6 +250,7 @@ struct HostErr { int64_t pos = -1; int plan = 0; int code = 0; std::string msg; 
 struct Slot {
   uint8_t* h_stage = nullptr;
   uint8_t* d_stage = nullptr;
+  int n_gcopies = 0;                  // zero-copy gather: payload copies the device gathers for this batch
   size_t cap = 0;
   SampleStatus* d_status = nullptr;
   SampleStatus* h_status = nullptr;
@@ -361,6 +362,9 @@ struct bbx_loader {
   bool zero_copy = false;             // requested: kernels read payloads from the pinned host heap
   const uint8_t* payload_dev = nullptr;   // set at finalize: HBM heap, mapped pinned heap, or null (staging)
   bool zc = false;                    // payload_dev is host memory (zero-copy)
+  bool zc_gather = true;              // zero-copy heap: a gather kernel stages the batch's rows (option "zc_gather")
+  bool zcg = false;                   // set at finalize: zero-copy gather in use
+  size_t gcopy_off = 0;               // GatherCopy list within a slot (zero-copy gather)
   size_t pay_base = 0;                // start of the compact payload region
   bool window_staging = true;         // stage only the rows/columns a RAW sample's chain reads
   int64_t par_desc_min = 256;         // batches of at least this many samples fill descriptors on the pool
@@ -1045,6 +1049,20 @@ static int finalize_impl(bbx_loader* L) {
   bool codec_stage = false;           // RLE / JPEG payloads are expanded from a staged copy
   for (const auto& pl : L->plans) codec_stage |= !pl.scalar && (pl.field_has_rle || pl.field_has_jpeg);
   L->zc = !L->ds->d_heap && L->zero_copy && L->ds->h_heap_dev && !codec_stage;
+  // zero-copy gather: the pinned heap's window rows are gathered into the slot by a
+  // kernel (PCIe reads at the copy engine's rate, one host DRAM read per byte), and K1
+  // reads them from HBM as a staged batch -- K1 pulling its rows over PCIe itself
+  // keeps too few reads in flight
+  L->zcg = L->zc && L->zc_gather && !L->direct_io && L->pp.capacity == 0;
+  if (L->zcg) {
+    L->zc = false;
+    size_t np = 0;
+    for (const auto& pl : L->plans) np += pl.scalar ? 0 : 1;
+    L->gcopy_off = off;
+    off += (size_t)L->batch * np * sizeof(GatherCopy);
+    off = (off + 255) / 256 * 256;
+    L->desc_bytes = off;
+  }
   L->payload_dev = L->ds->d_heap ? L->ds->d_heap : (L->zc ? L->ds->h_heap_dev : nullptr);
   bool resident = L->payload_dev != nullptr;
   L->pay_base = off;
@@ -1448,6 +1466,7 @@ static int process_slot(bbx_loader* L, int s) {
     collect_timing(L, S);
   }
   ++S.serial;
+  S.n_gcopies = 0;
   S.herr = HostErr{};
   S.plan_has_rle.assign(L->plans.size(), 0);
   S.plan_has_jpeg.assign(L->plans.size(), 0);
@@ -1707,6 +1726,14 @@ static int process_slot(bbx_loader* L, int s) {
     if (io_err) return fail(BBX_INVALID_FILE, "%s: short read", ds->path.c_str());
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.io_reads += (int64_t)copies.size();
+  } else if (!copies.empty() && L->zcg) {   // the device gathers them: only the copy list goes up
+    GatherCopy* g = reinterpret_cast<GatherCopy*>(H + L->gcopy_off);
+    const uint8_t* hb = ds->map + ds->heap_offset;
+    for (size_t k = 0; k < copies.size(); ++k) {
+      const Copy& c = copies[k];
+      g[k] = GatherCopy{(uint64_t)(c.src - hb), (uint64_t)(c.dst - H), c.row_bytes, c.rows, c.src_stride, c.dst_stride};
+    }
+    S.n_gcopies = (int)copies.size();
   } else if (!copies.empty()) {
     const uint8_t* map_end = ds->map + ds->map_len;
     // small payloads (CIFAR-sized: ~3 KB) are claimed several at a time, ~16 KB per claim
@@ -1758,9 +1785,10 @@ static int process_slot(bbx_loader* L, int s) {
       CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, cs));
       S.h2d_timed = false;
     } else {
-      // H2D on the copy stream (after the previous kernels reading d_stage)
+      // H2D on the copy stream (after the previous kernels reading d_stage); a
+      // zero-copy-gather batch uploads only its descriptors and copy list
       if (S.used) CK(cudaStreamWaitEvent(L->copy_st, S.done, 0));
-      CK(cudaMemcpyAsync(S.d_stage, S.h_stage, bytes, cudaMemcpyHostToDevice, L->copy_st));
+      CK(cudaMemcpyAsync(S.d_stage, S.h_stage, S.n_gcopies ? L->pay_base : bytes, cudaMemcpyHostToDevice, L->copy_st));
       CK(cudaEventRecord(S.h2d_done, L->copy_st));
       S.h2d_timed = false;
       if (L->profiling && L->prof_every == 1) {   // idle-gap attribution needs every batch timed
@@ -1783,6 +1811,12 @@ static int process_slot(bbx_loader* L, int s) {
       CK(cudaEventRecord(L->t_ref, cs));
     }
     if (prof) CK(cudaEventRecord(S.k0, cs));
+    if (S.n_gcopies) {
+      if (launch_host_gather(ds->h_heap_dev, (uint64_t)(ds->alloc_table_offset - ds->heap_offset), S.d_stage,
+                             reinterpret_cast<const GatherCopy*>(S.d_stage + L->gcopy_off), S.n_gcopies, cs))
+        return fail(BBX_CUDA_ERROR, "gather launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      ++launches;
+    }
     d2h = 0;
     ScalarArgs SA{};
     SA.idx = reinterpret_cast<const int64_t*>(S.d_stage + L->idx_off);
@@ -1932,7 +1966,9 @@ static int process_slot(bbx_loader* L, int s) {
     std::lock_guard<std::mutex> g(L->stats_mu);
     L->stats.batches += 1;
     L->stats.samples += count;
-    L->stats.h2d_bytes += (int64_t)bytes;
+    // zero-copy gather: the descriptors go by DMA, the payload rows by the gather kernel's PCIe reads
+    L->stats.h2d_bytes += (int64_t)(S.n_gcopies ? L->pay_base : bytes);
+    if (S.n_gcopies) zc_bytes += (int64_t)(bytes - L->pay_base);
     L->stats.d2h_bytes += d2h;
     L->stats.kernel_launches += launches;
     L->stats.stage_seconds += t1 - t0;
@@ -2384,6 +2420,7 @@ bbx_status bbx_loader_set_option(bbx_loader* L, const char* name, int64_t value)
   else if (n == "read_latency_ns") L->read_latency_ns = value > 0 ? value : 0;
   else if (n == "parallel_desc_min") L->par_desc_min = value;
   else if (n == "cuda_graphs") L->use_graphs = value != 0;
+  else if (n == "zc_gather") L->zc_gather = value != 0;
   else if (n == "compute_streams") {
     if (value < 1 || value > kStreams) return (bbx_status)fail(BBX_INVALID_ARGUMENT, "compute_streams must be 1 or %d", kStreams);
     L->nstreams = (int)value;

@@ -225,6 +225,53 @@ int launch_rle_expand(const PlanDev& P, const LaunchArgs& A, void* stream) {
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// Zero-copy gather: the batch's payload rows, read by the SMs straight from the
+// pinned + mapped host heap over PCIe (the CPU touches none of the bytes: one host
+// DRAM read per byte, against three for gather -> pinned slot -> DMA), into the
+// slot's device payload region, which K1 then reads as a staged batch.  CTA per
+// copy; a warp per 496-byte segment of a row: 32 lanes load the 32 aligned
+// 16-byte chunks that cover it and lanes 0..30 each assemble one unaligned
+// 16-byte output chunk from their chunk and the next lane's (shuffle + funnel).
+__global__ void __launch_bounds__(256) host_gather_kernel(const uint8_t* __restrict__ heap, uint64_t heap_bytes,
+                                                          uint8_t* __restrict__ slot,
+                                                          const GatherCopy* __restrict__ copies) {
+  const GatherCopy c = copies[blockIdx.x];
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr uint32_t kSeg = 31 * 16;
+  const uint32_t spr = (c.row_bytes + kSeg - 1) / kSeg;
+  for (uint32_t sg = threadIdx.x >> 5; sg < c.rows * spr; sg += nw) {
+    const uint32_t r = sg / spr, q = sg - r * spr;
+    const uint64_t row = c.src + (uint64_t)r * c.src_stride, s = row + (uint64_t)q * kSeg;
+    const uint64_t end = min(row + c.row_bytes, heap_bytes);          // loads never pass the row's last chunk
+    const uint64_t al = s & ~15ull, at = al + 16ull * (uint64_t)lane;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (at < end) v = *reinterpret_cast<const uint4*>(heap + at);
+    uint4 nx;
+    nx.x = __shfl_down_sync(0xffffffffu, v.x, 1);
+    nx.y = __shfl_down_sync(0xffffffffu, v.y, 1);
+    nx.z = __shfl_down_sync(0xffffffffu, v.z, 1);
+    nx.w = __shfl_down_sync(0xffffffffu, v.w, 1);
+    const uint32_t o = q * kSeg + 16u * (uint32_t)lane;               // output byte of this lane's chunk in the row
+    if (lane == 31 || o >= c.row_bytes) continue;
+    // bytes [sh, sh + 16) of the 32 bytes (v, nx): whole words first, then the byte shift
+    const uint32_t sh = (uint32_t)(s & 15);
+    uint32_t w0 = v.x, w1 = v.y, w2 = v.z, w3 = v.w, w4 = nx.x, w5 = nx.y, w6 = nx.z, w7 = nx.w;
+    if (sh & 8) { w0 = w2; w1 = w3; w2 = w4; w3 = w5; w4 = w6; w5 = w7; }
+    if (sh & 4) { w0 = w1; w1 = w2; w2 = w3; w3 = w4; w4 = w5; }
+    const uint32_t bs = (sh & 3) * 8;
+    const uint4 out = make_uint4(__funnelshift_r(w0, w1, bs), __funnelshift_r(w1, w2, bs), __funnelshift_r(w2, w3, bs),
+                                 __funnelshift_r(w3, w4, bs));
+    *reinterpret_cast<uint4*>(slot + c.dst + (uint64_t)r * c.dst_stride + o) = out;
+  }
+}
+
+int launch_host_gather(const uint8_t* heap, uint64_t heap_bytes, uint8_t* slot, const GatherCopy* copies, int n,
+                       void* stream) {
+  if (n <= 0) return 0;
+  host_gather_kernel<<<(unsigned)n, 256, 0, (cudaStream_t)stream>>>(heap, heap_bytes, slot, copies);
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int launch_array(const PlanDev& P, const LaunchArgs& A, void* stream) {
   if (A.count <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;

@@ -254,23 +254,26 @@ def test_nchw_view_and_opaque_rejected(golden):
     ds.close()
 
 
+@pytest.mark.parametrize("gather", [1, 0])
 @pytest.mark.parametrize("chain", ["rrc:24,24|flip:0.5|normpc:123.675,116.28,103.53/58.395,57.12,57.375/f16",
                                    "crop:48,40|resize:33,17|flip:0.5|normpc:1,2,3/4,5,6/f32",
                                    "center:40,28,1.0"])
-def test_zero_copy_payloads_match_oracle(tmp_path, chain):
-    """OsCache(zero_copy=True): kernels read RAW windows straight from the pinned
-    host heap over PCIe -- same batches as the oracle, and PCIe bytes are counted."""
+def test_zero_copy_payloads_match_oracle(tmp_path, chain, gather):
+    """OsCache(zero_copy=True): the batch's RAW windows come over PCIe from the
+    pinned host heap -- gathered into HBM by host_gather_kernel (default) or read by
+    K1 itself (option zc_gather=0) -- same batches as the oracle, PCIe bytes counted."""
     path = _variable_dataset(tmp_path, bx.CodecId.SUBSAMPLE2)
     raw = tmp_path / "raw.bbox"
     src = bx.SyntheticImageSource(70, 64, 64, 3, seed=2)
     bx.write_dataset(src, raw, bx.WriterConfig(page_size=1 << 18, seed=2))
     for p in (path, raw):
         got = run_gpu(p, 16, "random", seed=5, epoch=0, pipelines={"image": chain},
-                      strategy=bx.OsCache(zero_copy=True))
+                      strategy=bx.OsCache(zero_copy=True), options={"zc_gather": gather})
         want = list(O.loader_batches(p, 16, "random", 5, 0, pipelines={"image": oracle_spec(chain)}))
         assert_same(got, want)
     ds = bx.open_dataset(raw, bx.OsCache(zero_copy=True))
-    with bx.Loader(ds, bx.LoaderConfig(batch_size=16, pipelines={"image": bx.parse_pipeline(chain)})) as ld:
+    with bx.Loader(ds, bx.LoaderConfig(batch_size=16, pipelines={"image": bx.parse_pipeline(chain)},
+                                       options={"zc_gather": gather})) as ld:
         for _ in ld.iterate_epoch(0):
             pass
         st = ld.stats()
