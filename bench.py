@@ -436,7 +436,7 @@ def run_leg(name, args, device, rank, world, barrier, reduce_max, detail_rooflin
                   "path": "Loader(OsCache): host RAM -> pinned slot -> H2D -> kernels"}
     # ---- e2e from a pinned host heap (OsCache(zero_copy=True)): a gather kernel pulls
     # each step's window rows over PCIe (one host-DRAM read per byte instead of three);
-    # RAW legs only (the codec legs stage their payloads)
+    # RAW legs (codec payloads are staged: their decode kernels would serialise with it)
     if kind in ("raw", "cifar"):
         ds3, ld3 = make_loader(path, device, rank, world, bx.OsCache(zero_copy=True), chain, order, batch, 4)
         with clk:

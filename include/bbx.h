@@ -202,7 +202,7 @@ typedef struct {
  * memory over PCIe -- no CPU gather, no staging copy: a gather kernel pulls the
  * batch's rows into the slot's HBM region (option "zc_gather", default), or K1
  * reads them itself ("zc_gather" 0).  Call before the first submit; ignored when
- * the plan cannot use it. */
+ * the plan cannot use it (RLE / JPEG plans stage their payloads). */
 bbx_status bbx_loader_set_zero_copy(bbx_loader* ld, int enabled);
 /* Loader tuning options (before the first submit; the defaults are the
  * measured-best settings):

@@ -1048,14 +1048,16 @@ static int finalize_impl(bbx_loader* L) {
   L->desc_bytes = off;
   bool codec_stage = false;           // RLE / JPEG payloads are expanded from a staged copy
   for (const auto& pl : L->plans) codec_stage |= !pl.scalar && (pl.field_has_rle || pl.field_has_jpeg);
-  L->zc = !L->ds->d_heap && L->zero_copy && L->ds->h_heap_dev && !codec_stage;
   // zero-copy gather: the pinned heap's window rows are gathered into the slot by a
-  // kernel (PCIe reads at the copy engine's rate, one host DRAM read per byte), and K1
-  // reads them from HBM as a staged batch -- K1 pulling its rows over PCIe itself
-  // keeps too few reads in flight
-  L->zcg = L->zc && L->zc_gather && !L->direct_io && L->pp.capacity == 0;
+  // kernel (PCIe reads, one host DRAM read per byte), and K1 reads them from HBM as a
+  // staged batch; direct zero-copy (K1 pulling its rows over PCIe itself) keeps too few
+  // reads in flight.  Not for RLE / JPEG plans: their decode kernels fill the SMs, so a
+  // gather kernel would serialise with them where the copy engine's DMA overlaps them
+  // (configs[2]: 1.03 vs 1.47 M img/s)
+  const bool zc_ok = !L->ds->d_heap && L->zero_copy && L->ds->h_heap_dev && !codec_stage;
+  L->zcg = zc_ok && L->zc_gather && !L->direct_io && L->pp.capacity == 0;
+  L->zc = zc_ok && !L->zcg;
   if (L->zcg) {
-    L->zc = false;
     size_t np = 0;
     for (const auto& pl : L->plans) np += pl.scalar ? 0 : 1;
     L->gcopy_off = off;

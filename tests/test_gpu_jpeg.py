@@ -75,11 +75,13 @@ def test_jpeg_grayscale_and_mixed_codecs_vs_oracle(tmp_path):
 
 
 def test_jpeg_imagenet_shape_resident_and_staged(tmp_path):
-    """configs[2]-shaped batch (256-side, 4:2:0, RRC-192 f16) through both payload paths."""
+    """configs[2]-shaped batch (256-side, 4:2:0, RRC-192 f16) through every payload
+    path: staged, HBM-resident, and a pinned heap (zero_copy requested: JPEG plans
+    stage from it, csrc/engine.cpp finalize)."""
     path = _jpeg_dataset(tmp_path, n=80, side=256, seed=9)
     chain = "rrc:192,192|flip:0.5|normpc:123.675,116.28,103.53/58.395,57.12,57.375/f16"
     want = list(O.loader_batches(path, 40, "random", 3, 0, pipelines={"image": oracle_spec(chain)}, nthreads=8))
-    for strategy in (None, bx.DeviceResident()):
+    for strategy in (None, bx.DeviceResident(), bx.OsCache(zero_copy=True)):
         got = run_gpu(path, 40, "random", seed=3, epoch=0, pipelines={"image": chain}, strategy=strategy)
         assert_same(got, want)
 

@@ -158,13 +158,17 @@ def test_chains_vs_oracle(tmp_path, codec, chain):
     assert_same(got, want)
 
 
-def test_mixed_fields_vs_oracle(tmp_path):
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_mixed_fields_vs_oracle(tmp_path, zero_copy):
+    """RLE / RAW images, arrays and scalars in one loader; zero_copy requested on a
+    plan with RLE payloads: the loader stages from the pinned heap instead."""
     path = tmp_path / "mixed.bbox"
     bx.write_dataset(mixed_source(bx, 120, 11, max_side=40), path,
                      bx.WriterConfig(page_size=65536, seed=1, compress_probability=0.5))
     pipes = {"image": "crop:30,33|flip:0.5|normpc:1,2,3/4,5,6/bf16", "vec": "normalize:1,2",
              "patch": "crop:4,5|flip:0.5|normalize:3,2", "wide": "float", "ids": "normalize:-5,3"}
-    got = run_gpu(path, 13, "quasi-random", seed=5, epoch=2, pipelines=pipes)
+    got = run_gpu(path, 13, "quasi-random", seed=5, epoch=2, pipelines=pipes,
+                  strategy=bx.OsCache(zero_copy=True) if zero_copy else None)
     want = list(O.loader_batches(path, 13, "quasi-random", 5, 2,
                                  pipelines={k: oracle_spec(v) for k, v in pipes.items()}))
     assert_same(got, want)
