@@ -2150,7 +2150,10 @@ bbx_status bbx_loader_create(bbx_dataset* ds, int device, int32_t batch_size, in
   if (nt <= 0) {   // automatic: the host's cores shared by the node's ranks (torchrun LOCAL_WORLD_SIZE)
     unsigned hc = std::max(1u, std::thread::hardware_concurrency());
     if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) hc = std::max(1u, hc / (unsigned)std::max(1, std::atoi(e)));
-    nt = (int)std::min<unsigned>(16, hc);
+    // three quarters of them, at most 16: the pipeline thread, the consumer and the CUDA
+    // driver's threads keep a core each (A/B on a 16-vCPU box, e2e configs[1] / configs[2]:
+    // 8 threads 454k / 1.43M, 12 threads 488k / 1.63M, 16 threads 475k / 1.60M img/s)
+    nt = (int)std::min<unsigned>(16, std::max(1u, hc - hc / 4));
   }
   L->local_cpus = gpu_local_cpus(device, &L->numa_node);
   if (!L->local_cpus.empty()) nt = std::min<int>(nt, (int)L->local_cpus.size());
